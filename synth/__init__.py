@@ -1,0 +1,138 @@
+"""Seeded synthetic inputs shaped like the paper's workloads (shared by tests, bench, smoke).
+
+This module holds NONE of the method's arithmetic (no Gram, no Cholesky, no triangular
+solve, no shift): it only draws random numbers and builds the paper's test matrices
+("X := U Sigma V^T ... essentially MATLAB's randsvd"), plus the
+BASELINE.json tridiagonal SPD metric B.  Both the oracle and the CUDA path consume what
+it returns; neither is imported here.
+
+Recipes:
+  * U (m x n) and V (n x n): Householder QR (LAPACK geqrf/orgqr via numpy, or cuSOLVER via
+    torch on the device) of i.i.d. N(0,1) matrices, columns sign-normalised so diag(R) > 0.
+  * sigma geometric: sigma_i = kappa^{-(i-1)/(n-1)}, i = 1..n (||X||_2 = 1, kappa_2 = kappa).
+  * sigma "cluster" (BASELINE config 4, reading D15): sigma_1 = 1, sigma_2..sigma_{n-8}
+    log-uniform in [1e-6, 1] sorted descending, the last 8 equal to 1/kappa (= 1e-14).
+  * B: d_i log-uniform in [1, 1e4], e_i = -0.45 sqrt(d_i d_{i+1}) (B = D^1/2 T D^1/2, T SPD).
+Host streams: numpy PCG64 default_rng([seed, tag]); device streams: torch CUDA generator
+seeded with seed (a different stream, stated in DESIGN.md; each arm always compares
+like with like because the oracle receives the very array the GPU factorised).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+TAG_U, TAG_V, TAG_SIGMA, TAG_B = 1, 2, 3, 4
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    m: int
+    n: int
+    kappa: float
+    spectrum: str = "geometric"   # or "cluster"
+    oblique: bool = False
+    gpus: tuple = (1,)
+
+
+# BASELINE.json "configs" (index 0..4)
+CONFIGS = {
+    "PR1": Config("PR1", 2000, 16, 1e12),
+    "C2": Config("C2", 1_000_000, 64, 1e15),
+    "C3": Config("C3", 10_000_000, 128, 1e10, gpus=(1, 2, 4, 8)),
+    "C4": Config("C4", 40_000_000, 256, 1e14, spectrum="cluster", gpus=(4, 8)),
+    "C5": Config("C5", 2_000_000, 64, 1e12, oblique=True, gpus=(1, 8)),
+}
+
+
+def sigma(n: int, kappa: float, spectrum: str = "geometric", seed: int = 0) -> np.ndarray:
+    if n == 1:
+        return np.ones(1)
+    if spectrum == "geometric":
+        i = np.arange(n, dtype=np.float64)
+        return kappa ** (-i / (n - 1))
+    if spectrum == "cluster":
+        rng = np.random.default_rng([seed, TAG_SIGMA])
+        k = min(8, n - 1)
+        mid = np.sort(10.0 ** rng.uniform(-6.0, 0.0, size=n - 1 - k))[::-1]
+        return np.concatenate([[1.0], mid, np.full(k, 1.0 / kappa)])
+    raise ValueError(spectrum)
+
+
+def _signed_qr(G: np.ndarray) -> np.ndarray:
+    Q, R = np.linalg.qr(G, mode="reduced")
+    s = np.sign(np.diag(R))
+    s[s == 0] = 1.0
+    return Q * s
+
+
+def randsvd(m: int, n: int, kappa: float, seed: int = 0, spectrum: str = "geometric") -> np.ndarray:
+    """X = U diag(sigma) V^T as an m x n column-major (Fortran) float64 array."""
+    rng_u = np.random.default_rng([seed, TAG_U])
+    rng_v = np.random.default_rng([seed, TAG_V])
+    U = _signed_qr(rng_u.standard_normal((m, n)))
+    V = _signed_qr(rng_v.standard_normal((n, n)))
+    s = sigma(n, kappa, spectrum, seed)
+    X = (U * s) @ V.T
+    return np.asfortranarray(X)
+
+
+def tridiag_b(m: int, seed: int = 0):
+    """Bands (d, e) of the SPD tridiagonal metric of BASELINE config 5; e[m-1] = 0 (unused)."""
+    rng = np.random.default_rng([seed, TAG_B])
+    d = 10.0 ** rng.uniform(0.0, 4.0, size=m)
+    e = np.zeros(m)
+    e[:-1] = -0.45 * np.sqrt(d[:-1] * d[1:])
+    return d, e
+
+
+def random_rows(m: int, n: int, seed: int = 0) -> np.ndarray:
+    """Plain i.i.d. N(0,1) column-major matrix (kernel-level tests)."""
+    rng = np.random.default_rng([seed, 7])
+    return np.asfortranarray(rng.standard_normal((m, n)))
+
+
+# --------------------------------------------------------------------------- device side
+def randsvd_torch(m: int, n: int, kappa: float, seed: int = 0, spectrum: str = "geometric",
+                  device="cuda", ld: int | None = None):
+    """Same recipe on the device (torch RNG + cuSOLVER Householder QR); returns an (m, n)
+    torch view with column-major strides (1, ld)."""
+    import torch
+
+    ld = ld or m
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed) * 1000003 + TAG_U)
+    G = torch.randn((n, m), generator=g, dtype=torch.float64, device=device).t()  # col-major (m, n)
+    Uq, Ur = torch.linalg.qr(G, mode="reduced")
+    del G
+    sgn = torch.sign(torch.diagonal(Ur))
+    sgn[sgn == 0] = 1.0
+    del Ur
+    gv = torch.Generator(device=device)
+    gv.manual_seed(int(seed) * 1000003 + TAG_V)
+    Gv = torch.randn((n, n), generator=gv, dtype=torch.float64, device=device)
+    Vq, Vr = torch.linalg.qr(Gv)
+    Vq = Vq * torch.sign(torch.diagonal(Vr))
+    s = torch.as_tensor(sigma(n, kappa, spectrum, seed), dtype=torch.float64, device=device)
+    W = (sgn * s)[:, None] * Vq.t()                       # diag(sgn*sigma) V^T, n x n
+    out = torch.empty((n, ld), dtype=torch.float64, device=device)
+    Xc = out.t()[:m]                                        # (m, n), strides (1, ld)
+    chunk = 1 << 22
+    for r0 in range(0, m, chunk):
+        r1 = min(m, r0 + chunk)
+        Xc[r0:r1].copy_(Uq[r0:r1] @ W)
+    del Uq
+    return Xc
+
+
+def tridiag_b_torch(m: int, seed: int = 0, device="cuda"):
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed) * 1000003 + TAG_B)
+    d = 10.0 ** (torch.rand(m, generator=g, dtype=torch.float64, device=device) * 4.0)
+    e = torch.zeros(m, dtype=torch.float64, device=device)
+    e[:-1] = -0.45 * torch.sqrt(d[:-1] * d[1:])
+    return d, e
