@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""bench.py -- shifted CholeskyQR3 fp64 TFLOP/s and % of roofline (BASELINE.json metric).
+
+Workload (BASELINE.json configs[2], the headline): X fp64 m = 10,000,000 x n = 128, kappa_2 = 1e10,
+X = U diag(sigma) V^T with geometric sigma, seed 0, generated on the device.
+One "step" = one full scqr3_factor call (every pass of Gram -> shifted Cholesky -> TRSM -> R
+accumulation until the stop rule fires; 3 passes on this workload) through the C ABI.
+value = 6 m n^2 / t (the north star's 3-pass flop count, whole job over all ranks).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3]
+  python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N    (one rank per GPU)
+
+Rows are block-partitioned across ranks; each pass does one NCCL allreduce of the packed n x n
+Gram (the method's one exchange): total work is fixed as N grows -> "strong" scaling.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAKS = os.path.join(ROOT, "profiles", "fp64_peaks.json")
+NCU_TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+METRIC = "shifted CholeskyQR3 fp64 TFLOP/s & % roofline, m=1e7 n=128, 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--cpu-rows", type=int, default=0, help="rows of the oracle's bounded sample")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def flops_3pass(m, n):
+    return 6.0 * m * n * n
+
+
+def load_json(path):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx.append(float(p[2]))
+                power.append(float(p[3]))
+            except ValueError:
+                continue
+            for name, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(power) if power else None}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    import oracle
+    import synth
+
+    cfg = synth.CONFIGS[args.config]
+    n = cfg.n
+    rows = args.cpu_rows or max(n, int(5e5 * (128 / n) ** 2))
+    rows = min(rows, cfg.m)
+    X = synth.randsvd(rows, n, cfg.kappa, seed=0, spectrum=cfg.spectrum)
+    kw = {}
+    if cfg.oblique:
+        d, e = synth.tridiag_b(rows, seed=0)
+        kw = dict(d=d, e=e)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        r = oracle.scqr3(X, **kw) if not cfg.oblique else oracle.scqr3(X, kw["d"], kw["e"])
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    t = statistics.mean(times)
+    val = flops_3pass(rows, n) / t / 1e12
+    cores = oracle.num_threads()
+    sample = f"oracle.scqr3 on the first {rows} of {cfg.m} rows ({args.config} recipe, host numpy stream), per step"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} bounded sample: m={rows} n={n} kappa={cfg.kappa:g}",
+                   "m": rows, "n": n, "passes": r.passes, "status": r.status},
+        "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1809_11085_b200 as sq
+    from paper_1809_11085_b200 import _abi
+    import synth
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cfg = synth.CONFIGS[args.config]
+    m, n = cfg.m, cfg.n
+    r0, r1 = m * rank // world, m * (rank + 1) // world
+    mloc = r1 - r0
+
+    # ---- input: the same global X on every rank (same seed), keep this rank's row block
+    Xg = synth.randsvd_torch(m, n, cfg.kappa, seed=0, spectrum=cfg.spectrum, device=dev)
+    if world == 1:
+        X = Xg
+    else:
+        X = sq.colmajor_empty(mloc, n, device=dev)
+        X.copy_(Xg[r0:r1])
+        del Xg
+    d = e = None
+    if cfg.oblique:
+        dg, eg = synth.tridiag_b_torch(m, seed=0, device=dev)
+        d, e = dg[r0:r1].contiguous(), eg[r0:r1].contiguous()
+        del dg, eg
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+    comm = sq.Comm.create() if world > 1 else None
+    stream = torch.cuda.Stream(device=dev)
+    ws = sq.workspace(mloc, n, oblique=cfg.oblique, device=dev)
+    Q = sq.colmajor_empty(mloc, n, device=dev)
+    R = torch.empty((n, n), dtype=torch.float64, device=dev).t()
+    prof = _abi.Prof()
+
+    def step(with_prof=False):
+        kw = dict(Q=Q, R=R, ws=ws, comm=comm, m_global=m, stream=stream)
+        if with_prof:
+            kw["prof"] = prof
+        if cfg.oblique:
+            return sq.scqr3_factor_oblique(X, d, e, **kw)
+        return sq.scqr3_factor(X, **kw)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            res = step()
+            assert res.status == 0, f"warm-up step failed with status {res.status}"
+    stream.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    clocks = Clocks(local if world > 1 else 0)
+    sq.launch_count(reset=True)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    clocks.start()
+    time.sleep(0.3)
+    with torch.cuda.stream(stream):
+        ev0.record(stream)
+        for _ in range(args.steps):
+            res = step(with_prof=True)
+        ev1.record(stream)
+    stream.synchronize()
+    clk = clocks.stop()
+    launches = sq.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = flops_3pass(m, n) / (ms * 1e-3) / 1e12
+    passes = res.passes
+    actual = passes * m * (2.0 * n * n + n) / (ms * 1e-3) / 1e12
+
+    # ---- per-kernel device time measured live during the timed steps (events on `stream`)
+    peaks = load_json(FP64_PEAKS) or {}
+    peak = peaks.get("roofline_fp64_peak_tflops", 37.1)
+    kern = {}
+    for name, msum, cnt, fl in (("gram", prof.gram_ms, prof.gram_launches, mloc * n * (n + 1.0)),
+                                ("trsm", prof.trsm_ms, prof.trsm_launches, mloc * float(n) * n),
+                                ("chol", prof.chol_ms, prof.chol_launches, None),
+                                ("reduce", prof.reduce_ms, prof.reduce_launches, None),
+                                ("comm", prof.comm_ms, prof.comm_calls, None)):
+        if cnt:
+            avg = msum / cnt
+            kern[name] = {"avg_ms": avg, "launches": int(cnt), "share_of_step": msum / (ms * args.steps)}
+            if fl:
+                kern[name]["tflops"] = fl / (avg * 1e-3) / 1e12
+                kern[name]["frac_of_peak"] = kern[name]["tflops"] / peak
+    dom = max(("gram", "trsm"), key=lambda k: kern.get(k, {}).get("avg_ms", 0) * kern.get(k, {}).get("launches", 0))
+    traffic_tab = load_json(NCU_TRAFFIC) or {}
+    tr = traffic_tab.get(f"{args.config}:{dom}")
+    roofline = {"bound": "tensor", "achieved": kern[dom]["tflops"], "peak": peak, "unit": "TFLOP/s",
+                "frac": kern[dom]["tflops"] / peak, "traffic": tr.get("bytes_per_launch") if tr else None,
+                "kernel": f"{dom}_kernel (FP64 DMMA)",
+                "peak_source": "measured FP64 DMMA loop on this pool's B200 (profiles/fp64_peaks.json); "
+                               "MEASURED_PEAKS.json has no fp64 entry",
+                "algorithmic_flops_per_launch": mloc * n * (n + 1.0) if dom == "gram" else mloc * float(n) * n}
+    step_roof_ms = max(flops_3pass(mloc, n) / (peak * 1e12), (24.0 * mloc * n * 3) / 6536.7e9) * 1e3
+
+    # ---- end to end through the C ABI with host buffers (H2D of X, D2H of Q and R inside)
+    e2e = None
+    if not args.no_e2e and not cfg.oblique:
+        Xh = torch.empty((n, mloc), dtype=torch.float64, pin_memory=True).t()
+        Xh.copy_(X)
+        Qh = torch.empty((n, mloc), dtype=torch.float64, pin_memory=True).t()
+        Rh = torch.empty((n, n), dtype=torch.float64, pin_memory=True).t()
+        wsh = sq.workspace(mloc, n, host_io=True, device=dev)
+        del ws
+        torch.cuda.empty_cache()
+        with torch.cuda.stream(stream):
+            sq.scqr3_factor_host(Xh, Q=Qh, R=Rh, ws=wsh, comm=comm, m_global=m, stream=stream)  # warm-up
+            if world > 1:
+                dist.barrier()
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(args.e2e_steps):
+                rh = sq.scqr3_factor_host(Xh, Q=Qh, R=Rh, ws=wsh, comm=comm, m_global=m, stream=stream)
+            a1.record(stream)
+        stream.synchronize()
+        ems = a0.elapsed_time(a1) / args.e2e_steps
+        te = torch.tensor([ems], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        ems = float(te.item())
+        e2e = {"value": flops_3pass(m, n) / (ems * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": 8 * mloc * n, "d2h_bytes_per_step": 8 * mloc * n + 8 * n * n,
+               "ms_per_step": ems, "status": rh.status,
+               "api": "scqr3_factor_host (pinned host X in, pinned host Q and R out)"}
+
+    # ---- CPU oracle baseline on a bounded sample of the same X (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle
+
+        rows = args.cpu_rows or max(n, int(2e6 * (128 / n) ** 2))
+        rows = min(rows, mloc)
+        Xs = X[:rows].cpu().numpy()
+        t0 = time.perf_counter()
+        if cfg.oblique:
+            ro = oracle.scqr3(Xs, d[:rows].cpu().numpy(), e[:rows].cpu().numpy())
+        else:
+            ro = oracle.scqr3(Xs)
+        tc = time.perf_counter() - t0
+        cpu = {"value": flops_3pass(rows, n) / tc / 1e12, "unit": "TFLOP/s", "cores": oracle.num_threads(),
+               "kind": "oracle", "seconds": tc, "passes": ro.passes, "status": ro.status,
+               "sample": f"first {rows} of {m} rows of the same device-generated X ({args.config}), one factorisation"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: X fp64 m={m} n={n} kappa2={cfg.kappa:g} "
+                                   f"({cfg.spectrum} sigma, U,V Householder of N(0,1)), seed 0",
+                       "m": m, "n": n, "kappa": cfg.kappa, "passes": passes,
+                       "shifted": [t["shifted"] for t in res.trace], "parallelism": f"row-block x{world}",
+                       "l2": "no flush: X and Q (10.24 GB each) >> 126 MB L2"},
+            "roofline": roofline,
+            "roofline_step": {"ms": step_roof_ms, "frac": step_roof_ms / ms,
+                              "model": "max(6mn^2 / fp64 peak, 72mn bytes / 6536.7 GB/s) per GPU"},
+            "tflops_actual_passes": actual,
+            "kernels": kern,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,167 @@
+/*
+ * scqr3.h -- C ABI of libscqr3.so: shifted CholeskyQR3 for tall-skinny fp64 matrices on
+ * NVIDIA B200 (sm_100a).
+ *
+ * Method: Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa, "Shifted CholeskyQR for
+ * computing the QR factorization of ill-conditioned matrices" (arXiv:1809.11085).
+ * Citations "P:L" are lines of the paper's text; readings "Dn" are listed in
+ * DESIGN.md.  Everything is IEEE binary64 (u = 2^-53).
+ *
+ * Conventions common to every entry point
+ *   - Matrices are COLUMN-MAJOR.  X, Q are m x n with leading dimensions ld, ldq >= m.
+ *     R is n x n with leading dimension n; on success its strict lower triangle is zero
+ *     and its diagonal is positive, so it is the unique R factor.
+ *   - Pointers are DEVICE pointers unless the name ends in _host.  The caller owns all
+ *     memory (allocated e.g. with torch); the library allocates nothing per call on the
+ *     device (it keeps a small pinned host status block and two events per thread).
+ *   - TMA requirements: X, Q 16-byte aligned and ld, ldq even (8*ld % 16 == 0).
+ *   - Supported sizes: 1 <= n <= 256, m_global >= n, m >= 0 on every rank.
+ *   - All device work is ordered on opts->stream; every call returns only after that
+ *     work has finished (the pass count is data dependent).
+ *   - Return codes: SCQR3_OK; SCQR3_EINVAL (bad argument, CUDA or NCCL error -- detail in
+ *     scqr3_last_error()); SCQR3_EBREAKDOWN (Cholesky broke down even with the shift:
+ *     out of the method's regime or rank deficient); SCQR3_ENOCONV (no stop
+ *     within max_passes).  On a non-OK return Q and R are unspecified; the trace is valid.
+ */
+#ifndef SCQR3_H
+#define SCQR3_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SCQR3_ABI_VERSION 1
+
+enum { SCQR3_OK = 0, SCQR3_EINVAL = 1, SCQR3_EBREAKDOWN = 2, SCQR3_ENOCONV = 3 };
+
+/* Shift policy.  SAFE: s = 11{mn+n(n+1)} u N^2 (eq. finds2) or the
+ * oblique 11{2m sqrt(mn)+n(n+1)} u N^2 ||B|| (eq. finds2B) on pass 1 and on any
+ * later pass whose plain Cholesky breaks down (Alg. 2 lines 4-7).
+ * FIXED: shift_value on pass 1 (kernel-level parity tests), SAFE on breakdown.
+ * NONE: no shift ever (plain iterated CholeskyQR, for tests; breakdown is final). */
+enum { SCQR3_SHIFT_SAFE = 0, SCQR3_SHIFT_FIXED = 1, SCQR3_SHIFT_NONE = 2 };
+
+/* Estimate N^2 of ||Q||_2^2 for the shift (reading D2/D4).
+ * POWER: 1.01 * Rayleigh quotient after power_iters steps on the computed n x n Gram.
+ * FROBENIUS: trace of the Gram = ||Q||_F^2 (paper-sanctioned conservative choice).
+ * USER: norm2_bound^2 on pass 1 (POWER afterwards).  Oblique always uses ||Q||_F^2 for
+ * X (or USER on pass 1) and bnorm_bound, else the Gershgorin bound, for ||B||_2 (D4). */
+enum { SCQR3_NORM_POWER = 0, SCQR3_NORM_FROBENIUS = 1, SCQR3_NORM_USER = 2 };
+
+typedef struct scqr3_pass_trace {
+  double shift;            /* shift added on this pass (0 if none)                     */
+  int32_t shifted;         /* 1 if chol(A + sI) was used                               */
+  int32_t breakdown_pivot; /* 1-based pivot of the failed plain attempt, 0 if none     */
+  double pivot_value;      /* value of that pivot before the square root               */
+  double norm2_est;        /* N^2 used in the shift formula                            */
+  double dev_F;            /* ||A_k - I||_F of this pass's input Gram (stop test, D6)  */
+} scqr3_pass_trace;
+
+/* Optional per-kernel device time, accumulated over calls (caller zeroes it).  Measured with
+ * CUDA events recorded on opts->stream around each launch, so it adds two event records per
+ * launch and is meant for benchmarks. */
+typedef struct scqr3_prof {
+  double gram_ms;          /* gram_tma_kernel (Q^T Q or Q^T B Q partial tiles)            */
+  int64_t gram_launches;
+  double reduce_ms;        /* gram_reduce_kernel (+ the B*Q kernel for the oblique Gram)   */
+  int64_t reduce_launches;
+  double chol_ms;          /* chol_kernel                                                  */
+  int64_t chol_launches;
+  double trsm_ms;          /* trsm_kernel                                                  */
+  int64_t trsm_launches;
+  double comm_ms;          /* NCCL allreduce / halo exchange                               */
+  int64_t comm_calls;
+} scqr3_prof;
+
+typedef struct scqr3_opts {
+  int32_t abi_version;     /* = SCQR3_ABI_VERSION                                      */
+  int32_t shift_mode;      /* SCQR3_SHIFT_*                                            */
+  double shift_value;      /* for SCQR3_SHIFT_FIXED                                    */
+  int32_t norm_mode;       /* SCQR3_NORM_*                                             */
+  int32_t power_iters;     /* default 32                                               */
+  double norm2_bound;      /* USER: N >= ||X||_2                                       */
+  double bnorm_bound;      /* oblique: N_B >= ||B||_2 (0 => Gershgorin)                */
+  int32_t max_passes;      /* default 8                                        */
+  int32_t reserved0;
+  double stop_tol;         /* stop after a plain pass with ||A_k - I||_F <= stop_tol (D6); default 0.5 */
+  int64_t m_global;        /* rows over all ranks (shift uses the global m); 0 => sum over ranks */
+  void* stream;            /* cudaStream_t; NULL = legacy default stream                */
+  void* comm;              /* from scqr3_comm_init; NULL = single GPU                   */
+  void* workspace;         /* device memory of >= scqr3_workspace_size() bytes, 256-B aligned */
+  size_t workspace_bytes;
+  scqr3_pass_trace* trace; /* host array of trace_cap entries (may be NULL)            */
+  int32_t trace_cap;
+  int32_t* passes_out;     /* host; number of passes executed (may be NULL)            */
+  scqr3_prof* prof;        /* host; per-kernel device time (may be NULL)                */
+} scqr3_opts;
+
+/* Fills *o with the defaults above (abi_version, SAFE, POWER, 32 iterations, 8 passes,
+ * stop_tol 0.5, everything else zero). */
+void scqr3_default_opts(scqr3_opts* o);
+
+/* Device workspace bytes for scqr3_factor / scqr3_factor_oblique on this rank's m x n
+ * shard (independent of the data; oblique needs an extra m x n buffer for B*Q). */
+size_t scqr3_workspace_size(int64_t m, int64_t n, int32_t oblique);
+
+/* Shifted CholeskyQR3 X = QR (Alg. 3, with Alg. 2's breakdown re-shift,
+ * P:672-688; pass control D5/D6).  Per pass: Gram A = Q^T Q (one NCCL allreduce of
+ * the packed n x n Gram when opts->comm is set), norm estimate and shift,
+ * Cholesky R~ (replicated on every rank), Q := Q R~^{-1} row by row, and
+ * R := R~ R.  Q may alias X (then ldq == ld).  With opts->comm, X/Q/m are this
+ * rank's contiguous row block and R is identical on every rank. */
+int scqr3_factor(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, int64_t ldq,
+                 double* R, const scqr3_opts* opts);
+
+/* Oblique inner product (Alg. 5; B-Gram in every pass, reading D8):
+ * X = QR with Q^T B Q = I for the SPD tridiagonal B with B(i,i) = b_diag[i] and
+ * B(i,i+1) = B(i+1,i) = b_off[i] (b_off[m-1] couples this rank's last row to the next
+ * rank's first row; ignored on the last rank).  Bands are sharded with the rows; the
+ * one-row halo is exchanged with NCCL send/recv when opts->comm is set. */
+int scqr3_factor_oblique(int64_t m, int64_t n, const double* X, int64_t ld, const double* b_diag,
+                         const double* b_off, double* Q, int64_t ldq, double* R,
+                         const scqr3_opts* opts);
+
+/* Host-memory variant of scqr3_factor (the end-to-end call): copies X_host to the device
+ * (pinned host memory recommended), factors in place, copies Q and R back.  opts->workspace
+ * must hold scqr3_host_workspace_size(m, n) bytes. */
+size_t scqr3_host_workspace_size(int64_t m, int64_t n);
+int scqr3_factor_host(int64_t m, int64_t n, const double* X_host, int64_t ld, double* Q_host,
+                      int64_t ldq, double* R_host, const scqr3_opts* opts);
+
+/* ---- kernel-level entry points (parity tests call these through the same library) ---- */
+/* A = Q^T Q (n x n, column-major, both triangles) -- one Gram kernel + reduction. */
+int scqr3_gram(int64_t m, int64_t n, const double* X, int64_t ld, double* A, const scqr3_opts* opts);
+/* A = sym(X^T B X) for the tridiagonal B above; colsq[j] = sum_i x_ij^2. */
+int scqr3_gram_oblique(int64_t m, int64_t n, const double* X, int64_t ld, const double* b_diag,
+                       const double* b_off, double* A, double* colsq, const scqr3_opts* opts);
+/* R~ = chol(A + sI) (upper, n x n column-major) with breakdown detection (D9).
+ * Returns SCQR3_EBREAKDOWN with *pivot (1-based) and *pivot_value on a pivot <= 0 or
+ * non-finite, else SCQR3_OK with *pivot = 0. */
+int scqr3_cholesky(int64_t n, const double* A, double s, double* R, int32_t* pivot,
+                   double* pivot_value, const scqr3_opts* opts);
+/* Q = X R^{-1} for upper-triangular R with positive diagonal. */
+int scqr3_trsm(int64_t m, int64_t n, const double* X, int64_t ld, const double* R, double* Q,
+               int64_t ldq, const scqr3_opts* opts);
+
+/* ---- multi-GPU (one process per GPU; NCCL over NVLink) ---- */
+#define SCQR3_COMM_ID_BYTES 128
+/* Writes an NCCL unique id (SCQR3_COMM_ID_BYTES bytes) to id_out; call on rank 0 and
+ * broadcast the bytes (e.g. with torch.distributed). */
+int scqr3_comm_unique_id(void* id_out);
+/* Creates this rank's communicator on the current CUDA device; *comm_out is passed in
+ * scqr3_opts.comm.  Collective over all nranks. */
+int scqr3_comm_init(void** comm_out, int32_t nranks, const void* id, int32_t rank);
+int scqr3_comm_destroy(void* comm);
+
+/* Thread-local description of the last SCQR3_EINVAL. */
+const char* scqr3_last_error(void);
+/* Number of kernel launches issued by this thread since the last reset (bench evidence). */
+int64_t scqr3_launch_count(int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCQR3_H */

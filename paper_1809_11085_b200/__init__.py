@@ -1,0 +1,256 @@
+"""Shifted CholeskyQR3 (arXiv:1809.11085) on NVIDIA B200 -- thin Python binding of libscqr3.so.
+
+Every step of the factorisation runs in the library's sm_100a kernels; this module only
+marshals torch tensors (device memory, streams) into the C ABI of include/scqr3.h.  There is
+no CPU fallback: if the library is missing, every call raises.
+
+Matrices are column-major: an (m, n) torch tensor with strides (1, ld), ld even (TMA).  Use
+``colmajor_empty`` / ``to_colmajor`` to make one.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+from . import _abi
+from ._abi import (EBREAKDOWN, EINVAL, ENOCONV, NORM_FROBENIUS, NORM_POWER, NORM_USER, OK,  # noqa: F401
+                   SHIFT_FIXED, SHIFT_NONE, SHIFT_SAFE)
+
+__all__ = [
+    "scqr3_factor", "scqr3_factor_oblique", "scqr3_factor_host", "scqr3_gram", "scqr3_gram_oblique",
+    "scqr3_cholesky", "scqr3_trsm", "colmajor_empty", "to_colmajor", "workspace", "Comm", "Result",
+    "ScqrError", "launch_count", "library_path",
+]
+
+library_path = _abi.LIB_PATH
+
+
+class ScqrError(RuntimeError):
+    pass
+
+
+@dataclass
+class Result:
+    status: int
+    Q: object
+    R: object
+    passes: int
+    trace: list = field(default_factory=list)
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _check(rc: int) -> int:
+    if rc == EINVAL:
+        raise ScqrError(_abi.last_error())
+    return rc
+
+
+def even_ld(m: int) -> int:
+    return max(2, (m + 1) // 2 * 2)
+
+
+def colmajor_empty(m: int, n: int, device="cuda", ld: int | None = None):
+    """Uninitialised (m, n) float64 tensor with column-major strides (1, ld), ld even."""
+    torch = _torch()
+    ld = ld or even_ld(m)
+    return torch.empty((n, ld), dtype=torch.float64, device=device).t()[:m]
+
+
+def to_colmajor(X, device=None):
+    """Column-major float64 copy (or X itself if it already qualifies)."""
+    torch = _torch()
+    X = torch.as_tensor(X)
+    dev = device if device is not None else X.device
+    if (X.dtype == torch.float64 and X.device == torch.device(dev) and X.dim() == 2 and X.stride(0) == 1
+            and X.stride(1) >= max(X.shape[0], 1) and X.stride(1) % 2 == 0 and X.data_ptr() % 16 == 0):
+        return X
+    out = colmajor_empty(X.shape[0], X.shape[1], device=dev)
+    out.copy_(X)
+    return out
+
+
+def _ld(X) -> int:
+    if X.dim() != 2 or X.stride(0) != 1:
+        raise ScqrError("matrix must be column-major: an (m, n) tensor with stride (1, ld)")
+    return max(X.stride(1), 1) if X.shape[1] > 1 else even_ld(X.shape[0])
+
+
+def workspace(m: int, n: int, oblique: bool = False, device="cuda", host_io: bool = False):
+    torch = _torch()
+    L = _abi.lib()
+    nbytes = L.scqr3_host_workspace_size(m, n) if host_io else L.scqr3_workspace_size(m, n, int(oblique))
+    if nbytes == 0:
+        raise ScqrError(f"unsupported size m={m} n={n}")
+    return torch.empty(nbytes, dtype=torch.uint8, device=device)
+
+
+class Comm:
+    """NCCL communicator of libscqr3 for one rank (one process per GPU)."""
+
+    def __init__(self, handle, rank: int, world: int):
+        self.handle, self.rank, self.world = handle, rank, world
+
+    @classmethod
+    def create(cls, group=None):
+        """Collective over torch.distributed: rank 0 makes the NCCL id, everybody inits."""
+        torch = _torch()
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        buf = ctypes.create_string_buffer(_abi.COMM_ID_BYTES)
+        if rank == 0:
+            _check(_abi.lib().scqr3_comm_unique_id(buf))
+        backend = dist.get_backend(group)
+        dev = "cuda" if backend == "nccl" else "cpu"
+        t = torch.tensor(list(buf.raw), dtype=torch.uint8, device=dev)
+        dist.broadcast(t, src=0, group=group)
+        raw = bytes(t.cpu().tolist())
+        h = ctypes.c_void_p()
+        _check(_abi.lib().scqr3_comm_init(ctypes.byref(h), world, raw, rank))
+        return cls(h, rank, world)
+
+    def destroy(self):
+        if self.handle:
+            _abi.lib().scqr3_comm_destroy(self.handle)
+            self.handle = None
+
+
+def _opts(shift_mode=SHIFT_SAFE, shift_value=0.0, norm_mode=NORM_POWER, norm2_bound=0.0, bnorm_bound=0.0,
+          max_passes=8, stop_tol=0.5, power_iters=32, m_global=0, stream=None, comm=None, ws=None,
+          trace_cap=16, prof=None):
+    torch = _torch()
+    o = _abi.Opts()
+    _abi.lib().scqr3_default_opts(ctypes.byref(o))
+    o.shift_mode, o.shift_value = shift_mode, float(shift_value)
+    o.norm_mode, o.norm2_bound, o.bnorm_bound = norm_mode, float(norm2_bound), float(bnorm_bound)
+    o.max_passes, o.stop_tol, o.power_iters = int(max_passes), float(stop_tol), int(power_iters)
+    o.m_global = int(m_global)
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    o.stream = ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+    o.comm = comm.handle if isinstance(comm, Comm) else comm
+    if ws is not None:
+        o.workspace, o.workspace_bytes = ctypes.c_void_p(ws.data_ptr()), ws.numel()
+    tr = (_abi.PassTrace * trace_cap)()
+    passes = ctypes.c_int32(0)
+    o.trace = ctypes.cast(tr, ctypes.POINTER(_abi.PassTrace))
+    o.trace_cap = trace_cap
+    o.passes_out = ctypes.pointer(passes)
+    if prof is not None:
+        o.prof = ctypes.pointer(prof)
+    return o, tr, passes
+
+
+def _trace(tr, k):
+    return [dict(shift=t.shift, shifted=bool(t.shifted), breakdown_pivot=t.breakdown_pivot,
+                 pivot_value=t.pivot_value, norm2_est=t.norm2_est, dev_F=t.dev_F) for t in list(tr)[:k]]
+
+
+def scqr3_factor(X, *, Q=None, R=None, ws=None, inplace=False, **kw) -> Result:
+    """Shifted CholeskyQR3 of a column-major CUDA float64 X (Alg. 3 + Alg. 2 re-shift)."""
+    torch = _torch()
+    m, n = X.shape
+    if Q is None:
+        Q = X if inplace else colmajor_empty(m, n, device=X.device)
+    if R is None:
+        R = torch.empty((n, n), dtype=torch.float64, device=X.device).t()  # column-major n x n
+    if ws is None:
+        ws = workspace(m, n, device=X.device)
+    o, tr, passes = _opts(ws=ws, **kw)
+    rc = _check(_abi.lib().scqr3_factor(m, n, X.data_ptr(), _ld(X), Q.data_ptr(), _ld(Q), R.data_ptr(),
+                                        ctypes.byref(o)))
+    return Result(rc, Q, R, passes.value, _trace(tr, passes.value))
+
+
+def scqr3_factor_oblique(X, d, e, *, Q=None, R=None, ws=None, inplace=False, **kw) -> Result:
+    """Oblique shifted CholeskyQR3 (Alg. 5, B-Gram in all passes) for tridiagonal B=(d, e)."""
+    torch = _torch()
+    m, n = X.shape
+    if Q is None:
+        Q = X if inplace else colmajor_empty(m, n, device=X.device)
+    if R is None:
+        R = torch.empty((n, n), dtype=torch.float64, device=X.device).t()
+    if ws is None:
+        ws = workspace(m, n, oblique=True, device=X.device)
+    d = d.contiguous()
+    e = e.contiguous()
+    o, tr, passes = _opts(ws=ws, **kw)
+    rc = _check(_abi.lib().scqr3_factor_oblique(m, n, X.data_ptr(), _ld(X), d.data_ptr(), e.data_ptr(),
+                                                Q.data_ptr(), _ld(Q), R.data_ptr(), ctypes.byref(o)))
+    return Result(rc, Q, R, passes.value, _trace(tr, passes.value))
+
+
+def scqr3_factor_host(X, *, Q=None, R=None, ws=None, **kw) -> Result:
+    """End-to-end call on HOST (CPU, ideally pinned) column-major tensors."""
+    torch = _torch()
+    m, n = X.shape
+    if Q is None:
+        Q = torch.empty((n, m), dtype=torch.float64).t()
+    if R is None:
+        R = torch.empty((n, n), dtype=torch.float64).t()
+    if ws is None:
+        ws = workspace(m, n, host_io=True)
+    o, tr, passes = _opts(ws=ws, **kw)
+    rc = _check(_abi.lib().scqr3_factor_host(m, n, X.data_ptr(), max(X.stride(1), m), Q.data_ptr(),
+                                             max(Q.stride(1), m), R.data_ptr(), ctypes.byref(o)))
+    return Result(rc, Q, R, passes.value, _trace(tr, passes.value))
+
+
+def scqr3_gram(X, *, ws=None, **kw):
+    torch = _torch()
+    m, n = X.shape
+    A = torch.empty((n, n), dtype=torch.float64, device=X.device).t()
+    ws = ws if ws is not None else workspace(m, n, device=X.device)
+    o, _, _ = _opts(ws=ws, **kw)
+    _check(_abi.lib().scqr3_gram(m, n, X.data_ptr(), _ld(X), A.data_ptr(), ctypes.byref(o)))
+    return A
+
+
+def scqr3_gram_oblique(X, d, e, *, ws=None, **kw):
+    torch = _torch()
+    m, n = X.shape
+    A = torch.empty((n, n), dtype=torch.float64, device=X.device).t()
+    cs = torch.empty(1, dtype=torch.float64, device=X.device)
+    ws = ws if ws is not None else workspace(m, n, oblique=True, device=X.device)
+    o, _, _ = _opts(ws=ws, **kw)
+    _check(_abi.lib().scqr3_gram_oblique(m, n, X.data_ptr(), _ld(X), d.contiguous().data_ptr(),
+                                         e.contiguous().data_ptr(), A.data_ptr(), cs.data_ptr(),
+                                         ctypes.byref(o)))
+    return A, cs
+
+
+def scqr3_cholesky(A, s: float = 0.0, *, ws=None, **kw):
+    """R = chol(A + sI) or ('breakdown', pivot, value)."""
+    torch = _torch()
+    n = A.shape[0]
+    A = to_colmajor(A) if A.shape[0] > 1 else A.contiguous()
+    R = torch.empty((n, n), dtype=torch.float64, device=A.device).t()
+    ws = ws if ws is not None else workspace(n, n, device=A.device)
+    o, _, _ = _opts(ws=ws, **kw)
+    piv = ctypes.c_int32(0)
+    pv = ctypes.c_double(0)
+    rc = _check(_abi.lib().scqr3_cholesky(n, A.data_ptr(), float(s), R.data_ptr(), ctypes.byref(piv),
+                                          ctypes.byref(pv), ctypes.byref(o)))
+    if rc == EBREAKDOWN:
+        return ("breakdown", piv.value, pv.value)
+    return R
+
+
+def scqr3_trsm(X, R, *, Q=None, ws=None, **kw):
+    m, n = X.shape
+    Q = Q if Q is not None else colmajor_empty(m, n, device=X.device)
+    R = to_colmajor(R) if n > 1 else R.contiguous()
+    ws = ws if ws is not None else workspace(m, n, device=X.device)
+    o, _, _ = _opts(ws=ws, **kw)
+    _check(_abi.lib().scqr3_trsm(m, n, X.data_ptr(), _ld(X), R.data_ptr(), Q.data_ptr(), _ld(Q),
+                                 ctypes.byref(o)))
+    return Q
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(_abi.lib().scqr3_launch_count(int(reset)))

@@ -1,0 +1,97 @@
+"""ctypes declarations for libscqr3.so (include/scqr3.h).  Argument marshalling only."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libscqr3.so")
+
+SCQR3_ABI_VERSION = 1
+OK, EINVAL, EBREAKDOWN, ENOCONV = 0, 1, 2, 3
+SHIFT_SAFE, SHIFT_FIXED, SHIFT_NONE = 0, 1, 2
+NORM_POWER, NORM_FROBENIUS, NORM_USER = 0, 1, 2
+COMM_ID_BYTES = 128
+
+EXPORTED = [
+    "scqr3_default_opts", "scqr3_workspace_size", "scqr3_factor", "scqr3_factor_oblique",
+    "scqr3_host_workspace_size", "scqr3_factor_host", "scqr3_gram", "scqr3_gram_oblique",
+    "scqr3_cholesky", "scqr3_trsm", "scqr3_comm_unique_id", "scqr3_comm_init",
+    "scqr3_comm_destroy", "scqr3_last_error", "scqr3_launch_count",
+]
+
+
+class PassTrace(ctypes.Structure):
+    _fields_ = [
+        ("shift", ctypes.c_double), ("shifted", ctypes.c_int32),
+        ("breakdown_pivot", ctypes.c_int32), ("pivot_value", ctypes.c_double),
+        ("norm2_est", ctypes.c_double), ("dev_F", ctypes.c_double),
+    ]
+
+
+class Prof(ctypes.Structure):
+    _fields_ = [
+        ("gram_ms", ctypes.c_double), ("gram_launches", ctypes.c_int64),
+        ("reduce_ms", ctypes.c_double), ("reduce_launches", ctypes.c_int64),
+        ("chol_ms", ctypes.c_double), ("chol_launches", ctypes.c_int64),
+        ("trsm_ms", ctypes.c_double), ("trsm_launches", ctypes.c_int64),
+        ("comm_ms", ctypes.c_double), ("comm_calls", ctypes.c_int64),
+    ]
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [
+        ("abi_version", ctypes.c_int32), ("shift_mode", ctypes.c_int32),
+        ("shift_value", ctypes.c_double), ("norm_mode", ctypes.c_int32),
+        ("power_iters", ctypes.c_int32), ("norm2_bound", ctypes.c_double),
+        ("bnorm_bound", ctypes.c_double), ("max_passes", ctypes.c_int32),
+        ("reserved0", ctypes.c_int32), ("stop_tol", ctypes.c_double),
+        ("m_global", ctypes.c_int64), ("stream", ctypes.c_void_p), ("comm", ctypes.c_void_p),
+        ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
+        ("trace", ctypes.POINTER(PassTrace)), ("trace_cap", ctypes.c_int32),
+        ("passes_out", ctypes.POINTER(ctypes.c_int32)), ("prof", ctypes.POINTER(Prof)),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    """Load libscqr3.so; fails loudly (no fallback of any kind) if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is not built: run `python -m paper_1809_11085_b200.build` "
+                               "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        i64, vp, P = ctypes.c_int64, ctypes.c_void_p, ctypes.POINTER(Opts)
+        L.scqr3_default_opts.argtypes = [P]
+        L.scqr3_default_opts.restype = None
+        L.scqr3_workspace_size.argtypes = [i64, i64, ctypes.c_int32]
+        L.scqr3_workspace_size.restype = ctypes.c_size_t
+        L.scqr3_factor.argtypes = [i64, i64, vp, i64, vp, i64, vp, P]
+        L.scqr3_factor_oblique.argtypes = [i64, i64, vp, i64, vp, vp, vp, i64, vp, P]
+        L.scqr3_host_workspace_size.argtypes = [i64, i64]
+        L.scqr3_host_workspace_size.restype = ctypes.c_size_t
+        L.scqr3_factor_host.argtypes = [i64, i64, vp, i64, vp, i64, vp, P]
+        L.scqr3_gram.argtypes = [i64, i64, vp, i64, vp, P]
+        L.scqr3_gram_oblique.argtypes = [i64, i64, vp, i64, vp, vp, vp, vp, P]
+        L.scqr3_cholesky.argtypes = [i64, vp, ctypes.c_double, vp, ctypes.POINTER(ctypes.c_int32),
+                                     ctypes.POINTER(ctypes.c_double), P]
+        L.scqr3_trsm.argtypes = [i64, i64, vp, i64, vp, vp, i64, P]
+        L.scqr3_comm_unique_id.argtypes = [vp]
+        L.scqr3_comm_init.argtypes = [ctypes.POINTER(vp), ctypes.c_int32, vp, ctypes.c_int32]
+        L.scqr3_comm_destroy.argtypes = [vp]
+        L.scqr3_last_error.restype = ctypes.c_char_p
+        L.scqr3_launch_count.argtypes = [ctypes.c_int32]
+        L.scqr3_launch_count.restype = ctypes.c_int64
+        for name in ("scqr3_factor", "scqr3_factor_oblique", "scqr3_factor_host", "scqr3_gram",
+                     "scqr3_gram_oblique", "scqr3_cholesky", "scqr3_trsm", "scqr3_comm_unique_id",
+                     "scqr3_comm_init", "scqr3_comm_destroy"):
+            getattr(L, name).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    return lib().scqr3_last_error().decode()

@@ -1,0 +1,271 @@
+// gram.cu -- Gram matrix kernels (step a1 / a1b of the hot path).
+//
+//   A = Q^T Q            (eq. (1); Alg. 1 line 1 P:137; Alg. 2 line 3 P:678; Alg. 3)
+//   A = sym(Q^T (B Q))   (Alg. 4 line 1 P:878; symmetrised as in S:262; every pass, reading D8)
+//
+// Design: split-m persistent CTAs.  One producer warp streams 16-row
+// x npad-column stages of Q (and of Y = BQ for the oblique Gram) from HBM into shared memory
+// with 2-D TMA (SWIZZLE_128B, mbarrier pipeline).  Each consumer warp owns one 32x32 block
+// ("job", 4x4 tiles of 8x8) of the upper triangle of A (all blocks for the oblique Gram) and
+// accumulates it in registers with FP64 tensor-core MMA (mma.sync m8n8k4 f64 = SASS DMMA).
+// The k-index of each m8n8k4 step is mapped to rows {2s, 2s+1, 2s+8, 2s+9} of the stage so
+// that fragment loads from the swizzled stage are bank-conflict free.  Each CTA writes its
+// partial tiles to the workspace; gram_reduce sums the partials in CTA order, so the result
+// is bitwise deterministic run to run for a fixed GPU model and grid (reading D10).
+#include "scqr3_dev.cuh"
+#include "scqr3_kernels.h"
+
+namespace scqr3 {
+
+// Job j -> (bi, bj) block coordinates.  Symmetric: upper blocks enumerated column by column
+// (bi <= bj).  Full (oblique): row-major over NB x NB.
+__device__ __forceinline__ void decode_job(int j, int NB, bool full, int& bi, int& bj) {
+  if (full) {
+    bi = j / NB;
+    bj = j % NB;
+    return;
+  }
+  int c = 0;
+  while ((c + 1) * (c + 2) / 2 <= j) ++c;
+  bj = c;
+  bi = j - c * (c + 1) / 2;
+}
+
+__global__ void __launch_bounds__(32 * 13, 1)
+    gram_tma_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapY,
+                    GramParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-B alignment for SWIZZLE_128B
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ncons = blockDim.x / 32 - 1;
+  const int group = blockIdx.x % p.groups;
+  const int chunk = blockIdx.x / p.groups;
+  const bool full = p.oblique != 0;
+  const int nsrc = full ? 2 : 1;
+  const uint32_t stage_bytes = static_cast<uint32_t>(p.npad) * 128u;   // 16 rows x npad cols x 8 B
+  unsigned char* stages = smem;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(p.stages) * nsrc * stage_bytes);
+  uint64_t* empty_bar = full_bar + p.stages;
+
+  // contiguous row range of this chunk, in 16-row stages
+  const long long s_begin = (long long)p.total_stages * chunk / p.chunks;
+  const long long s_end = (long long)p.total_stages * (chunk + 1) / p.chunks;
+  const int nst = static_cast<int>(s_end - s_begin);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < p.stages; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], ncons);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ---------------- producer: TMA stream of this chunk's rows
+    if (lane == 0) {
+      tma_prefetch_desc(&mapQ);
+      if (full) tma_prefetch_desc(&mapY);
+      for (int i = 0; i < nst; ++i) {
+        const int st = i % p.stages;
+        const uint32_t ph = (i / p.stages) & 1;
+        if (i >= p.stages) mbar_wait(&empty_bar[st], ph ^ 1);
+        mbar_arrive_expect_tx(&full_bar[st], stage_bytes * nsrc);
+        const int row = static_cast<int>((s_begin + i) * kGramStageRows);
+        unsigned char* dst = stages + static_cast<size_t>(st) * nsrc * stage_bytes;
+        tma_load_2d(dst, &mapQ, row, 0, &full_bar[st]);
+        if (full) tma_load_2d(dst + stage_bytes, &mapY, row, 0, &full_bar[st]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers
+  const int cw = warp - 1;
+  const int job = p.job_begin[group] + cw;
+  const bool active = job < p.job_begin[group + 1];
+  int bi = 0, bj = 0;
+  if (active) decode_job(job, p.NB, full, bi, bj);
+  const bool diag = !full && bi == bj;
+  const int g = lane >> 2, t = lane & 3;
+
+  double acc[kJobTiles][kJobTiles][2];
+#pragma unroll
+  for (int a = 0; a < kJobTiles; ++a)
+#pragma unroll
+    for (int b = 0; b < kJobTiles; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  // per-lane smem offsets (without the k-step part) for this job's tile columns
+  uint32_t offA[kJobTiles], offB[kJobTiles];
+#pragma unroll
+  for (int a = 0; a < kJobTiles; ++a) {
+    offA[a] = static_cast<uint32_t>(8 * (bi * kJobTiles + a) + g) * 128u;
+    offB[a] = static_cast<uint32_t>(8 * (bj * kJobTiles + a) + g) * 128u;
+  }
+  const int NT = p.NT;
+
+  for (int i = 0; i < nst; ++i) {
+    const int st = i % p.stages;
+    const uint32_t ph = (i / p.stages) & 1;
+    mbar_wait(&full_bar[st], ph);
+    if (active) {
+      const unsigned char* srcA = stages + static_cast<size_t>(st) * nsrc * stage_bytes;
+      const unsigned char* srcB = full ? srcA + stage_bytes : srcA;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        // row of this lane's k slot: {2s, 2s+1, 2s+8, 2s+9}[t]; chunk = row>>1 = s + 4*(t>>1)
+        const uint32_t chunk16 = static_cast<uint32_t>(s + 4 * (t >> 1));
+        const uint32_t inner = (((chunk16 ^ static_cast<uint32_t>(g)) & 7u) << 4) + ((t & 1) << 3);
+        double fa[kJobTiles], fb[kJobTiles];
+#pragma unroll
+        for (int a = 0; a < kJobTiles; ++a) {
+          fa[a] = (bi * kJobTiles + a < NT) ? *reinterpret_cast<const double*>(srcA + offA[a] + inner) : 0.0;
+        }
+        if (diag) {
+#pragma unroll
+          for (int b = 0; b < kJobTiles; ++b) fb[b] = fa[b];
+        } else {
+#pragma unroll
+          for (int b = 0; b < kJobTiles; ++b)
+            fb[b] = (bj * kJobTiles + b < NT) ? *reinterpret_cast<const double*>(srcB + offB[b] + inner) : 0.0;
+        }
+#pragma unroll
+        for (int a = 0; a < kJobTiles; ++a)
+#pragma unroll
+          for (int b = 0; b < kJobTiles; ++b) {
+            const bool valid = (bi * kJobTiles + a < NT) && (bj * kJobTiles + b < NT) && (!diag || a <= b);
+            if (valid) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+          }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[st]);
+  }
+
+  if (!active) return;
+  // ---------------- write this CTA's partial tiles (8x8 row-major per tile)
+  double* out = p.partials + static_cast<size_t>(chunk) * p.tiles_per_partial * 64;
+#pragma unroll
+  for (int a = 0; a < kJobTiles; ++a)
+#pragma unroll
+    for (int b = 0; b < kJobTiles; ++b) {
+      const int TI = bi * kJobTiles + a, TJ = bj * kJobTiles + b;
+      const bool valid = (TI < NT) && (TJ < NT) && (!diag || a <= b);
+      if (!valid) continue;
+      const size_t tid = full ? static_cast<size_t>(TI) * NT + TJ : static_cast<size_t>(TJ) * (TJ + 1) / 2 + TI;
+      double2 v = make_double2(acc[a][b][0], acc[a][b][1]);
+      *reinterpret_cast<double2*>(out + tid * 64 + 8 * g + 2 * t) = v;
+    }
+}
+
+// Sum the per-chunk partials in chunk order.  Output: packed upper tiles (tile (TI,TJ),
+// TI <= TJ, at index TJ(TJ+1)/2 + TI, 8x8 row-major), plus for the oblique Gram the
+// symmetrisation 0.5 (A_ij + A_ji) of the full sums and the appended ||Q||_F^2.
+__global__ void gram_reduce_kernel(GramReduceParams p) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long nout = static_cast<long long>(p.NT) * (p.NT + 1) / 2 * 64;
+  if (e < nout) {
+    const int tile = static_cast<int>(e >> 6), w = static_cast<int>(e & 63);
+    int TJ = 0;
+    while ((TJ + 1) * (TJ + 2) / 2 <= tile) ++TJ;
+    const int TI = tile - TJ * (TJ + 1) / 2;
+    if (!p.oblique) {
+      double s = 0.0;
+      const double* src = p.partials + e;
+      for (int c = 0; c < p.chunks; ++c) s += src[static_cast<size_t>(c) * p.tiles_per_partial * 64];
+      p.tiles[e] = s;
+    } else {
+      const int r = w >> 3, cc = w & 7;
+      const size_t e1 = (static_cast<size_t>(TI) * p.NT + TJ) * 64 + 8 * r + cc;
+      const size_t e2 = (static_cast<size_t>(TJ) * p.NT + TI) * 64 + 8 * cc + r;
+      double s1 = 0.0, s2 = 0.0;
+      for (int c = 0; c < p.chunks; ++c) {
+        const double* base = p.partials + static_cast<size_t>(c) * p.tiles_per_partial * 64;
+        s1 += base[e1];
+        s2 += base[e2];
+      }
+      p.tiles[e] = (s1 + s2) * 0.5;
+    }
+  } else if (e == nout && p.colsq_partials) {
+    double s = 0.0;
+    for (int c = 0; c < p.colsq_count; ++c) s += p.colsq_partials[c];
+    p.tiles[nout] = s;
+  }
+}
+
+// Y = B Q for the tridiagonal B (Alg. 4 line 1): y_i = d_i q_i + e_{i-1} q_{i-1} + e_i q_{i+1}
+// (terms in the oracle's order; the halo rows come from the neighbouring ranks), plus per-block
+// partial sums of q_ij^2 (||Q||_F^2 for the oblique shift, reading D4).
+__global__ void oblique_y_kernel(ObliqueYParams p) {
+  __shared__ double red[32];
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long total = p.m * static_cast<long long>(p.n);
+  double sq = 0.0;
+  for (long long k = idx; k < total; k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = k % p.m, j = k / p.m;
+    const double* q = p.Q + j * p.ldq;
+    const double qi = q[i];
+    double v = p.d[i] * qi;
+    if (i > 0) v = fma(p.e[i - 1], q[i - 1], v);
+    else if (p.has_prev) v = fma(p.e_prev, p.halo_prev[j], v);
+    if (i + 1 < p.m) v = fma(p.e[i], q[i + 1], v);
+    else if (p.has_next) v = fma(p.e[i], p.halo_next[j], v);
+    p.Y[j * p.ldy + i] = v;
+    sq = fma(qi, qi, sq);
+  }
+  // deterministic block reduction
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) p.colsq_partials[blockIdx.x] = v;
+  }
+}
+
+// Gershgorin bound max_i d_i + |e_{i-1}| + |e_i| >= ||B||_2 (reading D4); one partial per block.
+__global__ void gershgorin_kernel(const double* d, const double* e, long long m, int has_prev, double e_prev,
+                                  int has_next, double* partial) {
+  __shared__ double red[32];
+  double mx = 0.0;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double r = d[i];
+    if (i > 0) r += fabs(e[i - 1]);
+    else if (has_prev) r += fabs(e_prev);
+    if (i + 1 < m || has_next) r += fabs(e[i]);
+    mx = fmax(mx, r);
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) partial[blockIdx.x] = v;
+  }
+}
+
+__global__ void max_reduce_kernel(const double* partial, int count, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double v = 0.0;
+    for (int i = 0; i < count; ++i) v = fmax(v, partial[i]);
+    *out = v;
+  }
+}
+
+// packed upper tiles -> full symmetric n x n column-major matrix (kernel-level API only)
+__global__ void tiles_to_full_kernel(const double* tiles, int n, double* A) {
+  const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= static_cast<long long>(n) * n) return;
+  const int i = static_cast<int>(k % n), j = static_cast<int>(k / n);
+  const int a = i <= j ? i : j, b = i <= j ? j : i;  // upper element (a, b)
+  const int TI = a >> 3, TJ = b >> 3;
+  const size_t tile = static_cast<size_t>(TJ) * (TJ + 1) / 2 + TI;
+  // inside a diagonal tile the upper element (a%8, b%8) is taken so A is exactly symmetric
+  A[k] = tiles[tile * 64 + 8 * (a & 7) + (b & 7)];
+}
+
+}  // namespace scqr3

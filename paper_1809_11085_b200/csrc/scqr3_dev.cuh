@@ -1,0 +1,95 @@
+// scqr3_dev.cuh -- device-side building blocks shared by the libscqr3 kernels (sm_100a).
+//
+// FP64 on B200: tcgen05 has no .kind::f64 (ptxas rejects it), so the FP64 tensor path is
+// the warp-level mma.sync m8n8k4 f64 instruction (SASS DMMA.8x8x4).  Measured on one B200
+// (profiles/fp64_peaks.json): DMMA 37.1 TF/s, DFMA 34.1 TF/s, cuBLAS DGEMM 35.5 TF/s.
+//
+// Fragment conventions of mma.sync.m8n8k4.row.col.f64 (lane = 4*g + t, g = lane>>2, t = lane&3):
+//   A (8x4, row):  lane holds A[g][t]
+//   B (4x8, col):  lane holds B[t][g]
+//   C/D (8x8):     lane holds C[g][2t], C[g][2t+1]
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace scqr3 {
+
+constexpr int kMaxN = 256;            // largest supported n
+constexpr int kGramStageRows = 16;    // rows of X per TMA stage (128 B per column: SWIZZLE_128B)
+constexpr int kJobTiles = 4;          // Gram warp job = 4x4 tiles of 8x8 = 32x32 outputs
+
+// Device status shared by the controller kernels (one per call, in the workspace).
+struct DevStatus {
+  int code;       // SCQR3_OK / SCQR3_EBREAKDOWN
+  int stop;       // 1 = this pass was the last one
+  int pass;
+  int shifted;
+  double shift;
+  int breakdown_pivot;
+  int pad;
+  double pivot_value;
+  double norm2_est;
+  double dev_F;
+};
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------- mbarrier / TMA (PTX)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+// 2-D tiled TMA load: box at (c0 = row, c1 = col) of a column-major matrix -> smem.
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];\n" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Byte offset of element (row r in [0,16), column c) inside a 16-row TMA stage stored with
+// CU_TENSOR_MAP_SWIZZLE_128B: each column is one 128-byte line, and the 16-byte chunk index
+// of the line is XOR-ed with (line index mod 8).
+__device__ __forceinline__ uint32_t swz128_offset(int r, int c) {
+  return static_cast<uint32_t>(c) * 128u + ((((r >> 1) ^ (c & 7)) & 7) << 4) + ((r & 1) << 3);
+}
+
+}  // namespace scqr3

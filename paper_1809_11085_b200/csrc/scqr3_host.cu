@@ -1,0 +1,750 @@
+// scqr3_host.cu -- the C ABI of libscqr3.so (include/scqr3.h): argument checking, workspace
+// carving, the pass controller (Alg. 3 P:698-711 + Alg. 2 re-shift P:672-688, readings D5/D6)
+// and the NCCL plumbing (one allreduce of the packed Gram per pass; one-row halo for
+// the tridiagonal oblique metric).  All arithmetic runs in the kernels of gram.cu, chol.cu
+// and trsm.cu; this file only launches them.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "scqr3.h"
+#include "scqr3_dev.cuh"
+#include "scqr3_kernels.h"
+
+using namespace scqr3;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+
+int fail(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return SCQR3_EINVAL;
+}
+
+#define CUDA_TRY(expr)                                                                      \
+  do {                                                                                      \
+    cudaError_t e_ = (expr);                                                                \
+    if (e_ != cudaSuccess) return fail("%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+#define NCCL_TRY(expr)                                                                      \
+  do {                                                                                      \
+    ncclResult_t r_ = (expr);                                                               \
+    if (r_ != ncclSuccess) return fail("%s: %s", #expr, ncclGetErrorString(r_));           \
+  } while (0)
+#define TRY(expr)              \
+  do {                         \
+    int rc_ = (expr);          \
+    if (rc_ != SCQR3_OK) return rc_; \
+  } while (0)
+
+struct Comm {
+  ncclComm_t nccl;
+  int rank, nranks;
+};
+
+struct Ctx {
+  bool init = false;
+  int device = -1;
+  int num_sms = 0;
+  PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  DevStatus* st_host = nullptr;      // pinned, mapped
+  DevStatus* st_host_dev = nullptr;  // device alias of st_host
+  cudaEvent_t ev = nullptr;
+  // profiling: event pairs recorded around launches when opts->prof is set
+  static constexpr int kMaxEv = 128;
+  cudaEvent_t ev_a[kMaxEv] = {}, ev_b[kMaxEv] = {};
+  int ev_kind[kMaxEv] = {};
+  int ev_used = 0;
+  scqr3_prof* prof = nullptr;
+  cudaStream_t prof_stream = nullptr;
+};
+thread_local Ctx g_ctx[16];
+
+enum ProfKind { PK_GRAM = 0, PK_REDUCE = 1, PK_CHOL = 2, PK_TRSM = 3, PK_COMM = 4 };
+
+// Opens a timed region on the stream (no-op unless profiling); returns the slot or -1.
+int prof_begin(Ctx* c, int kind) {
+  if (!c->prof || c->ev_used >= Ctx::kMaxEv) return -1;
+  const int i = c->ev_used++;
+  if (!c->ev_a[i]) {
+    cudaEventCreate(&c->ev_a[i]);
+    cudaEventCreate(&c->ev_b[i]);
+  }
+  c->ev_kind[i] = kind;
+  cudaEventRecord(c->ev_a[i], c->prof_stream);
+  return i;
+}
+void prof_end(Ctx* c, int slot) {
+  if (slot >= 0) cudaEventRecord(c->ev_b[slot], c->prof_stream);
+}
+// After the stream has been synchronised: fold the recorded pairs into *prof.
+void prof_flush(Ctx* c) {
+  if (!c->prof) return;
+  for (int i = 0; i < c->ev_used; ++i) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c->ev_a[i], c->ev_b[i]) != cudaSuccess) continue;
+    switch (c->ev_kind[i]) {
+      case PK_GRAM: c->prof->gram_ms += ms; c->prof->gram_launches++; break;
+      case PK_REDUCE: c->prof->reduce_ms += ms; c->prof->reduce_launches++; break;
+      case PK_CHOL: c->prof->chol_ms += ms; c->prof->chol_launches++; break;
+      case PK_TRSM: c->prof->trsm_ms += ms; c->prof->trsm_launches++; break;
+      default: c->prof->comm_ms += ms; c->prof->comm_calls++; break;
+    }
+  }
+  c->ev_used = 0;
+}
+
+int get_ctx(Ctx** out) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 16) return fail("device index %d out of range", dev);
+  Ctx& c = g_ctx[dev];
+  if (!c.init) {
+    c.device = dev;
+    CUDA_TRY(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, dev));
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail("cuTensorMapEncodeTiled not available");
+    c.encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c.st_host), sizeof(DevStatus), cudaHostAllocMapped));
+    CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.st_host_dev), c.st_host, 0));
+    CUDA_TRY(cudaEventCreateWithFlags(&c.ev, cudaEventDisableTiming));
+    c.init = true;
+  }
+  *out = &c;
+  return SCQR3_OK;
+}
+
+size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+int max_chunks_for_device() {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return std::max(sms, 1) * 4;
+}
+
+struct Layout {
+  int n, npad, NT;
+  long long tiles_sym;     // NT(NT+1)/2
+  long long tiles_part;    // per partial
+  int max_chunks;
+  long long ldy;
+  // offsets (bytes)
+  size_t st, partials, tiles, W, Rnew, bfrag, dblk, misc, colsq, y, halo, end;
+};
+
+Layout make_layout(int64_t m, int64_t n, int oblique) {
+  Layout L{};
+  L.n = static_cast<int>(n);
+  L.npad = npad_for(L.n);
+  L.NT = L.npad / 8;
+  L.tiles_sym = static_cast<long long>(L.NT) * (L.NT + 1) / 2;
+  L.tiles_part = oblique ? static_cast<long long>(L.NT) * L.NT : L.tiles_sym;
+  L.max_chunks = max_chunks_for_device();
+  L.ldy = std::max<long long>(2, (m + 1) & ~1LL);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  L.st = take(sizeof(DevStatus));
+  L.partials = take(static_cast<size_t>(L.max_chunks) * L.tiles_part * 64 * 8);
+  L.tiles = take(static_cast<size_t>(L.tiles_sym * 64 + 64) * 8);
+  L.W = take(static_cast<size_t>(n) * n * 8);
+  L.Rnew = take(static_cast<size_t>(n) * n * 8);
+  L.bfrag = take(static_cast<size_t>(L.NT) * (L.NT - 1) * 32 * 8 + 8);
+  L.dblk = take(static_cast<size_t>(L.NT) * 72 * 8);
+  L.misc = take(64 * 8);  // [0] nb, [1] e_prev, [2] m_global (int64), ...
+  L.colsq = oblique ? take(4096 * 8) : off;
+  L.y = oblique ? take(static_cast<size_t>(L.ldy) * n * 8) : off;
+  L.halo = oblique ? take(static_cast<size_t>(4 * n) * 8) : off;
+  L.end = off;
+  return L;
+}
+
+struct WS {
+  DevStatus* st;
+  double *partials, *tiles, *W, *Rnew, *bfrag, *dblk, *misc, *colsq, *y, *halo;
+};
+
+int carve(const Layout& L, const scqr3_opts* o, WS* w) {
+  if (!o->workspace) return fail("opts->workspace is NULL");
+  if (o->workspace_bytes < L.end) return fail("workspace too small: %zu < %zu bytes", o->workspace_bytes, L.end);
+  if (reinterpret_cast<uintptr_t>(o->workspace) % 256) return fail("workspace must be 256-byte aligned");
+  char* b = static_cast<char*>(o->workspace);
+  w->st = reinterpret_cast<DevStatus*>(b + L.st);
+  w->partials = reinterpret_cast<double*>(b + L.partials);
+  w->tiles = reinterpret_cast<double*>(b + L.tiles);
+  w->W = reinterpret_cast<double*>(b + L.W);
+  w->Rnew = reinterpret_cast<double*>(b + L.Rnew);
+  w->bfrag = reinterpret_cast<double*>(b + L.bfrag);
+  w->dblk = reinterpret_cast<double*>(b + L.dblk);
+  w->misc = reinterpret_cast<double*>(b + L.misc);
+  w->colsq = reinterpret_cast<double*>(b + L.colsq);
+  w->y = reinterpret_cast<double*>(b + L.y);
+  w->halo = reinterpret_cast<double*>(b + L.halo);
+  return SCQR3_OK;
+}
+
+int check_opts(const scqr3_opts* o) {
+  if (!o) return fail("opts is NULL");
+  if (o->abi_version != SCQR3_ABI_VERSION) return fail("abi_version %d != %d", o->abi_version, SCQR3_ABI_VERSION);
+  if (o->shift_mode < 0 || o->shift_mode > 2) return fail("bad shift_mode %d", o->shift_mode);
+  if (o->norm_mode < 0 || o->norm_mode > 2) return fail("bad norm_mode %d", o->norm_mode);
+  if (o->norm_mode == SCQR3_NORM_USER && !(o->norm2_bound > 0)) return fail("NORM_USER needs norm2_bound > 0");
+  if (o->shift_mode == SCQR3_SHIFT_FIXED && !(o->shift_value >= 0)) return fail("SHIFT_FIXED needs shift_value >= 0");
+  return SCQR3_OK;
+}
+
+int check_matrix(const char* name, const double* p, int64_t m, int64_t ld) {
+  if (m > 0 && !p) return fail("%s is NULL", name);
+  if (ld < std::max<int64_t>(m, 1)) return fail("%s: leading dimension %lld < m=%lld", name, (long long)ld, (long long)m);
+  if (ld % 2) return fail("%s: leading dimension must be even (TMA needs 16-byte row pitch)", name);
+  if (reinterpret_cast<uintptr_t>(p) % 16) return fail("%s must be 16-byte aligned", name);
+  return SCQR3_OK;
+}
+
+int encode_map(Ctx* c, CUtensorMap* map, const double* base, int64_t m, int64_t n, int64_t ld, int npad) {
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(m), static_cast<cuuint64_t>(n)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 8};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kGramStageRows), static_cast<cuuint32_t>(npad)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = c->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail("cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+  return SCQR3_OK;
+}
+
+// Gram of the m x n block at src into w.tiles (packed upper tiles; oblique: sym(Q^T Y) and ||Q||_F^2)
+int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld, int64_t m, bool oblique,
+             const ObliqueYParams* yp, cudaStream_t st) {
+  const long long nout = L.tiles_sym * 64;
+  if (m == 0) {
+    CUDA_TRY(cudaMemsetAsync(w.tiles, 0, static_cast<size_t>(nout + 1) * 8, st));
+    return SCQR3_OK;
+  }
+  int colsq_count = 0;
+  if (oblique) {
+    ObliqueYParams p = *yp;
+    const long long total = m * static_cast<long long>(L.n);
+    long long blocks = std::min<long long>((total + 255) / 256, 4096);
+    colsq_count = static_cast<int>(std::max<long long>(blocks, 1));
+    p.colsq_partials = w.colsq;
+    const int ps = prof_begin(c, PK_REDUCE);
+    oblique_y_kernel<<<colsq_count, 256, 0, st>>>(p);
+    prof_end(c, ps);
+    ++g_launches;
+    CUDA_TRY(cudaGetLastError());
+  }
+  CUtensorMap mq, my;
+  TRY(encode_map(c, &mq, src, m, L.n, ld, L.npad));
+  if (oblique) TRY(encode_map(c, &my, w.y, m, L.n, L.ldy, L.npad));
+  else my = mq;
+
+  GramParams gp{};
+  gp.NT = L.NT;
+  gp.NB = (L.NT + kJobTiles - 1) / kJobTiles;
+  gp.npad = L.npad;
+  gp.oblique = oblique ? 1 : 0;
+  gp.tiles_per_partial = static_cast<int>(L.tiles_part);
+  const int jobs = oblique ? gp.NB * gp.NB : gp.NB * (gp.NB + 1) / 2;
+  const int groups = (jobs + 11) / 12;
+  gp.groups = groups;
+  int ncons = 0;
+  for (int g = 0; g <= groups; ++g) gp.job_begin[g] = jobs * g / groups;
+  for (int g = 0; g < groups; ++g) ncons = std::max(ncons, gp.job_begin[g + 1] - gp.job_begin[g]);
+  const int threads = 32 * (1 + ncons);
+  const int nsrc = oblique ? 2 : 1;
+  const size_t stage_bytes = static_cast<size_t>(L.npad) * 128;
+  gp.stages = static_cast<int>(std::min<size_t>(8, std::max<size_t>(2, 98304 / (stage_bytes * nsrc))));
+  const size_t smem = gp.stages * nsrc * stage_bytes + 2 * gp.stages * 8 + 1024;
+  CUDA_TRY(cudaFuncSetAttribute(gram_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int occ = 1;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gram_tma_kernel, threads, smem));
+  occ = std::max(occ, 1);
+  gp.total_stages = (m + kGramStageRows - 1) / kGramStageRows;
+  long long chunks = std::min<long long>((gp.total_stages + 3) / 4, static_cast<long long>(c->num_sms) * occ / groups);
+  chunks = std::max<long long>(1, std::min<long long>(chunks, L.max_chunks));
+  gp.chunks = static_cast<int>(chunks);
+  gp.partials = w.partials;
+  const int pg = prof_begin(c, PK_GRAM);
+  gram_tma_kernel<<<static_cast<unsigned>(chunks * groups), threads, smem, st>>>(mq, my, gp);
+  prof_end(c, pg);
+  ++g_launches;
+  CUDA_TRY(cudaGetLastError());
+
+  GramReduceParams rp{};
+  rp.partials = w.partials;
+  rp.tiles = w.tiles;
+  rp.chunks = gp.chunks;
+  rp.tiles_per_partial = gp.tiles_per_partial;
+  rp.NT = L.NT;
+  rp.oblique = gp.oblique;
+  rp.colsq_partials = oblique ? w.colsq : nullptr;
+  rp.colsq_count = colsq_count;
+  const long long nthreads = nout + 1;
+  const int pr = prof_begin(c, PK_REDUCE);
+  gram_reduce_kernel<<<static_cast<unsigned>((nthreads + 255) / 256), 256, 0, st>>>(rp);
+  prof_end(c, pr);
+  ++g_launches;
+  CUDA_TRY(cudaGetLastError());
+  return SCQR3_OK;
+}
+
+int launch_chol(const CholParams& p, cudaStream_t st) {
+  const size_t smem = p.w_in_smem ? static_cast<size_t>(p.n) * p.n * 8 : 0;
+  CUDA_TRY(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  chol_kernel<<<1, 1024, smem, st>>>(p);
+  ++g_launches;
+  CUDA_TRY(cudaGetLastError());
+  return SCQR3_OK;
+}
+
+bool w_fits_smem(int n) { return static_cast<size_t>(n) * n * 8 <= 200 * 1024; }
+
+int halo_exchange(Comm* cm, const double* Qsrc, int64_t ld, int64_t m, int n, double* halo, cudaStream_t st) {
+  // halo layout: [0,n) my first row, [n,2n) my last row, [2n,3n) prev rank's last row, [3n,4n) next rank's first row
+  if (!cm) return SCQR3_OK;
+  if (m > 0) {
+    CUDA_TRY(cudaMemcpy2DAsync(halo, 8, Qsrc, ld * 8, 8, n, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaMemcpy2DAsync(halo + n, 8, Qsrc + (m - 1), ld * 8, 8, n, cudaMemcpyDeviceToDevice, st));
+  }
+  NCCL_TRY(ncclGroupStart());
+  if (cm->rank > 0) {
+    NCCL_TRY(ncclSend(halo, n, ncclDouble, cm->rank - 1, cm->nccl, st));
+    NCCL_TRY(ncclRecv(halo + 2 * n, n, ncclDouble, cm->rank - 1, cm->nccl, st));
+  }
+  if (cm->rank + 1 < cm->nranks) {
+    NCCL_TRY(ncclSend(halo + n, n, ncclDouble, cm->rank + 1, cm->nccl, st));
+    NCCL_TRY(ncclRecv(halo + 3 * n, n, ncclDouble, cm->rank + 1, cm->nccl, st));
+  }
+  NCCL_TRY(ncclGroupEnd());
+  return SCQR3_OK;
+}
+
+int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const double* bd, const double* be, double* Q,
+                int64_t ldq, double* R, const scqr3_opts* o) {
+  TRY(check_opts(o));
+  const bool oblique = bd != nullptr;
+  if (n < 1 || n > kMaxN) return fail("n=%lld outside [1, %d]", (long long)n, kMaxN);
+  if (m < 0) return fail("m < 0");
+  TRY(check_matrix("X", X, m, ld));
+  TRY(check_matrix("Q", Q, m, ldq));
+  if (!R) return fail("R is NULL");
+  if (oblique && m > 0 && !be) return fail("b_off is NULL");
+  Ctx* c;
+  TRY(get_ctx(&c));
+  cudaStream_t st = static_cast<cudaStream_t>(o->stream);
+  Comm* cm = static_cast<Comm*>(o->comm);
+  const Layout L = make_layout(m, n, oblique);
+  WS w;
+  TRY(carve(L, o, &w));
+  c->prof = o->prof;
+  c->prof_stream = st;
+  c->ev_used = 0;
+  const int max_passes = o->max_passes > 0 ? o->max_passes : 8;
+  const double stop_tol = o->stop_tol > 0 ? o->stop_tol : 0.5;
+  const int iters = o->power_iters > 0 ? o->power_iters : 32;
+
+  // global m (the shift uses the global m)
+  int64_t mg = o->m_global;
+  if (mg <= 0) {
+    if (cm) {
+      int64_t* dm = reinterpret_cast<int64_t*>(w.misc + 2);
+      CUDA_TRY(cudaMemcpyAsync(dm, &m, 8, cudaMemcpyHostToDevice, st));
+      NCCL_TRY(ncclAllReduce(dm, dm, 1, ncclInt64, ncclSum, cm->nccl, st));
+      CUDA_TRY(cudaMemcpyAsync(&mg, dm, 8, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+    } else {
+      mg = m;
+    }
+  }
+  if (mg < n) return fail("m_global=%lld < n=%lld", (long long)mg, (long long)n);
+
+  ObliqueYParams yp{};
+  double* nb_dev = w.misc;
+  if (oblique) {
+    const bool multi = cm != nullptr;
+    const int rank = multi ? cm->rank : 0, nranks = multi ? cm->nranks : 1;
+    yp.d = bd;
+    yp.e = be;
+    yp.Y = w.y;
+    yp.ldy = L.ldy;
+    yp.m = m;
+    yp.n = static_cast<int>(n);
+    yp.has_prev = rank > 0;
+    yp.has_next = rank + 1 < nranks;
+    yp.halo_prev = w.halo + 2 * n;
+    yp.halo_next = w.halo + 3 * n;
+    // e_prev = previous rank's b_off[m_prev - 1]
+    double e_prev = 0.0;
+    if (multi) {
+      double* ebuf = w.misc + 8;  // [8] send, [9] recv
+      if (m > 0) CUDA_TRY(cudaMemcpyAsync(ebuf, be + (m - 1), 8, cudaMemcpyDeviceToDevice, st));
+      NCCL_TRY(ncclGroupStart());
+      if (rank + 1 < nranks) NCCL_TRY(ncclSend(ebuf, 1, ncclDouble, rank + 1, cm->nccl, st));
+      if (rank > 0) NCCL_TRY(ncclRecv(ebuf + 1, 1, ncclDouble, rank - 1, cm->nccl, st));
+      NCCL_TRY(ncclGroupEnd());
+      CUDA_TRY(cudaMemcpyAsync(&e_prev, ebuf + 1, 8, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      if (rank == 0) e_prev = 0.0;
+    }
+    yp.e_prev = e_prev;
+    if (o->bnorm_bound > 0) {
+      CUDA_TRY(cudaMemcpyAsync(nb_dev, &o->bnorm_bound, 8, cudaMemcpyHostToDevice, st));
+    } else {
+      double* part = w.colsq;
+      const int blocks = static_cast<int>(std::max<long long>(1, std::min<long long>((m + 255) / 256, 1024)));
+      if (m > 0) {
+        gershgorin_kernel<<<blocks, 256, 0, st>>>(bd, be, m, yp.has_prev, e_prev, yp.has_next, part);
+        ++g_launches;
+        CUDA_TRY(cudaGetLastError());
+      } else {
+        CUDA_TRY(cudaMemsetAsync(part, 0, 8, st));
+      }
+      max_reduce_kernel<<<1, 32, 0, st>>>(part, m > 0 ? blocks : 1, nb_dev);
+      ++g_launches;
+      CUDA_TRY(cudaGetLastError());
+      if (multi) NCCL_TRY(ncclAllReduce(nb_dev, nb_dev, 1, ncclDouble, ncclMax, cm->nccl, st));
+    }
+  }
+
+  CholParams cp{};
+  cp.tiles = w.tiles;
+  cp.n = static_cast<int>(n);
+  cp.NT = L.NT;
+  cp.npad = L.npad;
+  cp.mode = CHOL_PASS;
+  cp.oblique = oblique ? 1 : 0;
+  cp.shift_mode = o->shift_mode;
+  cp.shift_value = o->shift_value;
+  cp.norm_mode = o->norm_mode;
+  cp.norm2_bound = o->norm2_bound;
+  cp.power_iters = iters;
+  cp.m_global = static_cast<double>(mg);
+  cp.nb_dev = nb_dev;
+  cp.stop_tol = stop_tol;
+  cp.W = w.W;
+  cp.w_in_smem = w_fits_smem(static_cast<int>(n)) ? 1 : 0;
+  cp.R = R;
+  cp.Rnew = w.Rnew;
+  cp.bfrag = w.bfrag;
+  cp.dblk = w.dblk;
+  cp.st_dev = w.st;
+  cp.st_host = c->st_host_dev;
+
+  TrsmParams tp{};
+  tp.m = m;
+  tp.n = static_cast<int>(n);
+  tp.bfrag = w.bfrag;
+  tp.dblk = w.dblk;
+  tp.st = w.st;
+  tp.Q = Q;
+  tp.ldq = ldq;
+
+  const double* src = X;
+  int64_t ldsrc = ld;
+  int status = SCQR3_ENOCONV, k;
+  for (k = 1; k <= max_passes; ++k) {
+    if (oblique) {
+      const int ph = cm ? prof_begin(c, PK_COMM) : -1;
+      TRY(halo_exchange(cm, src, ldsrc, m, static_cast<int>(n), w.halo, st));
+      prof_end(c, ph);
+      yp.Q = src;
+      yp.ldq = ldsrc;
+    }
+    TRY(run_gram(c, L, w, src, ldsrc, m, oblique, &yp, st));
+    if (cm) {
+      const size_t cnt = static_cast<size_t>(L.tiles_sym * 64 + (oblique ? 1 : 0));
+      const int pa = prof_begin(c, PK_COMM);
+      NCCL_TRY(ncclAllReduce(w.tiles, w.tiles, cnt, ncclDouble, ncclSum, cm->nccl, st));
+      prof_end(c, pa);
+    }
+    c->st_host->code = -1;
+    cp.pass = k;
+    const int pc = prof_begin(c, PK_CHOL);
+    TRY(launch_chol(cp, st));
+    prof_end(c, pc);
+    CUDA_TRY(cudaEventRecord(c->ev, st));
+    tp.X = src;
+    tp.ldx = ldsrc;
+    if (m > 0) {
+      const int pt = prof_begin(c, PK_TRSM);
+      CUDA_TRY(launch_trsm(tp, c->num_sms, st));
+      prof_end(c, pt);
+      ++g_launches;
+    }
+    CUDA_TRY(cudaEventSynchronize(c->ev));
+    const volatile DevStatus* h = c->st_host;
+    if (h->code < 0) return fail("status block not written by the Cholesky kernel");
+    if (o->trace && k - 1 < o->trace_cap) {
+      scqr3_pass_trace& t = o->trace[k - 1];
+      t.shift = h->shift;
+      t.shifted = h->shifted;
+      t.breakdown_pivot = h->breakdown_pivot;
+      t.pivot_value = h->pivot_value;
+      t.norm2_est = h->norm2_est;
+      t.dev_F = h->dev_F;
+    }
+    src = Q;
+    ldsrc = ldq;
+    if (h->code != SCQR3_OK) {
+      status = h->code;
+      break;
+    }
+    if (h->stop) {
+      status = SCQR3_OK;
+      break;
+    }
+  }
+  if (o->passes_out) *o->passes_out = std::min(k, max_passes);
+  CUDA_TRY(cudaStreamSynchronize(st));
+  prof_flush(c);
+  c->prof = nullptr;
+  return status;
+}
+
+}  // namespace
+
+extern "C" {
+
+void scqr3_default_opts(scqr3_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof *o);
+  o->abi_version = SCQR3_ABI_VERSION;
+  o->shift_mode = SCQR3_SHIFT_SAFE;
+  o->norm_mode = SCQR3_NORM_POWER;
+  o->power_iters = 32;
+  o->max_passes = 8;
+  o->stop_tol = 0.5;
+}
+
+size_t scqr3_workspace_size(int64_t m, int64_t n, int32_t oblique) {
+  if (n < 1 || n > kMaxN || m < 0) return 0;
+  return make_layout(m, n, oblique).end;
+}
+
+int scqr3_factor(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, int64_t ldq, double* R,
+                 const scqr3_opts* opts) {
+  return factor_impl(m, n, X, ld, nullptr, nullptr, Q, ldq, R, opts);
+}
+
+int scqr3_factor_oblique(int64_t m, int64_t n, const double* X, int64_t ld, const double* b_diag,
+                         const double* b_off, double* Q, int64_t ldq, double* R, const scqr3_opts* opts) {
+  if (!b_diag && m > 0) return fail("b_diag is NULL");
+  static const double dummy = 0.0;
+  return factor_impl(m, n, X, ld, b_diag ? b_diag : &dummy, b_off, Q, ldq, R, opts);
+}
+
+size_t scqr3_host_workspace_size(int64_t m, int64_t n) {
+  if (n < 1 || n > kMaxN || m < 0) return 0;
+  const int64_t ldd = std::max<int64_t>(2, (m + 1) & ~1LL);
+  return align256(static_cast<size_t>(ldd) * n * 8) + align256(static_cast<size_t>(n) * n * 8) +
+         make_layout(m, n, 0).end;
+}
+
+int scqr3_factor_host(int64_t m, int64_t n, const double* X_host, int64_t ld, double* Q_host, int64_t ldq,
+                      double* R_host, const scqr3_opts* opts) {
+  TRY(check_opts(opts));
+  if (n < 1 || n > kMaxN || m < 0) return fail("bad sizes m=%lld n=%lld", (long long)m, (long long)n);
+  if (!X_host || !Q_host || !R_host) return fail("host pointer is NULL");
+  if (ld < m || ldq < m) return fail("leading dimension < m");
+  if (!opts->workspace || opts->workspace_bytes < scqr3_host_workspace_size(m, n))
+    return fail("workspace too small for scqr3_factor_host");
+  const int64_t ldd = std::max<int64_t>(2, (m + 1) & ~1LL);
+  char* b = static_cast<char*>(opts->workspace);
+  double* D = reinterpret_cast<double*>(b);
+  double* Rd = reinterpret_cast<double*>(b + align256(static_cast<size_t>(ldd) * n * 8));
+  scqr3_opts o2 = *opts;
+  o2.workspace = b + align256(static_cast<size_t>(ldd) * n * 8) + align256(static_cast<size_t>(n) * n * 8);
+  o2.workspace_bytes = opts->workspace_bytes - (static_cast<char*>(o2.workspace) - b);
+  cudaStream_t st = static_cast<cudaStream_t>(opts->stream);
+  if (m > 0)
+    CUDA_TRY(cudaMemcpy2DAsync(D, ldd * 8, X_host, ld * 8, m * 8, n, cudaMemcpyHostToDevice, st));
+  int rc = factor_impl(m, n, D, ldd, nullptr, nullptr, D, ldd, Rd, &o2);
+  if (rc != SCQR3_OK) return rc;
+  if (m > 0)
+    CUDA_TRY(cudaMemcpy2DAsync(Q_host, ldq * 8, D, ldd * 8, m * 8, n, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(R_host, Rd, static_cast<size_t>(n) * n * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return SCQR3_OK;
+}
+
+int scqr3_gram(int64_t m, int64_t n, const double* X, int64_t ld, double* A, const scqr3_opts* opts) {
+  TRY(check_opts(opts));
+  if (n < 1 || n > kMaxN || m < 0) return fail("bad sizes");
+  TRY(check_matrix("X", X, m, ld));
+  Ctx* c;
+  TRY(get_ctx(&c));
+  const Layout L = make_layout(m, n, 0);
+  WS w;
+  TRY(carve(L, opts, &w));
+  cudaStream_t st = static_cast<cudaStream_t>(opts->stream);
+  TRY(run_gram(c, L, w, X, ld, m, false, nullptr, st));
+  Comm* cm = static_cast<Comm*>(opts->comm);
+  if (cm)
+    NCCL_TRY(ncclAllReduce(w.tiles, w.tiles, L.tiles_sym * 64, ncclDouble, ncclSum, cm->nccl, st));
+  const long long nn = n * n;
+  tiles_to_full_kernel<<<static_cast<unsigned>((nn + 255) / 256), 256, 0, st>>>(w.tiles, static_cast<int>(n), A);
+  ++g_launches;
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return SCQR3_OK;
+}
+
+int scqr3_gram_oblique(int64_t m, int64_t n, const double* X, int64_t ld, const double* b_diag, const double* b_off,
+                       double* A, double* colsq, const scqr3_opts* opts) {
+  TRY(check_opts(opts));
+  if (n < 1 || n > kMaxN || m < 1) return fail("bad sizes");
+  TRY(check_matrix("X", X, m, ld));
+  Ctx* c;
+  TRY(get_ctx(&c));
+  const Layout L = make_layout(m, n, 1);
+  WS w;
+  TRY(carve(L, opts, &w));
+  cudaStream_t st = static_cast<cudaStream_t>(opts->stream);
+  ObliqueYParams yp{};
+  yp.Q = X;
+  yp.ldq = ld;
+  yp.d = b_diag;
+  yp.e = b_off;
+  yp.Y = w.y;
+  yp.ldy = L.ldy;
+  yp.m = m;
+  yp.n = static_cast<int>(n);
+  TRY(run_gram(c, L, w, X, ld, m, true, &yp, st));
+  const long long nn = n * n;
+  tiles_to_full_kernel<<<static_cast<unsigned>((nn + 255) / 256), 256, 0, st>>>(w.tiles, static_cast<int>(n), A);
+  ++g_launches;
+  CUDA_TRY(cudaGetLastError());
+  if (colsq) CUDA_TRY(cudaMemcpyAsync(colsq, w.tiles + L.tiles_sym * 64, 8, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return SCQR3_OK;
+}
+
+int scqr3_cholesky(int64_t n, const double* A, double s, double* R, int32_t* pivot, double* pivot_value,
+                   const scqr3_opts* opts) {
+  TRY(check_opts(opts));
+  if (n < 1 || n > kMaxN) return fail("bad n");
+  if (!A || !R) return fail("NULL matrix");
+  Ctx* c;
+  TRY(get_ctx(&c));
+  const Layout L = make_layout(n, n, 0);
+  WS w;
+  TRY(carve(L, opts, &w));
+  cudaStream_t st = static_cast<cudaStream_t>(opts->stream);
+  CholParams cp{};
+  cp.Afull = A;
+  cp.n = static_cast<int>(n);
+  cp.NT = L.NT;
+  cp.npad = L.npad;
+  cp.mode = CHOL_ONLY;
+  cp.shift_value = s;
+  cp.W = w.W;
+  cp.w_in_smem = w_fits_smem(static_cast<int>(n)) ? 1 : 0;
+  cp.R = R;
+  cp.st_dev = w.st;
+  TRY(launch_chol(cp, st));
+  DevStatus hs;
+  CUDA_TRY(cudaMemcpyAsync(&hs, w.st, sizeof hs, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (pivot) *pivot = hs.breakdown_pivot;
+  if (pivot_value) *pivot_value = hs.pivot_value;
+  return hs.code;
+}
+
+int scqr3_trsm(int64_t m, int64_t n, const double* X, int64_t ld, const double* R, double* Q, int64_t ldq,
+               const scqr3_opts* opts) {
+  TRY(check_opts(opts));
+  if (n < 1 || n > kMaxN || m < 0) return fail("bad sizes");
+  TRY(check_matrix("X", X, m, ld));
+  TRY(check_matrix("Q", Q, m, ldq));
+  if (!R) return fail("R is NULL");
+  Ctx* c;
+  TRY(get_ctx(&c));
+  const Layout L = make_layout(m, n, 0);
+  WS w;
+  TRY(carve(L, opts, &w));
+  cudaStream_t st = static_cast<cudaStream_t>(opts->stream);
+  const int tot = L.NT * (L.NT - 1) * 32 + L.NT * 72;
+  trsm_prep_kernel<<<(tot + 255) / 256, 256, 0, st>>>(R, static_cast<int>(n), L.NT, w.bfrag, w.dblk);
+  ++g_launches;
+  CUDA_TRY(cudaGetLastError());
+  TrsmParams tp{};
+  tp.X = X;
+  tp.ldx = ld;
+  tp.Q = Q;
+  tp.ldq = ldq;
+  tp.m = m;
+  tp.n = static_cast<int>(n);
+  tp.bfrag = w.bfrag;
+  tp.dblk = w.dblk;
+  tp.st = nullptr;
+  if (m > 0) {
+    CUDA_TRY(launch_trsm(tp, c->num_sms, st));
+    ++g_launches;
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return SCQR3_OK;
+}
+
+int scqr3_comm_unique_id(void* id_out) {
+  if (!id_out) return fail("id_out is NULL");
+  static_assert(sizeof(ncclUniqueId) == SCQR3_COMM_ID_BYTES, "ncclUniqueId size");
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  std::memcpy(id_out, &id, sizeof id);
+  return SCQR3_OK;
+}
+
+int scqr3_comm_init(void** comm_out, int32_t nranks, const void* id, int32_t rank) {
+  if (!comm_out || !id) return fail("NULL argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail("bad rank %d / nranks %d", rank, nranks);
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof uid);
+  Comm* c = new Comm{};
+  c->rank = rank;
+  c->nranks = nranks;
+  ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, uid, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail("ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  *comm_out = c;
+  return SCQR3_OK;
+}
+
+int scqr3_comm_destroy(void* comm) {
+  if (!comm) return SCQR3_OK;
+  Comm* c = static_cast<Comm*>(comm);
+  ncclCommDestroy(c->nccl);
+  delete c;
+  return SCQR3_OK;
+}
+
+const char* scqr3_last_error(void) { return g_err.c_str(); }
+
+int64_t scqr3_launch_count(int32_t reset) {
+  int64_t v = g_launches;
+  if (reset) g_launches = 0;
+  return v;
+}
+
+}  // extern "C"

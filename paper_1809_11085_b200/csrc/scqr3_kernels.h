@@ -1,0 +1,115 @@
+// scqr3_kernels.h -- parameter blocks and kernel declarations shared by the .cu files of
+// libscqr3 (internal; the public ABI is include/scqr3.h).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace scqr3 {
+
+struct DevStatus;
+
+struct GramParams {
+  double* partials;          // [chunks][tiles_per_partial][64]
+  long long total_stages;    // ceil(m / 16)
+  int chunks;                // row chunks (CTAs per group)
+  int groups;                // job groups (CTAs per chunk)
+  int stages;                // pipeline depth
+  int npad;                  // padded column count (multiple of 8, TMA box width)
+  int NT;                    // npad / 8 tiles per side
+  int NB;                    // ceil(NT / 4) blocks per side
+  int oblique;               // 1 = full Q^T Y
+  int tiles_per_partial;     // NT(NT+1)/2 or NT^2
+  int job_begin[33];         // jobs of group g: [job_begin[g], job_begin[g+1]), <= 12 each
+};
+
+struct GramReduceParams {
+  const double* partials;
+  double* tiles;             // packed upper tiles (+1 double: ||Q||_F^2 for oblique)
+  int chunks;
+  int tiles_per_partial;
+  int NT;
+  int oblique;
+  const double* colsq_partials;
+  int colsq_count;
+};
+
+struct ObliqueYParams {
+  const double* Q;
+  long long ldq;
+  const double* d;
+  const double* e;
+  double* Y;
+  long long ldy;
+  long long m;
+  int n;
+  int has_prev, has_next;
+  double e_prev;
+  const double* halo_prev;   // n doubles: previous rank's last row of Q
+  const double* halo_next;   // n doubles: next rank's first row of Q
+  double* colsq_partials;    // one per block
+};
+
+enum CholMode { CHOL_PASS = 0, CHOL_ONLY = 1 };
+
+struct CholParams {
+  const double* tiles;       // packed upper tiles of the Gram (CHOL_PASS)
+  const double* Afull;       // or a full column-major n x n matrix (CHOL_ONLY)
+  int n, NT, npad;
+  int mode;
+  int pass;                  // 1-based
+  int oblique;
+  int shift_mode;
+  double shift_value;
+  int norm_mode;
+  double norm2_bound;
+  int power_iters;
+  double m_global;
+  const double* nb_dev;      // oblique: ||B||_2 bound (device scalar)
+  double stop_tol;
+  double* W;                 // n x n scratch (global) when it does not fit in shared memory
+  int w_in_smem;
+  double* R;                 // running R (n x n col-major), or the CHOL_ONLY output
+  double* Rnew;              // n x n scratch
+  double* bfrag;             // TRSM B fragments (negated R~), NT(NT-1) x 32
+  double* dblk;              // TRSM diagonal blocks, NT x 72
+  DevStatus* st_dev;
+  DevStatus* st_host;        // host-mapped copy (may be null)
+};
+
+struct TrsmParams {
+  const double* X;
+  long long ldx;
+  double* Q;
+  long long ldq;
+  long long m;
+  int n;
+  const double* bfrag;
+  const double* dblk;
+  const DevStatus* st;       // skip when st->code != 0 (may be null)
+};
+
+__global__ void gram_tma_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapY,
+                                GramParams p);
+__global__ void gram_reduce_kernel(GramReduceParams p);
+__global__ void oblique_y_kernel(ObliqueYParams p);
+__global__ void gershgorin_kernel(const double* d, const double* e, long long m, int has_prev, double e_prev,
+                                  int has_next, double* partial);
+__global__ void max_reduce_kernel(const double* partial, int count, double* out);
+__global__ void tiles_to_full_kernel(const double* tiles, int n, double* A);
+__global__ void chol_kernel(CholParams p);
+__global__ void trsm_prep_kernel(const double* R, int n, int NT, double* bfrag, double* dblk);
+
+// TRSM launcher (chooses the template instance for n)
+cudaError_t launch_trsm(const TrsmParams& p, int num_sms, cudaStream_t stream);
+
+inline int npad_for(int n) {
+  // tile counts with a compiled TRSM instance
+  static const int nts[] = {1, 2, 4, 8, 12, 16, 24, 32};
+  int nt = (n + 7) / 8;
+  for (int v : nts)
+    if (v >= nt) return v * 8;
+  return -1;
+}
+
+}  // namespace scqr3

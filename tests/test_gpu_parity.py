@@ -1,0 +1,267 @@
+"""Parity of the CUDA path (called through the C ABI via the thin binding) against the CPU oracle.
+
+Tolerances:
+  * Gram:    |A_gpu - A_orc| <= 2 gamma_m |X|^T|X| entrywise (both satisfy P:260-262's T1 bound)
+  * oblique: |A_gpu - A_orc| <= 4 gamma_m (|X|^T |B| |X|) entrywise
+  * Cholesky / TRSM: exact (bitwise) on integer cases; on floating cases within the T2 / T3
+    backward-error bounds evaluated in extended precision
+  * end to end (reading D14): max|R_gpu - R_orc| <= 1e-10 max|R_orc|; Q within 1e-10 max|Q| for
+    kappa <= 1e6, within 10 kappa u max|Q| for kappa <= 1e8; orthogonality and residual <= 10 n u
+    (north star) for both.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+gpu = pytest.mark.gpu
+U = 2.0 ** -53
+
+if torch.cuda.is_available():
+    import paper_1809_11085_b200 as sq
+
+
+def dev(X):
+    return sq.to_colmajor(torch.from_numpy(np.asfortranarray(X)), device="cuda")
+
+
+def host(T):
+    return np.asfortranarray(T.detach().cpu().numpy())
+
+
+def gamma(k):
+    return k * U / (1 - k * U)
+
+
+# ------------------------------------------------------------------ Gram
+@gpu
+@pytest.mark.parametrize("m,n", [(1, 1), (15, 3), (16, 16), (17, 8), (1000, 7), (4099, 33), (20001, 64),
+                                 (5000, 100), (30011, 128), (3000, 200), (2500, 256)])
+def test_gram_parity(m, n):
+    X = synth.random_rows(m, n, seed=m + n)
+    A = host(sq.scqr3_gram(dev(X)))
+    Ao = oracle.gram(X)
+    bound = 2 * gamma(m) * (np.abs(X).T @ np.abs(X))
+    assert np.all(np.abs(A - Ao) <= bound + 1e-300)
+    assert np.array_equal(A, A.T)
+
+
+@gpu
+def test_gram_exact_integers_bitwise():
+    rng = np.random.default_rng(5)
+    X = rng.integers(-40, 41, size=(7777, 72)).astype(float)
+    A = host(sq.scqr3_gram(dev(X)))
+    assert np.array_equal(A, (X.astype(np.int64).T @ X.astype(np.int64)).astype(float))
+
+
+@gpu
+def test_gram_ld_padding_and_determinism():
+    m, n = 12345, 40
+    X = synth.random_rows(m, n, seed=2)
+    Xd = sq.colmajor_empty(m, n, ld=m + 11 + 1)  # even ld > m
+    Xd.copy_(torch.from_numpy(X))
+    A1 = host(sq.scqr3_gram(Xd))
+    A2 = host(sq.scqr3_gram(Xd))
+    assert np.array_equal(A1, A2)
+    bound = 2 * gamma(m) * (np.abs(X).T @ np.abs(X))
+    assert np.all(np.abs(A1 - oracle.gram(X)) <= bound)
+
+
+@gpu
+@pytest.mark.parametrize("m,n", [(2, 1), (999, 16), (20000, 64), (3001, 128)])
+def test_gram_oblique_parity(m, n):
+    X = synth.random_rows(m, n, seed=n)
+    d, e = synth.tridiag_b(m, seed=n)
+    A, cs = sq.scqr3_gram_oblique(dev(X), torch.from_numpy(d).cuda(), torch.from_numpy(e).cuda())
+    Ao, cso = oracle.gram_oblique(X, d, e)
+    B = np.abs(d)[:, None] * np.abs(X)
+    B[1:] += np.abs(e[:-1])[:, None] * np.abs(X[:-1])
+    B[:-1] += np.abs(e[:-1])[:, None] * np.abs(X[1:])
+    bound = 4 * gamma(m + 2) * (np.abs(X).T @ B)
+    assert np.all(np.abs(host(A) - Ao) <= bound)
+    assert abs(cs.item() - cso.sum()) <= 4 * gamma(m * n) * cso.sum()
+
+
+# ------------------------------------------------------------------ Cholesky
+@gpu
+@pytest.mark.parametrize("n", [1, 2, 9, 40, 128, 200, 256])
+def test_cholesky_integer_exact(n):
+    rng = np.random.default_rng(n)
+    R = np.triu(rng.integers(-3, 4, size=(n, n))).astype(float)
+    R[np.diag_indices(n)] = rng.integers(1, 6, size=n)
+    A = R.T @ R
+    Rg = sq.scqr3_cholesky(dev(A))
+    assert np.array_equal(host(Rg), R)
+
+
+@gpu
+def test_cholesky_breakdown_matches_oracle():
+    for A, piv in [(np.array([[1.0, 1.0], [1.0, 1.0]]), 2), (np.diag([1.0, 2.0, -1.0, 3.0]), 3)]:
+        r = sq.scqr3_cholesky(dev(A))
+        o = oracle.cholesky(A)
+        assert r[0] == "breakdown" and r[1] == o.pivot == piv
+    X = synth.randsvd(1000, 30, 1e12, seed=1)
+    A = oracle.gram(X)
+    assert sq.scqr3_cholesky(dev(A))[0] == "breakdown"
+    s = oracle.shift(1000, 30, 1.0)
+    Rg = host(sq.scqr3_cholesky(dev(A), s))
+    Ro = oracle.cholesky(A, s)
+    assert np.max(np.abs(Rg - Ro)) <= 1e-8 * np.max(np.abs(Ro))   # kappa(A+sI) ~ 1/alpha
+    # T2 backward error of the GPU factor, evaluated in extended precision
+    Rl = Rg.astype(np.longdouble)
+    E = Rl.T @ Rl - (A.astype(np.longdouble) + s * np.eye(30, dtype=np.longdouble))
+    assert np.all(np.abs(E) <= 1.5 * gamma(31) * (np.abs(Rg).T @ np.abs(Rg)))
+
+
+# ------------------------------------------------------------------ TRSM
+@gpu
+@pytest.mark.parametrize("m,n", [(1, 1), (31, 5), (1000, 16), (4097, 64), (10007, 128), (3000, 200), (2049, 256)])
+def test_trsm_integer_exact(m, n):
+    rng = np.random.default_rng(m)
+    Q = rng.integers(-9, 10, size=(m, n)).astype(float)
+    R = np.triu(rng.integers(-3, 4, size=(n, n))).astype(float)
+    R[np.diag_indices(n)] = 2.0 ** rng.integers(0, 3, size=n)
+    X = Q @ R
+    assert np.array_equal(host(sq.scqr3_trsm(dev(X), dev(R))), Q)
+
+
+@gpu
+@pytest.mark.parametrize("m,n", [(777, 24), (5003, 128), (1500, 256)])
+def test_trsm_rowwise_backward_error(m, n):
+    X = synth.randsvd(m, n, 1e8, seed=3)
+    R = oracle.cholesky(oracle.gram(X), oracle.shift(m, n, 1.0))
+    Qg = host(sq.scqr3_trsm(dev(X), dev(R)))
+    Rl = R.astype(np.longdouble)
+    res = np.abs(Qg.astype(np.longdouble) @ Rl - X.astype(np.longdouble))
+    bound = 2 * gamma(n + 1) * (np.abs(Qg) @ np.abs(R))
+    assert np.all(res <= bound)
+    Qo = oracle.trsm_rows(X, R)
+    assert np.max(np.abs(Qg - Qo)) <= 1e-6 * np.max(np.abs(Qo))   # kappa(R) ~ 1e5
+
+
+# ------------------------------------------------------------------ end to end
+def _compare(X, rg, ro, kappa, d=None, e=None):
+    m, n = X.shape
+    Qg, Rg = host(rg.Q), host(rg.R)
+    assert rg.status == 0 and ro.status == 0
+    assert np.max(np.abs(Rg - ro.R)) <= 1e-10 * np.max(np.abs(ro.R))
+    if kappa <= 1e6:
+        assert np.max(np.abs(Qg - ro.Q)) <= 1e-10 * np.max(np.abs(ro.Q))
+    elif kappa <= 1e8:
+        assert np.max(np.abs(Qg - ro.Q)) <= 10 * kappa * U * np.max(np.abs(ro.Q))
+    assert np.array_equal(Rg, np.triu(Rg)) and np.all(np.diag(Rg) > 0)
+    orth = oracle.orth_F(Qg, d, e)
+    res = oracle.resid_F(X, Qg, Rg)
+    assert orth <= 10 * n * U, orth
+    assert res <= 10 * n * U, res
+    return orth, res
+
+
+@gpu
+@pytest.mark.parametrize("m,n,kappa", [(2000, 16, 1e12), (300, 10, 1e15), (1000, 30, 1e12), (100, 100, 1e13),
+                                       (5001, 64, 1e4), (20000, 128, 1e10), (8000, 100, 1e6), (4000, 256, 1e8),
+                                       (3000, 1, 1.0), (17, 17, 1e3)])
+def test_factor_parity(m, n, kappa):
+    X = synth.randsvd(m, n, kappa, seed=0)
+    rg = sq.scqr3_factor(dev(X))
+    ro = oracle.scqr3(X)
+    _compare(X, rg, ro, kappa)
+    assert [t["shifted"] for t in rg.trace] == [t.shifted for t in ro.trace]
+
+
+@gpu
+def test_pr1_exact_trace_and_shift():
+    """BASELINE config PR1: shifted, plain, plain; the same shift as the oracle up to rounding."""
+    X = synth.randsvd(2000, 16, 1e12, seed=0)
+    rg = sq.scqr3_factor(dev(X))
+    ro = oracle.scqr3(X)
+    assert rg.passes == ro.passes == 3
+    assert rg.trace[0]["shift"] == pytest.approx(ro.trace[0].shift, rel=1e-12)
+    for tg, to in zip(rg.trace, ro.trace):
+        assert tg["dev_F"] == pytest.approx(to.dev_F, rel=1e-6, abs=1e-12)
+    _compare(X, rg, ro, 1e12)
+    # unshifted CholeskyQR2 breaks down on the GPU too
+    rp = sq.scqr3_factor(dev(X), shift_mode=sq.SHIFT_NONE, max_passes=2)
+    assert rp.status == sq.EBREAKDOWN
+
+
+@gpu
+def test_fixed_shift_first_pass_matches_oracle():
+    X = synth.randsvd(3000, 40, 1e11, seed=4)
+    s = 1e-9
+    rg = sq.scqr3_factor(dev(X), shift_mode=sq.SHIFT_FIXED, shift_value=s, max_passes=1)
+    ro = oracle.scqr3(X, shift_mode=oracle.SHIFT_FIXED, shift_value=s, max_passes=1)
+    assert rg.status == ro.status == sq.ENOCONV
+    Rg = host(rg.R)
+    assert np.max(np.abs(Rg - ro.R)) <= 1e-9 * np.max(np.abs(ro.R))
+
+
+@gpu
+def test_inplace_and_ragged_and_determinism():
+    m, n = 40003, 72
+    X = synth.randsvd(m, n, 1e9, seed=8)
+    Xd = dev(X)
+    r1 = sq.scqr3_factor(Xd)
+    Q1, R1 = host(r1.Q), host(r1.R)
+    r2 = sq.scqr3_factor(Xd)
+    assert np.array_equal(Q1, host(r2.Q)) and np.array_equal(R1, host(r2.R))
+    Xi = dev(X)
+    r3 = sq.scqr3_factor(Xi, inplace=True)
+    assert r3.Q.data_ptr() == Xi.data_ptr()
+    assert np.array_equal(host(r3.Q), Q1) and np.array_equal(host(r3.R), R1)
+
+
+@gpu
+def test_status_codes_and_errors():
+    X = synth.randsvd(500, 8, 1e3, seed=0)
+    assert sq.scqr3_factor(dev(X), max_passes=1).status == sq.ENOCONV
+    Z = np.zeros((300, 4))
+    assert sq.scqr3_factor(dev(Z)).status in (sq.EBREAKDOWN, sq.ENOCONV)
+    with pytest.raises(sq.ScqrError):
+        sq.scqr3_factor(dev(np.ones((3, 5))))          # m < n
+    with pytest.raises(sq.ScqrError):
+        sq.scqr3_factor(dev(np.ones((300, 257))))      # n > 256
+
+
+@gpu
+@pytest.mark.parametrize("m,n,kappa", [(3000, 16, 1e12), (20000, 64, 1e12), (5000, 128, 1e8)])
+def test_factor_oblique_parity(m, n, kappa):
+    X = synth.randsvd(m, n, kappa, seed=1)
+    d, e = synth.tridiag_b(m, seed=1)
+    rg = sq.scqr3_factor_oblique(dev(X), torch.from_numpy(d).cuda(), torch.from_numpy(e).cuda())
+    ro = oracle.scqr3(X, d, e)
+    _compare(X, rg, ro, kappa, d, e)
+
+
+@gpu
+def test_host_api_matches_device_api():
+    X = synth.randsvd(10001, 48, 1e10, seed=2)
+    rd = sq.scqr3_factor(dev(X))
+    Xh = torch.from_numpy(np.asfortranarray(X)).t().contiguous().t()
+    rh = sq.scqr3_factor_host(Xh)
+    assert rh.status == 0
+    assert np.array_equal(rh.R.numpy(), host(rd.R))
+    assert np.array_equal(np.asarray(rh.Q.numpy()), host(rd.Q))
+
+
+@gpu
+def test_single_rank_nccl_comm_path():
+    """One-rank NCCL communicator: exercises ncclAllReduce / send-recv plumbing on one GPU."""
+    import ctypes
+    from paper_1809_11085_b200 import _abi
+    buf = ctypes.create_string_buffer(128)
+    assert _abi.lib().scqr3_comm_unique_id(buf) == 0
+    h = ctypes.c_void_p()
+    assert _abi.lib().scqr3_comm_init(ctypes.byref(h), 1, buf.raw, 0) == 0
+    comm = sq.Comm(h, 0, 1)
+    X = synth.randsvd(6000, 32, 1e11, seed=3)
+    a = sq.scqr3_factor(dev(X))
+    b = sq.scqr3_factor(dev(X), comm=comm)
+    assert np.array_equal(host(a.R), host(b.R))
+    d, e = synth.tridiag_b(6000, seed=3)
+    c1 = sq.scqr3_factor_oblique(dev(X), torch.from_numpy(d).cuda(), torch.from_numpy(e).cuda())
+    c2 = sq.scqr3_factor_oblique(dev(X), torch.from_numpy(d).cuda(), torch.from_numpy(e).cuda(), comm=comm)
+    assert np.array_equal(host(c1.R), host(c2.R))
+    comm.destroy()
