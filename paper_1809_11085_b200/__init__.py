@@ -74,6 +74,15 @@ def to_colmajor(X, device=None):
     return out
 
 
+def _square_colmajor(A):
+    """n x n float64 CUDA matrix with leading dimension exactly n (the ABI's R / A layout)."""
+    torch = _torch()
+    A = torch.as_tensor(A, dtype=torch.float64)
+    if not A.is_cuda:
+        A = A.cuda()
+    return A.t().contiguous().t()
+
+
 def _ld(X) -> int:
     if X.dim() != 2 or X.stride(0) != 1:
         raise ScqrError("matrix must be column-major: an (m, n) tensor with stride (1, ld)")
@@ -228,7 +237,7 @@ def scqr3_cholesky(A, s: float = 0.0, *, ws=None, **kw):
     """R = chol(A + sI) or ('breakdown', pivot, value)."""
     torch = _torch()
     n = A.shape[0]
-    A = to_colmajor(A) if A.shape[0] > 1 else A.contiguous()
+    A = _square_colmajor(A)
     R = torch.empty((n, n), dtype=torch.float64, device=A.device).t()
     ws = ws if ws is not None else workspace(n, n, device=A.device)
     o, _, _ = _opts(ws=ws, **kw)
@@ -244,7 +253,7 @@ def scqr3_cholesky(A, s: float = 0.0, *, ws=None, **kw):
 def scqr3_trsm(X, R, *, Q=None, ws=None, **kw):
     m, n = X.shape
     Q = Q if Q is not None else colmajor_empty(m, n, device=X.device)
-    R = to_colmajor(R) if n > 1 else R.contiguous()
+    R = _square_colmajor(R)
     ws = ws if ws is not None else workspace(m, n, device=X.device)
     o, _, _ = _opts(ws=ws, **kw)
     _check(_abi.lib().scqr3_trsm(m, n, X.data_ptr(), _ld(X), R.data_ptr(), Q.data_ptr(), _ld(Q),
