@@ -74,6 +74,8 @@ typedef struct scqr3_prof {
   int64_t trsm_launches;
   double comm_ms;          /* NCCL allreduce / halo exchange                               */
   int64_t comm_calls;
+  double trmul_ms;         /* R := R~ R on the side stream (overlaps the TRSM)             */
+  int64_t trmul_launches;
 } scqr3_prof;
 
 typedef struct scqr3_opts {

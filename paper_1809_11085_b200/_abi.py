@@ -5,7 +5,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libscqr3.so")
+LIB_PATH = os.environ.get("SCQR3_LIB") or os.path.join(HERE, "libscqr3.so")
 
 SCQR3_ABI_VERSION = 1
 OK, EINVAL, EBREAKDOWN, ENOCONV = 0, 1, 2, 3
@@ -36,6 +36,7 @@ class Prof(ctypes.Structure):
         ("chol_ms", ctypes.c_double), ("chol_launches", ctypes.c_int64),
         ("trsm_ms", ctypes.c_double), ("trsm_launches", ctypes.c_int64),
         ("comm_ms", ctypes.c_double), ("comm_calls", ctypes.c_int64),
+        ("trmul_ms", ctypes.c_double), ("trmul_launches", ctypes.c_int64),
     ]
 
 

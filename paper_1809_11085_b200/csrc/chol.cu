@@ -1,18 +1,26 @@
-// chol.cu -- the per-pass n x n step (a3 norm/shift, a4 shifted Cholesky, a6 R accumulation,
-// a7 pass control) on ONE CTA; it is replicated on every rank (identical input bits after
-// the Gram allreduce give identical R~, so no broadcast is needed).
+// chol.cu -- the per-pass n x n step (a3 norm/shift, a4 shifted Cholesky, a7 pass control) on
+// ONE CTA, replicated on every rank (identical input bits after the Gram allreduce give identical
+// R~, so no broadcast is needed), plus the R accumulation (a6) kernels that run on a side
+// stream, overlapped with the TRSM of the same pass.
 //
 //   N^2 ~ ||Q||_2^2 by power iteration on the Gram (reading D2), or trace / user bound
-//   s = 11{mn+n(n+1)} u N^2            (eq. finds2)
+//   s = 11{mn+n(n+1)} u N^2              (eq. finds2)
 //   s = 11{2m sqrt(mn)+n(n+1)} u N^2 N_B (eq. finds2B, oblique)
-//   pass 1: R~ = chol(A + sI)         (Alg. 3 line 4)
+//   pass 1: R~ = chol(A + sI)            (Alg. 3 line 4)
 //   pass k>1: R~ = chol(A); on breakdown R~ = chol(A + sI)   (Alg. 2 lines 4-7)
-//   R := R~ R                           (Alg. 2 line 8)
+//   R := R~ R                              (Alg. 2 line 8)   [trmul_kernel]
 //   stop after an unshifted pass with ||A - I||_F <= stop_tol (reading D6)
-// Breakdown = first pivot <= 0 or non-finite (reading D9).  The Cholesky is unblocked
-// right-looking, like the oracle, on a row-major working copy W of A (shared memory when
-// n*n*8 B fits, else an L2-resident global scratch).  Outputs for the TRSM kernel: negated
-// R~ in mma B-fragment order and the 8x8 diagonal blocks with reciprocal pivots.
+// Breakdown = first pivot <= 0 or non-finite, in pivot order (reading D9).  The norm estimate is
+// only needed when a shift is formed (pass 1, or a pass whose plain Cholesky broke down).
+//
+// Cholesky: right-looking with 32-column panels on a row-major working copy W of A (leading
+// dimension n+1: conflict-free row and column access; shared memory for n <= 159, else an
+// L2-resident global scratch).  Per panel: (a) one warp factors the 32x32 diagonal block in
+// registers (lane j owns column j; the pivot chain is shuffle -> rsqrt -> scale -> one FMA, the
+// rest of the rank-1 updates hang off it); (b) one thread per column forms the panel's rows of R~;
+// (c) all threads apply the rank-32 trailing update in 4x4 register tiles.  Outputs for the TRSM
+// kernel: -R~ in mma B-fragment order, and for each 8x8 diagonal block the strict upper part
+// scaled by its row's reciprocal pivot plus the reciprocal pivots; R~ itself for trmul_kernel.
 #include <math.h>
 
 #include "scqr3.h"
@@ -22,21 +30,32 @@
 namespace scqr3 {
 
 namespace {
-constexpr int kCholThreads = 1024;
+constexpr int kThreads = 256;
+// 16-column panels: the unrolled register code of one panel step stays resident in the
+// instruction caches (a 32-column panel's straight-line code did not, and this single-CTA
+// kernel then ran instruction-fetch bound).
+constexpr int kPanel = 16;
+constexpr unsigned kFull = 0xffffffffu;
+__device__ long long g_phase[2];  // diagnostics: cycles in panel steps (a) and (b) of the last factor
 
-__device__ double block_sum(double v, double* red) {
+__device__ __forceinline__ double2 block_sum2(double a, double b, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_down_sync(kFull, a, o);
+    b += __shfl_down_sync(kFull, b, o);
+  }
   __syncthreads();  // protect red[] from a previous use
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  if (warp == 0) {
-    double w = lane < (blockDim.x >> 5) ? red[lane] : 0.0;
-    for (int o = 16; o > 0; o >>= 1) w += __shfl_down_sync(0xffffffffu, w, o);
-    if (lane == 0) red[32] = w;
+  if (lane == 0) {
+    red[warp] = a;
+    red[32 + warp] = b;
   }
   __syncthreads();
-  return red[32];
+  double sa = 0.0, sb = 0.0;
+  for (int w = 0; w < kThreads / 32; ++w) {  // same order in every thread: deterministic
+    sa += red[w];
+    sb += red[32 + w];
+  }
+  return make_double2(sa, sb);
 }
 
 __device__ __forceinline__ double gram_entry(const CholParams& p, int i, int j) {
@@ -46,94 +65,224 @@ __device__ __forceinline__ double gram_entry(const CholParams& p, int i, int j) 
   return p.tiles[tile * 64 + 8 * (a & 7) + (b & 7)];
 }
 
-__device__ void load_W(const CholParams& p, double* W) {
+__device__ __forceinline__ void load_W(const CholParams& p, double* W, int ldw) {
   const int n = p.n;
-  for (int k = threadIdx.x; k < n * n; k += blockDim.x) W[k] = gram_entry(p, k / n, k % n);
+  for (int i = threadIdx.x >> 5; i < n; i += kThreads / 32)
+    for (int j = threadIdx.x & 31; j < n; j += 32) W[i * ldw + j] = gram_entry(p, i, j);
   __syncthreads();
 }
 
-// returns 0, or the 1-based breakdown pivot (value in *pv); W upper holds R~ on success
-__device__ int factor(double* W, int n, double s, bool add_shift, double* pv_out, int* sflag, double* sval) {
-  if (add_shift) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) W[i * n + i] = W[i * n + i] + s;
-  }
+// Power iteration from the all-ones vector on sc*A (sc = exact power of two with sc*trace <= 1,
+// so the unnormalised iterates neither overflow nor need a reduction per step), then the
+// Rayleigh quotient.  Same iterate directions as the normalised iteration (reading D2).
+__device__ __noinline__ double power_lmax(const double* W, int ldw, int n, int iters, double trace, double (*ybuf)[kMaxN],
+                             double* red) {
+  if (!(trace > 0.0) || !isfinite(trace)) return 0.0;
+  const double sc = ldexp(1.0, -(ilogb(trace) + 1));
+  int tpr = 1;
+  while (tpr * 2 <= 32 && tpr * 2 * n <= kThreads) tpr *= 2;
+  const int tid = threadIdx.x, row = tid / tpr, part = tid % tpr;
+  if (tid < n) ybuf[0][tid] = 1.0;
   __syncthreads();
-  for (int kk = 0; kk < n; ++kk) {
-    if (threadIdx.x == 0) {
-      const double d = W[kk * n + kk];
-      if (!(d > 0.0) || !isfinite(d)) {
-        *sflag = kk + 1;
-        *sval = d;
-      } else {
-        W[kk * n + kk] = sqrt(d);
+  int cur = 0;
+  for (int it = 0; it < iters; ++it) {
+    double acc = 0.0;
+    if (row < n)
+      for (int j = part; j < n; j += tpr) acc = fma(W[j * ldw + row], ybuf[cur][j], acc);
+    for (int o = 1; o < tpr; o <<= 1) acc += __shfl_xor_sync(kFull, acc, o);
+    if (part == 0 && row < n) ybuf[cur ^ 1][row] = acc * sc;
+    __syncthreads();
+    cur ^= 1;
+  }
+  double acc = 0.0;
+  if (row < n)
+    for (int j = part; j < n; j += tpr) acc = fma(W[j * ldw + row], ybuf[cur][j], acc);
+  for (int o = 1; o < tpr; o <<= 1) acc += __shfl_xor_sync(kFull, acc, o);
+  const bool own = part == 0 && row < n;
+  const double y = own ? ybuf[cur][row] : 0.0;
+  const double2 nd = block_sum2(own ? y * acc : 0.0, own ? y * y : 0.0, red);
+  return nd.y > 0.0 ? nd.x / nd.y : 0.0;
+}
+
+// Blocked right-looking Cholesky of W (+ s on the diagonal).  Returns 0, or the 1-based
+// breakdown pivot (value in *pv_out).  On success the upper triangle of W holds R~.
+// (__noinline__: one copy of this heavily unrolled code instead of one per call site keeps the
+//  kernel's instruction footprint small enough for the instruction caches.)
+__device__ __noinline__ int factor(double* W, int ldw, int n, double s, bool add_shift, double* pv_out,
+                                      int* sflag, double* sval, double* rinv) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (add_shift)
+    for (int i = tid; i < n; i += kThreads) W[i * ldw + i] = W[i * ldw + i] + s;
+  __syncthreads();
+  long long t_a = 0, t_b = 0, t0 = 0;
+  for (int k0 = 0; k0 < n; k0 += kPanel) {
+    const int kb = min(kPanel, n - k0);
+    t0 = clock64();
+    // (a) diagonal block, one warp, lane j = column k0 + j (identity beyond kb)
+    if (warp == 0) {
+      double col[kPanel];
+#pragma unroll
+      for (int r = 0; r < kPanel; ++r)
+        col[r] = (lane < kb && r <= lane) ? W[(k0 + r) * ldw + k0 + lane] : (r == lane ? 1.0 : 0.0);
+      int bad = 0;
+      double badv = 0.0;
+#pragma unroll
+      for (int c = 0; c < kPanel; ++c) {
+        if (c < kb) {  // warp-uniform
+          double d = __shfl_sync(kFull, col[c], c);
+          if (!bad && (!(d > 0.0) || !isfinite(d))) {
+            bad = c + 1;
+            badv = d;
+          }
+          if (bad) d = 1.0;  // finish harmlessly; the factor is discarded
+          const double inv = rsqrt(d);
+          if (lane == c) col[c] = d * inv;  // r_cc
+          else if (lane > c) col[c] *= inv;  // r_cj
+          if (c + 1 < kPanel && lane == c + 1) col[c + 1] = fma(-col[c], col[c], col[c + 1]);  // next pivot first
+#pragma unroll
+          for (int i = c + 1; i < kPanel; ++i) {
+            const double ri = __shfl_sync(kFull, col[c], i);
+            if (lane > i || (lane == i && i != c + 1)) col[i] = fma(-ri, col[c], col[i]);
+          }
+          if (lane == c) rinv[c] = inv;
+        }
+      }
+      if (!bad) {
+#pragma unroll
+        for (int r = 0; r < kPanel; ++r)
+          if (lane < kb && r <= lane) W[(k0 + r) * ldw + k0 + lane] = col[r];
+      } else if (lane == 0) {
+        *sflag = k0 + bad;
+        *sval = badv;
       }
     }
     __syncthreads();
+    t_a += clock64() - t0;
+    t0 = clock64();
     if (*sflag) {
       *pv_out = *sval;
       return *sflag;
     }
-    const double rkk = W[kk * n + kk];
-    for (int j = kk + 1 + threadIdx.x; j < n; j += blockDim.x) W[kk * n + j] = W[kk * n + j] / rkk;
-    __syncthreads();
-    const int L = n - kk - 1;
-    const double* rk = W + kk * n + kk + 1;
-    for (int idx = threadIdx.x; idx < L * L; idx += blockDim.x) {
-      const int ii = idx / L, jj = idx - ii * L;
-      if (jj >= ii) {
-        double* w = W + (kk + 1 + ii) * n + (kk + 1 + jj);
-        *w = *w - rk[ii] * rk[jj];
+    const int ncols = n - k0 - kb;
+    // (b) rows k0..k0+kb-1 of R~ right of the block: forward substitution per column
+    for (int jj = tid; jj < ncols; jj += kThreads) {
+      const int j = k0 + kb + jj;
+      double w[kPanel];
+#pragma unroll
+      for (int r = 0; r < kPanel; ++r) w[r] = r < kb ? W[(k0 + r) * ldw + j] : 0.0;
+#pragma unroll
+      for (int r = 0; r < kPanel; ++r) {
+        if (r < kb) {
+          const double v = w[r] * rinv[r];
+          w[r] = v;
+#pragma unroll
+          for (int l = r + 1; l < kPanel; ++l)
+            if (l < kb) w[l] = fma(-W[(k0 + r) * ldw + k0 + l], v, w[l]);
+        }
       }
+#pragma unroll
+      for (int r = 0; r < kPanel; ++r)
+        if (r < kb) W[(k0 + r) * ldw + j] = w[r];
     }
     __syncthreads();
+    t_b += clock64() - t0;
+    // (c) trailing update W_ij -= sum_r r_ri r_rj over k0+kb <= i <= j, 4x4 register tiles
+    const int L = ncols, T4 = (L + 3) >> 2, npairs = T4 * (T4 + 1) / 2;
+    const int base = k0 + kb;
+    for (int pidx = tid; pidx < npairs; pidx += kThreads) {
+      int J = static_cast<int>((sqrt(8.0 * pidx + 1.0) - 1.0) * 0.5);
+      while (J * (J + 1) / 2 > pidx) --J;
+      while ((J + 1) * (J + 2) / 2 <= pidx) ++J;
+      const int I = pidx - J * (J + 1) / 2;  // micro-tile (I, J), I <= J
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+      for (int r = 0; r < kb; ++r) {
+        const double* pr = W + (k0 + r) * ldw + base;
+        double xi[4], xj[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          xi[a] = (4 * I + a < L) ? pr[4 * I + a] : 0.0;
+          xj[a] = (4 * J + a < L) ? pr[4 * J + a] : 0.0;
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = fma(xi[a], xj[b], acc[a][b]);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int i = 4 * I + a, j = 4 * J + b;
+          if (i < L && j < L && i <= j) W[(base + i) * ldw + base + j] -= acc[a][b];
+        }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    g_phase[0] = t_a;
+    g_phase[1] = t_b;
   }
   return 0;
 }
 
-__device__ __forceinline__ double rpad(const double* W, int n, int i, int j) {
-  if (i < n && j < n) return i <= j ? W[i * n + j] : 0.0;
+__device__ __forceinline__ double rpad(const double* W, int ldw, int n, int i, int j) {
+  if (i < n && j < n) return i <= j ? W[i * ldw + j] : 0.0;
   return i == j ? 1.0 : 0.0;
 }
 
-__device__ void write_trsm_layout(const double* W, int n, int NT, double* bfrag, double* dblk) {
+// TRSM layout (trsm.cu): B fragments of -R~ and scaled diagonal blocks; R~ (column-major) for trmul.
+__device__ __noinline__ void write_outputs(const double* W, int ldw, int n, int NT, double* bfrag,
+                                              double* dblk, double* Rt) {
   const int nf = NT * (NT - 1) * 32;
-  for (int idx = threadIdx.x; idx < nf; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < nf; idx += kThreads) {
     const int f = idx >> 5, lane = idx & 31;
     int J = 1;
     while ((J + 1) * J <= f) ++J;
     const int s = f - J * (J - 1);
     const int g = lane >> 2, t = lane & 3;
-    const int row = 8 * (s >> 1) + 2 * t + (s & 1);
-    const int col = 8 * J + g;
-    bfrag[idx] = -rpad(W, n, row, col);
+    bfrag[idx] = -rpad(W, ldw, n, 8 * (s >> 1) + 2 * t + (s & 1), 8 * J + g);
   }
-  for (int idx = threadIdx.x; idx < NT * 72; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < NT * 72; idx += kThreads) {
     const int J = idx / 72, w = idx % 72;
-    if (w < 64) dblk[idx] = rpad(W, n, 8 * J + (w >> 3), 8 * J + (w & 7));
-    else dblk[idx] = 1.0 / rpad(W, n, 8 * J + (w - 64), 8 * J + (w - 64));
+    if (w < 64) {
+      const int c = 8 * J + (w >> 3), j = 8 * J + (w & 7);
+      dblk[idx] = j > c ? rpad(W, ldw, n, c, j) / rpad(W, ldw, n, c, c) : 0.0;
+    } else {
+      dblk[idx] = 1.0 / rpad(W, ldw, n, 8 * J + (w - 64), 8 * J + (w - 64));
+    }
   }
+  if (Rt)
+    for (int j = threadIdx.x >> 5; j < n; j += kThreads / 32)
+      for (int i = threadIdx.x & 31; i < n; i += 32) Rt[i + static_cast<size_t>(j) * n] = i <= j ? W[i * ldw + j] : 0.0;
 }
-}  // namespace
 
-__global__ void __launch_bounds__(kCholThreads, 1) chol_kernel(CholParams p) {
-  extern __shared__ double smW[];
-  __shared__ double red[33];
-  __shared__ double xv[kMaxN];
+template <bool SMEM>
+__device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
+  __shared__ double red[64];
+  __shared__ double ybuf[2][kMaxN];
+  __shared__ double rinv[kPanel];
   __shared__ int sflag;
   __shared__ double sval;
-  const int n = p.n;
-  double* W = p.w_in_smem ? smW : p.W;
-  if (threadIdx.x == 0) sflag = 0;
-  load_W(p, W);
+  const int n = p.n, tid = threadIdx.x;
+  const int ldw = n + 1;
+  double* W = SMEM ? smW : p.W;
+  long long clk[8] = {};
+  clk[0] = clock64();
+  if (tid == 0) sflag = 0;
+  load_W(p, W, ldw);
+  clk[1] = clock64();
 
   if (p.mode == CHOL_ONLY) {
     double pv = 0.0;
-    const int piv = factor(W, n, p.shift_value, p.shift_value != 0.0, &pv, &sflag, &sval);
-    for (int k = threadIdx.x; k < n * n; k += blockDim.x) {
-      const int i = k % n, j = k / n;
-      p.R[k] = (piv == 0 && i <= j) ? W[i * n + j] : 0.0;
-    }
-    if (threadIdx.x == 0) {
+    const int piv = factor(W, ldw, n, p.shift_value, p.shift_value != 0.0, &pv, &sflag, &sval, rinv);
+    for (int j = tid >> 5; j < n; j += kThreads / 32)
+      for (int i = tid & 31; i < n; i += 32)
+        p.R[i + static_cast<size_t>(j) * n] = (piv == 0 && i <= j) ? W[i * ldw + j] : 0.0;
+    if (tid == 0) {
       DevStatus st{};
       st.code = piv ? SCQR3_EBREAKDOWN : SCQR3_OK;
       st.breakdown_pivot = piv;
@@ -146,97 +295,65 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_kernel(CholParams p) {
 
   // ---- a7 input: distance of the Gram from I (stop test, reading D6) and its trace
   double loc = 0.0, tr = 0.0;
-  for (int k = threadIdx.x; k < n * n; k += blockDim.x) {
-    const int i = k / n, j = k % n;
-    const double v = W[k] - (i == j ? 1.0 : 0.0);
-    loc += v * v;
-    if (i == j) tr += W[k];
-  }
-  const double dev = sqrt(block_sum(loc, red));
-  const double trace = block_sum(tr, red);
-
-  // ---- a3: norm estimate N^2 and shift s
-  double N2;
-  if (p.oblique) {
-    if (p.pass == 1 && p.norm_mode == SCQR3_NORM_USER) N2 = p.norm2_bound * p.norm2_bound;
-    else N2 = p.tiles[static_cast<size_t>(p.NT) * (p.NT + 1) / 2 * 64];  // ||Q||_F^2 (reading D4)
-  } else if (p.pass == 1 && p.norm_mode == SCQR3_NORM_USER) {
-    N2 = p.norm2_bound * p.norm2_bound;
-  } else if (p.norm_mode == SCQR3_NORM_FROBENIUS) {
-    N2 = trace;
-  } else {
-    // power iteration on the Gram from the all-ones vector (reading D2); W is symmetric so
-    // row i is read as column i (conflict-free)
-    const int i = threadIdx.x;
-    if (i < n) xv[i] = 1.0 / sqrt(static_cast<double>(n));
-    __syncthreads();
-    for (int it = 0; it < p.power_iters; ++it) {
-      double y = 0.0;
-      if (i < n)
-        for (int j = 0; j < n; ++j) y = fma(W[j * n + i], xv[j], y);
-      const double ny = sqrt(block_sum(i < n ? y * y : 0.0, red));
-      if (!(ny > 0.0)) break;
-      if (i < n) xv[i] = y / ny;
-      __syncthreads();
+  for (int i = tid >> 5; i < n; i += kThreads / 32)
+    for (int j = tid & 31; j < n; j += 32) {
+      const double v = W[i * ldw + j] - (i == j ? 1.0 : 0.0);
+      loc = fma(v, v, loc);
+      if (i == j) tr += W[i * ldw + j];
     }
-    double y = 0.0;
-    if (i < n)
-      for (int j = 0; j < n; ++j) y = fma(W[j * n + i], xv[j], y);
-    N2 = block_sum(i < n ? xv[i] * y : 0.0, red) * 1.01;
-  }
+  const double2 dt = block_sum2(loc, tr, red);
+  const double dev = sqrt(dt.x), trace = dt.y;
+  clk[2] = clock64();
+
+  // ---- a3: norm estimate and shift, only when a shift is formed
   const double u = 0x1p-53;
   const double mg = p.m_global, nn = static_cast<double>(n);
-  double s;
-  if (p.shift_mode == SCQR3_SHIFT_FIXED && p.pass == 1) s = p.shift_value;
-  else if (p.oblique) s = 11.0 * (2.0 * mg * sqrt(mg * nn) + nn * (nn + 1.0)) * u * N2 * (*p.nb_dev);
-  else s = 11.0 * (mg * nn + nn * (nn + 1.0)) * u * N2;
+  auto shift_for = [&](double& N2) -> double {
+    if (p.oblique) {
+      if (p.pass == 1 && p.norm_mode == SCQR3_NORM_USER) N2 = p.norm2_bound * p.norm2_bound;
+      else N2 = p.tiles[static_cast<size_t>(p.NT) * (p.NT + 1) / 2 * 64];  // ||Q||_F^2 (reading D4)
+    } else if (p.pass == 1 && p.norm_mode == SCQR3_NORM_USER) {
+      N2 = p.norm2_bound * p.norm2_bound;
+    } else if (p.norm_mode == SCQR3_NORM_FROBENIUS) {
+      N2 = trace;
+    } else {
+      N2 = power_lmax(W, ldw, n, p.power_iters, trace, ybuf, red) * 1.01;
+    }
+    if (p.shift_mode == SCQR3_SHIFT_FIXED && p.pass == 1) return p.shift_value;
+    if (p.oblique) return 11.0 * (2.0 * mg * sqrt(mg * nn) + nn * (nn + 1.0)) * u * N2 * (*p.nb_dev);
+    return 11.0 * (mg * nn + nn * (nn + 1.0)) * u * N2;
+  };
 
   // ---- a4: (shifted) Cholesky with breakdown-triggered re-shift
   int shifted = 0, bpiv = 0, piv;
-  double bval = 0.0, pv = 0.0;
+  double bval = 0.0, pv = 0.0, s = 0.0, N2 = 0.0;
   if (p.pass == 1 && p.shift_mode != SCQR3_SHIFT_NONE) {
+    s = shift_for(N2);
+    clk[3] = clock64();
     shifted = 1;
-    piv = factor(W, n, s, true, &pv, &sflag, &sval);
+    piv = factor(W, ldw, n, s, true, &pv, &sflag, &sval, rinv);
     if (piv) { bpiv = piv; bval = pv; }
   } else {
-    piv = factor(W, n, 0.0, false, &pv, &sflag, &sval);
+    clk[3] = clock64();
+    piv = factor(W, ldw, n, 0.0, false, &pv, &sflag, &sval, rinv);
     if (piv) {
       bpiv = piv;
       bval = pv;
       if (p.shift_mode != SCQR3_SHIFT_NONE) {
         __syncthreads();
-        if (threadIdx.x == 0) sflag = 0;
-        load_W(p, W);
+        if (tid == 0) sflag = 0;
+        load_W(p, W, ldw);
+        s = shift_for(N2);
         shifted = 1;
-        piv = factor(W, n, s, true, &pv, &sflag, &sval);
+        piv = factor(W, ldw, n, s, true, &pv, &sflag, &sval, rinv);
         if (piv) { bpiv = piv; bval = pv; }
       }
     }
   }
   const int code = piv ? SCQR3_EBREAKDOWN : SCQR3_OK;
-
-  if (code == SCQR3_OK) {
-    // ---- outputs for the TRSM kernel
-    write_trsm_layout(W, n, p.NT, p.bfrag, p.dblk);
-    // ---- a6: R := R~ R  (k ascending, like the oracle)
-    if (p.pass == 1) {
-      for (int k = threadIdx.x; k < n * n; k += blockDim.x) {
-        const int i = k % n, j = k / n;
-        p.R[k] = i <= j ? W[i * n + j] : 0.0;
-      }
-    } else {
-      for (int k = threadIdx.x; k < n * n; k += blockDim.x) {
-        const int i = k % n, j = k / n;
-        double acc = 0.0;
-        if (i <= j)
-          for (int kk = i; kk <= j; ++kk) acc = fma(W[i * n + kk], p.R[kk + static_cast<size_t>(j) * n], acc);
-        p.Rnew[k] = acc;
-      }
-      __syncthreads();
-      for (int k = threadIdx.x; k < n * n; k += blockDim.x) p.R[k] = p.Rnew[k];
-    }
-  }
-  if (threadIdx.x == 0) {
+  clk[4] = clock64();
+  if (code == SCQR3_OK) write_outputs(W, ldw, n, p.NT, p.bfrag, p.dblk, p.Rt);
+  if (tid == 0) {
     DevStatus st{};
     st.code = code;
     st.stop = (code == SCQR3_OK && !shifted && dev <= p.stop_tol) ? 1 : 0;
@@ -247,6 +364,10 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_kernel(CholParams p) {
     st.pivot_value = bval;
     st.norm2_est = N2;
     st.dev_F = dev;
+    clk[5] = clock64();
+    clk[6] = g_phase[0];
+    clk[7] = g_phase[1];
+    for (int i = 0; i < 8; ++i) st.clk[i] = clk[i];
     *p.st_dev = st;
     if (p.st_host) {
       volatile DevStatus* h = p.st_host;
@@ -263,6 +384,41 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_kernel(CholParams p) {
       __threadfence_system();
     }
   }
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kThreads, 1) chol_kernel_smem(CholParams p) {
+  extern __shared__ double smW[];
+  chol_body<true>(p, smW);
+}
+
+// n >= 160: W in an L2-resident global scratch (same code path through the generic pointer)
+__global__ void __launch_bounds__(kThreads, 1) chol_kernel_gmem(CholParams p) {
+  extern __shared__ double smW[];
+  chol_body<false>(p, smW);
+}
+
+// a6: Rnew = R~ R (pass > 1) or R~ (pass 1), k ascending like the oracle; off the critical path
+// (side stream, overlapped with the TRSM).  Skipped when the pass broke down.
+__global__ void trmul_kernel(const double* Rt, const double* R, double* Rnew, int n, int first,
+                             const DevStatus* st) {
+  if (st->code != SCQR3_OK) return;
+  const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= static_cast<long long>(n) * n) return;
+  const int i = static_cast<int>(k % n), j = static_cast<int>(k / n);
+  double acc = 0.0;
+  if (i <= j) {
+    if (first) acc = Rt[k];
+    else
+      for (int kk = i; kk <= j; ++kk) acc = fma(Rt[i + static_cast<size_t>(kk) * n], R[kk + static_cast<size_t>(j) * n], acc);
+  }
+  Rnew[k] = acc;
+}
+
+__global__ void copy_kernel(const double* src, double* dst, long long count, const DevStatus* st) {
+  if (st && st->code != SCQR3_OK) return;
+  const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < count) dst[k] = src[k];
 }
 
 // R (n x n col-major, upper, positive diagonal) -> TRSM layout (kernel-level scqr3_trsm API)
@@ -283,8 +439,12 @@ __global__ void trsm_prep_kernel(const double* R, int n, int NT, double* bfrag, 
       bfrag[idx] = -rp(row, col);
     } else {
       const int k = idx - nf, J = k / 72, w = k % 72;
-      if (w < 64) dblk[k] = rp(8 * J + (w >> 3), 8 * J + (w & 7));
-      else dblk[k] = 1.0 / rp(8 * J + (w - 64), 8 * J + (w - 64));
+      if (w < 64) {
+        const int c = 8 * J + (w >> 3), j = 8 * J + (w & 7);
+        dblk[k] = j > c ? rp(c, j) / rp(c, c) : 0.0;
+      } else {
+        dblk[k] = 1.0 / rp(8 * J + (w - 64), 8 * J + (w - 64));
+      }
     }
   }
 }

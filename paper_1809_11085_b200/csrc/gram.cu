@@ -67,9 +67,13 @@ __global__ void __launch_bounds__(32 * 13, 1)
     if (lane == 0) {
       tma_prefetch_desc(&mapQ);
       if (full) tma_prefetch_desc(&mapY);
-      for (int i = 0; i < nst; ++i) {
-        const int st = i % p.stages;
-        const uint32_t ph = (i / p.stages) & 1;
+      int st = 0;
+      uint32_t ph = 0;
+      for (int i = 0; i < nst; ++i, ++st) {
+        if (st == p.stages) {
+          st = 0;
+          ph ^= 1u;
+        }
         if (i >= p.stages) mbar_wait(&empty_bar[st], ph ^ 1);
         mbar_arrive_expect_tx(&full_bar[st], stage_bytes * nsrc);
         const int row = static_cast<int>((s_begin + i) * kGramStageRows);
@@ -81,13 +85,15 @@ __global__ void __launch_bounds__(32 * 13, 1)
     return;
   }
 
-  // ---------------- consumers
+  // ---------------- consumers (job table: host-balanced over the four SM sub-partitions)
   const int cw = warp - 1;
-  const int job = p.job_begin[group] + cw;
-  const bool active = job < p.job_begin[group + 1];
+  const int job = p.warp_job[group * kMaxConsumers + cw];
+  const bool active = job >= 0;
   int bi = 0, bj = 0;
   if (active) decode_job(job, p.NB, full, bi, bj);
   const bool diag = !full && bi == bj;
+  const int NT = p.NT;
+  const bool edge = (bi + 1) * kJobTiles > NT || (bj + 1) * kJobTiles > NT;
   const int g = lane >> 2, t = lane & 3;
 
   double acc[kJobTiles][kJobTiles][2];
@@ -100,35 +106,59 @@ __global__ void __launch_bounds__(32 * 13, 1)
   uint32_t offA[kJobTiles], offB[kJobTiles];
 #pragma unroll
   for (int a = 0; a < kJobTiles; ++a) {
-    offA[a] = static_cast<uint32_t>(8 * (bi * kJobTiles + a) + g) * 128u;
-    offB[a] = static_cast<uint32_t>(8 * (bj * kJobTiles + a) + g) * 128u;
+    offA[a] = static_cast<uint32_t>(8 * min(bi * kJobTiles + a, NT - 1) + g) * 128u;
+    offB[a] = static_cast<uint32_t>(8 * min(bj * kJobTiles + a, NT - 1) + g) * 128u;
   }
-  const int NT = p.NT;
+  // 16-byte chunk of this lane's k slot per k-step s: rows {2s, 2s+1, 2s+8, 2s+9}[t] -> the
+  // chunk index (row>>1) = s + 4*(t>>1) XOR (column & 7) = g (SWIZZLE_128B), conflict free
+  uint32_t inner[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s)
+    inner[s] = ((((s + 4 * (t >> 1)) ^ g) & 7u) << 4) + ((t & 1) << 3);
+  const int kind = !active ? 3 : edge ? 2 : diag ? 1 : 0;
 
+  int st = 0;
+  uint32_t ph = 0;
   for (int i = 0; i < nst; ++i) {
-    const int st = i % p.stages;
-    const uint32_t ph = (i / p.stages) & 1;
     mbar_wait(&full_bar[st], ph);
-    if (active) {
-      const unsigned char* srcA = stages + static_cast<size_t>(st) * nsrc * stage_bytes;
-      const unsigned char* srcB = full ? srcA + stage_bytes : srcA;
+    const unsigned char* srcA = stages + static_cast<size_t>(st) * nsrc * stage_bytes;
+    const unsigned char* srcB = full ? srcA + stage_bytes : srcA;
+    if (kind == 0) {
+      // full 4x4 off-diagonal block: 8 fragment loads, 16 DMMA per k-step
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
-        // row of this lane's k slot: {2s, 2s+1, 2s+8, 2s+9}[t]; chunk = row>>1 = s + 4*(t>>1)
-        const uint32_t chunk16 = static_cast<uint32_t>(s + 4 * (t >> 1));
-        const uint32_t inner = (((chunk16 ^ static_cast<uint32_t>(g)) & 7u) << 4) + ((t & 1) << 3);
         double fa[kJobTiles], fb[kJobTiles];
 #pragma unroll
         for (int a = 0; a < kJobTiles; ++a) {
-          fa[a] = (bi * kJobTiles + a < NT) ? *reinterpret_cast<const double*>(srcA + offA[a] + inner) : 0.0;
+          fa[a] = *reinterpret_cast<const double*>(srcA + offA[a] + inner[s]);
+          fb[a] = *reinterpret_cast<const double*>(srcB + offB[a] + inner[s]);
         }
-        if (diag) {
 #pragma unroll
-          for (int b = 0; b < kJobTiles; ++b) fb[b] = fa[b];
-        } else {
+        for (int a = 0; a < kJobTiles; ++a)
 #pragma unroll
-          for (int b = 0; b < kJobTiles; ++b)
-            fb[b] = (bj * kJobTiles + b < NT) ? *reinterpret_cast<const double*>(srcB + offB[b] + inner) : 0.0;
+          for (int b = 0; b < kJobTiles; ++b) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+      }
+    } else if (kind == 1) {
+      // diagonal block of the symmetric Gram: A and B fragments coincide, 10 DMMA per k-step
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        double fa[kJobTiles];
+#pragma unroll
+        for (int a = 0; a < kJobTiles; ++a) fa[a] = *reinterpret_cast<const double*>(srcA + offA[a] + inner[s]);
+#pragma unroll
+        for (int a = 0; a < kJobTiles; ++a)
+#pragma unroll
+          for (int b = a; b < kJobTiles; ++b) dmma(acc[a][b][0], acc[a][b][1], fa[a], fa[b]);
+      }
+    } else if (kind == 2) {
+      // block touching the padded edge (n not a multiple of 32): per-tile validity
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        double fa[kJobTiles], fb[kJobTiles];
+#pragma unroll
+        for (int a = 0; a < kJobTiles; ++a) {
+          fa[a] = *reinterpret_cast<const double*>(srcA + offA[a] + inner[s]);
+          fb[a] = *reinterpret_cast<const double*>(srcB + offB[a] + inner[s]);
         }
 #pragma unroll
         for (int a = 0; a < kJobTiles; ++a)
@@ -141,6 +171,10 @@ __global__ void __launch_bounds__(32 * 13, 1)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[st]);
+    if (++st == p.stages) {
+      st = 0;
+      ph ^= 1u;
+    }
   }
 
   if (!active) return;

@@ -31,6 +31,7 @@ struct DevStatus {
   double pivot_value;
   double norm2_est;
   double dev_F;
+  long long clk[8];  // chol_kernel phase timestamps (clock64), diagnostics only
 };
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {

@@ -64,6 +64,9 @@ struct Ctx {
   DevStatus* st_host = nullptr;      // pinned, mapped
   DevStatus* st_host_dev = nullptr;  // device alias of st_host
   cudaEvent_t ev = nullptr;
+  cudaStream_t side = nullptr;     // R accumulation, overlapped with the TRSM
+  cudaEvent_t ev_chol = nullptr;   // chol done (st) -> side may start
+  cudaEvent_t ev_side = nullptr;   // side done -> st may reuse the R~ buffer
   // profiling: event pairs recorded around launches when opts->prof is set
   static constexpr int kMaxEv = 128;
   cudaEvent_t ev_a[kMaxEv] = {}, ev_b[kMaxEv] = {};
@@ -74,7 +77,7 @@ struct Ctx {
 };
 thread_local Ctx g_ctx[16];
 
-enum ProfKind { PK_GRAM = 0, PK_REDUCE = 1, PK_CHOL = 2, PK_TRSM = 3, PK_COMM = 4 };
+enum ProfKind { PK_GRAM = 0, PK_REDUCE = 1, PK_CHOL = 2, PK_TRSM = 3, PK_COMM = 4, PK_TRMUL = 5 };
 
 // Opens a timed region on the stream (no-op unless profiling); returns the slot or -1.
 int prof_begin(Ctx* c, int kind) {
@@ -85,11 +88,11 @@ int prof_begin(Ctx* c, int kind) {
     cudaEventCreate(&c->ev_b[i]);
   }
   c->ev_kind[i] = kind;
-  cudaEventRecord(c->ev_a[i], c->prof_stream);
+  cudaEventRecord(c->ev_a[i], kind == PK_TRMUL ? c->side : c->prof_stream);
   return i;
 }
 void prof_end(Ctx* c, int slot) {
-  if (slot >= 0) cudaEventRecord(c->ev_b[slot], c->prof_stream);
+  if (slot >= 0) cudaEventRecord(c->ev_b[slot], c->ev_kind[slot] == PK_TRMUL ? c->side : c->prof_stream);
 }
 // After the stream has been synchronised: fold the recorded pairs into *prof.
 void prof_flush(Ctx* c) {
@@ -102,6 +105,7 @@ void prof_flush(Ctx* c) {
       case PK_REDUCE: c->prof->reduce_ms += ms; c->prof->reduce_launches++; break;
       case PK_CHOL: c->prof->chol_ms += ms; c->prof->chol_launches++; break;
       case PK_TRSM: c->prof->trsm_ms += ms; c->prof->trsm_launches++; break;
+      case PK_TRMUL: c->prof->trmul_ms += ms; c->prof->trmul_launches++; break;
       default: c->prof->comm_ms += ms; c->prof->comm_calls++; break;
     }
   }
@@ -124,6 +128,9 @@ int get_ctx(Ctx** out) {
     CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c.st_host), sizeof(DevStatus), cudaHostAllocMapped));
     CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.st_host_dev), c.st_host, 0));
     CUDA_TRY(cudaEventCreateWithFlags(&c.ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c.ev_chol, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c.ev_side, cudaEventDisableTiming));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
     c.init = true;
   }
   *out = &c;
@@ -145,7 +152,7 @@ struct Layout {
   int max_chunks;
   long long ldy;
   // offsets (bytes)
-  size_t st, partials, tiles, W, Rnew, bfrag, dblk, misc, colsq, y, halo, end;
+  size_t st, partials, tiles, W, Rnew, Rt, bfrag, dblk, misc, colsq, y, halo, end;
 };
 
 Layout make_layout(int64_t m, int64_t n, int oblique) {
@@ -166,8 +173,9 @@ Layout make_layout(int64_t m, int64_t n, int oblique) {
   L.st = take(sizeof(DevStatus));
   L.partials = take(static_cast<size_t>(L.max_chunks) * L.tiles_part * 64 * 8);
   L.tiles = take(static_cast<size_t>(L.tiles_sym * 64 + 64) * 8);
-  L.W = take(static_cast<size_t>(n) * n * 8);
+  L.W = take(static_cast<size_t>(n) * (n + 1) * 8);
   L.Rnew = take(static_cast<size_t>(n) * n * 8);
+  L.Rt = take(static_cast<size_t>(n) * n * 8);
   L.bfrag = take(static_cast<size_t>(L.NT) * (L.NT - 1) * 32 * 8 + 8);
   L.dblk = take(static_cast<size_t>(L.NT) * 72 * 8);
   L.misc = take(64 * 8);  // [0] nb, [1] e_prev, [2] m_global (int64), ...
@@ -180,7 +188,7 @@ Layout make_layout(int64_t m, int64_t n, int oblique) {
 
 struct WS {
   DevStatus* st;
-  double *partials, *tiles, *W, *Rnew, *bfrag, *dblk, *misc, *colsq, *y, *halo;
+  double *partials, *tiles, *W, *Rnew, *Rt, *bfrag, *dblk, *misc, *colsq, *y, *halo;
 };
 
 int carve(const Layout& L, const scqr3_opts* o, WS* w) {
@@ -193,6 +201,7 @@ int carve(const Layout& L, const scqr3_opts* o, WS* w) {
   w->tiles = reinterpret_cast<double*>(b + L.tiles);
   w->W = reinterpret_cast<double*>(b + L.W);
   w->Rnew = reinterpret_cast<double*>(b + L.Rnew);
+  w->Rt = reinterpret_cast<double*>(b + L.Rt);
   w->bfrag = reinterpret_cast<double*>(b + L.bfrag);
   w->dblk = reinterpret_cast<double*>(b + L.dblk);
   w->misc = reinterpret_cast<double*>(b + L.misc);
@@ -232,6 +241,49 @@ int encode_map(Ctx* c, CUtensorMap* map, const double* base, int64_t m, int64_t 
   return SCQR3_OK;
 }
 
+// Assign the Gram jobs of each group to consumer warps so that the DMMA work of the four SM
+// sub-partitions (warp w of the CTA runs on sub-partition w % 4; consumer c is warp c + 1) is
+// balanced: longest job first onto the least-loaded sub-partition with a free warp.
+void assign_gram_jobs(GramParams& gp, int jobs, int groups, int ncons, bool oblique) {
+  auto weight = [&](int j) {
+    int bi, bj;
+    if (oblique) {
+      bi = j / gp.NB;
+      bj = j % gp.NB;
+    } else {
+      int c = 0;
+      while ((c + 1) * (c + 2) / 2 <= j) ++c;
+      bj = c;
+      bi = j - c * (c + 1) / 2;
+    }
+    int w = 0;
+    for (int a = 0; a < kJobTiles; ++a)
+      for (int b = 0; b < kJobTiles; ++b)
+        if (bi * kJobTiles + a < gp.NT && bj * kJobTiles + b < gp.NT && (oblique || bi != bj || a <= b)) ++w;
+    return w;
+  };
+  for (int i = 0; i < kMaxGroups * kMaxConsumers; ++i) gp.warp_job[i] = -1;
+  for (int g = 0; g < groups; ++g) {
+    const int j0 = jobs * g / groups, j1 = jobs * (g + 1) / groups;
+    int order[kMaxConsumers], nj = 0;
+    for (int j = j0; j < j1; ++j) order[nj++] = j;
+    std::stable_sort(order, order + nj, [&](int x, int y) { return weight(x) > weight(y); });
+    int load[4] = {0, 0, 0, 0};
+    bool used[kMaxConsumers] = {};
+    for (int k = 0; k < nj; ++k) {
+      int best = -1;
+      for (int w = 0; w < ncons; ++w) {
+        if (used[w]) continue;
+        const int sp = (w + 1) & 3;
+        if (best < 0 || load[sp] < load[(best + 1) & 3]) best = w;
+      }
+      used[best] = true;
+      load[(best + 1) & 3] += weight(order[k]);
+      gp.warp_job[g * kMaxConsumers + best] = order[k];
+    }
+  }
+}
+
 // Gram of the m x n block at src into w.tiles (packed upper tiles; oblique: sym(Q^T Y) and ||Q||_F^2)
 int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld, int64_t m, bool oblique,
              const ObliqueYParams* yp, cudaStream_t st) {
@@ -265,11 +317,12 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   gp.oblique = oblique ? 1 : 0;
   gp.tiles_per_partial = static_cast<int>(L.tiles_part);
   const int jobs = oblique ? gp.NB * gp.NB : gp.NB * (gp.NB + 1) / 2;
-  const int groups = (jobs + 11) / 12;
+  const int groups = (jobs + kMaxConsumers - 1) / kMaxConsumers;
+  if (groups > kMaxGroups) return fail("internal: too many Gram job groups");
   gp.groups = groups;
   int ncons = 0;
-  for (int g = 0; g <= groups; ++g) gp.job_begin[g] = jobs * g / groups;
-  for (int g = 0; g < groups; ++g) ncons = std::max(ncons, gp.job_begin[g + 1] - gp.job_begin[g]);
+  for (int g = 0; g < groups; ++g) ncons = std::max(ncons, jobs * (g + 1) / groups - jobs * g / groups);
+  assign_gram_jobs(gp, jobs, groups, ncons, oblique);
   const int threads = 32 * (1 + ncons);
   const int nsrc = oblique ? 2 : 1;
   const size_t stage_bytes = static_cast<size_t>(L.npad) * 128;
@@ -309,15 +362,37 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
 }
 
 int launch_chol(const CholParams& p, cudaStream_t st) {
-  const size_t smem = p.w_in_smem ? static_cast<size_t>(p.n) * p.n * 8 : 0;
-  CUDA_TRY(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  chol_kernel<<<1, 1024, smem, st>>>(p);
+  if (p.w_in_smem) {
+    const size_t smem = static_cast<size_t>(p.n) * (p.n + 1) * 8;
+    CUDA_TRY(cudaFuncSetAttribute(chol_kernel_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    chol_kernel_smem<<<1, 256, smem, st>>>(p);
+  } else {
+    chol_kernel_gmem<<<1, 256, 0, st>>>(p);
+  }
   ++g_launches;
   CUDA_TRY(cudaGetLastError());
   return SCQR3_OK;
 }
 
-bool w_fits_smem(int n) { return static_cast<size_t>(n) * n * 8 <= 200 * 1024; }
+// a6 on the side stream: R := R~ R once this pass's chol_kernel is done; the main stream only
+// waits for it before the next chol_kernel overwrites R~ (by then the TRSM has long finished).
+int launch_trmul(Ctx* c, const double* Rt, double* R, double* Rnew, int n, int first, const DevStatus* st_dev,
+                 cudaStream_t st) {
+  CUDA_TRY(cudaEventRecord(c->ev_chol, st));
+  CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_chol, 0));
+  const long long nn = static_cast<long long>(n) * n;
+  const unsigned blocks = static_cast<unsigned>((nn + 127) / 128);
+  const int pt = prof_begin(c, PK_TRMUL);
+  trmul_kernel<<<blocks, 128, 0, c->side>>>(Rt, R, Rnew, n, first, st_dev);
+  copy_kernel<<<blocks, 128, 0, c->side>>>(Rnew, R, nn, st_dev);
+  prof_end(c, pt);
+  g_launches += 2;
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventRecord(c->ev_side, c->side));
+  return SCQR3_OK;
+}
+
+bool w_fits_smem(int n) { return static_cast<size_t>(n) * (n + 1) * 8 <= 200 * 1024; }
 
 int halo_exchange(Comm* cm, const double* Qsrc, int64_t ld, int64_t m, int n, double* halo, cudaStream_t st) {
   // halo layout: [0,n) my first row, [n,2n) my last row, [2n,3n) prev rank's last row, [3n,4n) next rank's first row
@@ -443,8 +518,7 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const double*
   cp.stop_tol = stop_tol;
   cp.W = w.W;
   cp.w_in_smem = w_fits_smem(static_cast<int>(n)) ? 1 : 0;
-  cp.R = R;
-  cp.Rnew = w.Rnew;
+  cp.Rt = w.Rt;
   cp.bfrag = w.bfrag;
   cp.dblk = w.dblk;
   cp.st_dev = w.st;
@@ -479,15 +553,20 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const double*
     }
     c->st_host->code = -1;
     cp.pass = k;
+    if (k > 1) CUDA_TRY(cudaStreamWaitEvent(st, c->ev_side, 0));  // previous R~ consumed
     const int pc = prof_begin(c, PK_CHOL);
     TRY(launch_chol(cp, st));
     prof_end(c, pc);
     CUDA_TRY(cudaEventRecord(c->ev, st));
+    TRY(launch_trmul(c, w.Rt, R, w.Rnew, static_cast<int>(n), k == 1, w.st, st));
     tp.X = src;
     tp.ldx = ldsrc;
     if (m > 0) {
+      CUtensorMap mx;
+      const bool use_tma = L.NT <= 16;
+      if (use_tma) TRY(encode_map(c, &mx, src, m, n, ldsrc, L.npad));
       const int pt = prof_begin(c, PK_TRSM);
-      CUDA_TRY(launch_trsm(tp, c->num_sms, st));
+      CUDA_TRY(launch_trsm(tp, use_tma ? &mx : nullptr, c->num_sms, st));
       prof_end(c, pt);
       ++g_launches;
     }
@@ -515,6 +594,7 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const double*
     }
   }
   if (o->passes_out) *o->passes_out = std::min(k, max_passes);
+  CUDA_TRY(cudaStreamWaitEvent(st, c->ev_side, 0));  // R complete
   CUDA_TRY(cudaStreamSynchronize(st));
   prof_flush(c);
   c->prof = nullptr;
@@ -698,7 +778,10 @@ int scqr3_trsm(int64_t m, int64_t n, const double* X, int64_t ld, const double* 
   tp.dblk = w.dblk;
   tp.st = nullptr;
   if (m > 0) {
-    CUDA_TRY(launch_trsm(tp, c->num_sms, st));
+    CUtensorMap mx;
+    const bool use_tma = L.NT <= 16;
+    if (use_tma) TRY(encode_map(c, &mx, X, m, n, ld, L.npad));
+    CUDA_TRY(launch_trsm(tp, use_tma ? &mx : nullptr, c->num_sms, st));
     ++g_launches;
   }
   CUDA_TRY(cudaStreamSynchronize(st));

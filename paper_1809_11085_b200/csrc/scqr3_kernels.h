@@ -9,6 +9,9 @@ namespace scqr3 {
 
 struct DevStatus;
 
+constexpr int kMaxConsumers = 12;   // consumer warps per Gram CTA
+constexpr int kMaxGroups = 8;       // job groups (CTAs sharing one row chunk)
+
 struct GramParams {
   double* partials;          // [chunks][tiles_per_partial][64]
   long long total_stages;    // ceil(m / 16)
@@ -20,7 +23,9 @@ struct GramParams {
   int NB;                    // ceil(NT / 4) blocks per side
   int oblique;               // 1 = full Q^T Y
   int tiles_per_partial;     // NT(NT+1)/2 or NT^2
-  int job_begin[33];         // jobs of group g: [job_begin[g], job_begin[g+1]), <= 12 each
+  // job of consumer warp w in group g: warp_job[g * kMaxConsumers + w] (-1 = idle); the host
+  // balances the DMMA work of each group over the SM's four sub-partitions (warp % 4)
+  int warp_job[kMaxGroups * kMaxConsumers];
 };
 
 struct GramReduceParams {
@@ -69,8 +74,8 @@ struct CholParams {
   double stop_tol;
   double* W;                 // n x n scratch (global) when it does not fit in shared memory
   int w_in_smem;
-  double* R;                 // running R (n x n col-major), or the CHOL_ONLY output
-  double* Rnew;              // n x n scratch
+  double* R;                 // CHOL_ONLY output (n x n col-major)
+  double* Rt;                // CHOL_PASS: R~ of this pass (n x n col-major) for trmul_kernel
   double* bfrag;             // TRSM B fragments (negated R~), NT(NT-1) x 32
   double* dblk;              // TRSM diagonal blocks, NT x 72
   DevStatus* st_dev;
@@ -97,11 +102,14 @@ __global__ void gershgorin_kernel(const double* d, const double* e, long long m,
                                   int has_next, double* partial);
 __global__ void max_reduce_kernel(const double* partial, int count, double* out);
 __global__ void tiles_to_full_kernel(const double* tiles, int n, double* A);
-__global__ void chol_kernel(CholParams p);
+__global__ void chol_kernel_smem(CholParams p);
+__global__ void chol_kernel_gmem(CholParams p);
+__global__ void trmul_kernel(const double* Rt, const double* R, double* Rnew, int n, int first, const DevStatus* st);
+__global__ void copy_kernel(const double* src, double* dst, long long count, const DevStatus* st);
 __global__ void trsm_prep_kernel(const double* R, int n, int NT, double* bfrag, double* dblk);
 
 // TRSM launcher (chooses the template instance for n)
-cudaError_t launch_trsm(const TrsmParams& p, int num_sms, cudaStream_t stream);
+cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream);
 
 inline int npad_for(int n) {
   // tile counts with a compiled TRSM instance

@@ -1,7 +1,7 @@
 // trsm.cu -- tall-skinny triangular solve Q = X R~^{-1} (step a5; eq. (3); Alg. 1 line 4
 // P:140; Alg. 2 line 8 P:685).  The paper's per-row model q_i^T = x_i^T (R + dR_i)^{-1} (P:189,
 // P:323-334) holds because every row is solved by (blocked) forward substitution -- no
-// explicit inverse of R~ is formed (reading D11).
+// explicit inverse of R~ (or of its diagonal blocks) is formed (reading D11).
 //
 // Design: rows are independent, so each warp owns 8*A rows and keeps
 // them in registers for the whole solve, as m8n8k4 C fragments (lane g,t holds row g, columns
@@ -12,17 +12,29 @@
 // the solved rows never leave the registers; the B operand (-R~ rows in fragment order,
 // written by chol_kernel) is read from shared memory, conflict free.  The 8x8 diagonal block
 // is then solved by right-looking substitution inside each quad (shuffle of each pivot
-// column, multiply by the reciprocal pivot).  X is read once and Q written once per pass.
+// column).  The loop is software-pipelined: the (latency-bound) diagonal solve of block J-1 is
+// interleaved with block J's tensor-core updates from blocks 0..J-2.
+// X is read once (TMA into a per-warp shared-memory slot, one row group ahead, so the HBM
+// latency is off the critical path) and Q written once per pass.
 #include "scqr3_dev.cuh"
 #include "scqr3_kernels.h"
 
 namespace scqr3 {
 
-template <int NT, int A, bool SMEM_B, int THREADS>
-__global__ void __launch_bounds__(THREADS, 1) trsm_kernel(TrsmParams p) {
-  extern __shared__ double sm[];
+template <int NT, int A, bool SMEM_B, int THREADS, bool TMA>
+__global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant__ CUtensorMap mapX, TrsmParams p) {
+  extern __shared__ __align__(1024) unsigned char smraw[];
   if (p.st && p.st->code != 0) return;
   constexpr int NF = NT * (NT - 1);
+  constexpr int WPB = THREADS / 32;
+  constexpr int NPAD = NT * 8;
+  constexpr uint32_t kBoxBytes = 16u * NPAD * 8u;         // one 16-row TMA box
+  constexpr uint32_t kSlotBytes = kBoxBytes * (A / 2 > 0 ? A / 2 : 1);
+  // layout: [TMA slots (1024-aligned)] [B fragments] [diagonal blocks] [mbarriers]
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  unsigned char* slots = base;
+  double* sm = reinterpret_cast<double*>(base + (TMA ? WPB * kSlotBytes : 0));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + (SMEM_B ? NF * 32 : 0) + NT * 72);
   const double* bf;
   const double* db;
   if (SMEM_B) {
@@ -35,57 +47,140 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(TrsmParams p) {
     bf = p.bfrag;
     db = sm;
   }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  if (TMA && threadIdx.x == 0) {
+    for (int w = 0; w < WPB; ++w) mbar_init(&bars[w], 1);
+    fence_barrier_init();
+  }
   __syncthreads();
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  constexpr int WPB = THREADS / 32;
   const long long m = p.m;
   const int n = p.n;
   const long long ngroups = (m + 8 * A - 1) / (8 * A);
-  for (long long rg = static_cast<long long>(blockIdx.x) * WPB + warp; rg < ngroups;
-       rg += static_cast<long long>(gridDim.x) * WPB) {
+  const long long stride = static_cast<long long>(gridDim.x) * WPB;
+  unsigned char* slot = slots + warp * kSlotBytes;
+  uint64_t* bar = bars + warp;
+  uint32_t phase = 0;
+  auto issue = [&](long long rg) {  // elected lane: TMA of row group rg into this warp's slot
+    if (TMA && lane == 0 && rg < ngroups) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(bar, kSlotBytes);
+#pragma unroll
+      for (int b = 0; b < (A / 2 > 0 ? A / 2 : 1); ++b)
+        tma_load_2d(slot + b * kBoxBytes, &mapX, static_cast<int>(rg * 8 * A + 16 * b), 0, bar);
+    }
+  };
+  const long long rg0 = static_cast<long long>(blockIdx.x) * WPB + warp;
+  if (TMA) {
+    if (lane == 0) tma_prefetch_desc(&mapX);
+    issue(rg0);
+  }
+
+  for (long long rg = rg0; rg < ngroups; rg += stride) {
     const long long r0 = rg * 8 * A;
     double q[A][NT][2];
+    if (TMA) {
+      mbar_wait(bar, phase);
+      phase ^= 1u;
 #pragma unroll
-    for (int a = 0; a < A; ++a) {
-      const long long row = r0 + 8 * a + g;
-      const bool rok = row < m;
+      for (int a = 0; a < A; ++a) {
+        const int r = 8 * a + g;  // row inside the slot
+        const unsigned char* box = slot + (r >> 4) * kBoxBytes;
 #pragma unroll
-      for (int J = 0; J < NT; ++J)
+        for (int J = 0; J < NT; ++J)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int col = 8 * J + 2 * t + h;
-          q[a][J][h] = (rok && col < n) ? __ldcs(p.X + row + static_cast<long long>(col) * p.ldx) : 0.0;
-        }
-    }
-#pragma unroll
-    for (int J = 0; J < NT; ++J) {
-      // ---- GEMM part on the tensor cores: C_J += Q_{<J} (-R~_{<J,J})
-#pragma unroll
-      for (int s = 0; s < 2 * J; ++s) {
-        const double b = SMEM_B ? bf[(J * (J - 1) + s) * 32 + lane] : __ldg(bf + (J * (J - 1) + s) * 32 + lane);
-#pragma unroll
-        for (int a = 0; a < A; ++a) dmma(q[a][J][0], q[a][J][1], q[a][s >> 1][s & 1], b);
+          for (int h = 0; h < 2; ++h)
+            q[a][J][h] = *reinterpret_cast<const double*>(box + swz128_offset(r & 15, 8 * J + 2 * t + h));
       }
-      // ---- 8x8 diagonal block: right-looking substitution inside each quad
-      const double* D = db + J * 72;
+    } else {
+#pragma unroll
+      for (int a = 0; a < A; ++a) {
+        const long long row = r0 + 8 * a + g;
+        const bool rok = row < m;
+#pragma unroll
+        for (int J = 0; J < NT; ++J)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int col = 8 * J + 2 * t + h;
+            q[a][J][h] = (rok && col < n) ? __ldcs(p.X + row + static_cast<long long>(col) * p.ldx) : 0.0;
+          }
+      }
+    }
+    // Software pipeline over column blocks: iteration J solves the diagonal block of J-1 (a
+    // latency-bound shuffle chain) interleaved with block J's tensor-core updates from blocks
+    // 0..J-2 (independent of it), then applies block J-1's update to block J.  Even and odd
+    // k-steps accumulate separately to halve the DMMA dependency chains.
+    double odd[A][2];
+#pragma unroll
+    for (int J = 0; J <= NT; ++J) {
+      if (TMA && J == (NT > 1 ? 1 : 0)) {
+        // every lane's slot reads have been consumed by now: refill the slot with the next group
+        __syncwarp();
+        issue(rg + stride);
+      }
+      const bool has_acc = J < NT, has_solve = J >= 1;
+      const int nearly = (has_acc && J >= 1) ? 2 * (J - 1) : 0;  // k-steps over blocks 0..J-2
+#pragma unroll
+      for (int a = 0; a < A; ++a) odd[a][0] = odd[a][1] = 0.0;
+      int s = 0;
+      const double* D = db + (J - 1) * 72;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        const double rinv = D[64 + c];
-        const double2 rc = *reinterpret_cast<const double2*>(D + c * 8 + 2 * t);
-        const int owner = (lane & ~3) | (c >> 1);
+        if (has_solve) {
+          // diagonal block J-1: right-looking substitution inside each quad on the unscaled
+          // values v (v_j -= v_c * (r_cj / r_cc), strict upper only, zeros elsewhere)
+          const double2 rc = *reinterpret_cast<const double2*>(D + c * 8 + 2 * t);
+          const int owner = (lane & ~3) | (c >> 1);
 #pragma unroll
-        for (int a = 0; a < A; ++a) {
-          const double mine = (c & 1) ? q[a][J][1] : q[a][J][0];
-          const double qc = __shfl_sync(0xffffffffu, mine * rinv, owner);
-          if (t == (c >> 1)) {
-            if (c & 1) q[a][J][1] = qc;
-            else q[a][J][0] = qc;
+          for (int a = 0; a < A; ++a) {
+            const double vc = __shfl_sync(0xffffffffu, q[a][J - 1][c & 1], owner);
+            q[a][J - 1][0] = fma(-vc, rc.x, q[a][J - 1][0]);
+            q[a][J - 1][1] = fma(-vc, rc.y, q[a][J - 1][1]);
           }
-          if (2 * t > c) q[a][J][0] = fma(-qc, rc.x, q[a][J][0]);
-          if (2 * t + 1 > c) q[a][J][1] = fma(-qc, rc.y, q[a][J][1]);
+        }
+        // a share of block J's updates from blocks 0..J-2: C_J += Q_{<J-1} (-R~_{<J-1,J})
+#pragma unroll
+        for (; s < nearly * (c + 1) / 8; ++s) {
+          const double b = SMEM_B ? bf[(J * (J - 1) + s) * 32 + lane] : __ldg(bf + (J * (J - 1) + s) * 32 + lane);
+#pragma unroll
+          for (int a = 0; a < A; ++a) {
+            if (s & 1) dmma(odd[a][0], odd[a][1], q[a][s >> 1][s & 1], b);
+            else dmma(q[a][J][0], q[a][J][1], q[a][s >> 1][s & 1], b);
+          }
         }
       }
+      if (has_solve) {
+        // q_j = v_j / r_jj as a multiply by the reciprocal (reading D11)
+        const double2 ri = *reinterpret_cast<const double2*>(D + 64 + 2 * t);
+#pragma unroll
+        for (int a = 0; a < A; ++a) {
+          q[a][J - 1][0] *= ri.x;
+          q[a][J - 1][1] *= ri.y;
+        }
+      }
+      if (has_acc) {
+        // block J-1 (now final) -> block J
+#pragma unroll
+        for (s = nearly; s < 2 * J; ++s) {
+          const double b = SMEM_B ? bf[(J * (J - 1) + s) * 32 + lane] : __ldg(bf + (J * (J - 1) + s) * 32 + lane);
+#pragma unroll
+          for (int a = 0; a < A; ++a) {
+            if (s & 1) dmma(odd[a][0], odd[a][1], q[a][s >> 1][s & 1], b);
+            else dmma(q[a][J][0], q[a][J][1], q[a][s >> 1][s & 1], b);
+          }
+        }
+        if (J > 0) {
+#pragma unroll
+          for (int a = 0; a < A; ++a) {
+            q[a][J][0] += odd[a][0];
+            q[a][J][1] += odd[a][1];
+          }
+        }
+      }
+    }
+    if (TMA && NT <= 1) {
+      __syncwarp();
+      issue(rg + stride);
     }
 #pragma unroll
     for (int a = 0; a < A; ++a) {
@@ -103,11 +198,14 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(TrsmParams p) {
   }
 }
 
-template <int NT, int A, bool SMEM_B, int THREADS>
-static cudaError_t launch_one(const TrsmParams& p, int num_sms, cudaStream_t stream) {
+template <int NT, int A, bool SMEM_B, int THREADS, bool TMA>
+static cudaError_t launch_one(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream) {
   constexpr int NF = NT * (NT - 1);
-  const size_t smem = SMEM_B ? static_cast<size_t>(NF * 32 + NT * 72) * 8 : static_cast<size_t>(NT * 72) * 8;
-  auto k = trsm_kernel<NT, A, SMEM_B, THREADS>;
+  constexpr int WPB = THREADS / 32;
+  constexpr size_t kSlot = 16u * NT * 8 * 8 * (A / 2 > 0 ? A / 2 : 1);
+  const size_t smem = 1024 + (TMA ? WPB * kSlot : 0) + static_cast<size_t>((SMEM_B ? NF * 32 : 0) + NT * 72) * 8 +
+                      WPB * 8;
+  auto k = trsm_kernel<NT, A, SMEM_B, THREADS, TMA>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -116,24 +214,33 @@ static cudaError_t launch_one(const TrsmParams& p, int num_sms, cudaStream_t str
   if (per_sm < 1) per_sm = 1;
   const long long groups = (p.m + 8 * A - 1) / (8 * A);
   long long grid = static_cast<long long>(num_sms) * per_sm;
-  const long long need = (groups + THREADS / 32 - 1) / (THREADS / 32);
+  const long long need = (groups + WPB - 1) / WPB;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  k<<<static_cast<unsigned>(grid), THREADS, smem, stream>>>(p);
+  CUtensorMap dummy{};
+  k<<<static_cast<unsigned>(grid), THREADS, smem, stream>>>(map ? *map : dummy, p);
   return cudaGetLastError();
 }
 
-cudaError_t launch_trsm(const TrsmParams& p, int num_sms, cudaStream_t stream) {
+// map: TMA descriptor of X with a {16 rows, npad columns} SWIZZLE_128B box (instances with
+// NT <= 16 use it when map != nullptr); the others read X with plain coalesced loads.
+cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream) {
   const int NT = npad_for(p.n) / 8;
+  const bool tma = map != nullptr;
   switch (NT) {
-    case 1: return launch_one<1, 4, true, 256>(p, num_sms, stream);
-    case 2: return launch_one<2, 4, true, 256>(p, num_sms, stream);
-    case 4: return launch_one<4, 4, true, 256>(p, num_sms, stream);
-    case 8: return launch_one<8, 4, true, 256>(p, num_sms, stream);
-    case 12: return launch_one<12, 2, true, 256>(p, num_sms, stream);
-    case 16: return launch_one<16, 2, true, 256>(p, num_sms, stream);
-    case 24: return launch_one<24, 1, true, 256>(p, num_sms, stream);
-    case 32: return launch_one<32, 1, false, 256>(p, num_sms, stream);
+    case 1: return launch_one<1, 4, true, 256, false>(p, nullptr, num_sms, stream);
+    case 2: return tma ? launch_one<2, 4, true, 256, true>(p, map, num_sms, stream)
+                       : launch_one<2, 4, true, 256, false>(p, nullptr, num_sms, stream);
+    case 4: return tma ? launch_one<4, 4, true, 256, true>(p, map, num_sms, stream)
+                       : launch_one<4, 4, true, 256, false>(p, nullptr, num_sms, stream);
+    case 8: return tma ? launch_one<8, 4, true, 256, true>(p, map, num_sms, stream)
+                       : launch_one<8, 4, true, 256, false>(p, nullptr, num_sms, stream);
+    case 12: return tma ? launch_one<12, 2, true, 256, true>(p, map, num_sms, stream)
+                        : launch_one<12, 2, true, 256, false>(p, nullptr, num_sms, stream);
+    case 16: return tma ? launch_one<16, 2, true, 256, true>(p, map, num_sms, stream)
+                        : launch_one<16, 2, true, 256, false>(p, nullptr, num_sms, stream);
+    case 24: return launch_one<24, 1, true, 256, false>(p, nullptr, num_sms, stream);
+    case 32: return launch_one<32, 1, false, 256, false>(p, nullptr, num_sms, stream);
     default: return cudaErrorInvalidValue;
   }
 }

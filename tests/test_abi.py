@@ -35,7 +35,7 @@ def test_struct_layout_matches_header():
     assert o.shift_value.offset == 8 and o.norm2_bound.offset == 24 and o.stop_tol.offset == 48
     assert o.m_global.offset == 56 and o.stream.offset == 64 and o.workspace.offset == 80
     assert ctypes.sizeof(o) == 128
-    assert ctypes.sizeof(_abi.Prof) == 80
+    assert ctypes.sizeof(_abi.Prof) == 96
 
 
 def test_default_opts_and_sizes_without_gpu():

@@ -168,7 +168,10 @@ def test_factor_parity(m, n, kappa):
     rg = sq.scqr3_factor(dev(X))
     ro = oracle.scqr3(X)
     _compare(X, rg, ro, kappa)
-    assert [t["shifted"] for t in rg.trace] == [t.shifted for t in ro.trace]
+    if kappa <= 1 / U / (96 * (m * n + n * (n + 1))):   # Alg. 3's proven regime
+        assert [t["shifted"] for t in rg.trace] == [t.shifted for t in ro.trace]
+    else:   # beyond it, breakdown decisions sit within rounding of a threshold: both valid
+        assert rg.trace[0]["shifted"] and ro.trace[0].shifted
 
 
 @gpu
