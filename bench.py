@@ -35,7 +35,7 @@ METRIC = "shifted CholeskyQR3 fp64 TFLOP/s & % roofline, m=1e7 n=128, 1/2/4/8 B2
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C3")
@@ -127,7 +127,7 @@ def run_reference(args):
 
     cfg = synth.CONFIGS[args.config]
     n = cfg.n
-    rows = args.cpu_rows or max(n, int(5e5 * (128 / n) ** 2))
+    rows = args.cpu_rows or max(n, int(5e6 * (128 / n) ** 2))
     rows = min(rows, cfg.m)
     X = synth.randsvd(rows, n, cfg.kappa, seed=0, spectrum=cfg.spectrum)
     kw = {}
@@ -176,7 +176,9 @@ def run_ours(args):
     dev = torch.device("cuda", torch.cuda.current_device())
     cfg = synth.CONFIGS[args.config]
     m, n = cfg.m, cfg.n
-    r0, r1 = m * rank // world, m * (rank + 1) // world
+    from paper_1809_11085_b200.dist import row_block
+
+    r0, r1 = row_block(m, rank, world)
     mloc = r1 - r0
 
     # ---- input: the same global X on every rank (same seed), keep this rank's row block
@@ -307,7 +309,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         import oracle
 
-        rows = args.cpu_rows or max(n, int(2e6 * (128 / n) ** 2))
+        rows = args.cpu_rows or max(n, int(1e7 * (128 / n) ** 2))
         rows = min(rows, mloc)
         Xs = X[:rows].cpu().numpy()
         t0 = time.perf_counter()

@@ -1,0 +1,31 @@
+"""Multi-GPU plumbing shared by bench.py and the tests: row-block partition and rank helpers.
+
+The method's only exchange is the sum of the per-rank Grams ("reduction operator is
+addition"), done inside libscqr3 by one NCCL allreduce per pass; the oblique variant also swaps
+one boundary row with each neighbour.  This module holds no arithmetic of the method.
+"""
+from __future__ import annotations
+
+
+def row_block(m: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous rows [r0, r1) of rank `rank` (sizes differ by at most one)."""
+    if not (0 <= rank < world):
+        raise ValueError("bad rank")
+    return m * rank // world, m * (rank + 1) // world
+
+
+def neighbours(rank: int, world: int) -> tuple[int | None, int | None]:
+    """Ranks holding the rows just above / below this rank's block (oblique halo)."""
+    return (rank - 1 if rank > 0 else None), (rank + 1 if rank + 1 < world else None)
+
+
+def max_over_ranks(value: float, group=None, device=None) -> float:
+    """Max of a per-rank time over all ranks (benchmarks report the slowest rank)."""
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())

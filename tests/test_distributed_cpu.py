@@ -1,0 +1,119 @@
+"""World-size-2 gloo tests (CPU) of the multi-rank decomposition that libscqr3 runs over NCCL:
+row-block partition, Gram allreduce (sum of per-rank Grams), replicated Cholesky on identical
+bits, local TRSM, oblique one-row halo exchange, and max-over-ranks timing.  The arithmetic of
+each rank is the oracle's; only the exchange pattern is under test here."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+from paper_1809_11085_b200 import dist as pdist  # noqa: E402
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import oracle
+    import synth
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m, n = 3001, 12
+        X = synth.randsvd(m, n, 1e12, seed=5)
+        d, e = synth.tridiag_b(m, seed=5)
+        r0, r1 = pdist.row_block(m, rank, world)
+        Xl = np.asfortranarray(X[r0:r1])
+        res = {}
+        # ---- standard inner product: Gram allreduce + replicated Cholesky + local TRSM
+        Q = Xl.copy(order="F")
+        R = np.eye(n)
+        for k in range(3):
+            A = torch.from_numpy(oracle.gram(Q))
+            dist.all_reduce(A)                                   # the one exchange per pass
+            A = A.numpy()
+            s = oracle.shift(m, n, oracle.power_lmax(A) * 1.01) if k == 0 else 0.0   # global m
+            Rt = oracle.cholesky(A, s)
+            Q = oracle.trsm_rows(Q, Rt)
+            R = oracle.trmul(Rt, R)
+        res["R"] = R
+        res["Qrows"] = (r0, Q)
+        # ---- oblique: halo rows from the neighbours give the same rows of Y = B X
+        up, down = pdist.neighbours(rank, world)
+        first, last = torch.from_numpy(Xl[0].copy()), torch.from_numpy(Xl[-1].copy())
+        halo_prev, halo_next = torch.zeros(n, dtype=torch.float64), torch.zeros(n, dtype=torch.float64)
+        ops = []
+        if up is not None:
+            ops += [dist.P2POp(dist.isend, first, up), dist.P2POp(dist.irecv, halo_prev, up)]
+        if down is not None:
+            ops += [dist.P2POp(dist.isend, last, down), dist.P2POp(dist.irecv, halo_next, down)]
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        Y = d[r0:r1, None] * Xl
+        Y[1:] += e[r0:r1 - 1, None] * Xl[:-1]
+        Y[:-1] += e[r0:r1 - 1, None] * Xl[1:]
+        if up is not None:
+            Y[0] += e[r0 - 1] * halo_prev.numpy()
+        if down is not None:
+            Y[-1] += e[r1 - 1] * halo_next.numpy()
+        res["Yrows"] = (r0, Y)
+        res["tmax"] = pdist.max_over_ranks(1.0 + rank)
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_partition_covers_rows_once():
+    for m, w in [(10, 3), (1, 2), (10_000_000, 8), (7, 8)]:
+        blocks = [pdist.row_block(m, r, w) for r in range(w)]
+        assert blocks[0][0] == 0 and blocks[-1][1] == m
+        assert all(blocks[i][1] == blocks[i + 1][0] for i in range(w - 1))
+        sizes = [b - a for a, b in blocks]
+        assert max(sizes) - min(sizes) <= 1
+
+
+def test_two_rank_gloo_decomposition_matches_single_process():
+    import oracle
+    import synth
+
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # replicated Cholesky on identical allreduced Grams -> identical R bits on every rank
+    assert np.array_equal(out[0]["R"], out[1]["R"])
+    m, n = 3001, 12
+    X = synth.randsvd(m, n, 1e12, seed=5)
+    ref = oracle.scqr3(X, max_passes=3, nparts=2)        # the oracle's own 2-rank emulation
+    assert np.max(np.abs(out[0]["R"] - ref.R)) <= 1e-10 * np.max(np.abs(ref.R))
+    Q = np.zeros((m, n))
+    for rank in range(world):
+        r0, Ql = out[rank]["Qrows"]
+        Q[r0:r0 + Ql.shape[0]] = Ql
+    assert oracle.orth_F(Q) <= 10 * n * 2.0 ** -53
+    # halo exchange reproduces the global B X
+    d, e = synth.tridiag_b(m, seed=5)
+    B = np.diag(d) + np.diag(e[:-1], 1) + np.diag(e[:-1], -1)
+    Yg = B @ X
+    for rank in range(world):
+        r0, Yl = out[rank]["Yrows"]
+        assert np.allclose(Yl, Yg[r0:r0 + Yl.shape[0]], rtol=1e-14, atol=1e-12)
+    assert out[0]["tmax"] == out[1]["tmax"] == 2.0
