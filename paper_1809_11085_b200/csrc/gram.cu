@@ -31,12 +31,13 @@ __device__ __forceinline__ void decode_job(int j, int NB, bool full, int& bi, in
   bi = j - c * (c + 1) / 2;
 }
 
-__global__ void __launch_bounds__(32 * 13, 1)
+__global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
     gram_tma_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapY,
                     GramParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-B alignment for SWIZZLE_128B
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // (pointer arithmetic on the shared array itself keeps the shared address space -> LDS)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ncons = blockDim.x / 32 - 1;
   const int group = blockIdx.x % p.groups;

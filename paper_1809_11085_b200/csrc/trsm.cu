@@ -21,19 +21,23 @@
 
 namespace scqr3 {
 
-template <int NT, int A, bool SMEM_B, int THREADS, bool TMA>
+// P = warps sharing one TMA slot (P = 2 when a warp owns 8 rows: the slot is one 16-row box).
+template <int NT, int A, bool SMEM_B, int THREADS, bool TMA, int P = 1>
 __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant__ CUtensorMap mapX, TrsmParams p) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   if (p.st && p.st->code != 0) return;
   constexpr int NF = NT * (NT - 1);
   constexpr int WPB = THREADS / 32;
   constexpr int NPAD = NT * 8;
+  constexpr int RS = 8 * A * P;                            // rows per slot (multiple of 16)
   constexpr uint32_t kBoxBytes = 16u * NPAD * 8u;         // one 16-row TMA box
-  constexpr uint32_t kSlotBytes = kBoxBytes * (A / 2 > 0 ? A / 2 : 1);
+  constexpr uint32_t kSlotBytes = kBoxBytes * (RS / 16);
+  static_assert(!TMA || RS % 16 == 0, "TMA slots hold whole 16-row boxes");
   // layout: [TMA slots (1024-aligned)] [B fragments] [diagonal blocks] [mbarriers]
-  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  // (pointer arithmetic on the shared array itself keeps the shared address space -> LDS)
+  unsigned char* base = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
   unsigned char* slots = base;
-  double* sm = reinterpret_cast<double*>(base + (TMA ? WPB * kSlotBytes : 0));
+  double* sm = reinterpret_cast<double*>(base + (TMA ? (WPB / P) * kSlotBytes : 0));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + (SMEM_B ? NF * 32 : 0) + NT * 72);
   const double* bf;
   const double* db;
@@ -49,42 +53,57 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   if (TMA && threadIdx.x == 0) {
-    for (int w = 0; w < WPB; ++w) mbar_init(&bars[w], 1);
+    for (int w = 0; w < WPB / P; ++w) mbar_init(&bars[w], 1);
     fence_barrier_init();
   }
   __syncthreads();
 
   const long long m = p.m;
   const int n = p.n;
-  const long long ngroups = (m + 8 * A - 1) / (8 * A);
-  const long long stride = static_cast<long long>(gridDim.x) * WPB;
-  unsigned char* slot = slots + warp * kSlotBytes;
-  uint64_t* bar = bars + warp;
+  // work unit = one slot group of RS rows (P warps, 8A rows each)
+  const long long ngroups = (m + RS - 1) / RS;
+  const long long stride = static_cast<long long>(gridDim.x) * (WPB / P);
+  const int sidx = warp / P, sub = warp % P;
+  unsigned char* slot = slots + sidx * kSlotBytes;
+  uint64_t* bar = bars + sidx;
   uint32_t phase = 0;
-  auto issue = [&](long long rg) {  // elected lane: TMA of row group rg into this warp's slot
-    if (TMA && lane == 0 && rg < ngroups) {
+  auto issue = [&](long long rg) {  // elected lane: TMA of slot group rg into this slot
+    if (TMA && sub == 0 && lane == 0 && rg < ngroups) {
       fence_proxy_async();
       mbar_arrive_expect_tx(bar, kSlotBytes);
 #pragma unroll
-      for (int b = 0; b < (A / 2 > 0 ? A / 2 : 1); ++b)
-        tma_load_2d(slot + b * kBoxBytes, &mapX, static_cast<int>(rg * 8 * A + 16 * b), 0, bar);
+      for (int b = 0; b < RS / 16; ++b)
+        tma_load_2d(slot + b * kBoxBytes, &mapX, static_cast<int>(rg * RS + 16 * b), 0, bar);
     }
   };
-  const long long rg0 = static_cast<long long>(blockIdx.x) * WPB + warp;
+  const long long rg0 = static_cast<long long>(blockIdx.x) * (WPB / P) + sidx;
   if (TMA) {
     if (lane == 0) tma_prefetch_desc(&mapX);
     issue(rg0);
   }
 
   for (long long rg = rg0; rg < ngroups; rg += stride) {
-    const long long r0 = rg * 8 * A;
+    const long long r0 = rg * RS + sub * 8 * A;
     double q[A][NT][2];
+    auto store_block = [&](double (&qq)[A][NT][2], int J) {
+#pragma unroll
+      for (int a = 0; a < A; ++a) {
+        const long long row = r0 + 8 * a + g;
+        if (row < m) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int col = 8 * J + 2 * t + h;
+            if (col < n) __stcs(p.Q + row + static_cast<long long>(col) * p.ldq, qq[a][J][h]);
+          }
+        }
+      }
+    };
     if (TMA) {
       mbar_wait(bar, phase);
       phase ^= 1u;
 #pragma unroll
       for (int a = 0; a < A; ++a) {
-        const int r = 8 * a + g;  // row inside the slot
+        const int r = sub * 8 * A + 8 * a + g;  // row inside the slot
         const unsigned char* box = slot + (r >> 4) * kBoxBytes;
 #pragma unroll
         for (int J = 0; J < NT; ++J)
@@ -106,115 +125,107 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
           }
       }
     }
-    // Software pipeline over column blocks: iteration J solves the diagonal block of J-1 (a
-    // latency-bound shuffle chain) interleaved with block J's tensor-core updates from blocks
-    // 0..J-2 (independent of it), then applies block J-1's update to block J.  Even and odd
-    // k-steps accumulate separately to halve the DMMA dependency chains.
-    double odd[A][2];
+    // Software pipeline over column blocks: iteration J gives block J its last update (from
+    // block J-1), then solves block J's diagonal block (a latency-bound shuffle chain)
+    // interleaved with block J-1's updates to the later blocks, which do not depend on it.
+    // (Right-looking order: block K receives one k-step pair per iteration, so no DMMA
+    //  accumulator chain is longer than two, and the updates from block J-1 to blocks > J are
+    //  independent MMAs that fill the pipe while block J's shuffle chain runs.)
+#ifdef SCQR3_TRSM_NOLDS_EXPERIMENT
+    const double bfake = bf[lane];
+    auto bfrag = [&](int K, int s) -> double { return bfake * (K + s); };
+#else
+    auto bfrag = [&](int K, int s) -> double {  // -R~ fragment of k-step s for target block K
+      return SMEM_B ? bf[(K * (K - 1) + s) * 32 + lane] : __ldg(bf + (K * (K - 1) + s) * 32 + lane);
+    };
+#endif
 #pragma unroll
-    for (int J = 0; J <= NT; ++J) {
+    for (int J = 0; J < NT; ++J) {
       if (TMA && J == (NT > 1 ? 1 : 0)) {
         // every lane's slot reads have been consumed by now: refill the slot with the next group
-        __syncwarp();
+        if (P > 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + sidx), "r"(32 * P) : "memory");
+        else __syncwarp();
         issue(rg + stride);
       }
-      const bool has_acc = J < NT, has_solve = J >= 1;
-      const int nearly = (has_acc && J >= 1) ? 2 * (J - 1) : 0;  // k-steps over blocks 0..J-2
+      // (i) block J's last update, from block J-1 (final since the previous iteration)
+      if (J >= 1) {
 #pragma unroll
-      for (int a = 0; a < A; ++a) odd[a][0] = odd[a][1] = 0.0;
-      int s = 0;
-      const double* D = db + (J - 1) * 72;
+        for (int s = 2 * (J - 1); s < 2 * J; ++s) {
+          const double b = bfrag(J, s);
+#pragma unroll
+          for (int a = 0; a < A; ++a) dmma(q[a][J][0], q[a][J][1], q[a][J - 1][s & 1], b);
+        }
+      }
+      // (ii) diagonal block J: right-looking substitution inside each quad on the unscaled
+      // values v (v_j -= v_c * (r_cj / r_cc), strict upper only, zeros elsewhere), interleaved
+      // with the updates C_K += Q_{J-1} (-R~_{J-1,K}) of the later blocks K = J+1..NT-1
+      const int nup = J >= 1 ? NT - 1 - J : 0;
+      int u = 0;
+      const double* D = db + J * 72;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        if (has_solve) {
-          // diagonal block J-1: right-looking substitution inside each quad on the unscaled
-          // values v (v_j -= v_c * (r_cj / r_cc), strict upper only, zeros elsewhere)
-          const double2 rc = *reinterpret_cast<const double2*>(D + c * 8 + 2 * t);
-          const int owner = (lane & ~3) | (c >> 1);
-#pragma unroll
-          for (int a = 0; a < A; ++a) {
-            const double vc = __shfl_sync(0xffffffffu, q[a][J - 1][c & 1], owner);
-            q[a][J - 1][0] = fma(-vc, rc.x, q[a][J - 1][0]);
-            q[a][J - 1][1] = fma(-vc, rc.y, q[a][J - 1][1]);
-          }
-        }
-        // a share of block J's updates from blocks 0..J-2: C_J += Q_{<J-1} (-R~_{<J-1,J})
-#pragma unroll
-        for (; s < nearly * (c + 1) / 8; ++s) {
-          const double b = SMEM_B ? bf[(J * (J - 1) + s) * 32 + lane] : __ldg(bf + (J * (J - 1) + s) * 32 + lane);
-#pragma unroll
-          for (int a = 0; a < A; ++a) {
-            if (s & 1) dmma(odd[a][0], odd[a][1], q[a][s >> 1][s & 1], b);
-            else dmma(q[a][J][0], q[a][J][1], q[a][s >> 1][s & 1], b);
-          }
-        }
-      }
-      if (has_solve) {
-        // q_j = v_j / r_jj as a multiply by the reciprocal (reading D11)
-        const double2 ri = *reinterpret_cast<const double2*>(D + 64 + 2 * t);
+        const double2 rc = *reinterpret_cast<const double2*>(D + c * 8 + 2 * t);
+        const int owner = (lane & ~3) | (c >> 1);
+#ifndef SCQR3_TRSM_NODIAG_EXPERIMENT
 #pragma unroll
         for (int a = 0; a < A; ++a) {
-          q[a][J - 1][0] *= ri.x;
-          q[a][J - 1][1] *= ri.y;
+          const double vc = __shfl_sync(0xffffffffu, q[a][J][c & 1], owner);
+          q[a][J][0] = fma(-vc, rc.x, q[a][J][0]);
+          q[a][J][1] = fma(-vc, rc.y, q[a][J][1]);
         }
-      }
-      if (has_acc) {
-        // block J-1 (now final) -> block J
+#else
+        (void)owner;
+        (void)rc;
+#endif
 #pragma unroll
-        for (s = nearly; s < 2 * J; ++s) {
-          const double b = SMEM_B ? bf[(J * (J - 1) + s) * 32 + lane] : __ldg(bf + (J * (J - 1) + s) * 32 + lane);
+        for (; u < nup * (c + 1) / 8; ++u) {
+          const int K = J + 1 + u;
 #pragma unroll
-          for (int a = 0; a < A; ++a) {
-            if (s & 1) dmma(odd[a][0], odd[a][1], q[a][s >> 1][s & 1], b);
-            else dmma(q[a][J][0], q[a][J][1], q[a][s >> 1][s & 1], b);
-          }
-        }
-        if (J > 0) {
+          for (int s = 2 * (J - 1); s < 2 * J; ++s) {
+            const double b = bfrag(K, s);
 #pragma unroll
-          for (int a = 0; a < A; ++a) {
-            q[a][J][0] += odd[a][0];
-            q[a][J][1] += odd[a][1];
+            for (int a = 0; a < A; ++a) dmma(q[a][K][0], q[a][K][1], q[a][J - 1][s & 1], b);
           }
         }
       }
+      // (iii) q_j = v_j / r_jj as a multiply by the reciprocal (reading D11)
+      const double2 ri = *reinterpret_cast<const double2*>(D + 64 + 2 * t);
+#pragma unroll
+      for (int a = 0; a < A; ++a) {
+        q[a][J][0] *= ri.x;
+        q[a][J][1] *= ri.y;
+      }
+      // block J-1 had its last use above: store it now (spreads the stores over the solve
+      // instead of one burst per row group that fills the LSU queue)
+      if (J >= 1) store_block(q, J - 1);
     }
+    store_block(q, NT - 1);
     if (TMA && NT <= 1) {
-      __syncwarp();
+      if (P > 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + sidx), "r"(32 * P) : "memory");
+      else __syncwarp();
       issue(rg + stride);
-    }
-#pragma unroll
-    for (int a = 0; a < A; ++a) {
-      const long long row = r0 + 8 * a + g;
-      if (row < m) {
-#pragma unroll
-        for (int J = 0; J < NT; ++J)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int col = 8 * J + 2 * t + h;
-            if (col < n) __stcs(p.Q + row + static_cast<long long>(col) * p.ldq, q[a][J][h]);
-          }
-      }
     }
   }
 }
 
-template <int NT, int A, bool SMEM_B, int THREADS, bool TMA>
+template <int NT, int A, bool SMEM_B, int THREADS, bool TMA, int P = 1>
 static cudaError_t launch_one(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream) {
   constexpr int NF = NT * (NT - 1);
   constexpr int WPB = THREADS / 32;
-  constexpr size_t kSlot = 16u * NT * 8 * 8 * (A / 2 > 0 ? A / 2 : 1);
-  const size_t smem = 1024 + (TMA ? WPB * kSlot : 0) + static_cast<size_t>((SMEM_B ? NF * 32 : 0) + NT * 72) * 8 +
-                      WPB * 8;
-  auto k = trsm_kernel<NT, A, SMEM_B, THREADS, TMA>;
+  constexpr int RS = 8 * A * P;
+  constexpr size_t kSlot = 16u * NT * 8 * 8 * (RS / 16 > 0 ? RS / 16 : 1);
+  const size_t smem = 1024 + (TMA ? (WPB / P) * kSlot : 0) +
+                      static_cast<size_t>((SMEM_B ? NF * 32 : 0) + NT * 72) * 8 + WPB * 8;
+  auto k = trsm_kernel<NT, A, SMEM_B, THREADS, TMA, P>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  const long long groups = (p.m + 8 * A - 1) / (8 * A);
+  const long long groups = (p.m + RS - 1) / RS;
   long long grid = static_cast<long long>(num_sms) * per_sm;
-  const long long need = (groups + WPB - 1) / WPB;
+  const long long need = (groups + WPB / P - 1) / (WPB / P);
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
   CUtensorMap dummy{};
@@ -237,8 +248,13 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
                        : launch_one<8, 4, true, 256, false>(p, nullptr, num_sms, stream);
     case 12: return tma ? launch_one<12, 2, true, 256, true>(p, map, num_sms, stream)
                         : launch_one<12, 2, true, 256, false>(p, nullptr, num_sms, stream);
+#if SCQR3_TRSM16_PAIRS
+    case 16: return tma ? launch_one<16, 1, true, 512, true, 2>(p, map, num_sms, stream)
+                        : launch_one<16, 2, true, 256, false>(p, nullptr, num_sms, stream);
+#else
     case 16: return tma ? launch_one<16, 2, true, 256, true>(p, map, num_sms, stream)
                         : launch_one<16, 2, true, 256, false>(p, nullptr, num_sms, stream);
+#endif
     case 24: return launch_one<24, 1, true, 256, false>(p, nullptr, num_sms, stream);
     case 32: return launch_one<32, 1, false, 256, false>(p, nullptr, num_sms, stream);
     default: return cudaErrorInvalidValue;
