@@ -87,36 +87,42 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
   }
 
   // ---------------- consumers (job table: host-balanced over the four SM sub-partitions)
+  // Every job is one "part": two tile rows (rows 2*part, 2*part+1 of the 4x4-tile block) by
+  // the block's four tile columns -- 8 DMMA per k-step for an off-diagonal block, 7 (top) or 3
+  // (bottom) for a diagonal block of the symmetric Gram.  Small parts keep the accumulators at
+  // 32 registers and let the host balance the sub-partitions exactly.
   const int cw = warp - 1;
-  const int job = p.warp_job[group * kMaxConsumers + cw];
-  const bool active = job >= 0;
+  const int code = p.warp_job[group * kMaxConsumers + cw];  // 2 * block + part, -1 = idle
+  const bool active = code >= 0;
+  const int part = active ? (code & 1) : 0;
   int bi = 0, bj = 0;
-  if (active) decode_job(job, p.NB, full, bi, bj);
+  if (active) decode_job(code >> 1, p.NB, full, bi, bj);
   const bool diag = !full && bi == bj;
   const int NT = p.NT;
   const bool edge = (bi + 1) * kJobTiles > NT || (bj + 1) * kJobTiles > NT;
+  const int rr0 = 2 * part;  // first tile row of the part within the block
   const int g = lane >> 2, t = lane & 3;
 
-  double acc[kJobTiles][kJobTiles][2];
+  double acc[2][kJobTiles][2];
 #pragma unroll
-  for (int a = 0; a < kJobTiles; ++a)
+  for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int b = 0; b < kJobTiles; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
-  // per-lane smem offsets (without the k-step part) for this job's tile columns
-  uint32_t offA[kJobTiles], offB[kJobTiles];
+  // per-lane smem offsets (without the k-step part) of the part's tile rows / the block's columns
+  uint32_t offA[2], offB[kJobTiles];
 #pragma unroll
-  for (int a = 0; a < kJobTiles; ++a) {
-    offA[a] = static_cast<uint32_t>(8 * min(bi * kJobTiles + a, NT - 1) + g) * 128u;
-    offB[a] = static_cast<uint32_t>(8 * min(bj * kJobTiles + a, NT - 1) + g) * 128u;
-  }
+  for (int a = 0; a < 2; ++a) offA[a] = static_cast<uint32_t>(8 * min(bi * kJobTiles + rr0 + a, NT - 1) + g) * 128u;
+#pragma unroll
+  for (int b = 0; b < kJobTiles; ++b) offB[b] = static_cast<uint32_t>(8 * min(bj * kJobTiles + b, NT - 1) + g) * 128u;
   // 16-byte chunk of this lane's k slot per k-step s: rows {2s, 2s+1, 2s+8, 2s+9}[t] -> the
   // chunk index (row>>1) = s + 4*(t>>1) XOR (column & 7) = g (SWIZZLE_128B), conflict free
   uint32_t inner[4];
 #pragma unroll
   for (int s = 0; s < 4; ++s)
     inner[s] = ((((s + 4 * (t >> 1)) ^ g) & 7u) << 4) + ((t & 1) << 3);
-  const int kind = !active ? 3 : edge ? 2 : diag ? 1 : 0;
+  // 0 off-diagonal interior, 1 diagonal top part, 2 diagonal bottom part, 3 edge, 4 idle
+  const int kind = !active ? 4 : edge ? 3 : diag ? 1 + part : 0;
 
   int st = 0;
   uint32_t ph = 0;
@@ -125,47 +131,55 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
     const unsigned char* srcA = stages + static_cast<size_t>(st) * nsrc * stage_bytes;
     const unsigned char* srcB = full ? srcA + stage_bytes : srcA;
     if (kind == 0) {
-      // full 4x4 off-diagonal block: 8 fragment loads, 16 DMMA per k-step
+      // 2 x 4 tiles of an off-diagonal block: 6 fragment loads, 8 DMMA per k-step
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
-        double fa[kJobTiles], fb[kJobTiles];
+        double fa[2], fb[kJobTiles];
 #pragma unroll
-        for (int a = 0; a < kJobTiles; ++a) {
-          fa[a] = *reinterpret_cast<const double*>(srcA + offA[a] + inner[s]);
-          fb[a] = *reinterpret_cast<const double*>(srcB + offB[a] + inner[s]);
-        }
+        for (int a = 0; a < 2; ++a) fa[a] = *reinterpret_cast<const double*>(srcA + offA[a] + inner[s]);
 #pragma unroll
-        for (int a = 0; a < kJobTiles; ++a)
+        for (int b = 0; b < kJobTiles; ++b) fb[b] = *reinterpret_cast<const double*>(srcB + offB[b] + inner[s]);
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
 #pragma unroll
           for (int b = 0; b < kJobTiles; ++b) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
       }
     } else if (kind == 1) {
-      // diagonal block of the symmetric Gram: A and B fragments coincide, 10 DMMA per k-step
+      // diagonal block, tile rows 0-1: tiles (0,0..3), (1,1..3); A fragments are B fragments
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
-        double fa[kJobTiles];
+        double fb[kJobTiles];
 #pragma unroll
-        for (int a = 0; a < kJobTiles; ++a) fa[a] = *reinterpret_cast<const double*>(srcA + offA[a] + inner[s]);
+        for (int b = 0; b < kJobTiles; ++b) fb[b] = *reinterpret_cast<const double*>(srcB + offB[b] + inner[s]);
 #pragma unroll
-        for (int a = 0; a < kJobTiles; ++a)
+        for (int a = 0; a < 2; ++a)
 #pragma unroll
-          for (int b = a; b < kJobTiles; ++b) dmma(acc[a][b][0], acc[a][b][1], fa[a], fa[b]);
+          for (int b = a; b < kJobTiles; ++b) dmma(acc[a][b][0], acc[a][b][1], fb[a], fb[b]);
       }
     } else if (kind == 2) {
-      // block touching the padded edge (n not a multiple of 32): per-tile validity
+      // diagonal block, tile rows 2-3: tiles (2,2), (2,3), (3,3)
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
-        double fa[kJobTiles], fb[kJobTiles];
+        const double f2 = *reinterpret_cast<const double*>(srcB + offB[2] + inner[s]);
+        const double f3 = *reinterpret_cast<const double*>(srcB + offB[3] + inner[s]);
+        dmma(acc[0][2][0], acc[0][2][1], f2, f2);
+        dmma(acc[0][3][0], acc[0][3][1], f2, f3);
+        dmma(acc[1][3][0], acc[1][3][1], f3, f3);
+      }
+    } else if (kind == 3) {
+      // part of a block touching the padded edge (n not a multiple of 32): per-tile validity
 #pragma unroll
-        for (int a = 0; a < kJobTiles; ++a) {
-          fa[a] = *reinterpret_cast<const double*>(srcA + offA[a] + inner[s]);
-          fb[a] = *reinterpret_cast<const double*>(srcB + offB[a] + inner[s]);
-        }
+      for (int s = 0; s < 4; ++s) {
+        double fa[2], fb[kJobTiles];
 #pragma unroll
-        for (int a = 0; a < kJobTiles; ++a)
+        for (int a = 0; a < 2; ++a) fa[a] = *reinterpret_cast<const double*>(srcA + offA[a] + inner[s]);
+#pragma unroll
+        for (int b = 0; b < kJobTiles; ++b) fb[b] = *reinterpret_cast<const double*>(srcB + offB[b] + inner[s]);
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
 #pragma unroll
           for (int b = 0; b < kJobTiles; ++b) {
-            const bool valid = (bi * kJobTiles + a < NT) && (bj * kJobTiles + b < NT) && (!diag || a <= b);
+            const bool valid = (bi * kJobTiles + rr0 + a < NT) && (bj * kJobTiles + b < NT) && (!diag || rr0 + a <= b);
             if (valid) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
           }
       }
@@ -182,11 +196,11 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
   // ---------------- write this CTA's partial tiles (8x8 row-major per tile)
   double* out = p.partials + static_cast<size_t>(chunk) * p.tiles_per_partial * 64;
 #pragma unroll
-  for (int a = 0; a < kJobTiles; ++a)
+  for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int b = 0; b < kJobTiles; ++b) {
-      const int TI = bi * kJobTiles + a, TJ = bj * kJobTiles + b;
-      const bool valid = (TI < NT) && (TJ < NT) && (!diag || a <= b);
+      const int TI = bi * kJobTiles + rr0 + a, TJ = bj * kJobTiles + b;
+      const bool valid = (TI < NT) && (TJ < NT) && (!diag || rr0 + a <= b);
       if (!valid) continue;
       const size_t tid = full ? static_cast<size_t>(TI) * NT + TJ : static_cast<size_t>(TJ) * (TJ + 1) / 2 + TI;
       double2 v = make_double2(acc[a][b][0], acc[a][b][1]);

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "scqr3.h"
 #include "scqr3_dev.cuh"
@@ -241,12 +242,13 @@ int encode_map(Ctx* c, CUtensorMap* map, const double* base, int64_t m, int64_t 
   return SCQR3_OK;
 }
 
-// Assign the Gram jobs of each group to consumer warps so that the DMMA work of the four SM
-// sub-partitions (warp w of the CTA runs on sub-partition w % 4; consumer c is warp c + 1) is
-// balanced: longest job first onto the least-loaded sub-partition with a free warp.
-void assign_gram_jobs(GramParams& gp, int jobs, int groups, int ncons, bool oblique) {
-  auto weight = [&](int j) {
-    int bi, bj;
+// Gram jobs for the consumer warps.  Job codes: 2*block + part (tile rows 2*part, 2*part+1 of a 4x4-tile block: 8 tiles off the
+// diagonal, 7 / 3 on it), assigned longest first to the least-loaded SM sub-partition (warp w of
+// the CTA runs on sub-partition w % 4; consumer c is warp c + 1).  Returns the number of groups
+// (CTAs sharing a row chunk) and sets *ncons_out.
+int assign_gram_jobs(GramParams& gp, bool oblique, int* ncons_out) {
+  const int nblocks = oblique ? gp.NB * gp.NB : gp.NB * (gp.NB + 1) / 2;
+  auto coords = [&](int j, int& bi, int& bj) {
     if (oblique) {
       bi = j / gp.NB;
       bj = j % gp.NB;
@@ -256,32 +258,47 @@ void assign_gram_jobs(GramParams& gp, int jobs, int groups, int ncons, bool obli
       bj = c;
       bi = j - c * (c + 1) / 2;
     }
+  };
+  auto weight = [&](int code) {
+    int bi, bj;
+    coords(code >> 1, bi, bj);
+    const int r0 = 2 * (code & 1);
     int w = 0;
-    for (int a = 0; a < kJobTiles; ++a)
+    for (int a = r0; a < r0 + 2; ++a)
       for (int b = 0; b < kJobTiles; ++b)
         if (bi * kJobTiles + a < gp.NT && bj * kJobTiles + b < gp.NT && (oblique || bi != bj || a <= b)) ++w;
     return w;
   };
+  std::vector<int> codes;  // job code = 2 * block + part (tile rows 2*part, 2*part+1)
+  for (int j = 0; j < nblocks; ++j)
+    for (int part = 0; part < 2; ++part) {
+      const int code = 2 * j + part;
+      if (weight(code) > 0) codes.push_back(code);
+    }
+  const int jobs = static_cast<int>(codes.size());
+  const int groups = (jobs + kMaxConsumers - 1) / kMaxConsumers;
+  int ncons = 0;
+  for (int g = 0; g < groups; ++g) ncons = std::max(ncons, jobs * (g + 1) / groups - jobs * g / groups);
   for (int i = 0; i < kMaxGroups * kMaxConsumers; ++i) gp.warp_job[i] = -1;
-  for (int g = 0; g < groups; ++g) {
+  for (int g = 0; g < groups && g < kMaxGroups; ++g) {
     const int j0 = jobs * g / groups, j1 = jobs * (g + 1) / groups;
-    int order[kMaxConsumers], nj = 0;
-    for (int j = j0; j < j1; ++j) order[nj++] = j;
-    std::stable_sort(order, order + nj, [&](int x, int y) { return weight(x) > weight(y); });
+    std::vector<int> order(codes.begin() + j0, codes.begin() + j1);
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return weight(x) > weight(y); });
     int load[4] = {0, 0, 0, 0};
     bool used[kMaxConsumers] = {};
-    for (int k = 0; k < nj; ++k) {
+    for (int code : order) {
       int best = -1;
       for (int w = 0; w < ncons; ++w) {
         if (used[w]) continue;
-        const int sp = (w + 1) & 3;
-        if (best < 0 || load[sp] < load[(best + 1) & 3]) best = w;
+        if (best < 0 || load[(w + 1) & 3] < load[(best + 1) & 3]) best = w;
       }
       used[best] = true;
-      load[(best + 1) & 3] += weight(order[k]);
-      gp.warp_job[g * kMaxConsumers + best] = order[k];
+      load[(best + 1) & 3] += weight(code);
+      gp.warp_job[g * kMaxConsumers + best] = code;
     }
   }
+  *ncons_out = ncons;
+  return groups;
 }
 
 // Gram of the m x n block at src into w.tiles (packed upper tiles; oblique: sym(Q^T Y) and ||Q||_F^2)
@@ -316,13 +333,10 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   gp.npad = L.npad;
   gp.oblique = oblique ? 1 : 0;
   gp.tiles_per_partial = static_cast<int>(L.tiles_part);
-  const int jobs = oblique ? gp.NB * gp.NB : gp.NB * (gp.NB + 1) / 2;
-  const int groups = (jobs + kMaxConsumers - 1) / kMaxConsumers;
+  int ncons = 0;
+  const int groups = assign_gram_jobs(gp, oblique, &ncons);
   if (groups > kMaxGroups) return fail("internal: too many Gram job groups");
   gp.groups = groups;
-  int ncons = 0;
-  for (int g = 0; g < groups; ++g) ncons = std::max(ncons, jobs * (g + 1) / groups - jobs * g / groups);
-  assign_gram_jobs(gp, jobs, groups, ncons, oblique);
   const int threads = 32 * (1 + ncons);
   const int nsrc = oblique ? 2 : 1;
   const size_t stage_bytes = static_cast<size_t>(L.npad) * 128;

@@ -9,7 +9,7 @@ namespace scqr3 {
 
 struct DevStatus;
 
-constexpr int kMaxConsumers = 11;   // consumer warps per Gram CTA (+1 producer = 384 threads)
+constexpr int kMaxConsumers = 20;   // consumer warps per Gram CTA (+1 producer = 672 threads)
 constexpr int kMaxGroups = 8;       // job groups (CTAs sharing one row chunk)
 
 struct GramParams {
