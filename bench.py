@@ -39,6 +39,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C3")
+    ap.add_argument("--m", type=int, default=0, help="override the config's m (exploration only)")
     ap.add_argument("--cpu-rows", type=int, default=0, help="rows of the oracle's bounded sample")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
@@ -175,7 +176,7 @@ def run_ours(args):
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
     cfg = synth.CONFIGS[args.config]
-    m, n = cfg.m, cfg.n
+    m, n = (args.m or cfg.m), cfg.n
     from paper_1809_11085_b200.dist import row_block
 
     r0, r1 = row_block(m, rank, world)

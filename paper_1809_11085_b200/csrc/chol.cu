@@ -31,10 +31,9 @@ namespace scqr3 {
 
 namespace {
 constexpr int kThreads = 256;
-// 16-column panels: the unrolled register code of one panel step stays resident in the
-// instruction caches (a 32-column panel's straight-line code did not, and this single-CTA
-// kernel then ran instruction-fetch bound).
-constexpr int kPanel = 16;
+// 8-column panels: the diagonal block (36 doubles) fits one thread's registers, and the
+// unrolled code of a panel step stays resident in the instruction caches.
+constexpr int kPanel = 8;
 constexpr unsigned kFull = 0xffffffffu;
 __device__ long long g_phase[2];  // diagnostics: cycles in panel steps (a) and (b) of the last factor
 
@@ -75,8 +74,12 @@ __device__ __forceinline__ void load_W(const CholParams& p, double* W, int ldw) 
 // Power iteration from the all-ones vector on sc*A (sc = exact power of two with sc*trace <= 1,
 // so the unnormalised iterates neither overflow nor need a reduction per step), then the
 // Rayleigh quotient.  Same iterate directions as the normalised iteration (reading D2).
-__device__ __noinline__ double power_lmax(const double* W, int ldw, int n, int iters, double trace, double (*ybuf)[kMaxN],
-                             double* red) {
+// (SMEM: W is the dynamic shared-memory array -- addressed as such so loads are LDS.)
+template <bool SMEM>
+__device__ __noinline__ double power_lmax(const double* Wg, int ldw, int n, int iters, double trace,
+                                          double (*ybuf)[kMaxN], double* red) {
+  extern __shared__ double smdyn[];
+  const double* W = SMEM ? smdyn : Wg;
   if (!(trace > 0.0) || !isfinite(trace)) return 0.0;
   const double sc = ldexp(1.0, -(ilogb(trace) + 1));
   int tpr = 1;
@@ -108,8 +111,11 @@ __device__ __noinline__ double power_lmax(const double* W, int ldw, int n, int i
 // breakdown pivot (value in *pv_out).  On success the upper triangle of W holds R~.
 // (__noinline__: one copy of this heavily unrolled code instead of one per call site keeps the
 //  kernel's instruction footprint small enough for the instruction caches.)
-__device__ __noinline__ int factor(double* W, int ldw, int n, double s, bool add_shift, double* pv_out,
-                                      int* sflag, double* sval, double* rinv) {
+template <bool SMEM>
+__device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool add_shift, double* pv_out,
+                                   int* sflag, double* sval, double* rinv) {
+  extern __shared__ double smdyn[];
+  double* W = SMEM ? smdyn : Wg;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (add_shift)
     for (int i = tid; i < n; i += kThreads) W[i * ldw + i] = W[i * ldw + i] + s;
@@ -118,40 +124,43 @@ __device__ __noinline__ int factor(double* W, int ldw, int n, double s, bool add
   for (int k0 = 0; k0 < n; k0 += kPanel) {
     const int kb = min(kPanel, n - k0);
     t0 = clock64();
-    // (a) diagonal block, one warp, lane j = column k0 + j (identity beyond kb)
-    if (warp == 0) {
-      double col[kPanel];
+    // (a) diagonal block on ONE thread, entirely in registers (identity beyond kb): the pivot
+    // chain is rsqrt -> scale -> one FMA per column, with no shuffle or barrier in it, and the
+    // rest of each rank-1 update is independent work that fills the rsqrt latency.
+    if (tid == 0) {
+      double a[kPanel][kPanel];
 #pragma unroll
       for (int r = 0; r < kPanel; ++r)
-        col[r] = (lane < kb && r <= lane) ? W[(k0 + r) * ldw + k0 + lane] : (r == lane ? 1.0 : 0.0);
+#pragma unroll
+        for (int j = r; j < kPanel; ++j)
+          a[r][j] = (j < kb) ? W[(k0 + r) * ldw + k0 + j] : (r == j ? 1.0 : 0.0);
       int bad = 0;
       double badv = 0.0;
 #pragma unroll
       for (int c = 0; c < kPanel; ++c) {
-        if (c < kb) {  // warp-uniform
-          double d = __shfl_sync(kFull, col[c], c);
-          if (!bad && (!(d > 0.0) || !isfinite(d))) {
-            bad = c + 1;
-            badv = d;
-          }
-          if (bad) d = 1.0;  // finish harmlessly; the factor is discarded
-          const double inv = rsqrt(d);
-          if (lane == c) col[c] = d * inv;  // r_cc
-          else if (lane > c) col[c] *= inv;  // r_cj
-          if (c + 1 < kPanel && lane == c + 1) col[c + 1] = fma(-col[c], col[c], col[c + 1]);  // next pivot first
-#pragma unroll
-          for (int i = c + 1; i < kPanel; ++i) {
-            const double ri = __shfl_sync(kFull, col[c], i);
-            if (lane > i || (lane == i && i != c + 1)) col[i] = fma(-ri, col[c], col[i]);
-          }
-          if (lane == c) rinv[c] = inv;
+        double d = a[c][c];
+        if (c < kb && !bad && (!(d > 0.0) || !isfinite(d))) {
+          bad = c + 1;
+          badv = d;
         }
+        if (bad) d = 1.0;  // finish harmlessly; the factor is discarded
+        const double inv = rsqrt(d);
+        a[c][c] = d * inv;  // r_cc
+#pragma unroll
+        for (int j = c + 1; j < kPanel; ++j) a[c][j] *= inv;  // r_cj
+#pragma unroll
+        for (int i = c + 1; i < kPanel; ++i)
+#pragma unroll
+          for (int j = i; j < kPanel; ++j) a[i][j] = fma(-a[c][i], a[c][j], a[i][j]);
+        rinv[c] = inv;
       }
       if (!bad) {
 #pragma unroll
         for (int r = 0; r < kPanel; ++r)
-          if (lane < kb && r <= lane) W[(k0 + r) * ldw + k0 + lane] = col[r];
-      } else if (lane == 0) {
+#pragma unroll
+          for (int j = r; j < kPanel; ++j)
+            if (j < kb) W[(k0 + r) * ldw + k0 + j] = a[r][j];
+      } else {
         *sflag = k0 + bad;
         *sval = badv;
       }
@@ -186,39 +195,45 @@ __device__ __noinline__ int factor(double* W, int ldw, int n, double s, bool add
     }
     __syncthreads();
     t_b += clock64() - t0;
-    // (c) trailing update W_ij -= sum_r r_ri r_rj over k0+kb <= i <= j, 4x4 register tiles
-    const int L = ncols, T4 = (L + 3) >> 2, npairs = T4 * (T4 + 1) / 2;
+    // (c) trailing update W_ij -= sum_r r_ri r_rj over k0+kb <= i <= j.  A warp takes 4 rows
+    // (broadcast loads) and 128 columns (lane + 32b: consecutive, conflict-free loads), so each
+    // lane keeps a 4x4 register tile.
+    const int L = ncols, T4 = (L + 3) >> 2;
     const int base = k0 + kb;
-    for (int pidx = tid; pidx < npairs; pidx += kThreads) {
-      int J = static_cast<int>((sqrt(8.0 * pidx + 1.0) - 1.0) * 0.5);
-      while (J * (J + 1) / 2 > pidx) --J;
-      while ((J + 1) * (J + 2) / 2 <= pidx) ++J;
-      const int I = pidx - J * (J + 1) / 2;  // micro-tile (I, J), I <= J
-      double acc[4][4];
+    for (int I = warp; I < T4; I += kThreads / 32) {
+      const int i0 = 4 * I;
+      for (int jc = i0 & ~31; jc < L; jc += 128) {
+        double acc[4][4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-      for (int r = 0; r < kb; ++r) {
-        const double* pr = W + (k0 + r) * ldw + base;
-        double xi[4], xj[4];
+          for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          xi[a] = (4 * I + a < L) ? pr[4 * I + a] : 0.0;
-          xj[a] = (4 * J + a < L) ? pr[4 * J + a] : 0.0;
+        for (int r = 0; r < kPanel; ++r) {
+          if (r < kb) {
+            const double* pr = W + (k0 + r) * ldw + base;
+            double xi[4], xj[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) xi[a] = (i0 + a < L) ? pr[i0 + a] : 0.0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const int j = jc + lane + 32 * b;
+              xj[b] = (j < L) ? pr[j] : 0.0;
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int b = 0; b < 4; ++b) acc[a][b] = fma(xi[a], xj[b], acc[a][b]);
+          }
         }
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
-          for (int b = 0; b < 4; ++b) acc[a][b] = fma(xi[a], xj[b], acc[a][b]);
+          for (int b = 0; b < 4; ++b) {
+            const int i = i0 + a, j = jc + lane + 32 * b;
+            if (i < L && j < L && i <= j) W[(base + i) * ldw + base + j] -= acc[a][b];
+          }
       }
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int i = 4 * I + a, j = 4 * J + b;
-          if (i < L && j < L && i <= j) W[(base + i) * ldw + base + j] -= acc[a][b];
-        }
     }
     __syncthreads();
   }
@@ -235,8 +250,11 @@ __device__ __forceinline__ double rpad(const double* W, int ldw, int n, int i, i
 }
 
 // TRSM layout (trsm.cu): B fragments of -R~ and scaled diagonal blocks; R~ (column-major) for trmul.
-__device__ __noinline__ void write_outputs(const double* W, int ldw, int n, int NT, double* bfrag,
+template <bool SMEM>
+__device__ __noinline__ void write_outputs(const double* Wg, int ldw, int n, int NT, double* bfrag,
                                               double* dblk, double* Rt) {
+  extern __shared__ double smdyn[];
+  const double* W = SMEM ? smdyn : Wg;
   const int nf = NT * (NT - 1) * 32;
   for (int idx = threadIdx.x; idx < nf; idx += kThreads) {
     const int f = idx >> 5, lane = idx & 31;
@@ -278,7 +296,7 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
 
   if (p.mode == CHOL_ONLY) {
     double pv = 0.0;
-    const int piv = factor(W, ldw, n, p.shift_value, p.shift_value != 0.0, &pv, &sflag, &sval, rinv);
+    const int piv = factor<SMEM>(W, ldw, n, p.shift_value, p.shift_value != 0.0, &pv, &sflag, &sval, rinv);
     for (int j = tid >> 5; j < n; j += kThreads / 32)
       for (int i = tid & 31; i < n; i += 32)
         p.R[i + static_cast<size_t>(j) * n] = (piv == 0 && i <= j) ? W[i * ldw + j] : 0.0;
@@ -317,7 +335,7 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
     } else if (p.norm_mode == SCQR3_NORM_FROBENIUS) {
       N2 = trace;
     } else {
-      N2 = power_lmax(W, ldw, n, p.power_iters, trace, ybuf, red) * 1.01;
+      N2 = power_lmax<SMEM>(W, ldw, n, p.power_iters, trace, ybuf, red) * 1.01;
     }
     if (p.shift_mode == SCQR3_SHIFT_FIXED && p.pass == 1) return p.shift_value;
     if (p.oblique) return 11.0 * (2.0 * mg * sqrt(mg * nn) + nn * (nn + 1.0)) * u * N2 * (*p.nb_dev);
@@ -331,11 +349,11 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
     s = shift_for(N2);
     clk[3] = clock64();
     shifted = 1;
-    piv = factor(W, ldw, n, s, true, &pv, &sflag, &sval, rinv);
+    piv = factor<SMEM>(W, ldw, n, s, true, &pv, &sflag, &sval, rinv);
     if (piv) { bpiv = piv; bval = pv; }
   } else {
     clk[3] = clock64();
-    piv = factor(W, ldw, n, 0.0, false, &pv, &sflag, &sval, rinv);
+    piv = factor<SMEM>(W, ldw, n, 0.0, false, &pv, &sflag, &sval, rinv);
     if (piv) {
       bpiv = piv;
       bval = pv;
@@ -345,14 +363,14 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
         load_W(p, W, ldw);
         s = shift_for(N2);
         shifted = 1;
-        piv = factor(W, ldw, n, s, true, &pv, &sflag, &sval, rinv);
+        piv = factor<SMEM>(W, ldw, n, s, true, &pv, &sflag, &sval, rinv);
         if (piv) { bpiv = piv; bval = pv; }
       }
     }
   }
   const int code = piv ? SCQR3_EBREAKDOWN : SCQR3_OK;
   clk[4] = clock64();
-  if (code == SCQR3_OK) write_outputs(W, ldw, n, p.NT, p.bfrag, p.dblk, p.Rt);
+  if (code == SCQR3_OK) write_outputs<SMEM>(W, ldw, n, p.NT, p.bfrag, p.dblk, p.Rt);
   if (tid == 0) {
     DevStatus st{};
     st.code = code;

@@ -21,6 +21,10 @@
 
 namespace scqr3 {
 
+#ifndef SCQR3_TRSM16_THREADS
+#define SCQR3_TRSM16_THREADS 256
+#endif
+
 // P = warps sharing one TMA slot (P = 2 when a warp owns 8 rows: the slot is one 16-row box).
 template <int NT, int A, bool SMEM_B, int THREADS, bool TMA, int P = 1>
 __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant__ CUtensorMap mapX, TrsmParams p) {
@@ -252,7 +256,7 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
     case 16: return tma ? launch_one<16, 1, true, 512, true, 2>(p, map, num_sms, stream)
                         : launch_one<16, 2, true, 256, false>(p, nullptr, num_sms, stream);
 #else
-    case 16: return tma ? launch_one<16, 2, true, 256, true>(p, map, num_sms, stream)
+    case 16: return tma ? launch_one<16, 2, true, SCQR3_TRSM16_THREADS, true>(p, map, num_sms, stream)
                         : launch_one<16, 2, true, 256, false>(p, nullptr, num_sms, stream);
 #endif
     case 24: return launch_one<24, 1, true, 256, false>(p, nullptr, num_sms, stream);
