@@ -237,6 +237,148 @@ static cudaError_t launch_one(const TrsmParams& p, const CUtensorMap* map, int n
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------------------------
+// Wide TRSM (n in (192, 256]): -R~'s B fragments (254 KB at n=256) do not fit shared memory,
+// so the target column blocks are processed in phases whose fragments do; the next phase's
+// fragments stream into the second buffer with cp.async while the current phase computes.
+// Each warp owns 8 rows (q: 64 doubles).  Per phase [K0, K1): (i) the updates of its targets
+// from all earlier blocks (a dependency-free DMMA stream, targets interleaved), then (ii) the
+// right-looking triangular part inside the phase, as in trsm_kernel.
+struct Phases32 {
+  static constexpr int P = 4;
+  __host__ __device__ static constexpr int b(int i) { return i == 0 ? 0 : i == 1 ? 16 : i == 2 ? 22 : i == 3 ? 27 : 32; }
+};
+constexpr int phase_frags(int k0, int k1) { return k1 * (k1 - 1) - k0 * (k0 - 1); }
+constexpr int kMaxPhaseFrags32 = 290;  // max over Phases32 of phase_frags (27..32)
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// One phase [K0, K1) of the wide TRSM for one warp's 8 rows; every index is compile-time.
+template <int PH>
+__device__ __forceinline__ void phase32(double (&q)[32][2], const double* __restrict__ cur,
+                                        const double* __restrict__ db, int lane, int t, bool rok,
+                                        long long row, const TrsmParams& p) {
+  constexpr int K0 = Phases32::b(PH), K1 = Phases32::b(PH + 1);
+  auto frag = [&](int K, int s) { return cur[(K * (K - 1) - K0 * (K0 - 1) + s) * 32 + lane]; };
+  // (i) updates from the blocks of earlier phases, targets interleaved
+#pragma unroll
+  for (int s = 0; s < 2 * K0; ++s)
+#pragma unroll
+    for (int K = K0; K < K1; ++K) dmma(q[K][0], q[K][1], q[s >> 1][s & 1], frag(K, s));
+  // (ii) triangular part inside the phase (right-looking, as in trsm_kernel)
+#pragma unroll
+  for (int J = K0; J < K1; ++J) {
+    if (J > K0) {
+#pragma unroll
+      for (int s = 2 * (J - 1); s < 2 * J; ++s) dmma(q[J][0], q[J][1], q[J - 1][s & 1], frag(J, s));
+    }
+    const int nup = J > K0 ? K1 - 1 - J : 0;
+    const double* D = db + J * 72;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double2 rc = *reinterpret_cast<const double2*>(D + c * 8 + 2 * t);
+      const double vc = __shfl_sync(0xffffffffu, q[J][c & 1], (lane & ~3) | (c >> 1));
+      q[J][0] = fma(-vc, rc.x, q[J][0]);
+      q[J][1] = fma(-vc, rc.y, q[J][1]);
+#pragma unroll
+      for (int u = nup * c / 8; u < nup * (c + 1) / 8; ++u) {
+        const int K = J + 1 + u;
+#pragma unroll
+        for (int s = 2 * (J - 1); s < 2 * J; ++s) dmma(q[K][0], q[K][1], q[J - 1][s & 1], frag(K, s));
+      }
+    }
+    const double2 ri = *reinterpret_cast<const double2*>(D + 64 + 2 * t);
+    q[J][0] *= ri.x;
+    q[J][1] *= ri.y;
+    if (rok) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = 8 * J + 2 * t + h;
+        if (col < p.n) __stcs(p.Q + row + static_cast<long long>(col) * p.ldq, q[J][h]);
+      }
+    }
+  }
+}
+
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) trsm_phased32_kernel(TrsmParams p) {
+  constexpr int NT = 32, WPB = THREADS / 32, MAXF = kMaxPhaseFrags32;
+  static_assert(Phases32::P == 4, "buffer parity below assumes 4 phases");
+  extern __shared__ __align__(16) double smp[];
+  if (p.st && p.st->code != 0) return;
+  double* const buf0 = smp;
+  double* const buf1 = smp + MAXF * 32;
+  double* const db = smp + 2 * MAXF * 32;
+  for (int i = threadIdx.x; i < NT * 72; i += THREADS) db[i] = p.dblk[i];
+  auto stage = [&](int ph, double* dst) {  // cooperative cp.async of phase ph's fragments
+    const int k0 = Phases32::b(ph), k1 = Phases32::b(ph + 1);
+    const double* src = p.bfrag + static_cast<size_t>(k0) * (k0 - 1) * 32;
+    const int chunks = phase_frags(k0, k1) * 32 / 2;  // 16-byte chunks
+    for (int c = threadIdx.x; c < chunks; c += THREADS) cp_async16(dst + 2 * c, src + 2 * c);
+    cp_async_commit();
+  };
+  stage(0, buf0);
+  cp_async_wait_all();
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const long long m = p.m;
+  const int n = p.n;
+  const long long ngroups = (m + 7) / 8;
+  const long long stride = static_cast<long long>(gridDim.x) * WPB;
+  for (long long base = static_cast<long long>(blockIdx.x) * WPB; base < ngroups; base += stride) {
+    const long long rg = base + warp;
+    const bool act = rg < ngroups;
+    const long long row = rg * 8 + g;
+    const bool rok = act && row < m;
+    double q[NT][2];
+#pragma unroll
+    for (int J = 0; J < NT; ++J)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = 8 * J + 2 * t + h;
+        q[J][h] = (rok && col < n) ? __ldcs(p.X + row + static_cast<long long>(col) * p.ldx) : 0.0;
+      }
+    // phase PH computes from buffer PH&1 while phase PH+1 (or the next row group's phase 0)
+    // streams into the other one
+    stage(1, buf1);
+    if (act) phase32<0>(q, buf0, db, lane, t, rok, row, p);
+    cp_async_wait_all();
+    __syncthreads();
+    stage(2, buf0);
+    if (act) phase32<1>(q, buf1, db, lane, t, rok, row, p);
+    cp_async_wait_all();
+    __syncthreads();
+    stage(3, buf1);
+    if (act) phase32<2>(q, buf0, db, lane, t, rok, row, p);
+    cp_async_wait_all();
+    __syncthreads();
+    if (base + stride < ngroups) stage(0, buf0);
+    if (act) phase32<3>(q, buf1, db, lane, t, rok, row, p);
+    cp_async_wait_all();
+    __syncthreads();
+  }
+}
+
+template <int THREADS>
+static cudaError_t launch_phased32(const TrsmParams& p, int num_sms, cudaStream_t stream) {
+  const size_t smem = static_cast<size_t>(2 * kMaxPhaseFrags32 * 32 + 32 * 72) * 8;
+  auto k = trsm_phased32_kernel<THREADS>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const long long groups = (p.m + 7) / 8;
+  long long grid = num_sms;
+  const long long need = (groups + THREADS / 32 - 1) / (THREADS / 32);
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  k<<<static_cast<unsigned>(grid), THREADS, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
 // map: TMA descriptor of X with a {16 rows, npad columns} SWIZZLE_128B box (instances with
 // NT <= 16 use it when map != nullptr); the others read X with plain coalesced loads.
 cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream) {
@@ -260,7 +402,7 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
                         : launch_one<16, 2, true, 256, false>(p, nullptr, num_sms, stream);
 #endif
     case 24: return launch_one<24, 1, true, 256, false>(p, nullptr, num_sms, stream);
-    case 32: return launch_one<32, 1, false, 256, false>(p, nullptr, num_sms, stream);
+    case 32: return launch_phased32<256>(p, num_sms, stream);
     default: return cudaErrorInvalidValue;
   }
 }
