@@ -15,7 +15,9 @@
  *     memory (allocated e.g. with torch); the library allocates nothing per call on the
  *     device (it keeps a small pinned host status block and two events per thread).
  *   - TMA requirements: X, Q 16-byte aligned and ld, ldq even (8*ld % 16 == 0).
- *   - Supported sizes: 1 <= n <= 256, m_global >= n, m >= 0 on every rank.
+ *   - Supported sizes: 1 <= n <= 512 (SURVEY 8(b) contract), m_global >= n, m >= 0 on
+ *     every rank.  n in (256, 512] is padded to 512 internally (its TRSM runs as two
+ *     block-column launches).
  *   - All device work is ordered on opts->stream; every call returns only after that
  *     work has finished (the pass count is data dependent).
  *   - Return codes: SCQR3_OK; SCQR3_EINVAL (bad argument, CUDA or NCCL error -- detail in

@@ -84,26 +84,36 @@ __device__ __noinline__ double power_lmax(const double* Wg, int ldw, int n, int 
   const double sc = ldexp(1.0, -(ilogb(trace) + 1));
   int tpr = 1;
   while (tpr * 2 <= 32 && tpr * 2 * n <= kThreads) tpr *= 2;
-  const int tid = threadIdx.x, row = tid / tpr, part = tid % tpr;
-  if (tid < n) ybuf[0][tid] = 1.0;
+  const int tid = threadIdx.x, part = tid % tpr, rstep = kThreads / tpr;  // rows strided when n > kThreads
+  for (int i = tid; i < n; i += kThreads) ybuf[0][i] = 1.0;
   __syncthreads();
   int cur = 0;
   for (int it = 0; it < iters; ++it) {
+    for (int r0 = 0; r0 < n; r0 += rstep) {
+      const int row = r0 + tid / tpr;
+      double acc = 0.0;
+      if (row < n)
+        for (int j = part; j < n; j += tpr) acc = fma(W[j * ldw + row], ybuf[cur][j], acc);
+      for (int o = 1; o < tpr; o <<= 1) acc += __shfl_xor_sync(kFull, acc, o);
+      if (part == 0 && row < n) ybuf[cur ^ 1][row] = acc * sc;
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+  double num = 0.0, den = 0.0;
+  for (int r0 = 0; r0 < n; r0 += rstep) {
+    const int row = r0 + tid / tpr;
     double acc = 0.0;
     if (row < n)
       for (int j = part; j < n; j += tpr) acc = fma(W[j * ldw + row], ybuf[cur][j], acc);
     for (int o = 1; o < tpr; o <<= 1) acc += __shfl_xor_sync(kFull, acc, o);
-    if (part == 0 && row < n) ybuf[cur ^ 1][row] = acc * sc;
-    __syncthreads();
-    cur ^= 1;
+    if (part == 0 && row < n) {
+      const double y = ybuf[cur][row];
+      num = fma(y, acc, num);
+      den = fma(y, y, den);
+    }
   }
-  double acc = 0.0;
-  if (row < n)
-    for (int j = part; j < n; j += tpr) acc = fma(W[j * ldw + row], ybuf[cur][j], acc);
-  for (int o = 1; o < tpr; o <<= 1) acc += __shfl_xor_sync(kFull, acc, o);
-  const bool own = part == 0 && row < n;
-  const double y = own ? ybuf[cur][row] : 0.0;
-  const double2 nd = block_sum2(own ? y * acc : 0.0, own ? y * y : 0.0, red);
+  const double2 nd = block_sum2(num, den, red);
   return nd.y > 0.0 ? nd.x / nd.y : 0.0;
 }
 

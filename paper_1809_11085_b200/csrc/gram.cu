@@ -79,8 +79,11 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
         mbar_arrive_expect_tx(&full_bar[st], stage_bytes * nsrc);
         const int row = static_cast<int>((s_begin + i) * kGramStageRows);
         unsigned char* dst = stages + static_cast<size_t>(st) * nsrc * stage_bytes;
-        tma_load_2d(dst, &mapQ, row, 0, &full_bar[st]);
-        if (full) tma_load_2d(dst + stage_bytes, &mapY, row, 0, &full_bar[st]);
+        // a TMA box spans at most 256 columns: wider stages take several boxes (npad 512)
+        for (int c0 = 0; c0 < p.npad; c0 += kTmaBoxCols) {
+          tma_load_2d(dst + c0 * 128u, &mapQ, row, c0, &full_bar[st]);
+          if (full) tma_load_2d(dst + stage_bytes + c0 * 128u, &mapY, row, c0, &full_bar[st]);
+        }
       }
     }
     return;

@@ -15,8 +15,10 @@
 
 namespace scqr3 {
 
-constexpr int kMaxN = 256;            // largest supported n
+constexpr int kMaxN = 512;            // largest supported n
+constexpr int kTmaBoxCols = 256;      // TMA box limit per dimension
 constexpr int kGramStageRows = 16;    // rows of X per TMA stage (128 B per column: SWIZZLE_128B)
+constexpr size_t kGramSmemCap = 227 * 1024;  // opt-in dynamic shared memory per CTA
 constexpr int kJobTiles = 4;          // Gram warp job = 4x4 tiles of 8x8 = 32x32 outputs
 
 // Device status shared by the controller kernels (one per call, in the workspace).

@@ -163,7 +163,13 @@ Layout make_layout(int64_t m, int64_t n, int oblique) {
   L.NT = L.npad / 8;
   L.tiles_sym = static_cast<long long>(L.NT) * (L.NT + 1) / 2;
   L.tiles_part = oblique ? static_cast<long long>(L.NT) * L.NT : L.tiles_sym;
-  L.max_chunks = max_chunks_for_device();
+  {
+    // CTAs per row chunk = job groups (assign_gram_jobs); fewer chunks fit on the GPU when there are more
+    const long long nb = (L.NT + kJobTiles - 1) / kJobTiles;
+    const long long codes = 2 * (oblique ? nb * nb : nb * (nb + 1) / 2);
+    const int groups_hi = static_cast<int>(std::max<long long>(1, (codes + kMaxConsumers - 1) / kMaxConsumers));
+    L.max_chunks = std::max(1, max_chunks_for_device() / groups_hi);
+  }
   L.ldy = std::max<long long>(2, (m + 1) & ~1LL);
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -233,7 +239,7 @@ int check_matrix(const char* name, const double* p, int64_t m, int64_t ld) {
 int encode_map(Ctx* c, CUtensorMap* map, const double* base, int64_t m, int64_t n, int64_t ld, int npad) {
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(m), static_cast<cuuint64_t>(n)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 8};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(kGramStageRows), static_cast<cuuint32_t>(npad)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kGramStageRows), static_cast<cuuint32_t>(std::min(npad, kTmaBoxCols))};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = c->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -340,7 +346,9 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   const int threads = 32 * (1 + ncons);
   const int nsrc = oblique ? 2 : 1;
   const size_t stage_bytes = static_cast<size_t>(L.npad) * 128;
-  gp.stages = static_cast<int>(std::min<size_t>(8, std::max<size_t>(2, 98304 / (stage_bytes * nsrc))));
+  // 2..8 stages within ~96 KB; a single (serialising) stage only where two do not fit (oblique, npad 512)
+  const size_t max_stages = (kGramSmemCap - 2048) / (stage_bytes * nsrc);
+  gp.stages = static_cast<int>(std::min<size_t>(std::min<size_t>(8, max_stages), std::max<size_t>(2, 98304 / (stage_bytes * nsrc))));
   const size_t smem = gp.stages * nsrc * stage_bytes + 2 * gp.stages * 8 + 1024;
   CUDA_TRY(cudaFuncSetAttribute(gram_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int occ = 1;

@@ -10,7 +10,7 @@ namespace scqr3 {
 struct DevStatus;
 
 constexpr int kMaxConsumers = 20;   // consumer warps per Gram CTA (+1 producer = 672 threads)
-constexpr int kMaxGroups = 8;       // job groups (CTAs sharing one row chunk)
+constexpr int kMaxGroups = 32;      // job groups (CTAs sharing one row chunk)
 
 struct GramParams {
   double* partials;          // [chunks][tiles_per_partial][64]
@@ -113,7 +113,7 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
 
 inline int npad_for(int n) {
   // tile counts with a compiled TRSM instance
-  static const int nts[] = {1, 2, 4, 8, 12, 16, 24, 32};
+  static const int nts[] = {1, 2, 4, 8, 12, 16, 24, 32, 64};
   int nt = (n + 7) / 8;
   for (int v : nts)
     if (v >= nt) return v * 8;

@@ -238,18 +238,32 @@ static cudaError_t launch_one(const TrsmParams& p, const CUtensorMap* map, int n
 }
 
 // ------------------------------------------------------------------------------------------
-// Wide TRSM (n in (192, 256]): -R~'s B fragments (254 KB at n=256) do not fit shared memory,
-// so the target column blocks are processed in phases whose fragments do; the next phase's
-// fragments stream into the second buffer with cp.async while the current phase computes.
-// Each warp owns 8 rows (q: 64 doubles).  Per phase [K0, K1): (i) the updates of its targets
-// from all earlier blocks (a dependency-free DMMA stream, targets interleaved), then (ii) the
-// right-looking triangular part inside the phase, as in trsm_kernel.
-struct Phases32 {
-  static constexpr int P = 4;
+// Wide TRSM (n in (192, 512]): -R~'s B fragments (254 KB at n=256, 1 MB at n=512) do not fit
+// shared memory, so the target column blocks are processed in phases whose fragments do; the
+// next phase's fragments stream into the second buffer with cp.async while the current phase
+// computes.  Each warp owns 8 rows and 32 target blocks in registers (q: 64 doubles).  Per
+// phase [K0, K1): (i) the updates of its targets from all earlier blocks (a dependency-free
+// DMMA stream, targets interleaved), then (ii) the right-looking triangular part inside the
+// phase, as in trsm_kernel.  n > 256 runs as two launches (block-column TRSM): targets 0..31,
+// then targets 32..63, whose updates from blocks 0..31 read the finished Q columns back.
+constexpr int phase_frags(int k0, int k1) { return k1 * (k1 - 1) - k0 * (k0 - 1); }
+template <int TB> struct WidePhases;
+template <> struct WidePhases<0> {  // targets 0..31
+  static constexpr int P = 4, MAXF = 290;
   __host__ __device__ static constexpr int b(int i) { return i == 0 ? 0 : i == 1 ? 16 : i == 2 ? 22 : i == 3 ? 27 : 32; }
 };
-constexpr int phase_frags(int k0, int k1) { return k1 * (k1 - 1) - k0 * (k0 - 1); }
-constexpr int kMaxPhaseFrags32 = 290;  // max over Phases32 of phase_frags (27..32)
+template <> struct WidePhases<32> {  // targets 32..63 (greedy, <= MAXF fragments per phase)
+  static constexpr int P = 10, MAXF = 370;
+  __host__ __device__ static constexpr int b(int i) {
+    return i == 0 ? 32 : i == 1 ? 37 : i == 2 ? 41 : i == 3 ? 45 : i == 4 ? 48 : i == 5 ? 51
+         : i == 6 ? 54 : i == 7 ? 57 : i == 8 ? 60 : i == 9 ? 62 : 64;
+  }
+};
+template <int TB> constexpr bool phases_ok(int i = 0) {
+  return i == WidePhases<TB>::P ||
+         (phase_frags(WidePhases<TB>::b(i), WidePhases<TB>::b(i + 1)) <= WidePhases<TB>::MAXF && phases_ok<TB>(i + 1));
+}
+static_assert(phases_ok<0>() && phases_ok<32>(), "phase fragment counts exceed the buffers");
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
@@ -257,71 +271,113 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-// One phase [K0, K1) of the wide TRSM for one warp's 8 rows; every index is compile-time.
-template <int PH>
-__device__ __forceinline__ void phase32(double (&q)[32][2], const double* __restrict__ cur,
-                                        const double* __restrict__ db, int lane, int t, bool rok,
-                                        long long row, const TrsmParams& p) {
-  constexpr int K0 = Phases32::b(PH), K1 = Phases32::b(PH + 1);
+// One phase of the wide TRSM for one warp's 8 rows; every register index is compile-time.
+// q[k] holds target block TB + k; qe points at this lane's row of the finished Q (blocks < TB).
+template <int TB, int PH>
+__device__ __forceinline__ void wide_phase(double (&q)[32][2], const double* __restrict__ cur,
+                                           const double* __restrict__ db, int lane, int t, bool rok,
+                                           long long row, const double* __restrict__ qe, const TrsmParams& p) {
+  constexpr int K0 = WidePhases<TB>::b(PH), K1 = WidePhases<TB>::b(PH + 1);
   auto frag = [&](int K, int s) { return cur[(K * (K - 1) - K0 * (K0 - 1) + s) * 32 + lane]; };
-  // (i) updates from the blocks of earlier phases, targets interleaved
+  // (i-a) updates from the blocks of the previous launch (finished Q columns, read back)
+  if (TB > 0) {
+    double a[8];
 #pragma unroll
-  for (int s = 0; s < 2 * K0; ++s)
+    for (int i = 0; i < 8; ++i) a[i] = __ldg(qe + static_cast<long long>(8 * (i >> 1) + 2 * t + (i & 1)) * p.ldq);
+#pragma unroll 1
+    for (int sb = 0; sb < 2 * TB; sb += 8) {
+      double b[8];
+      const int sn = sb + 8 < 2 * TB ? sb + 8 : sb;  // (last batch reloads itself, harmless)
 #pragma unroll
-    for (int K = K0; K < K1; ++K) dmma(q[K][0], q[K][1], q[s >> 1][s & 1], frag(K, s));
+      for (int i = 0; i < 8; ++i)
+        b[i] = __ldg(qe + static_cast<long long>(8 * ((sn + i) >> 1) + 2 * t + (i & 1)) * p.ldq);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int K = K0; K < K1; ++K) dmma(q[K - TB][0], q[K - TB][1], a[i], frag(K, sb + i));
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = b[i];
+    }
+  }
+  // (i-b) updates from the blocks of earlier phases of this launch, targets interleaved
+#pragma unroll
+  for (int s = 2 * TB; s < 2 * K0; ++s)
+#pragma unroll
+    for (int K = K0; K < K1; ++K) dmma(q[K - TB][0], q[K - TB][1], q[(s >> 1) - TB][s & 1], frag(K, s));
   // (ii) triangular part inside the phase (right-looking, as in trsm_kernel)
 #pragma unroll
   for (int J = K0; J < K1; ++J) {
     if (J > K0) {
 #pragma unroll
-      for (int s = 2 * (J - 1); s < 2 * J; ++s) dmma(q[J][0], q[J][1], q[J - 1][s & 1], frag(J, s));
+      for (int s = 2 * (J - 1); s < 2 * J; ++s) dmma(q[J - TB][0], q[J - TB][1], q[J - 1 - TB][s & 1], frag(J, s));
     }
     const int nup = J > K0 ? K1 - 1 - J : 0;
-    const double* D = db + J * 72;
+    const double* D = db + (J - TB) * 72;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const double2 rc = *reinterpret_cast<const double2*>(D + c * 8 + 2 * t);
-      const double vc = __shfl_sync(0xffffffffu, q[J][c & 1], (lane & ~3) | (c >> 1));
-      q[J][0] = fma(-vc, rc.x, q[J][0]);
-      q[J][1] = fma(-vc, rc.y, q[J][1]);
+      const double vc = __shfl_sync(0xffffffffu, q[J - TB][c & 1], (lane & ~3) | (c >> 1));
+      q[J - TB][0] = fma(-vc, rc.x, q[J - TB][0]);
+      q[J - TB][1] = fma(-vc, rc.y, q[J - TB][1]);
 #pragma unroll
       for (int u = nup * c / 8; u < nup * (c + 1) / 8; ++u) {
         const int K = J + 1 + u;
 #pragma unroll
-        for (int s = 2 * (J - 1); s < 2 * J; ++s) dmma(q[K][0], q[K][1], q[J - 1][s & 1], frag(K, s));
+        for (int s = 2 * (J - 1); s < 2 * J; ++s) dmma(q[K - TB][0], q[K - TB][1], q[J - 1 - TB][s & 1], frag(K, s));
       }
     }
     const double2 ri = *reinterpret_cast<const double2*>(D + 64 + 2 * t);
-    q[J][0] *= ri.x;
-    q[J][1] *= ri.y;
+    q[J - TB][0] *= ri.x;
+    q[J - TB][1] *= ri.y;
     if (rok) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int col = 8 * J + 2 * t + h;
-        if (col < p.n) __stcs(p.Q + row + static_cast<long long>(col) * p.ldq, q[J][h]);
+        if (col < p.n) __stcs(p.Q + row + static_cast<long long>(col) * p.ldq, q[J - TB][h]);
       }
     }
   }
 }
 
-template <int THREADS>
-__global__ void __launch_bounds__(THREADS, 1) trsm_phased32_kernel(TrsmParams p) {
-  constexpr int NT = 32, WPB = THREADS / 32, MAXF = kMaxPhaseFrags32;
-  static_assert(Phases32::P == 4, "buffer parity below assumes 4 phases");
+// Phases PH.. of one row group: phase PH computes from buffer PH&1 while phase PH+1 (or, after
+// the last phase, the next row group's phase 0) streams into the other one.
+template <int TB, int PH, typename Stage>
+__device__ __forceinline__ void wide_phases(double (&q)[32][2], double* const (&buf)[2], const double* db,
+                                            int lane, int t, bool act, bool rok, long long row,
+                                            const double* qe, const TrsmParams& p, bool more, Stage& stage) {
+  constexpr int P = WidePhases<TB>::P;
+  if constexpr (PH + 1 < P) stage(PH + 1, buf[(PH + 1) & 1]);
+  else if ((P - 1) & 1) { if (more) stage(0, buf[0]); }  // buf[0] is free during an odd last phase
+  if (act) wide_phase<TB, PH>(q, buf[PH & 1], db, lane, t, rok, row, qe, p);
+  cp_async_wait_all();
+  __syncthreads();
+  if constexpr (PH + 1 < P) {
+    wide_phases<TB, PH + 1>(q, buf, db, lane, t, act, rok, row, qe, p, more, stage);
+  } else if (!((P - 1) & 1)) {  // even last phase used buf[0]: stage the next phase 0 now
+    if (more) {
+      stage(0, buf[0]);
+      cp_async_wait_all();
+      __syncthreads();
+    }
+  }
+}
+
+template <int TB, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) trsm_wide_kernel(TrsmParams p) {
+  constexpr int NTT = 32, WPB = THREADS / 32, MAXF = WidePhases<TB>::MAXF;
   extern __shared__ __align__(16) double smp[];
   if (p.st && p.st->code != 0) return;
-  double* const buf0 = smp;
-  double* const buf1 = smp + MAXF * 32;
+  double* const buf[2] = {smp, smp + MAXF * 32};
   double* const db = smp + 2 * MAXF * 32;
-  for (int i = threadIdx.x; i < NT * 72; i += THREADS) db[i] = p.dblk[i];
+  for (int i = threadIdx.x; i < NTT * 72; i += THREADS) db[i] = p.dblk[TB * 72 + i];
   auto stage = [&](int ph, double* dst) {  // cooperative cp.async of phase ph's fragments
-    const int k0 = Phases32::b(ph), k1 = Phases32::b(ph + 1);
+    const int k0 = WidePhases<TB>::b(ph), k1 = WidePhases<TB>::b(ph + 1);
     const double* src = p.bfrag + static_cast<size_t>(k0) * (k0 - 1) * 32;
     const int chunks = phase_frags(k0, k1) * 32 / 2;  // 16-byte chunks
     for (int c = threadIdx.x; c < chunks; c += THREADS) cp_async16(dst + 2 * c, src + 2 * c);
     cp_async_commit();
   };
-  stage(0, buf0);
+  stage(0, buf[0]);
   cp_async_wait_all();
   __syncthreads();
 
@@ -335,39 +391,23 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_phased32_kernel(TrsmParams p)
     const bool act = rg < ngroups;
     const long long row = rg * 8 + g;
     const bool rok = act && row < m;
-    double q[NT][2];
+    const double* qe = p.Q + (rok ? row : 0);
+    double q[NTT][2];
 #pragma unroll
-    for (int J = 0; J < NT; ++J)
+    for (int J = 0; J < NTT; ++J)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int col = 8 * J + 2 * t + h;
+        const int col = 8 * (TB + J) + 2 * t + h;
         q[J][h] = (rok && col < n) ? __ldcs(p.X + row + static_cast<long long>(col) * p.ldx) : 0.0;
       }
-    // phase PH computes from buffer PH&1 while phase PH+1 (or the next row group's phase 0)
-    // streams into the other one
-    stage(1, buf1);
-    if (act) phase32<0>(q, buf0, db, lane, t, rok, row, p);
-    cp_async_wait_all();
-    __syncthreads();
-    stage(2, buf0);
-    if (act) phase32<1>(q, buf1, db, lane, t, rok, row, p);
-    cp_async_wait_all();
-    __syncthreads();
-    stage(3, buf1);
-    if (act) phase32<2>(q, buf0, db, lane, t, rok, row, p);
-    cp_async_wait_all();
-    __syncthreads();
-    if (base + stride < ngroups) stage(0, buf0);
-    if (act) phase32<3>(q, buf1, db, lane, t, rok, row, p);
-    cp_async_wait_all();
-    __syncthreads();
+    wide_phases<TB, 0>(q, buf, db, lane, t, act, rok, row, qe, p, base + stride < ngroups, stage);
   }
 }
 
-template <int THREADS>
-static cudaError_t launch_phased32(const TrsmParams& p, int num_sms, cudaStream_t stream) {
-  const size_t smem = static_cast<size_t>(2 * kMaxPhaseFrags32 * 32 + 32 * 72) * 8;
-  auto k = trsm_phased32_kernel<THREADS>;
+template <int TB, int THREADS>
+static cudaError_t launch_wide(const TrsmParams& p, int num_sms, cudaStream_t stream) {
+  const size_t smem = static_cast<size_t>(2 * WidePhases<TB>::MAXF * 32 + 32 * 72) * 8;
+  auto k = trsm_wide_kernel<TB, THREADS>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const long long groups = (p.m + 7) / 8;
@@ -402,7 +442,13 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
                         : launch_one<16, 2, true, 256, false>(p, nullptr, num_sms, stream);
 #endif
     case 24: return launch_one<24, 1, true, 256, false>(p, nullptr, num_sms, stream);
-    case 32: return launch_phased32<256>(p, num_sms, stream);
+    case 32: return launch_wide<0, 256>(p, num_sms, stream);
+    case 64: {
+      // block-column TRSM: Q(:, 0:256) first; the second launch reads it back for its updates
+      cudaError_t e = launch_wide<0, 256>(p, num_sms, stream);
+      if (e != cudaSuccess) return e;
+      return launch_wide<32, 256>(p, num_sms, stream);
+    }
     default: return cudaErrorInvalidValue;
   }
 }

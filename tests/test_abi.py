@@ -45,7 +45,8 @@ def test_default_opts_and_sizes_without_gpu():
     assert o.abi_version == _abi.SCQR3_ABI_VERSION and o.max_passes == 8 and o.stop_tol == 0.5
     assert o.power_iters == 32 and o.shift_mode == _abi.SHIFT_SAFE and o.norm_mode == _abi.NORM_POWER
     assert lib.scqr3_workspace_size(1000, 0, 0) == 0
-    assert lib.scqr3_workspace_size(1000, 257, 0) == 0
+    assert lib.scqr3_workspace_size(1000, 513, 0) == 0
+    assert lib.scqr3_workspace_size(1000, 512, 0) > 0
     a = lib.scqr3_workspace_size(10_000_000, 128, 0)
     b = lib.scqr3_workspace_size(10_000_000, 128, 1)
     assert 0 < a < b and b >= 8 * 10_000_000 * 128       # oblique holds B*Q

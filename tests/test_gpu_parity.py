@@ -38,7 +38,8 @@ def gamma(k):
 # ------------------------------------------------------------------ Gram
 @gpu
 @pytest.mark.parametrize("m,n", [(1, 1), (15, 3), (16, 16), (17, 8), (1000, 7), (4099, 33), (20001, 64),
-                                 (5000, 100), (30011, 128), (3000, 200), (2500, 256)])
+                                 (5000, 100), (30011, 128), (3000, 200), (2500, 256),
+                                 (1500, 300), (1200, 512)])
 def test_gram_parity(m, n):
     X = synth.random_rows(m, n, seed=m + n)
     A = host(sq.scqr3_gram(dev(X)))
@@ -70,7 +71,7 @@ def test_gram_ld_padding_and_determinism():
 
 
 @gpu
-@pytest.mark.parametrize("m,n", [(2, 1), (999, 16), (20000, 64), (3001, 128)])
+@pytest.mark.parametrize("m,n", [(2, 1), (999, 16), (20000, 64), (3001, 128), (1500, 300)])
 def test_gram_oblique_parity(m, n):
     X = synth.random_rows(m, n, seed=n)
     d, e = synth.tridiag_b(m, seed=n)
@@ -86,7 +87,7 @@ def test_gram_oblique_parity(m, n):
 
 # ------------------------------------------------------------------ Cholesky
 @gpu
-@pytest.mark.parametrize("n", [1, 2, 9, 40, 128, 200, 256])
+@pytest.mark.parametrize("n", [1, 2, 9, 40, 128, 200, 256, 301, 512])
 def test_cholesky_integer_exact(n):
     rng = np.random.default_rng(n)
     R = np.triu(rng.integers(-3, 4, size=(n, n))).astype(float)
@@ -117,7 +118,8 @@ def test_cholesky_breakdown_matches_oracle():
 
 # ------------------------------------------------------------------ TRSM
 @gpu
-@pytest.mark.parametrize("m,n", [(1, 1), (31, 5), (1000, 16), (4097, 64), (10007, 128), (3000, 200), (2049, 256)])
+@pytest.mark.parametrize("m,n", [(1, 1), (31, 5), (1000, 16), (4097, 64), (10007, 128), (3000, 200), (2049, 256),
+                                 (2001, 264), (1800, 512)])
 def test_trsm_integer_exact(m, n):
     rng = np.random.default_rng(m)
     Q = rng.integers(-9, 10, size=(m, n)).astype(float)
@@ -128,7 +130,7 @@ def test_trsm_integer_exact(m, n):
 
 
 @gpu
-@pytest.mark.parametrize("m,n", [(777, 24), (5003, 128), (1500, 256)])
+@pytest.mark.parametrize("m,n", [(777, 24), (5003, 128), (1500, 256), (1100, 400)])
 def test_trsm_rowwise_backward_error(m, n):
     X = synth.randsvd(m, n, 1e8, seed=3)
     R = oracle.cholesky(oracle.gram(X), oracle.shift(m, n, 1.0))
@@ -161,7 +163,7 @@ def _compare(X, rg, ro, kappa, d=None, e=None):
 
 @gpu
 @pytest.mark.parametrize("m,n,kappa", [(2000, 16, 1e12), (300, 10, 1e15), (1000, 30, 1e12), (100, 100, 1e13),
-                                       (5001, 64, 1e4), (20000, 128, 1e10), (8000, 100, 1e6), (4000, 256, 1e8),
+                                       (5001, 64, 1e4), (20000, 128, 1e10), (8000, 100, 1e6), (4000, 256, 1e8), (3000, 512, 1e10),
                                        (3000, 1, 1.0), (17, 17, 1e3)])
 def test_factor_parity(m, n, kappa):
     X = synth.randsvd(m, n, kappa, seed=0)
@@ -228,7 +230,7 @@ def test_status_codes_and_errors():
     with pytest.raises(sq.ScqrError):
         sq.scqr3_factor(dev(np.ones((3, 5))))          # m < n
     with pytest.raises(sq.ScqrError):
-        sq.scqr3_factor(dev(np.ones((300, 257))))      # n > 256
+        sq.scqr3_factor(dev(np.ones((600, 513))))      # n > 512
 
 
 @gpu
