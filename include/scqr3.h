@@ -89,7 +89,7 @@ typedef struct scqr3_opts {
   double norm2_bound;      /* USER: N >= ||X||_2                                       */
   double bnorm_bound;      /* oblique: N_B >= ||B||_2 (0 => Gershgorin)                */
   int32_t max_passes;      /* default 8                                        */
-  int32_t reserved0;
+  int32_t deterministic;   /* with comm: 1 = allgather the Gram and sum it in rank order: bitwise reproducible whatever NCCL algorithm runs; up to >= 22 ranks at every n (Gram slots of the workspace), else SCQR3_EINVAL */
   double stop_tol;         /* stop after a plain pass with ||A_k - I||_F <= stop_tol (D6); default 0.5 */
   int64_t m_global;        /* rows over all ranks (shift uses the global m); 0 => sum over ranks */
   void* stream;            /* cudaStream_t; NULL = legacy default stream                */

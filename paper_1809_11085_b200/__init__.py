@@ -131,7 +131,7 @@ class Comm:
 
 def _opts(shift_mode=SHIFT_SAFE, shift_value=0.0, norm_mode=NORM_POWER, norm2_bound=0.0, bnorm_bound=0.0,
           max_passes=8, stop_tol=0.5, power_iters=32, m_global=0, stream=None, comm=None, ws=None,
-          trace_cap=16, prof=None):
+          trace_cap=16, prof=None, deterministic=False):
     torch = _torch()
     o = _abi.Opts()
     _abi.lib().scqr3_default_opts(ctypes.byref(o))
@@ -139,6 +139,7 @@ def _opts(shift_mode=SHIFT_SAFE, shift_value=0.0, norm_mode=NORM_POWER, norm2_bo
     o.norm_mode, o.norm2_bound, o.bnorm_bound = norm_mode, float(norm2_bound), float(bnorm_bound)
     o.max_passes, o.stop_tol, o.power_iters = int(max_passes), float(stop_tol), int(power_iters)
     o.m_global = int(m_global)
+    o.deterministic = 1 if deterministic else 0
     if stream is None:
         stream = torch.cuda.current_stream()
     o.stream = ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))

@@ -46,7 +46,7 @@ class Opts(ctypes.Structure):
         ("shift_value", ctypes.c_double), ("norm_mode", ctypes.c_int32),
         ("power_iters", ctypes.c_int32), ("norm2_bound", ctypes.c_double),
         ("bnorm_bound", ctypes.c_double), ("max_passes", ctypes.c_int32),
-        ("reserved0", ctypes.c_int32), ("stop_tol", ctypes.c_double),
+        ("deterministic", ctypes.c_int32), ("stop_tol", ctypes.c_double),
         ("m_global", ctypes.c_int64), ("stream", ctypes.c_void_p), ("comm", ctypes.c_void_p),
         ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
         ("trace", ctypes.POINTER(PassTrace)), ("trace_cap", ctypes.c_int32),

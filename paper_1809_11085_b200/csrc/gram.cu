@@ -320,4 +320,14 @@ __global__ void tiles_to_full_kernel(const double* tiles, int n, double* A) {
   A[k] = tiles[tile * 64 + 8 * (a & 7) + (b & 7)];
 }
 
+// Deterministic cross-rank sum (opts.deterministic): parts holds nparts rank Grams of count
+// entries back to back (ncclAllGather); summed in rank order, identical bits on every rank.
+__global__ void rank_sum_kernel(const double* parts, int nparts, long long count, double* out) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  double s = parts[i];
+  for (int r = 1; r < nparts; ++r) s += parts[static_cast<long long>(r) * count + i];
+  out[i] = s;
+}
+
 }  // namespace scqr3

@@ -570,7 +570,20 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const double*
     if (cm) {
       const size_t cnt = static_cast<size_t>(L.tiles_sym * 64 + (oblique ? 1 : 0));
       const int pa = prof_begin(c, PK_COMM);
-      NCCL_TRY(ncclAllReduce(w.tiles, w.tiles, cnt, ncclDouble, ncclSum, cm->nccl, st));
+      if (o->deterministic) {
+        // every rank's Gram side by side (the partials area is free once gram_reduce ran), then
+        // one fixed-order sum: the same bits on every rank and every run
+        if (static_cast<long long>(cm->nranks) * static_cast<long long>(cnt) >
+            static_cast<long long>(L.max_chunks) * L.tiles_part * 64)
+          return fail("deterministic mode: %d ranks exceed the workspace's Gram slots", cm->nranks);
+        NCCL_TRY(ncclAllGather(w.tiles, w.partials, cnt, ncclDouble, cm->nccl, st));
+        rank_sum_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, st>>>(w.partials, cm->nranks,
+                                                                                   static_cast<long long>(cnt), w.tiles);
+        ++g_launches;
+        CUDA_TRY(cudaGetLastError());
+      } else {
+        NCCL_TRY(ncclAllReduce(w.tiles, w.tiles, cnt, ncclDouble, ncclSum, cm->nccl, st));
+      }
       prof_end(c, pa);
     }
     c->st_host->code = -1;

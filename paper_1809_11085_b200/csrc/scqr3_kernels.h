@@ -97,6 +97,7 @@ struct TrsmParams {
 __global__ void gram_tma_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapY,
                                 GramParams p);
 __global__ void gram_reduce_kernel(GramReduceParams p);
+__global__ void rank_sum_kernel(const double* parts, int nparts, long long count, double* out);
 __global__ void oblique_y_kernel(ObliqueYParams p);
 __global__ void gershgorin_kernel(const double* d, const double* e, long long m, int has_prev, double e_prev,
                                   int has_next, double* partial);

@@ -272,4 +272,10 @@ def test_single_rank_nccl_comm_path():
     c1 = sq.scqr3_factor_oblique(dev(X), torch.from_numpy(d).cuda(), torch.from_numpy(e).cuda())
     c2 = sq.scqr3_factor_oblique(dev(X), torch.from_numpy(d).cuda(), torch.from_numpy(e).cuda(), comm=comm)
     assert np.array_equal(host(c1.R), host(c2.R))
+    # deterministic mode (allgather + rank-ordered sum): same bits as the plain path at one rank
+    b2 = sq.scqr3_factor(dev(X), comm=comm, deterministic=True)
+    assert np.array_equal(host(a.R), host(b2.R)) and b2.passes == a.passes
+    c3 = sq.scqr3_factor_oblique(dev(X), torch.from_numpy(d).cuda(), torch.from_numpy(e).cuda(), comm=comm,
+                                 deterministic=True)
+    assert np.array_equal(host(c1.R), host(c3.R))
     comm.destroy()
