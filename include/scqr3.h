@@ -43,8 +43,14 @@ enum { SCQR3_OK = 0, SCQR3_EINVAL = 1, SCQR3_EBREAKDOWN = 2, SCQR3_ENOCONV = 3 }
  * oblique 11{2m sqrt(mn)+n(n+1)} u N^2 ||B|| (eq. finds2B) on pass 1 and on any
  * later pass whose plain Cholesky breaks down (Alg. 2 lines 4-7).
  * FIXED: shift_value on pass 1 (kernel-level parity tests), SAFE on breakdown.
- * NONE: no shift ever (plain iterated CholeskyQR, for tests; breakdown is final). */
-enum { SCQR3_SHIFT_SAFE = 0, SCQR3_SHIFT_FIXED = 1, SCQR3_SHIFT_NONE = 2 };
+ * NONE: no shift ever (plain iterated CholeskyQR, for tests; breakdown is final).
+ * ADAPTIVE: Alg. 2 literally -- pass 1 is also tried unshifted and shifted only
+ *   when its Cholesky breaks down: CholeskyQR2 (2 passes) for kappa(X) up to ~u^-1/2.
+ * PRACTICAL: pass 1 (and any breakdown) first shifted by s_p = u N^2 (oblique: u N^2 ||B||),
+ *   the Remark's smaller shift (Fig. 2); if chol(A + s_p I) breaks down the SAFE
+ *   shift follows (reading D21), keeping Alg. 3's guarantee. */
+enum { SCQR3_SHIFT_SAFE = 0, SCQR3_SHIFT_FIXED = 1, SCQR3_SHIFT_NONE = 2, SCQR3_SHIFT_ADAPTIVE = 3,
+       SCQR3_SHIFT_PRACTICAL = 4 };
 
 /* Estimate N^2 of ||Q||_2^2 for the shift (reading D2/D4).
  * POWER: 1.01 * Rayleigh quotient after power_iters steps on the computed n x n Gram.

@@ -24,7 +24,7 @@ _lib = None
 
 U = 2.0 ** -53  # unit roundoff
 
-SHIFT_SAFE, SHIFT_FIXED, SHIFT_NONE = 0, 1, 2
+SHIFT_SAFE, SHIFT_FIXED, SHIFT_NONE, SHIFT_ADAPTIVE, SHIFT_PRACTICAL = 0, 1, 2, 3, 4
 NORM_POWER, NORM_FROBENIUS, NORM_USER = 0, 1, 2
 
 
@@ -224,6 +224,9 @@ def scqr3(X, d=None, e=None, *, shift_mode=SHIFT_SAFE, shift_value=0.0, norm_mod
           norm2_bound=0.0, bnorm_bound=0.0, max_passes=8, stop_tol=0.5, power_iters=32,
           m_global=0, nparts=1) -> Result:
     """Shifted CholeskyQR3 with breakdown re-shift (Alg. 3 P:698-711 + Alg. 2).
+
+    shift_mode ADAPTIVE: Alg. 2 literally (no shift on pass 1 unless chol breaks down);
+    PRACTICAL: shifted attempts try s_p = u*N2 first (Remark P:1600-1606), then the safe s.
 
     Oblique (d, e given): Alg. 5 with the B-Gram in every pass (D8)."""
     X = _colmajor(X)

@@ -345,13 +345,18 @@ double orc_resid_F(int64_t m, int64_t n, const double* X, int64_t ldx, const dou
  *     s := 11{mn+n(n+1)} u N2  (oblique: eq. finds2B)
  *     if k == 1: R~ := chol(A + sI)                       (Alg. 3 line 4)
  *     else:      R~ := chol(A); on breakdown R~ := chol(A + sI)   (Alg. 2 lines 4-7)
+ *   shift_mode ADAPTIVE (Alg. 2 literal): pass 1 too is tried unshifted first.
+ *   shift_mode PRACTICAL (the Remark after eq. finds2B, Fig. 2): every shifted
+ *     attempt first uses s_p = u N2 (oblique: u N2 N_B); if chol(A + s_p I) breaks down it
+ *     falls back to the safe s (reading D21), so Alg. 3's guarantee is kept.
  *     breakdown with the shift -> status 2
  *     Q := Q R~^{-1},  R := R~ R                           (Alg. 2 line 8)
  *   until (R~ was unshifted and ||A - I||_F <= stop_tol)    (D6)
  *   k == max_passes without stopping -> status 3
  */
 typedef struct orc_opts {
-  int shift_mode;      /* 0 SAFE (eq. finds2/finds2B), 1 FIXED (shift_value on pass 1), 2 NONE */
+  int shift_mode;      /* 0 SAFE (eq. finds2/finds2B), 1 FIXED (shift_value on pass 1), 2 NONE,
+                          3 ADAPTIVE (Alg. 2: shift only on breakdown), 4 PRACTICAL (s_p = u N2 first) */
   double shift_value;
   int norm_mode;       /* 0 POWER (lambda_max of the Gram x 1.01), 1 FROBENIUS (trace), 2 USER */
   double norm2_bound;  /* USER: N >= ||X||_2 for pass 1 */
@@ -492,31 +497,35 @@ int orc_scqr3(int64_t m, int64_t n, const double* X, int64_t ld, const double* d
     else if (oblique) s = orc_shift_oblique(mg, (double)n, N2, NB);
     else s = orc_shift(mg, (double)n, N2);
 
+    /* the practical shift of the Remark: u ||X||_2^2 ||B||_2 */
+    const double sp = 0x1p-53 * N2 * (oblique ? NB : 1.0);
+    const int practical = o->shift_mode == 4;
     int64_t piv = 0;
     double pv = 0.0;
     int shifted = 0, bpiv = 0;
-    double bval = 0.0;
+    double bval = 0.0, s_used = 0.0;
     int rc;
-    if (k == 1 && o->shift_mode != 2) {
-      shifted = 1;
-      rc = orc_cholesky(n, A, s, Rt, &piv, &pv);
+    const int shift_first = k == 1 && (o->shift_mode == 0 || o->shift_mode == 1 || practical);
+    if (!shift_first) {
+      rc = orc_cholesky(n, A, 0.0, Rt, &piv, &pv);
       if (rc) { bpiv = (int)piv; bval = pv; }
     } else {
-      rc = orc_cholesky(n, A, 0.0, Rt, &piv, &pv);
-      if (rc) {
-        bpiv = (int)piv;
-        bval = pv;
-        if (o->shift_mode == 2) {
-          /* plain CholeskyQR2/3 (tests only): breakdown is final */
-        } else {
-          shifted = 1;
-          rc = orc_cholesky(n, A, s, Rt, &piv, &pv);
-          if (rc) { bpiv = (int)piv; bval = pv; }
-        }
+      rc = 1;
+    }
+    if (rc && o->shift_mode != 2) {
+      /* shifted attempt(s): PRACTICAL tries s_p before the safe s */
+      shifted = 1;
+      s_used = practical ? sp : s;
+      rc = orc_cholesky(n, A, s_used, Rt, &piv, &pv);
+      if (rc) { bpiv = (int)piv; bval = pv; }
+      if (rc && practical) {
+        s_used = s;
+        rc = orc_cholesky(n, A, s_used, Rt, &piv, &pv);
+        if (rc) { bpiv = (int)piv; bval = pv; }
       }
     }
     if (trace && k - 1 < trace_cap) {
-      trace[k - 1].shift = shifted ? s : 0.0;
+      trace[k - 1].shift = shifted ? s_used : 0.0;
       trace[k - 1].shifted = shifted;
       trace[k - 1].breakdown_pivot = bpiv;
       trace[k - 1].pivot_value = bval;

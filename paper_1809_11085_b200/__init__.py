@@ -14,7 +14,7 @@ from dataclasses import dataclass, field
 
 from . import _abi
 from ._abi import (EBREAKDOWN, EINVAL, ENOCONV, NORM_FROBENIUS, NORM_POWER, NORM_USER, OK,  # noqa: F401
-                   SHIFT_FIXED, SHIFT_NONE, SHIFT_SAFE)
+                   SHIFT_ADAPTIVE, SHIFT_FIXED, SHIFT_NONE, SHIFT_PRACTICAL, SHIFT_SAFE)
 
 __all__ = [
     "scqr3_factor", "scqr3_factor_oblique", "scqr3_factor_host", "scqr3_gram", "scqr3_gram_oblique",

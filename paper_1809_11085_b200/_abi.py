@@ -9,7 +9,7 @@ LIB_PATH = os.environ.get("SCQR3_LIB") or os.path.join(HERE, "libscqr3.so")
 
 SCQR3_ABI_VERSION = 1
 OK, EINVAL, EBREAKDOWN, ENOCONV = 0, 1, 2, 3
-SHIFT_SAFE, SHIFT_FIXED, SHIFT_NONE = 0, 1, 2
+SHIFT_SAFE, SHIFT_FIXED, SHIFT_NONE, SHIFT_ADAPTIVE, SHIFT_PRACTICAL = 0, 1, 2, 3, 4
 NORM_POWER, NORM_FROBENIUS, NORM_USER = 0, 1, 2
 COMM_ID_BYTES = 128
 

@@ -352,30 +352,37 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
     return 11.0 * (mg * nn + nn * (nn + 1.0)) * u * N2;
   };
 
-  // ---- a4: (shifted) Cholesky with breakdown-triggered re-shift
-  int shifted = 0, bpiv = 0, piv;
+  // ---- a4: (shifted) Cholesky with breakdown-triggered re-shift.  SAFE / FIXED shift pass 1
+  // (Alg. 3 line 4); ADAPTIVE tries every pass unshifted first (Alg. 2); PRACTICAL
+  // shifts pass 1 with s_p = u N2 (N_B) (Remark P:1600-1606) and falls back to the safe s when
+  // chol(A + s_p I) breaks down (reading D21).
+  int shifted = 0, bpiv = 0, piv = 1;
   double bval = 0.0, pv = 0.0, s = 0.0, N2 = 0.0;
-  if (p.pass == 1 && p.shift_mode != SCQR3_SHIFT_NONE) {
-    s = shift_for(N2);
-    clk[3] = clock64();
-    shifted = 1;
-    piv = factor<SMEM>(W, ldw, n, s, true, &pv, &sflag, &sval, rinv);
-    if (piv) { bpiv = piv; bval = pv; }
-  } else {
-    clk[3] = clock64();
+  const bool practical = p.shift_mode == SCQR3_SHIFT_PRACTICAL;
+  const bool shift_first = p.pass == 1 && (p.shift_mode == SCQR3_SHIFT_SAFE || p.shift_mode == SCQR3_SHIFT_FIXED ||
+                                           practical);
+  bool w_dirty = false;
+  clk[3] = clock64();
+  if (!shift_first) {
     piv = factor<SMEM>(W, ldw, n, 0.0, false, &pv, &sflag, &sval, rinv);
-    if (piv) {
-      bpiv = piv;
-      bval = pv;
-      if (p.shift_mode != SCQR3_SHIFT_NONE) {
+    w_dirty = true;
+    if (piv) { bpiv = piv; bval = pv; }
+  }
+  if (piv && p.shift_mode != SCQR3_SHIFT_NONE) {
+    const double s_safe = shift_for(N2);
+    const double s_p = 0x1p-53 * N2 * (p.oblique ? *p.nb_dev : 1.0);
+    clk[3] = clock64();
+    for (int attempt = practical ? 0 : 1; attempt < 2 && piv; ++attempt) {
+      if (w_dirty) {
         __syncthreads();
         if (tid == 0) sflag = 0;
         load_W(p, W, ldw);
-        s = shift_for(N2);
-        shifted = 1;
-        piv = factor<SMEM>(W, ldw, n, s, true, &pv, &sflag, &sval, rinv);
-        if (piv) { bpiv = piv; bval = pv; }
       }
+      s = attempt == 0 ? s_p : s_safe;
+      shifted = 1;
+      piv = factor<SMEM>(W, ldw, n, s, true, &pv, &sflag, &sval, rinv);
+      w_dirty = true;
+      if (piv) { bpiv = piv; bval = pv; }
     }
   }
   const int code = piv ? SCQR3_EBREAKDOWN : SCQR3_OK;

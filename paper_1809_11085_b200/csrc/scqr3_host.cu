@@ -221,7 +221,7 @@ int carve(const Layout& L, const scqr3_opts* o, WS* w) {
 int check_opts(const scqr3_opts* o) {
   if (!o) return fail("opts is NULL");
   if (o->abi_version != SCQR3_ABI_VERSION) return fail("abi_version %d != %d", o->abi_version, SCQR3_ABI_VERSION);
-  if (o->shift_mode < 0 || o->shift_mode > 2) return fail("bad shift_mode %d", o->shift_mode);
+  if (o->shift_mode < 0 || o->shift_mode > 4) return fail("bad shift_mode %d", o->shift_mode);
   if (o->norm_mode < 0 || o->norm_mode > 2) return fail("bad norm_mode %d", o->norm_mode);
   if (o->norm_mode == SCQR3_NORM_USER && !(o->norm2_bound > 0)) return fail("NORM_USER needs norm2_bound > 0");
   if (o->shift_mode == SCQR3_SHIFT_FIXED && !(o->shift_value >= 0)) return fail("SHIFT_FIXED needs shift_value >= 0");

@@ -72,3 +72,13 @@ def test_no_oracle_in_the_product_path():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"(#|//).*", "", text).lower() or f == "build.py", f
+
+
+def test_header_enums_match_binding():
+    import re
+    hdr = open(os.path.join(ROOT, "include", "scqr3.h")).read()
+    vals = {k: int(v) for k, v in re.findall(r"SCQR3_(\w+) = (\d+)", hdr)}
+    for name in ["OK", "EINVAL", "EBREAKDOWN", "ENOCONV", "NORM_POWER", "NORM_FROBENIUS", "NORM_USER"]:
+        assert vals[name] == getattr(_abi, name)
+    for name in ["SAFE", "FIXED", "NONE", "ADAPTIVE", "PRACTICAL"]:
+        assert vals["SHIFT_" + name] == getattr(_abi, "SHIFT_" + name)

@@ -279,3 +279,23 @@ def test_single_rank_nccl_comm_path():
                                  deterministic=True)
     assert np.array_equal(host(c1.R), host(c3.R))
     comm.destroy()
+
+
+@gpu
+@pytest.mark.parametrize("mode", ["adaptive", "practical"])
+@pytest.mark.parametrize("m,n,kappa", [(3000, 12, 1e5), (20000, 64, 1e5), (2000, 16, 1e12), (1000, 50, 1e15),
+                                       (30000, 128, 1e10)])
+def test_shift_policies_parity(mode, m, n, kappa):
+    """ADAPTIVE (Alg. 2) and PRACTICAL (Remark P:1600-1606, reading D21) on the GPU
+    against the oracle: same shift decisions where they are not within rounding of a
+    threshold, R parity and the BJ accuracy target."""
+    sm = {"adaptive": sq.SHIFT_ADAPTIVE, "practical": sq.SHIFT_PRACTICAL}[mode]
+    X = synth.randsvd(m, n, kappa, seed=0)
+    rg = sq.scqr3_factor(dev(X), shift_mode=sm)
+    ro = oracle.scqr3(X, shift_mode=sm)
+    _compare(X, rg, ro, kappa)
+    if kappa <= 1e5:   # far below u^-1/2: CholeskyQR2 (adaptive) / tiny shift (practical)
+        assert rg.passes == ro.passes == 2
+        assert [t["shifted"] for t in rg.trace] == [t.shifted for t in ro.trace]
+    if mode == "practical":   # pass 1 is always shifted (by s_p, or by the safe s after a
+        assert rg.trace[0]["shifted"] and ro.trace[0].shifted   # breakdown within rounding)

@@ -190,3 +190,60 @@ def test_status_codes():
     Z = np.zeros((50, 3))                               # rank-deficient: unsupported
     r = oracle.scqr3(Z)
     assert r.status in (2, 3)
+
+
+# ------------------------------------------------ shift policies beyond Alg. 3
+@pytest.mark.parametrize("kappa", [1e2, 1e5, 1e7])
+def test_adaptive_is_cholesky_qr2_below_u_half(kappa):
+    """Alg. 2 shifts only on breakdown: for kappa(X) < u^-1/2 no Cholesky breaks
+    down and two plain passes (CholeskyQR2) give R = Householder's R."""
+    X = synth.randsvd(3000, 12, kappa, seed=4)
+    r = oracle.scqr3(X, shift_mode=oracle.SHIFT_ADAPTIVE)
+    assert r.status == 0 and r.passes == 2
+    assert not any(t.shifted for t in r.trace) and all(t.breakdown_pivot == 0 for t in r.trace)
+    _, Rh = householder_R(X)
+    assert np.max(np.abs(r.R - Rh)) <= 1e3 * 12 * U * kappa * np.linalg.norm(X, 2)
+    assert oracle.orth_F(r.Q) <= 10 * 12 * U and oracle.resid_F(X, r.Q, r.R) <= 10 * 12 * U
+
+
+def test_adaptive_shifts_after_a_pass1_breakdown():
+    """PR1 (kappa=1e12): pass 1's plain Cholesky breaks down (the CholeskyQR2 failure pinned
+    above), so Alg. 2 introduces the safe shift on that pass and then runs like Alg. 3."""
+    X = synth.randsvd(2000, 16, 1e12, seed=0)
+    r = oracle.scqr3(X, shift_mode=oracle.SHIFT_ADAPTIVE)
+    plain = oracle.scqr3(X, shift_mode=oracle.SHIFT_NONE, max_passes=1)
+    assert plain.status == 2
+    assert r.status == 0 and r.trace[0].shifted and r.trace[0].breakdown_pivot == plain.trace[0].breakdown_pivot
+    safe = oracle.scqr3(X)
+    assert r.trace[0].shift == safe.trace[0].shift
+    assert np.array_equal(r.R, safe.R)   # same shift on the same Gram: identical arithmetic
+
+
+def test_practical_shift_first_pass_closed_form():
+    """X = [diag(sigma); 0] has the exact Gram diag(sigma^2), so pass 1 of PRACTICAL gives
+    R~ = diag(sqrt(sigma^2 + s)) with s = u * N^2, N^2 ~ sigma_1^2 (Remark P:1600-1606), and
+    kappa(Q1) equals the closed form of P:555-563."""
+    sig = np.array([1.0, 0.5, 1e-3, 2e-5, 1e-6, 3e-7])
+    n = sig.size
+    X = np.zeros((40, n))
+    X[np.arange(n), np.arange(n)] = sig
+    r = oracle.scqr3(X, shift_mode=oracle.SHIFT_PRACTICAL, max_passes=1)
+    t = r.trace[0]
+    assert t.shifted and t.breakdown_pivot == 0
+    assert 1.0 <= t.shift / U <= 1.02     # u * 1.01 * lambda_max, lambda_max = sigma_1^2 = 1
+    assert np.allclose(np.diag(r.R), np.sqrt(sig ** 2 + t.shift), rtol=4 * U, atol=0)
+    kq = np.linalg.cond(r.Q)
+    assert abs(kq / closed_form_kappa_q1(sig, t.shift) - 1) <= 1e-9
+    safe = oracle.scqr3(X, max_passes=1)
+    assert kq < np.linalg.cond(safe.Q)   # the smaller shift reduces kappa(Q1) further (Fig. 2)
+
+
+def test_practical_falls_back_to_safe_shift_on_breakdown():
+    """Fig. 2's setting (m=1000, n=50, kappa=1e15): chol(A + u||X||^2 I) is not guaranteed
+     and breaks down here; the fallback is the safe shift (reading D21)."""
+    X = synth.randsvd(1000, 50, 1e15, seed=0)
+    r = oracle.scqr3(X, shift_mode=oracle.SHIFT_PRACTICAL)
+    safe = oracle.scqr3(X)
+    assert r.status == 0 and r.trace[0].breakdown_pivot > 0
+    assert r.trace[0].shift == safe.trace[0].shift
+    assert oracle.orth_F(r.Q) <= 10 * 50 * U
