@@ -332,7 +332,7 @@ def run_ours(args):
                                    f"({cfg.spectrum} sigma, U,V Householder of N(0,1)), seed 0",
                        "m": m, "n": n, "kappa": cfg.kappa, "passes": passes,
                        "shifted": [t["shifted"] for t in res.trace], "parallelism": f"row-block x{world}",
-                       "l2": "no flush: X and Q (10.24 GB each) >> 126 MB L2"},
+                       "l2": f"no flush: X and Q ({8 * mloc * n / 1e9:.2f} GB each per GPU) >> 126 MB L2"},
             "roofline": roofline,
             "roofline_step": {"ms": step_roof_ms, "frac": step_roof_ms / ms,
                               "model": "max(6mn^2 / fp64 peak, 72mn bytes / 6536.7 GB/s) per GPU"},

@@ -8,7 +8,8 @@ it returns; neither is imported here.
 
 Recipes (DESIGN.md "Inputs"):
   * U (m x n) and V (n x n): Householder QR (LAPACK geqrf/orgqr via numpy, or cuSOLVER via
-    torch on the device) of i.i.d. N(0,1) matrices, columns sign-normalised so diag(R) > 0.
+    torch on the device; above 16 GB a chunked Householder TSQR, reading D17) of i.i.d. N(0,1)
+    matrices, columns sign-normalised so diag(R) > 0.
   * sigma geometric: sigma_i = kappa^{-(i-1)/(n-1)}, i = 1..n (||X||_2 = 1, kappa_2 = kappa).
   * sigma "cluster" (BASELINE config 4, reading D15): sigma_1 = 1, sigma_2..sigma_{n-8}
     log-uniform in [1e-6, 1] sorted descending, the last 8 equal to 1/kappa (= 1e-14).
@@ -104,12 +105,35 @@ def randsvd_torch(m: int, n: int, kappa: float, seed: int = 0, spectrum: str = "
     ld = ld or m
     g = torch.Generator(device=device)
     g.manual_seed(int(seed) * 1000003 + TAG_U)
-    G = torch.randn((n, m), generator=g, dtype=torch.float64, device=device).t()  # col-major (m, n)
-    Uq, Ur = torch.linalg.qr(G, mode="reduced")
-    del G
-    sgn = torch.sign(torch.diagonal(Ur))
-    sgn[sgn == 0] = 1.0
-    del Ur
+    chunk = 1 << 20
+    if m * n * 8 <= (16 << 30):
+        G = torch.randn((n, m), generator=g, dtype=torch.float64, device=device).t()  # col-major (m, n)
+        Uq, Ur = torch.linalg.qr(G, mode="reduced")
+        del G
+        sgn = torch.sign(torch.diagonal(Ur))
+        sgn[sgn == 0] = 1.0
+        del Ur
+    else:
+        # Too large for one device Householder QR next to X and Q (C4: 82 GB): Householder TSQR
+        # in place (reading D17) -- per-chunk QR, QR of the stacked chunk R's, then each chunk's
+        # Q times its block of the second Q.  Same thin Q factor up to rounding.
+        buf = torch.empty((n, ld), dtype=torch.float64, device=device)
+        Uq = buf.t()[:m]
+        Rs = []
+        for r0 in range(0, m, chunk):
+            r1 = min(m, r0 + chunk)
+            Gc = torch.randn((n, r1 - r0), generator=g, dtype=torch.float64, device=device).t()
+            Qc, Rc = torch.linalg.qr(Gc, mode="reduced")
+            Uq[r0:r1].copy_(Qc)
+            Rs.append(Rc)
+            del Gc, Qc
+        Q2, R2 = torch.linalg.qr(torch.cat(Rs, 0), mode="reduced")
+        for i, r0 in enumerate(range(0, m, chunk)):
+            r1 = min(m, r0 + chunk)
+            Uq[r0:r1].copy_(Uq[r0:r1] @ Q2[i * n:(i + 1) * n])
+        sgn = torch.sign(torch.diagonal(R2))
+        sgn[sgn == 0] = 1.0
+        del Rs, Q2, R2
     gv = torch.Generator(device=device)
     gv.manual_seed(int(seed) * 1000003 + TAG_V)
     Gv = torch.randn((n, n), generator=gv, dtype=torch.float64, device=device)
@@ -117,9 +141,11 @@ def randsvd_torch(m: int, n: int, kappa: float, seed: int = 0, spectrum: str = "
     Vq = Vq * torch.sign(torch.diagonal(Vr))
     s = torch.as_tensor(sigma(n, kappa, spectrum, seed), dtype=torch.float64, device=device)
     W = (sgn * s)[:, None] * Vq.t()                       # diag(sgn*sigma) V^T, n x n
-    out = torch.empty((n, ld), dtype=torch.float64, device=device)
-    Xc = out.t()[:m]                                        # (m, n), strides (1, ld)
-    chunk = 1 << 22
+    if m * n * 8 > (16 << 30):
+        Xc = Uq                                             # overwrite U in place, row chunk by chunk
+    else:
+        out = torch.empty((n, ld), dtype=torch.float64, device=device)
+        Xc = out.t()[:m]                                    # (m, n), strides (1, ld)
     for r0 in range(0, m, chunk):
         r1 = min(m, r0 + chunk)
         Xc[r0:r1].copy_(Uq[r0:r1] @ W)
