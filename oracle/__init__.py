@@ -64,6 +64,13 @@ def _load():
         i64, dbl = ctypes.c_int64, ctypes.c_double
         lib.orc_gram.argtypes = [i64, i64, P, i64, P]
         lib.orc_gram_oblique.argtypes = [i64, i64, P, i64, P, P, P, P]
+        PI64, PI32 = ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int32)
+        lib.orc_gram_oblique_csr.argtypes = [i64, i64, P, i64, PI64, PI32, P, P, P]
+        lib.orc_orth_F_csr.argtypes = [i64, i64, P, i64, PI64, PI32, P]
+        lib.orc_orth_F_csr.restype = dbl
+        lib.orc_scqr3_csr.argtypes = [i64, i64, P, i64, PI64, PI32, P, P, i64, P, ctypes.POINTER(_Opts),
+                                      ctypes.POINTER(_Trace), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+        lib.orc_scqr3_csr.restype = ctypes.c_int
         lib.orc_cholesky.argtypes = [i64, P, dbl, P, ctypes.POINTER(i64), P]
         lib.orc_cholesky.restype = ctypes.c_int
         lib.orc_trsm_rows.argtypes = [i64, i64, P, i64, P, P, i64]
@@ -127,6 +134,39 @@ def gram_oblique(X, d, e):
     cs = np.zeros(n)
     _load().orc_gram_oblique(m, n, _p(X), m, _p(d), _p(e), _p(A), _p(cs))
     return A, cs
+
+
+def _csr(B):
+    """(row_ptr int64[m+1], col_idx int32[nnz], vals float64[nnz]) -> ctypes pointers."""
+    rp, ci, cv = B
+    rp = np.ascontiguousarray(rp, dtype=np.int64)
+    ci = np.ascontiguousarray(ci, dtype=np.int32)
+    cv = np.ascontiguousarray(cv, dtype=np.float64)
+    keep = (rp, ci, cv)
+    return (rp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), ci.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+            _p(cv), keep)
+
+
+def gram_oblique_csr(X, B):
+    """A = X^T B X for a CSR metric B, symmetrised; also diag(X^T X)."""
+    X = _colmajor(X)
+    m, n = X.shape
+    prp, pci, pcv, keep = _csr(B)
+    A = np.zeros((n, n), order="F")
+    cs = np.zeros(n)
+    _load().orc_gram_oblique_csr(m, n, _p(X), m, prp, pci, pcv, _p(A), _p(cs))
+    del keep
+    return A, cs
+
+
+def orth_F_csr(Q, B) -> float:
+    """||Q^T B Q - I||_F for a CSR metric, Dot2-compensated."""
+    Q = _colmajor(Q)
+    m, n = Q.shape
+    prp, pci, pcv, keep = _csr(B)
+    r = float(_load().orc_orth_F_csr(m, n, _p(Q), m, prp, pci, pcv))
+    del keep
+    return r
 
 
 @dataclass
@@ -222,13 +262,13 @@ class Result:
 
 def scqr3(X, d=None, e=None, *, shift_mode=SHIFT_SAFE, shift_value=0.0, norm_mode=NORM_POWER,
           norm2_bound=0.0, bnorm_bound=0.0, max_passes=8, stop_tol=0.5, power_iters=32,
-          m_global=0, nparts=1) -> Result:
+          m_global=0, nparts=1, csr=None) -> Result:
     """Shifted CholeskyQR3 with breakdown re-shift (Alg. 3 P:698-711 + Alg. 2).
 
     shift_mode ADAPTIVE: Alg. 2 literally (no shift on pass 1 unless chol breaks down);
     PRACTICAL: shifted attempts try s_p = u*N2 first (Remark P:1600-1606), then the safe s.
-
-    Oblique (d, e given): Alg. 5 with the B-Gram in every pass (D8)."""
+    Oblique (d, e given, or csr=(row_ptr, col_idx, vals)): Alg. 5 with the
+    B-Gram in every pass (D8)."""
     X = _colmajor(X)
     m, n = X.shape
     Q = np.zeros((m, n), order="F")
@@ -241,8 +281,14 @@ def scqr3(X, d=None, e=None, *, shift_mode=SHIFT_SAFE, shift_value=0.0, norm_mod
     cap = max(max_passes, 1)
     tr = (_Trace * cap)()
     passes = ctypes.c_int(0)
-    st = _load().orc_scqr3(m, n, _p(X), m, _p(d), _p(e), _p(Q), m, _p(R), ctypes.byref(o), tr, cap,
-                           ctypes.byref(passes))
+    if csr is not None:
+        prp, pci, pcv, keep = _csr(csr)
+        st = _load().orc_scqr3_csr(m, n, _p(X), m, prp, pci, pcv, _p(Q), m, _p(R), ctypes.byref(o), tr, cap,
+                                   ctypes.byref(passes))
+        del keep
+    else:
+        st = _load().orc_scqr3(m, n, _p(X), m, _p(d), _p(e), _p(Q), m, _p(R), ctypes.byref(o), tr, cap,
+                               ctypes.byref(passes))
     k = passes.value
     trace = [PassTrace(t.shift, bool(t.shifted), t.breakdown_pivot, t.pivot_value, t.norm2_est, t.dev_F)
              for t in list(tr)[:k]]

@@ -22,6 +22,11 @@
  *                         against an exact rational/extended reference, symmetry)
  *   orc_gram_oblique      pinned (B=I reduces to orc_gram; exact integer cases;
  *                         brute force dense X^T B X)
+ *   orc_gram_oblique_csr  pinned (CSR of the tridiagonal B in the same term order is
+ *                         bitwise orc_gram_oblique; CSR identity = orc_gram; exact integer
+ *                         cases against int64 arithmetic)
+ *   orc_scqr3_csr         pinned (CSR-tridiagonal equals orc_scqr3 bitwise; 2-D Laplacian
+ *                         B: Q^T B Q = I and X = QR within the T9 ceilings)
  *   orc_cholesky          pinned (exact hand cases, S:69 breakdown, T2 backward error)
  *   orc_trsm_rows         pinned (S:78 hand case, T3 row-wise backward error)
  *   orc_trmul             pinned (brute force)
@@ -92,25 +97,61 @@ void orc_gram(int64_t m, int64_t n, const double* X, int64_t ld, double* A) {
 }
 
 /* ------------------------------------------------------------------------- */
-/* Oblique Gram A = X^T B X for SPD tridiagonal B (Alg. 4 line 1).
- * B(i,i) = d[i], B(i,i+1) = B(i+1,i) = e[i] (e[m-1] unused).
- * Y = B X row by row: y_i = d_i x_i + e_{i-1} x_{i-1} + e_i x_{i+1} (terms in this
- * order, missing neighbours omitted), then A = X^T Y summed over rows ascending,
- * then symmetrised A <- (A + A^T)/2 because fl(X^T (BX)) is not exactly symmetric
- * (S:262).  colsq[j] = sum_i x_ij^2 (= diag(X^T X), for the Frobenius bound, D4). */
-void orc_gram_oblique(int64_t m, int64_t n, const double* X, int64_t ld, const double* d,
-                      const double* e, double* A, double* colsq) {
+/* The SPD metric B of the oblique inner product (Alg. 4/5).
+ *   tridiagonal: B(i,i) = d[i], B(i,i+1) = B(i+1,i) = e[i] (e[m-1] unused);
+ *   CSR: row i holds cv[k] at column ci[k] for
+ *   k = rp[i] .. rp[i+1]-1 (0-based global columns, B symmetric).
+ * (B x)_i is formed row by row: tridiagonal d_i x_i + e_{i-1} x_{i-1} + e_i x_{i+1} (terms
+ * in this order, missing neighbours omitted); CSR sum of cv[k] x[ci[k]] in storage order. */
+typedef struct orc_metric {
+  const double* d;
+  const double* e;
+  const int64_t* rp;
+  const int32_t* ci;
+  const double* cv;
+} orc_metric;
+
+static double bx_row(const orc_metric* B, int64_t m, const double* x, int64_t i) {
+  if (B->rp) {
+    double v = 0.0;
+    for (int64_t k = B->rp[i]; k < B->rp[i + 1]; ++k) v = v + B->cv[k] * x[B->ci[k]];
+    return v;
+  }
+  double v = B->d[i] * x[i];
+  if (i > 0) v = v + B->e[i - 1] * x[i - 1];
+  if (i + 1 < m) v = v + B->e[i] * x[i + 1];
+  return v;
+}
+
+/* ||B||_inf = max_i sum_k |B_ik| >= ||B||_2 (Gershgorin, reading D4). */
+static double metric_norm_inf(const orc_metric* B, int64_t m) {
+  double nb = 0.0;
+  for (int64_t i = 0; i < m; ++i) {
+    double r = 0.0;
+    if (B->rp) {
+      for (int64_t k = B->rp[i]; k < B->rp[i + 1]; ++k) r = r + fabs(B->cv[k]);
+    } else {
+      r = B->d[i];
+      if (i > 0) r = r + fabs(B->e[i - 1]);
+      if (i + 1 < m) r = r + fabs(B->e[i]);
+    }
+    if (r > nb) nb = r;
+  }
+  return nb;
+}
+
+/* Oblique Gram A = X^T B X (Alg. 4 line 1): Y = B X row by row, then
+ * A = X^T Y summed over rows ascending, then symmetrised A <- (A + A^T)/2 because
+ * fl(X^T (BX)) is not exactly symmetric.  colsq[j] = sum_i x_ij^2 (= diag(X^T X),
+ * for the Frobenius bound, D4). */
+static void gram_metric(int64_t m, int64_t n, const double* X, int64_t ld, const orc_metric* B, double* A,
+                        double* colsq) {
   double* Y = (double*)malloc((size_t)m * (size_t)n * sizeof(double));
 #pragma omp parallel for schedule(static)
   for (int64_t j = 0; j < n; ++j) {
     const double* x = X + j * ld;
     double* y = Y + j * m;
-    for (int64_t i = 0; i < m; ++i) {
-      double v = d[i] * x[i];
-      if (i > 0) v = v + e[i - 1] * x[i - 1];
-      if (i + 1 < m) v = v + e[i] * x[i + 1];
-      y[i] = v;
-    }
+    for (int64_t i = 0; i < m; ++i) y[i] = bx_row(B, m, x, i);
   }
   double* G = (double*)malloc((size_t)n * (size_t)n * sizeof(double));
 #pragma omp parallel for schedule(dynamic)
@@ -135,6 +176,18 @@ void orc_gram_oblique(int64_t m, int64_t n, const double* X, int64_t ld, const d
   }
   free(G);
   free(Y);
+}
+
+void orc_gram_oblique(int64_t m, int64_t n, const double* X, int64_t ld, const double* d,
+                      const double* e, double* A, double* colsq) {
+  const orc_metric B = {d, e, NULL, NULL, NULL};
+  gram_metric(m, n, X, ld, &B, A, colsq);
+}
+
+void orc_gram_oblique_csr(int64_t m, int64_t n, const double* X, int64_t ld, const int64_t* rp,
+                          const int32_t* ci, const double* cv, double* A, double* colsq) {
+  const orc_metric B = {NULL, NULL, rp, ci, cv};
+  gram_metric(m, n, X, ld, &B, A, colsq);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -272,8 +325,31 @@ static inline void two_prod(double a, double b, double* p, double* e) {
   *p = x;
 }
 
-/* ||Q^T B Q - I||_F with compensated (Dot2) accumulation of every entry
- * (B = I when d == NULL).  Orthogonality measure of P:1547, P:1633 (Frobenius). */
+/* ||Q^T Y - I||_F with compensated (Dot2) accumulation of every entry, Y = B Q (Y == NULL:
+ * B = I).  Orthogonality measure of P:1547, P:1633 (Frobenius). */
+static double orth_core(int64_t m, int64_t n, const double* Q, int64_t ld, const double* Y) {
+  double tot = 0.0;
+#pragma omp parallel for schedule(dynamic) reduction(+ : tot)
+  for (int64_t jl = 0; jl < n * n; ++jl) {
+    int64_t j = jl % n, l = jl / n;
+    if (j > l) continue;
+    const double* a = Q + j * ld;
+    const double* b = Y ? Y + l * m : Q + l * ld;
+    double s = 0, c = 0, p, pe, t, te;
+    for (int64_t i = 0; i < m; ++i) {
+      two_prod(a[i], b[i], &p, &pe);
+      two_sum(s, p, &t, &te);
+      s = t;
+      c += te + pe;
+    }
+    double v = s + c;
+    if (j == l) v = v - 1.0;
+    tot += (j == l ? 1.0 : 2.0) * v * v;
+  }
+  return sqrt(tot);
+}
+
+/* ||Q^T B Q - I||_F, B tridiagonal (d, e) or I (d == NULL); y = B q in double-double. */
 double orc_orth_F(int64_t m, int64_t n, const double* Q, int64_t ld, const double* d, const double* e) {
   double* Y = NULL;
   if (d) {
@@ -289,26 +365,30 @@ double orc_orth_F(int64_t m, int64_t n, const double* Q, int64_t ld, const doubl
         Y[i + j * m] = s + c;
       }
   }
-  double tot = 0.0;
-#pragma omp parallel for schedule(dynamic) reduction(+ : tot)
-  for (int64_t jl = 0; jl < n * n; ++jl) {
-    int64_t j = jl % n, l = jl / n;
-    if (j > l) continue;
-    const double* a = Q + j * ld;
-    const double* b = d ? Y + l * m : Q + l * ld;
-    double s = 0, c = 0, p, pe, t, te;
-    for (int64_t i = 0; i < m; ++i) {
-      two_prod(a[i], b[i], &p, &pe);
-      two_sum(s, p, &t, &te);
-      s = t;
-      c += te + pe;
-    }
-    double v = s + c;
-    if (j == l) v = v - 1.0;
-    tot += (j == l ? 1.0 : 2.0) * v * v;
-  }
+  const double r = orth_core(m, n, Q, ld, Y);
   free(Y);
-  return sqrt(tot);
+  return r;
+}
+
+/* ||Q^T B Q - I||_F for a CSR metric B; y = B q in double-double. */
+double orc_orth_F_csr(int64_t m, int64_t n, const double* Q, int64_t ld, const int64_t* rp, const int32_t* ci,
+                      const double* cv) {
+  double* Y = (double*)malloc((size_t)m * (size_t)n * sizeof(double));
+#pragma omp parallel for schedule(static)
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t i = 0; i < m; ++i) {
+      double s = 0, c = 0, p, pe, t, te;
+      for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+        two_prod(cv[k], Q[ci[k] + j * ld], &p, &pe);
+        two_sum(s, p, &t, &te);
+        s = t;
+        c += te + pe;
+      }
+      Y[i + j * m] = s + c;
+    }
+  const double r = orth_core(m, n, Q, ld, Y);
+  free(Y);
+  return r;
 }
 
 /* ||X - Q R||_F / ||X||_F with compensated row products (D13). */
@@ -377,10 +457,11 @@ typedef struct orc_trace {
   double dev_F;        /* ||A_k - I||_F of the pass's input Gram */
 } orc_trace;
 
-static void gram_any(int64_t m, int64_t n, const double* Q, int64_t ld, const double* d, const double* e,
+static void gram_any(int64_t m, int64_t n, const double* Q, int64_t ld, const orc_metric* B,
                      int nparts, double* A, double* colsq) {
+  const int d = B != NULL; /* oblique */
   if (nparts <= 1) {
-    if (d) orc_gram_oblique(m, n, Q, ld, d, e, A, colsq);
+    if (d) gram_metric(m, n, Q, ld, B, A, colsq);
     else orc_gram(m, n, Q, ld, A);
     return;
   }
@@ -400,12 +481,7 @@ static void gram_any(int64_t m, int64_t n, const double* Q, int64_t ld, const do
       int64_t mp = r1 - r0;
       double* Y = (double*)malloc((size_t)mp * (size_t)n * sizeof(double));
       for (int64_t j = 0; j < n; ++j)
-        for (int64_t i = r0; i < r1; ++i) {
-          double v = d[i] * Q[i + j * ld];
-          if (i > 0) v = v + e[i - 1] * Q[i - 1 + j * ld];
-          if (i + 1 < m) v = v + e[i] * Q[i + 1 + j * ld];
-          Y[(i - r0) + j * mp] = v;
-        }
+        for (int64_t i = r0; i < r1; ++i) Y[(i - r0) + j * mp] = bx_row(B, m, Q + j * ld, i);
       for (int64_t l = 0; l < n; ++l)
         for (int64_t j = 0; j < n; ++j) {
           double s = 0.0;
@@ -436,27 +512,18 @@ static void gram_any(int64_t m, int64_t n, const double* Q, int64_t ld, const do
 }
 
 /* Returns 0 ok, 2 breakdown even with the shift, 3 not converged, 1 bad argument. */
-int orc_scqr3(int64_t m, int64_t n, const double* X, int64_t ld, const double* d, const double* e,
-              double* Q, int64_t ldq, double* R, const orc_opts* o, orc_trace* trace, int trace_cap,
-              int* passes_out) {
+static int scqr3_impl(int64_t m, int64_t n, const double* X, int64_t ld, const orc_metric* B,
+                      double* Q, int64_t ldq, double* R, const orc_opts* o, orc_trace* trace, int trace_cap,
+                      int* passes_out) {
   if (m < 1 || n < 1 || ld < m || ldq < m) return 1;
   const int max_passes = o->max_passes > 0 ? o->max_passes : 8;
   const double stop_tol = o->stop_tol > 0 ? o->stop_tol : 0.5;
   const int iters = o->power_iters > 0 ? o->power_iters : 32;
   const double mg = o->m_global > 0 ? o->m_global : (double)m;
-  const int oblique = d != NULL;
+  const int oblique = B != NULL;
 
   double NB = 0.0;
-  if (oblique) {
-    if (o->bnorm_bound > 0) NB = o->bnorm_bound;
-    else
-      for (int64_t i = 0; i < m; ++i) { /* Gershgorin: ||B||_2 <= ||B||_inf (D4) */
-        double r = d[i];
-        if (i > 0) r = r + fabs(e[i - 1]);
-        if (i + 1 < m) r = r + fabs(e[i]);
-        if (r > NB) NB = r;
-      }
-  }
+  if (oblique) NB = o->bnorm_bound > 0 ? o->bnorm_bound : metric_norm_inf(B, m); /* (D4) */
 
   for (int64_t j = 0; j < n; ++j)
     for (int64_t i = 0; i < m; ++i) Q[i + j * ldq] = X[i + j * ld];
@@ -468,7 +535,7 @@ int orc_scqr3(int64_t m, int64_t n, const double* X, int64_t ld, const double* d
   double* colsq = (double*)malloc((size_t)n * sizeof(double));
   int status = 3, k = 0;
   for (k = 1; k <= max_passes; ++k) {
-    gram_any(m, n, Q, ldq, d, e, o->nparts, A, colsq);
+    gram_any(m, n, Q, ldq, B, o->nparts, A, colsq);
     double dev = 0.0;
     for (int64_t l = 0; l < n; ++l)
       for (int64_t j = 0; j < n; ++j) {
@@ -548,6 +615,22 @@ int orc_scqr3(int64_t m, int64_t n, const double* X, int64_t ld, const double* d
   free(Rt);
   free(colsq);
   return status;
+}
+
+int orc_scqr3(int64_t m, int64_t n, const double* X, int64_t ld, const double* d, const double* e,
+              double* Q, int64_t ldq, double* R, const orc_opts* o, orc_trace* trace, int trace_cap,
+              int* passes_out) {
+  const orc_metric B = {d, e, NULL, NULL, NULL};
+  return scqr3_impl(m, n, X, ld, d ? &B : NULL, Q, ldq, R, o, trace, trace_cap, passes_out);
+}
+
+/* Oblique shifted CholeskyQR3 with a general sparse SPD B in CSR. */
+int orc_scqr3_csr(int64_t m, int64_t n, const double* X, int64_t ld, const int64_t* rp, const int32_t* ci,
+                  const double* cv, double* Q, int64_t ldq, double* R, const orc_opts* o, orc_trace* trace,
+                  int trace_cap, int* passes_out) {
+  if (!rp || !ci || !cv) return 1;
+  const orc_metric B = {NULL, NULL, rp, ci, cv};
+  return scqr3_impl(m, n, X, ld, &B, Q, ldq, R, o, trace, trace_cap, passes_out);
 }
 
 int orc_num_threads(void) {

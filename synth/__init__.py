@@ -89,6 +89,59 @@ def tridiag_b(m: int, seed: int = 0):
     return d, e
 
 
+def tridiag_csr(d: np.ndarray, e: np.ndarray):
+    """The tridiagonal metric (d, e) in CSR, each row's entries in the order (i, i-1, i+1)
+    (the term order of the banded formula), so both forms describe the same operation."""
+    m = d.size
+    rp = np.zeros(m + 1, dtype=np.int64)
+    ci, cv = [], []
+    for i in range(m):
+        ci.append(i); cv.append(d[i])
+        if i > 0:
+            ci.append(i - 1); cv.append(e[i - 1])
+        if i + 1 < m:
+            ci.append(i + 1); cv.append(e[i])
+        rp[i + 1] = len(ci)
+    return rp, np.asarray(ci, dtype=np.int32), np.asarray(cv, dtype=np.float64)
+
+
+def laplacian2d(nx: int, ny: int, seed: int | None = None, wmax: float = 1.0):
+    """5-point 2-D Laplacian on an nx x ny grid (Dirichlet), m = nx*ny rows in row-major grid
+    order, as CSR (row_ptr int64, col_idx int32, vals float64) with each row's diagonal first,
+    then the neighbours ascending -- the synthetic stand-in for the paper's sparse SPD B
+    (not available).  With seed: D^1/2 L D^1/2, d_i log-uniform in
+    [1, wmax] (still SPD)."""
+    m = nx * ny
+    i = np.arange(m)
+    gx, gy = i % nx, i // nx
+    w = np.ones(m) if seed is None else 10.0 ** np.random.default_rng([seed, TAG_B]).uniform(0.0, np.log10(wmax), m)
+    sw = np.sqrt(w)
+    nbr = [(gy > 0, -nx), (gx > 0, -1), (gx + 1 < nx, 1), (gy + 1 < ny, nx)]
+    cnt = 1 + sum(ok.astype(np.int64) for ok, _ in nbr)
+    rp = np.zeros(m + 1, dtype=np.int64)
+    rp[1:] = np.cumsum(cnt)
+    ci = np.empty(rp[-1], dtype=np.int32)
+    cv = np.empty(rp[-1], dtype=np.float64)
+    pos = rp[:-1].copy()
+    ci[pos] = i
+    cv[pos] = 4.0 * w
+    pos += 1
+    for ok, off in nbr:
+        rows = i[ok]
+        ci[pos[ok]] = rows + off
+        cv[pos[ok]] = -sw[rows] * sw[rows + off]
+        pos[ok] += 1
+    return rp, ci, cv
+
+
+def csr_rows(B, r0: int, r1: int):
+    """Rows [r0, r1) of a CSR matrix with column indices made relative to r0 (a rank's shard;
+    neighbours' rows appear as negative / >= r1-r0 indices, served by the halo)."""
+    rp, ci, cv = B
+    a, b = rp[r0], rp[r1]
+    return rp[r0:r1 + 1] - a, (ci[a:b].astype(np.int64) - r0).astype(np.int32), cv[a:b].copy()
+
+
 def random_rows(m: int, n: int, seed: int = 0) -> np.ndarray:
     """Plain i.i.d. N(0,1) column-major matrix (kernel-level tests)."""
     rng = np.random.default_rng([seed, 7])

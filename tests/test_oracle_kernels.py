@@ -84,6 +84,50 @@ def test_gram_oblique_exact_integers(m, n):
     assert np.array_equal(cs, (Xi.astype(np.int64) ** 2).sum(0).astype(float))
 
 
+def _random_sym_csr(m, rng, density=0.05):
+    """Random symmetric integer sparse matrix as CSR (diagonal first, then ascending)."""
+    M = np.zeros((m, m), dtype=np.int64)
+    mask = np.triu(rng.random((m, m)) < density, 1)
+    M[mask] = rng.integers(-9, 10, size=mask.sum())
+    M = M + M.T
+    M[np.diag_indices(m)] = rng.integers(1, 40, size=m)
+    rp, ci, cv = [0], [], []
+    for i in range(m):
+        cols = [i] + [j for j in range(m) if j != i and M[i, j] != 0]
+        ci += cols
+        cv += [float(M[i, j]) for j in cols]
+        rp.append(len(ci))
+    return M, (np.array(rp), np.array(ci), np.array(cv))
+
+
+@pytest.mark.parametrize("m,n", [(3, 2), (40, 5), (120, 9)])
+def test_gram_oblique_csr_exact_integers(m, n):
+    """General sparse B: integer X and B keep every product and sum exact,
+    so the result must equal int64 arithmetic X^T B X bit for bit."""
+    rng = np.random.default_rng(3 * m + n)
+    M, B = _random_sym_csr(m, rng)
+    Xi = rng.integers(-20, 21, size=(m, n))
+    ref = Xi.T @ M @ Xi
+    A, cs = oracle.gram_oblique_csr(Xi.astype(float), B)
+    assert np.array_equal(A, ref.astype(float))
+    assert np.array_equal(cs, (Xi ** 2).sum(0).astype(float))
+
+
+def test_gram_oblique_csr_tridiagonal_and_identity():
+    """The tridiagonal metric written as CSR in the banded term order is the same operation
+    (bitwise equal to the pinned banded Gram); the CSR identity gives the plain Gram."""
+    X = synth.random_rows(700, 11, seed=4)
+    d, e = synth.tridiag_b(700, seed=2)
+    A1, c1 = oracle.gram_oblique(X, d, e)
+    A2, c2 = oracle.gram_oblique_csr(X, synth.tridiag_csr(d, e))
+    assert np.array_equal(A1, A2) and np.array_equal(c1, c2)
+    eye = (np.arange(701), np.arange(700, dtype=np.int32), np.ones(700))
+    A3, _ = oracle.gram_oblique_csr(X, eye)
+    assert np.array_equal(A3, oracle.gram(X))
+    Q = synth.random_rows(700, 6, seed=5)
+    assert oracle.orth_F_csr(Q, synth.tridiag_csr(d, e)) == oracle.orth_F(Q, d, e)
+
+
 # --------------------------------------------------------------------------- Cholesky (P:139, P:271-289)
 def test_cholesky_spec_examples():
     g = GOLD["chol_25_20"]

@@ -247,3 +247,42 @@ def test_practical_falls_back_to_safe_shift_on_breakdown():
     assert r.status == 0 and r.trace[0].breakdown_pivot > 0
     assert r.trace[0].shift == safe.trace[0].shift
     assert oracle.orth_F(r.Q) <= 10 * 50 * U
+
+
+# ------------------------------------------------ general sparse SPD metric
+def test_csr_tridiagonal_is_the_banded_method():
+    """Same metric, same term order: the CSR path reproduces the pinned banded path bitwise."""
+    m, n = 3000, 16
+    X = synth.randsvd(m, n, 1e12, seed=0)
+    d, e = synth.tridiag_b(m, seed=0)
+    a = oracle.scqr3(X, d, e)
+    b = oracle.scqr3(X, csr=synth.tridiag_csr(d, e))
+    assert a.status == b.status == 0 and a.passes == b.passes
+    assert np.array_equal(a.R, b.R) and np.array_equal(a.Q, b.Q)
+    assert [t.shift for t in a.trace] == [t.shift for t in b.trace]
+
+
+def test_csr_laplacian_metric_ceilings():
+    """2-D Laplacian metric (stand-in for the paper's sparse SPD matrices):
+    Q^T B Q = I and X = QR within Thm. thm:Bsta's ceilings, and Q is genuinely
+    B-orthonormal (not orthonormal)."""
+    import scipy.sparse as sp
+    nx, ny, n = 60, 50, 12
+    m = nx * ny
+    B = synth.laplacian2d(nx, ny, seed=3, wmax=1e2)
+    X = synth.randsvd(m, n, 1e10, seed=1)
+    r = oracle.scqr3(X, csr=B)
+    assert r.status == 0 and r.trace[0].shifted
+    Bd = sp.csr_matrix((B[2], B[1], B[0]), shape=(m, m)).toarray()
+    ev = np.linalg.eigvalsh(Bd)
+    kB = ev[-1] / ev[0]
+    orthB = oracle.orth_F_csr(r.Q, B)
+    res = oracle.resid_F(X, r.Q, r.R)
+    assert orthB <= 8 * (m * np.sqrt(m * n) + n * (n + 1)) * U * kB
+    assert res <= 16 * n * n * U * kB ** 1.5
+    assert orthB <= 10 * n * U and res <= 10 * n * U
+    assert oracle.orth_F(r.Q) > 1e-3
+    # brute force: Q^T B Q against the dense B in extended precision
+    Ql = r.Q.astype(np.longdouble)
+    G = Ql.T @ (Bd.astype(np.longdouble) @ Ql)
+    assert abs(float(np.linalg.norm(G - np.eye(n), "fro")) - orthB) <= 1e-16 + 1e-3 * orthB
