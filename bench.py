@@ -130,15 +130,15 @@ def run_reference(args):
     n = cfg.n
     rows = args.cpu_rows or max(n, int(5e6 * (128 / n) ** 2))
     rows = min(rows, cfg.m)
-    X = synth.randsvd(rows, n, cfg.kappa, seed=0, spectrum=cfg.spectrum)
     kw = {}
     if cfg.oblique:
-        d, e = synth.tridiag_b(rows, seed=0)
-        kw = dict(d=d, e=e)
+        kind, B, rows = synth.config_metric(cfg, rows)
+        kw = dict(csr=B) if kind == "csr" else dict(d=B[0], e=B[1])
+    X = synth.randsvd(rows, n, cfg.kappa, seed=0, spectrum=cfg.spectrum)
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        r = oracle.scqr3(X, **kw) if not cfg.oblique else oracle.scqr3(X, kw["d"], kw["e"])
+        r = oracle.scqr3(X, **kw)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
@@ -177,6 +177,8 @@ def run_ours(args):
     dev = torch.device("cuda", torch.cuda.current_device())
     cfg = synth.CONFIGS[args.config]
     m, n = (args.m or cfg.m), cfg.n
+    if cfg.oblique and cfg.metric == "laplacian":
+        m = max(cfg.grid_nx, (m // cfg.grid_nx) * cfg.grid_nx)   # whole grid lines
     from paper_1809_11085_b200.dist import row_block
 
     r0, r1 = row_block(m, rank, world)
@@ -190,8 +192,12 @@ def run_ours(args):
         X = sq.colmajor_empty(mloc, n, device=dev)
         X.copy_(Xg[r0:r1])
         del Xg
-    d = e = None
-    if cfg.oblique:
+    d = e = csr = None
+    if cfg.oblique and cfg.metric == "laplacian":
+        Bg = synth.laplacian2d(cfg.grid_nx, m // cfg.grid_nx, seed=0, wmax=1e4)
+        csr = sq.CsrMetric(*synth.csr_rows(Bg, r0, r1), halo=cfg.grid_nx if world > 1 else 0, device=dev)
+        del Bg
+    elif cfg.oblique:
         dg, eg = synth.tridiag_b_torch(m, seed=0, device=dev)
         d, e = dg[r0:r1].contiguous(), eg[r0:r1].contiguous()
         del dg, eg
@@ -200,7 +206,8 @@ def run_ours(args):
 
     comm = sq.Comm.create() if world > 1 else None
     stream = torch.cuda.Stream(device=dev)
-    ws = sq.workspace(mloc, n, oblique=cfg.oblique, device=dev)
+    ws = (sq.workspace(mloc, n, device=dev, csr_halo=csr.halo) if csr is not None
+          else sq.workspace(mloc, n, oblique=cfg.oblique, device=dev))
     Q = sq.colmajor_empty(mloc, n, device=dev)
     R = torch.empty((n, n), dtype=torch.float64, device=dev).t()
     prof = _abi.Prof()
@@ -209,6 +216,8 @@ def run_ours(args):
         kw = dict(Q=Q, R=R, ws=ws, comm=comm, m_global=m, stream=stream)
         if with_prof:
             kw["prof"] = prof
+        if csr is not None:
+            return sq.scqr3_factor_oblique_csr(X, csr, **kw)
         if cfg.oblique:
             return sq.scqr3_factor_oblique(X, d, e, **kw)
         return sq.scqr3_factor(X, **kw)
@@ -312,12 +321,15 @@ def run_ours(args):
 
         rows = args.cpu_rows or max(n, int(1e7 * (128 / n) ** 2))
         rows = min(rows, mloc)
+        okw = {}
+        if csr is not None:
+            _, Bs, rows = synth.config_metric(cfg, rows)
+            okw = dict(csr=Bs)
+        elif cfg.oblique:
+            okw = dict(d=d[:rows].cpu().numpy(), e=e[:rows].cpu().numpy())
         Xs = X[:rows].cpu().numpy()
         t0 = time.perf_counter()
-        if cfg.oblique:
-            ro = oracle.scqr3(Xs, d[:rows].cpu().numpy(), e[:rows].cpu().numpy())
-        else:
-            ro = oracle.scqr3(Xs)
+        ro = oracle.scqr3(Xs, **okw)
         tc = time.perf_counter() - t0
         cpu = {"value": flops_3pass(rows, n) / tc / 1e12, "unit": "TFLOP/s", "cores": oracle.num_threads(),
                "kind": "oracle", "seconds": tc, "passes": ro.passes, "status": ro.status,

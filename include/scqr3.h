@@ -134,6 +134,35 @@ int scqr3_factor_oblique(int64_t m, int64_t n, const double* X, int64_t ld, cons
                          const double* b_off, double* Q, int64_t ldq, double* R,
                          const scqr3_opts* opts);
 
+/* General sparse SPD metric B in CSR (the paper's sparse-B experiments,
+ * P:1876-1888).  All arrays are DEVICE arrays owned by the caller and hold this
+ * rank's rows of B:
+ *   row_ptr[m+1]  int64, row_ptr[0] = 0, non-decreasing;
+ *   col_idx[nnz]  int32 column indices RELATIVE to this rank's first row: a value c in
+ *                 [0, m) is a local row of Q, c in [-halo, 0) a row of the previous rank
+ *                 (its last halo rows), c in [m, m + halo) one of the next rank's first
+ *                 halo rows;
+ *   vals[nnz]     float64, B symmetric positive definite (not checked).
+ * halo: rows exchanged with each neighbouring rank per pass (NCCL send/recv, like the
+ * tridiagonal halo); 0 on one GPU (required without opts->comm).  Each rank must own at
+ * least halo rows.  Index and row_ptr violations are detected on the device -> EINVAL. */
+typedef struct scqr3_csr {
+  const int64_t* row_ptr;
+  const int32_t* col_idx;
+  const double* vals;
+  int64_t halo;
+} scqr3_csr;
+
+/* Workspace bytes for the CSR-metric calls (the halo buffers scale with halo * n). */
+size_t scqr3_workspace_size_csr(int64_t m, int64_t n, int64_t halo);
+
+/* Oblique shifted CholeskyQR3 (Alg. 5 with the B-Gram in all passes, D8) for a CSR metric:
+ * Y = B Q by csr_y_kernel, then the same Gram / shift / Cholesky / TRSM path; the shift's
+ * ||B||_2 bound is opts->bnorm_bound or the Gershgorin max_i sum_k |B_ik| (allreduce-max
+ * over ranks).  Target Q^T B Q = I, X = QR. */
+int scqr3_factor_oblique_csr(int64_t m, int64_t n, const double* X, int64_t ld, const scqr3_csr* B,
+                             double* Q, int64_t ldq, double* R, const scqr3_opts* opts);
+
 /* Host-memory variant of scqr3_factor (the end-to-end call): copies X_host to the device
  * (pinned host memory recommended), factors in place, copies Q and R back.  opts->workspace
  * must hold scqr3_host_workspace_size(m, n) bytes. */
@@ -144,9 +173,13 @@ int scqr3_factor_host(int64_t m, int64_t n, const double* X_host, int64_t ld, do
 /* ---- kernel-level entry points (parity tests call these through the same library) ---- */
 /* A = Q^T Q (n x n, column-major, both triangles) -- one Gram kernel + reduction. */
 int scqr3_gram(int64_t m, int64_t n, const double* X, int64_t ld, double* A, const scqr3_opts* opts);
-/* A = sym(X^T B X) for the tridiagonal B above; colsq[j] = sum_i x_ij^2. */
+/* A = sym(X^T B X) for the tridiagonal B above; *colsq = ||X||_F^2 (D4). */
 int scqr3_gram_oblique(int64_t m, int64_t n, const double* X, int64_t ld, const double* b_diag,
                        const double* b_off, double* A, double* colsq, const scqr3_opts* opts);
+/* A = sym(X^T B X) for a CSR metric (B->halo must be 0; single GPU), *colsq = ||X||_F^2.
+ * Workspace: scqr3_workspace_size_csr(m, n, 0). */
+int scqr3_gram_oblique_csr(int64_t m, int64_t n, const double* X, int64_t ld, const scqr3_csr* B,
+                           double* A, double* colsq, const scqr3_opts* opts);
 /* R~ = chol(A + sI) (upper, n x n column-major) with breakdown detection (D9).
  * Returns SCQR3_EBREAKDOWN with *pivot (1-based) and *pivot_value on a pivot <= 0 or
  * non-finite, else SCQR3_OK with *pivot = 0. */

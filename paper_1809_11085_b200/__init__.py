@@ -19,7 +19,8 @@ from ._abi import (EBREAKDOWN, EINVAL, ENOCONV, NORM_FROBENIUS, NORM_POWER, NORM
 __all__ = [
     "scqr3_factor", "scqr3_factor_oblique", "scqr3_factor_host", "scqr3_gram", "scqr3_gram_oblique",
     "scqr3_cholesky", "scqr3_trsm", "colmajor_empty", "to_colmajor", "workspace", "Comm", "Result",
-    "ScqrError", "launch_count", "library_path",
+    "ScqrError", "launch_count", "library_path", "CsrMetric", "scqr3_factor_oblique_csr",
+    "scqr3_gram_oblique_csr",
 ]
 
 library_path = _abi.LIB_PATH
@@ -89,10 +90,13 @@ def _ld(X) -> int:
     return max(X.stride(1), 1) if X.shape[1] > 1 else even_ld(X.shape[0])
 
 
-def workspace(m: int, n: int, oblique: bool = False, device="cuda", host_io: bool = False):
+def workspace(m: int, n: int, oblique: bool = False, device="cuda", host_io: bool = False, csr_halo=None):
     torch = _torch()
     L = _abi.lib()
-    nbytes = L.scqr3_host_workspace_size(m, n) if host_io else L.scqr3_workspace_size(m, n, int(oblique))
+    if csr_halo is not None:
+        nbytes = L.scqr3_workspace_size_csr(m, n, int(csr_halo))
+    else:
+        nbytes = L.scqr3_host_workspace_size(m, n) if host_io else L.scqr3_workspace_size(m, n, int(oblique))
     if nbytes == 0:
         raise ScqrError(f"unsupported size m={m} n={n}")
     return torch.empty(nbytes, dtype=torch.uint8, device=device)
@@ -193,6 +197,52 @@ def scqr3_factor_oblique(X, d, e, *, Q=None, R=None, ws=None, inplace=False, **k
     rc = _check(_abi.lib().scqr3_factor_oblique(m, n, X.data_ptr(), _ld(X), d.data_ptr(), e.data_ptr(),
                                                 Q.data_ptr(), _ld(Q), R.data_ptr(), ctypes.byref(o)))
     return Result(rc, Q, R, passes.value, _trace(tr, passes.value))
+
+
+class CsrMetric:
+    """This rank's rows of a sparse SPD metric B in CSR on the device:
+    row_ptr int64[m+1], col_idx int32[nnz] relative to the rank's first row (halo rows of the
+    neighbours are negative / >= m), vals float64[nnz]."""
+
+    def __init__(self, row_ptr, col_idx, vals, halo: int = 0, device="cuda"):
+        torch = _torch()
+        self.row_ptr = torch.as_tensor(row_ptr, dtype=torch.int64, device=device).contiguous()
+        self.col_idx = torch.as_tensor(col_idx, dtype=torch.int32, device=device).contiguous()
+        self.vals = torch.as_tensor(vals, dtype=torch.float64, device=device).contiguous()
+        self.halo = int(halo)
+
+    def c(self):
+        return _abi.Csr(self.row_ptr.data_ptr(), self.col_idx.data_ptr(), self.vals.data_ptr(), self.halo)
+
+
+def scqr3_factor_oblique_csr(X, B: CsrMetric, *, Q=None, R=None, ws=None, inplace=False, **kw) -> Result:
+    """Oblique shifted CholeskyQR3 for a general sparse SPD metric B (CSR)."""
+    torch = _torch()
+    m, n = X.shape
+    if Q is None:
+        Q = X if inplace else colmajor_empty(m, n, device=X.device)
+    if R is None:
+        R = torch.empty((n, n), dtype=torch.float64, device=X.device).t()
+    if ws is None:
+        ws = workspace(m, n, device=X.device, csr_halo=B.halo)
+    o, tr, passes = _opts(ws=ws, **kw)
+    cb = B.c()
+    rc = _check(_abi.lib().scqr3_factor_oblique_csr(m, n, X.data_ptr(), _ld(X), ctypes.byref(cb), Q.data_ptr(),
+                                                    _ld(Q), R.data_ptr(), ctypes.byref(o)))
+    return Result(rc, Q, R, passes.value, _trace(tr, passes.value))
+
+
+def scqr3_gram_oblique_csr(X, B: CsrMetric, *, ws=None, **kw):
+    torch = _torch()
+    m, n = X.shape
+    A = torch.empty((n, n), dtype=torch.float64, device=X.device).t()
+    cs = torch.empty(1, dtype=torch.float64, device=X.device)
+    ws = ws if ws is not None else workspace(m, n, device=X.device, csr_halo=0)
+    o, _, _ = _opts(ws=ws, **kw)
+    cb = B.c()
+    _check(_abi.lib().scqr3_gram_oblique_csr(m, n, X.data_ptr(), _ld(X), ctypes.byref(cb), A.data_ptr(),
+                                             cs.data_ptr(), ctypes.byref(o)))
+    return A, cs
 
 
 def scqr3_factor_host(X, *, Q=None, R=None, ws=None, **kw) -> Result:

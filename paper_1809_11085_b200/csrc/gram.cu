@@ -277,6 +277,95 @@ __global__ void oblique_y_kernel(ObliqueYParams p) {
   }
 }
 
+// Y = B Q for a general sparse metric in CSR, plus the
+// ||Q||_F^2 partials like oblique_y_kernel.  One thread per (row, 8-column chunk): consecutive
+// threads take consecutive rows, so each nonzero's Q reads are coalesced along the column;
+// rows outside [0, m) come from the halo buffers (neighbouring ranks' rows).
+__global__ void csr_y_kernel(ObliqueYParams p) {
+  __shared__ double red[32];
+  const int nch = (p.n + 7) / 8;
+  const long long total = p.m * nch;
+  double sq = 0.0;
+  for (long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
+       k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = k % p.m;
+    const int c0 = static_cast<int>(k / p.m) * 8;
+    const int cw = min(8, p.n - c0);
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+    for (long long z = p.rp[i]; z < p.rp[i + 1]; ++z) {
+      const long long col = p.ci[z];
+      const double v = p.cv[z];
+      const double* src;
+      long long ld;
+      if (col < 0) {
+        src = p.halo_prev + (col + p.halo);
+        ld = p.halo;
+      } else if (col >= p.m) {
+        src = p.halo_next + (col - p.m);
+        ld = p.halo;
+      } else {
+        src = p.Q + col;
+        ld = p.ldq;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < cw) acc[j] = fma(v, src[(c0 + j) * ld], acc[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < cw) {
+        p.Y[(c0 + j) * p.ldy + i] = acc[j];
+        const double qi = p.Q[i + (c0 + j) * p.ldq];
+        sq = fma(qi, qi, sq);
+      }
+  }
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) p.colsq_partials[blockIdx.x] = v;
+  }
+}
+
+// Gershgorin bound max_i sum_k |B_ik| >= ||B||_2 for a CSR metric (reading D4).
+__global__ void csr_gershgorin_kernel(const long long* rp, const double* cv, long long m, double* partial) {
+  __shared__ double red[32];
+  double mx = 0.0;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double r = 0.0;
+    for (long long z = rp[i]; z < rp[i + 1]; ++z) r += fabs(cv[z]);
+    mx = fmax(mx, r);
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) partial[blockIdx.x] = v;
+  }
+}
+
+// Argument check of a CSR metric on the device: row_ptr non-decreasing from 0, every column
+// index inside [-halo, m + halo).  *bad is set to 1 on any violation.
+__global__ void csr_check_kernel(const long long* rp, const int* ci, long long m, long long halo, int* bad) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long a = rp[i], b = rp[i + 1];
+    if ((i == 0 && a != 0) || b < a) {
+      *bad = 1;
+      continue;
+    }
+    for (long long z = a; z < b; ++z)
+      if (ci[z] < -halo || ci[z] >= m + halo) *bad = 1;
+  }
+}
+
 // Gershgorin bound max_i d_i + |e_{i-1}| + |e_i| >= ||B||_2 (reading D4); one partial per block.
 __global__ void gershgorin_kernel(const double* d, const double* e, long long m, int has_prev, double e_prev,
                                   int has_next, double* partial) {

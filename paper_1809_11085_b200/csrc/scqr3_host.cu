@@ -156,7 +156,7 @@ struct Layout {
   size_t st, partials, tiles, W, Rnew, Rt, bfrag, dblk, misc, colsq, y, halo, end;
 };
 
-Layout make_layout(int64_t m, int64_t n, int oblique) {
+Layout make_layout(int64_t m, int64_t n, int oblique, int64_t halo = 1) {
   Layout L{};
   L.n = static_cast<int>(n);
   L.npad = npad_for(L.n);
@@ -188,7 +188,7 @@ Layout make_layout(int64_t m, int64_t n, int oblique) {
   L.misc = take(64 * 8);  // [0] nb, [1] e_prev, [2] m_global (int64), ...
   L.colsq = oblique ? take(4096 * 8) : off;
   L.y = oblique ? take(static_cast<size_t>(L.ldy) * n * 8) : off;
-  L.halo = oblique ? take(static_cast<size_t>(4 * n) * 8) : off;
+  L.halo = oblique ? take(static_cast<size_t>(4 * std::max<int64_t>(halo, 1) * n) * 8) : off;
   L.end = off;
   return L;
 }
@@ -323,7 +323,8 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
     colsq_count = static_cast<int>(std::max<long long>(blocks, 1));
     p.colsq_partials = w.colsq;
     const int ps = prof_begin(c, PK_REDUCE);
-    oblique_y_kernel<<<colsq_count, 256, 0, st>>>(p);
+    if (p.rp) csr_y_kernel<<<colsq_count, 256, 0, st>>>(p);
+    else oblique_y_kernel<<<colsq_count, 256, 0, st>>>(p);
     prof_end(c, ps);
     ++g_launches;
     CUDA_TRY(cudaGetLastError());
@@ -416,41 +417,59 @@ int launch_trmul(Ctx* c, const double* Rt, double* R, double* Rnew, int n, int f
 
 bool w_fits_smem(int n) { return static_cast<size_t>(n) * (n + 1) * 8 <= 200 * 1024; }
 
-int halo_exchange(Comm* cm, const double* Qsrc, int64_t ld, int64_t m, int n, double* halo, cudaStream_t st) {
-  // halo layout: [0,n) my first row, [n,2n) my last row, [2n,3n) prev rank's last row, [3n,4n) next rank's first row
-  if (!cm) return SCQR3_OK;
-  if (m > 0) {
-    CUDA_TRY(cudaMemcpy2DAsync(halo, 8, Qsrc, ld * 8, 8, n, cudaMemcpyDeviceToDevice, st));
-    CUDA_TRY(cudaMemcpy2DAsync(halo + n, 8, Qsrc + (m - 1), ld * 8, 8, n, cudaMemcpyDeviceToDevice, st));
-  }
+int halo_exchange(Comm* cm, const double* Qsrc, int64_t ld, int64_t m, int n, int64_t h, double* halo,
+                  cudaStream_t st) {
+  // halo layout, each block h x n column-major (ld h): [0] my first h rows, [1] my last h rows,
+  // [2] the previous rank's last h rows, [3] the next rank's first h rows
+  if (!cm || h <= 0) return SCQR3_OK;
+  if (m < h) return fail("halo of %lld rows exceeds this rank's %lld rows", (long long)h, (long long)m);
+  const size_t blk = static_cast<size_t>(h) * n;
+  CUDA_TRY(cudaMemcpy2DAsync(halo, h * 8, Qsrc, ld * 8, h * 8, n, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(cudaMemcpy2DAsync(halo + blk, h * 8, Qsrc + (m - h), ld * 8, h * 8, n, cudaMemcpyDeviceToDevice, st));
   NCCL_TRY(ncclGroupStart());
   if (cm->rank > 0) {
-    NCCL_TRY(ncclSend(halo, n, ncclDouble, cm->rank - 1, cm->nccl, st));
-    NCCL_TRY(ncclRecv(halo + 2 * n, n, ncclDouble, cm->rank - 1, cm->nccl, st));
+    NCCL_TRY(ncclSend(halo, blk, ncclDouble, cm->rank - 1, cm->nccl, st));
+    NCCL_TRY(ncclRecv(halo + 2 * blk, blk, ncclDouble, cm->rank - 1, cm->nccl, st));
   }
   if (cm->rank + 1 < cm->nranks) {
-    NCCL_TRY(ncclSend(halo + n, n, ncclDouble, cm->rank + 1, cm->nccl, st));
-    NCCL_TRY(ncclRecv(halo + 3 * n, n, ncclDouble, cm->rank + 1, cm->nccl, st));
+    NCCL_TRY(ncclSend(halo + blk, blk, ncclDouble, cm->rank + 1, cm->nccl, st));
+    NCCL_TRY(ncclRecv(halo + 3 * blk, blk, ncclDouble, cm->rank + 1, cm->nccl, st));
   }
   NCCL_TRY(ncclGroupEnd());
   return SCQR3_OK;
 }
 
-int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const double* bd, const double* be, double* Q,
-                int64_t ldq, double* R, const scqr3_opts* o) {
+// The oblique metric of a factorisation: none (standard), tridiagonal bands, or CSR.
+struct Metric {
+  const double* d = nullptr;
+  const double* e = nullptr;
+  const scqr3_csr* csr = nullptr;
+  bool oblique() const { return d != nullptr || csr != nullptr; }
+  int64_t halo() const { return csr ? csr->halo : 1; }
+};
+
+int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric& B, double* Q, int64_t ldq,
+                double* R, const scqr3_opts* o) {
   TRY(check_opts(o));
-  const bool oblique = bd != nullptr;
+  const bool oblique = B.oblique();
+  const double* bd = B.d;
+  const double* be = B.e;
   if (n < 1 || n > kMaxN) return fail("n=%lld outside [1, %d]", (long long)n, kMaxN);
   if (m < 0) return fail("m < 0");
   TRY(check_matrix("X", X, m, ld));
   TRY(check_matrix("Q", Q, m, ldq));
   if (!R) return fail("R is NULL");
-  if (oblique && m > 0 && !be) return fail("b_off is NULL");
+  if (B.d && m > 0 && !be) return fail("b_off is NULL");
+  if (B.csr) {
+    if (m > 0 && (!B.csr->row_ptr || !B.csr->col_idx || !B.csr->vals)) return fail("CSR metric has a NULL array");
+    if (B.csr->halo < 0) return fail("CSR halo < 0");
+    if (!o->comm && B.csr->halo != 0) return fail("CSR halo must be 0 without a communicator");
+  }
   Ctx* c;
   TRY(get_ctx(&c));
   cudaStream_t st = static_cast<cudaStream_t>(o->stream);
   Comm* cm = static_cast<Comm*>(o->comm);
-  const Layout L = make_layout(m, n, oblique);
+  const Layout L = make_layout(m, n, oblique, B.halo());
   WS w;
   TRY(carve(L, o, &w));
   c->prof = o->prof;
@@ -488,11 +507,30 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const double*
     yp.n = static_cast<int>(n);
     yp.has_prev = rank > 0;
     yp.has_next = rank + 1 < nranks;
-    yp.halo_prev = w.halo + 2 * n;
-    yp.halo_next = w.halo + 3 * n;
+    const int64_t hb = B.halo() * n;  // one halo block (halo x n)
+    yp.halo_prev = w.halo + 2 * hb;
+    yp.halo_next = w.halo + 3 * hb;
+    if (B.csr) {
+      yp.rp = reinterpret_cast<const long long*>(B.csr->row_ptr);
+      yp.ci = B.csr->col_idx;
+      yp.cv = B.csr->vals;
+      yp.halo = B.csr->halo;
+      if (m > 0) {  // argument check on the device (indices inside this rank's rows + halo)
+        int* bad = reinterpret_cast<int*>(w.misc + 12);
+        CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), st));
+        const int blocks = static_cast<int>(std::max<long long>(1, std::min<long long>((m + 255) / 256, 1024)));
+        csr_check_kernel<<<blocks, 256, 0, st>>>(yp.rp, yp.ci, m, yp.halo, bad);
+        ++g_launches;
+        CUDA_TRY(cudaGetLastError());
+        int hbad = 0;
+        CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (hbad) return fail("CSR metric: row_ptr not monotone from 0 or a column index outside [-halo, m+halo)");
+      }
+    }
     // e_prev = previous rank's b_off[m_prev - 1]
     double e_prev = 0.0;
-    if (multi) {
+    if (multi && B.d) {
       double* ebuf = w.misc + 8;  // [8] send, [9] recv
       if (m > 0) CUDA_TRY(cudaMemcpyAsync(ebuf, be + (m - 1), 8, cudaMemcpyDeviceToDevice, st));
       NCCL_TRY(ncclGroupStart());
@@ -510,7 +548,8 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const double*
       double* part = w.colsq;
       const int blocks = static_cast<int>(std::max<long long>(1, std::min<long long>((m + 255) / 256, 1024)));
       if (m > 0) {
-        gershgorin_kernel<<<blocks, 256, 0, st>>>(bd, be, m, yp.has_prev, e_prev, yp.has_next, part);
+        if (B.csr) csr_gershgorin_kernel<<<blocks, 256, 0, st>>>(yp.rp, yp.cv, m, part);
+        else gershgorin_kernel<<<blocks, 256, 0, st>>>(bd, be, m, yp.has_prev, e_prev, yp.has_next, part);
         ++g_launches;
         CUDA_TRY(cudaGetLastError());
       } else {
@@ -561,7 +600,7 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const double*
   for (k = 1; k <= max_passes; ++k) {
     if (oblique) {
       const int ph = cm ? prof_begin(c, PK_COMM) : -1;
-      TRY(halo_exchange(cm, src, ldsrc, m, static_cast<int>(n), w.halo, st));
+      TRY(halo_exchange(cm, src, ldsrc, m, static_cast<int>(n), B.halo(), w.halo, st));
       prof_end(c, ph);
       yp.Q = src;
       yp.ldq = ldsrc;
@@ -658,14 +697,30 @@ size_t scqr3_workspace_size(int64_t m, int64_t n, int32_t oblique) {
 
 int scqr3_factor(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, int64_t ldq, double* R,
                  const scqr3_opts* opts) {
-  return factor_impl(m, n, X, ld, nullptr, nullptr, Q, ldq, R, opts);
+  return factor_impl(m, n, X, ld, Metric{}, Q, ldq, R, opts);
 }
 
 int scqr3_factor_oblique(int64_t m, int64_t n, const double* X, int64_t ld, const double* b_diag,
                          const double* b_off, double* Q, int64_t ldq, double* R, const scqr3_opts* opts) {
   if (!b_diag && m > 0) return fail("b_diag is NULL");
   static const double dummy = 0.0;
-  return factor_impl(m, n, X, ld, b_diag ? b_diag : &dummy, b_off, Q, ldq, R, opts);
+  Metric B;
+  B.d = b_diag ? b_diag : &dummy;
+  B.e = b_off;
+  return factor_impl(m, n, X, ld, B, Q, ldq, R, opts);
+}
+
+size_t scqr3_workspace_size_csr(int64_t m, int64_t n, int64_t halo) {
+  if (n < 1 || n > kMaxN || m < 0 || halo < 0) return 0;
+  return make_layout(m, n, 1, halo).end;
+}
+
+int scqr3_factor_oblique_csr(int64_t m, int64_t n, const double* X, int64_t ld, const scqr3_csr* B_csr, double* Q,
+                             int64_t ldq, double* R, const scqr3_opts* opts) {
+  if (!B_csr) return fail("CSR metric is NULL");
+  Metric B;
+  B.csr = B_csr;
+  return factor_impl(m, n, X, ld, B, Q, ldq, R, opts);
 }
 
 size_t scqr3_host_workspace_size(int64_t m, int64_t n) {
@@ -693,7 +748,7 @@ int scqr3_factor_host(int64_t m, int64_t n, const double* X_host, int64_t ld, do
   cudaStream_t st = static_cast<cudaStream_t>(opts->stream);
   if (m > 0)
     CUDA_TRY(cudaMemcpy2DAsync(D, ldd * 8, X_host, ld * 8, m * 8, n, cudaMemcpyHostToDevice, st));
-  int rc = factor_impl(m, n, D, ldd, nullptr, nullptr, D, ldd, Rd, &o2);
+  int rc = factor_impl(m, n, D, ldd, Metric{}, D, ldd, Rd, &o2);
   if (rc != SCQR3_OK) return rc;
   if (m > 0)
     CUDA_TRY(cudaMemcpy2DAsync(Q_host, ldq * 8, D, ldd * 8, m * 8, n, cudaMemcpyDeviceToHost, st));
@@ -744,6 +799,40 @@ int scqr3_gram_oblique(int64_t m, int64_t n, const double* X, int64_t ld, const 
   yp.ldy = L.ldy;
   yp.m = m;
   yp.n = static_cast<int>(n);
+  TRY(run_gram(c, L, w, X, ld, m, true, &yp, st));
+  const long long nn = n * n;
+  tiles_to_full_kernel<<<static_cast<unsigned>((nn + 255) / 256), 256, 0, st>>>(w.tiles, static_cast<int>(n), A);
+  ++g_launches;
+  CUDA_TRY(cudaGetLastError());
+  if (colsq) CUDA_TRY(cudaMemcpyAsync(colsq, w.tiles + L.tiles_sym * 64, 8, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return SCQR3_OK;
+}
+
+int scqr3_gram_oblique_csr(int64_t m, int64_t n, const double* X, int64_t ld, const scqr3_csr* B, double* A,
+                           double* colsq, const scqr3_opts* opts) {
+  TRY(check_opts(opts));
+  if (n < 1 || n > kMaxN || m < 1) return fail("bad sizes");
+  TRY(check_matrix("X", X, m, ld));
+  if (!B || !B->row_ptr || !B->col_idx || !B->vals) return fail("CSR metric has a NULL array");
+  if (B->halo != 0) return fail("kernel-level CSR Gram takes no halo (halo must be 0)");
+  Ctx* c;
+  TRY(get_ctx(&c));
+  const Layout L = make_layout(m, n, 1, 0);
+  WS w;
+  TRY(carve(L, opts, &w));
+  cudaStream_t st = static_cast<cudaStream_t>(opts->stream);
+  ObliqueYParams yp{};
+  yp.Q = X;
+  yp.ldq = ld;
+  yp.Y = w.y;
+  yp.ldy = L.ldy;
+  yp.m = m;
+  yp.n = static_cast<int>(n);
+  yp.rp = reinterpret_cast<const long long*>(B->row_ptr);
+  yp.ci = B->col_idx;
+  yp.cv = B->vals;
+  yp.halo = 0;
   TRY(run_gram(c, L, w, X, ld, m, true, &yp, st));
   const long long nn = n * n;
   tiles_to_full_kernel<<<static_cast<unsigned>((nn + 255) / 256), 256, 0, st>>>(w.tiles, static_cast<int>(n), A);

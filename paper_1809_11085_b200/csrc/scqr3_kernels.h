@@ -50,9 +50,15 @@ struct ObliqueYParams {
   int n;
   int has_prev, has_next;
   double e_prev;
-  const double* halo_prev;   // n doubles: previous rank's last row of Q
-  const double* halo_next;   // n doubles: next rank's first row of Q
+  const double* halo_prev;   // halo x n (ld halo): previous rank's last rows of Q
+  const double* halo_next;   // halo x n (ld halo): next rank's first rows of Q
   double* colsq_partials;    // one per block
+  // general sparse metric in CSR (rp != nullptr): column indices relative to
+  // this rank's first row, in [-halo, m + halo)
+  const long long* rp;
+  const int* ci;
+  const double* cv;
+  long long halo;
 };
 
 enum CholMode { CHOL_PASS = 0, CHOL_ONLY = 1 };
@@ -97,6 +103,9 @@ struct TrsmParams {
 __global__ void gram_tma_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapY,
                                 GramParams p);
 __global__ void gram_reduce_kernel(GramReduceParams p);
+__global__ void csr_y_kernel(ObliqueYParams p);
+__global__ void csr_gershgorin_kernel(const long long* rp, const double* cv, long long m, double* partial);
+__global__ void csr_check_kernel(const long long* rp, const int* ci, long long m, long long halo, int* bad);
 __global__ void rank_sum_kernel(const double* parts, int nparts, long long count, double* out);
 __global__ void oblique_y_kernel(ObliqueYParams p);
 __global__ void gershgorin_kernel(const double* d, const double* e, long long m, int has_prev, double e_prev,

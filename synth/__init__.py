@@ -36,6 +36,8 @@ class Config:
     spectrum: str = "geometric"   # or "cluster"
     oblique: bool = False
     gpus: tuple = (1,)
+    metric: str = "tridiag"       # oblique metric: "tridiag" (BASELINE config 5) or "laplacian"
+    grid_nx: int = 1000           # laplacian: grid width (m = grid_nx * ny)
 
 
 # BASELINE.json "configs" (index 0..4)
@@ -45,7 +47,20 @@ CONFIGS = {
     "C3": Config("C3", 10_000_000, 128, 1e10, gpus=(1, 2, 4, 8)),
     "C4": Config("C4", 40_000_000, 256, 1e14, spectrum="cluster", gpus=(4, 8)),
     "C5": Config("C5", 2_000_000, 64, 1e12, oblique=True, gpus=(1, 8)),
+    # C5 with a general sparse SPD metric in CSR (stand-in for the paper's
+    # sparse matrices): weighted 5-point Laplacian on a 1000 x 2000 grid
+    "C5L": Config("C5L", 2_000_000, 64, 1e12, oblique=True, gpus=(1, 8), metric="laplacian"),
 }
+
+
+def config_metric(cfg: Config, rows: int):
+    """The oblique metric of a config restricted to its first `rows` rows (a principal
+    submatrix): tridiagonal bands (d, e), or the weighted Laplacian of the first rows // nx
+    grid lines as CSR.  Returns (kind, data, rows_used)."""
+    if cfg.metric == "laplacian":
+        ny = max(1, rows // cfg.grid_nx)
+        return "csr", laplacian2d(cfg.grid_nx, ny, seed=0, wmax=1e4), cfg.grid_nx * ny
+    return "tridiag", tridiag_b(rows, seed=0), rows
 
 
 def sigma(n: int, kappa: float, spectrum: str = "geometric", seed: int = 0) -> np.ndarray:

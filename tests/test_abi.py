@@ -82,3 +82,26 @@ def test_header_enums_match_binding():
         assert vals[name] == getattr(_abi, name)
     for name in ["SAFE", "FIXED", "NONE", "ADAPTIVE", "PRACTICAL"]:
         assert vals["SHIFT_" + name] == getattr(_abi, "SHIFT_" + name)
+
+
+def test_struct_layouts_against_the_compiled_header(tmp_path):
+    """sizeof/offsetof of every ABI struct as gcc lays out include/scqr3.h, vs the ctypes mirror."""
+    import subprocess
+    fields = {"scqr3_opts": (_abi.Opts, "Opts"), "scqr3_pass_trace": (_abi.PassTrace, "PassTrace"),
+              "scqr3_prof": (_abi.Prof, "Prof"), "scqr3_csr": (_abi.Csr, "Csr")}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "scqr3.h"', "int main(void) {"]
+    for cname, (cls, _) in fields.items():
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _t in cls._fields_:
+            lines.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    out = subprocess.check_output([str(exe)], text=True).split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
+    for cname, (cls, _) in fields.items():
+        assert got[(cname, "size")] == ctypes.sizeof(cls), cname
+        for f, _t in cls._fields_:
+            assert got[(cname, f)] == getattr(cls, f).offset, (cname, f)

@@ -69,6 +69,35 @@ def _worker(rank, world, port, q):
         if down is not None:
             Y[-1] += e[r1 - 1] * halo_next.numpy()
         res["Yrows"] = (r0, Y)
+        # ---- CSR metric: libscqr3's h-row halo protocol -- first h rows to
+        # the previous rank, last h rows to the next; column indices relative to the rank's
+        # first row, [-h, 0) -> previous rank's rows, [m_loc, m_loc + h) -> next rank's rows
+        nx, ny = 30, 40
+        mc = nx * ny
+        Bc = synth.laplacian2d(nx, ny, seed=1, wmax=10.0)
+        Xc = synth.randsvd(mc, n, 1e6, seed=6)
+        c0, c1 = pdist.row_block(mc, rank, world)
+        rp, ci, cv = synth.csr_rows(Bc, c0, c1)
+        h = nx                                                  # grid width = band half-width
+        Xcl = Xc[c0:c1]
+        hp, hn = torch.zeros((h, n), dtype=torch.float64), torch.zeros((h, n), dtype=torch.float64)
+        ops = []
+        if up is not None:
+            ops += [dist.P2POp(dist.isend, torch.from_numpy(Xcl[:h].copy()), up), dist.P2POp(dist.irecv, hp, up)]
+        if down is not None:
+            ops += [dist.P2POp(dist.isend, torch.from_numpy(Xcl[-h:].copy()), down),
+                    dist.P2POp(dist.irecv, hn, down)]
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        ext = np.vstack([hp.numpy(), Xcl, hn.numpy()])          # rows -h .. m_loc + h - 1
+        assert ci.min() >= -h and ci.max() < (c1 - c0) + h
+        Yc = np.zeros_like(Xcl)
+        for i in range(c1 - c0):
+            for z in range(rp[i], rp[i + 1]):
+                Yc[i] += cv[z] * ext[ci[z] + h]
+        G = torch.from_numpy(np.asfortranarray(Xcl.T @ Yc))
+        dist.all_reduce(G)
+        res["Gcsr"] = G.numpy()
         res["tmax"] = pdist.max_over_ranks(1.0 + rank)
         q.put((rank, res))
     finally:
@@ -117,3 +146,10 @@ def test_two_rank_gloo_decomposition_matches_single_process():
         r0, Yl = out[rank]["Yrows"]
         assert np.allclose(Yl, Yg[r0:r0 + Yl.shape[0]], rtol=1e-14, atol=1e-12)
     assert out[0]["tmax"] == out[1]["tmax"] == 2.0
+    # CSR halo protocol: the allreduced per-rank X^T (B X) equals the global Gram
+    Bc = synth.laplacian2d(30, 40, seed=1, wmax=10.0)
+    Xc = synth.randsvd(1200, n, 1e6, seed=6)
+    Ac, _ = oracle.gram_oblique_csr(Xc, Bc)
+    G = out[0]["Gcsr"]
+    assert np.array_equal(G, out[1]["Gcsr"])
+    assert np.max(np.abs((G + G.T) / 2 - Ac)) <= 1e-12 * np.max(np.abs(Ac))

@@ -299,3 +299,77 @@ def test_shift_policies_parity(mode, m, n, kappa):
         assert [t["shifted"] for t in rg.trace] == [t.shifted for t in ro.trace]
     if mode == "practical":   # pass 1 is always shifted (by s_p, or by the safe s after a
         assert rg.trace[0]["shifted"] and ro.trace[0].shifted   # breakdown within rounding)
+
+
+# ------------------------------------------------------------------ sparse SPD metric (CSR)
+def _csr_dev(B, halo=0):
+    return sq.CsrMetric(torch.from_numpy(B[0]), torch.from_numpy(B[1]), torch.from_numpy(B[2]), halo=halo)
+
+
+@gpu
+@pytest.mark.parametrize("m,n", [(3, 2), (40, 5), (513, 33), (3000, 64)])
+def test_gram_oblique_csr_exact_integers(m, n):
+    rng = np.random.default_rng(3 * m + n)
+    M = np.zeros((m, m), dtype=np.int64)
+    k = min(m * 6, m * m)
+    r, c = rng.integers(0, m, k), rng.integers(0, m, k)
+    M[r, c] = rng.integers(-9, 10, k)
+    M = np.triu(M, 1)
+    M = M + M.T
+    M[np.diag_indices(m)] = rng.integers(1, 40, m)
+    rp, ci, cv = [0], [], []
+    for i in range(m):
+        cols = [i] + [int(j) for j in np.nonzero(M[i])[0] if j != i]
+        ci += cols
+        cv += [float(M[i, j]) for j in cols]
+        rp.append(len(ci))
+    B = (np.array(rp, dtype=np.int64), np.array(ci, dtype=np.int32), np.array(cv))
+    Xi = rng.integers(-20, 21, size=(m, n))
+    A, cs = sq.scqr3_gram_oblique_csr(dev(Xi.astype(float)), _csr_dev(B))
+    assert np.array_equal(host(A), (Xi.T @ M @ Xi).astype(float))
+    assert cs.item() == float((Xi ** 2).sum())
+
+
+@gpu
+@pytest.mark.parametrize("nx,ny,n", [(60, 50, 12), (250, 200, 64), (100, 40, 128)])
+def test_factor_oblique_csr_laplacian(nx, ny, n):
+    """2-D Laplacian metric (stand-in for the paper's sparse SPD B): R parity with the oracle,
+    B-orthogonality and residual at the BJ target."""
+    m = nx * ny
+    B = synth.laplacian2d(nx, ny, seed=3, wmax=1e2)
+    X = synth.randsvd(m, n, 1e10, seed=1)
+    rg = sq.scqr3_factor_oblique_csr(dev(X), _csr_dev(B))
+    ro = oracle.scqr3(X, csr=B)
+    assert rg.status == 0 and ro.status == 0
+    Rg, Qg = host(rg.R), host(rg.Q)
+    assert np.max(np.abs(Rg - ro.R)) <= 1e-10 * np.max(np.abs(ro.R))
+    assert oracle.orth_F_csr(Qg, B) <= 10 * n * U
+    assert oracle.resid_F(X, Qg, Rg) <= 10 * n * U
+    assert rg.trace[0]["shifted"] and ro.trace[0].shifted
+
+
+@gpu
+def test_csr_tridiagonal_matches_banded_path():
+    m, n = 20000, 32
+    X = synth.randsvd(m, n, 1e12, seed=2)
+    d, e = synth.tridiag_b(m, seed=2)
+    a = sq.scqr3_factor_oblique(dev(X), torch.from_numpy(d).cuda(), torch.from_numpy(e).cuda())
+    b = sq.scqr3_factor_oblique_csr(dev(X), _csr_dev(synth.tridiag_csr(d, e)))
+    assert a.status == b.status == 0 and a.passes == b.passes
+    Ra, Rb = host(a.R), host(b.R)
+    assert np.max(np.abs(Ra - Rb)) <= 1e-12 * np.max(np.abs(Ra))
+
+
+@gpu
+def test_csr_argument_errors():
+    m, n = 100, 4
+    X = dev(synth.random_rows(m, n, seed=1))
+    rp, ci, cv = synth.laplacian2d(10, 10)
+    bad = ci.copy()
+    bad[5] = m + 3                       # outside [0, m) with halo 0
+    with pytest.raises(sq.ScqrError):
+        sq.scqr3_factor_oblique_csr(X, _csr_dev((rp, bad, cv)))
+    with pytest.raises(sq.ScqrError):    # halo without a communicator
+        sq.scqr3_factor_oblique_csr(X, _csr_dev((rp, ci, cv), halo=2))
+    r = sq.scqr3_factor_oblique_csr(X, _csr_dev((rp, ci, cv)))
+    assert r.status == 0
