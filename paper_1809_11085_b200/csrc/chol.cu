@@ -290,6 +290,7 @@ __device__ __noinline__ void write_outputs(const double* Wg, int ldw, int n, int
 
 template <bool SMEM>
 __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
+  if (p.last_pass && p.pass > *(volatile const int*)p.last_pass) return;  // speculative pass after stop
   __shared__ double red[64];
   __shared__ double ybuf[2][kMaxN];
   __shared__ double rinv[kPanel];
@@ -404,8 +405,12 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
     clk[7] = g_phase[1];
     for (int i = 0; i < 8; ++i) st.clk[i] = clk[i];
     *p.st_dev = st;
+    if (p.last_pass) {  // device-side pass control: later (speculative) passes become no-ops
+      if (st.code != SCQR3_OK) *(volatile int*)p.last_pass = p.pass - 1;
+      else if (st.stop) *(volatile int*)p.last_pass = p.pass;
+    }
     if (p.st_host) {
-      volatile DevStatus* h = p.st_host;
+      volatile DevStatus* h = p.st_host + (p.mode == CHOL_PASS ? p.pass - 1 : 0);
       h->stop = st.stop;
       h->pass = st.pass;
       h->shifted = st.shifted;
@@ -436,8 +441,8 @@ __global__ void __launch_bounds__(kThreads, 1) chol_kernel_gmem(CholParams p) {
 // a6: Rnew = R~ R (pass > 1) or R~ (pass 1), k ascending like the oracle; off the critical path
 // (side stream, overlapped with the TRSM).  Skipped when the pass broke down.
 __global__ void trmul_kernel(const double* Rt, const double* R, double* Rnew, int n, int first,
-                             const DevStatus* st) {
-  if (st->code != SCQR3_OK) return;
+                             const DevStatus* st, PassGate gate) {
+  if (gate.skip() || st->code != SCQR3_OK) return;
   const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= static_cast<long long>(n) * n) return;
   const int i = static_cast<int>(k % n), j = static_cast<int>(k / n);
@@ -450,8 +455,8 @@ __global__ void trmul_kernel(const double* Rt, const double* R, double* Rnew, in
   Rnew[k] = acc;
 }
 
-__global__ void copy_kernel(const double* src, double* dst, long long count, const DevStatus* st) {
-  if (st && st->code != SCQR3_OK) return;
+__global__ void copy_kernel(const double* src, double* dst, long long count, const DevStatus* st, PassGate gate) {
+  if (gate.skip() || (st && st->code != SCQR3_OK)) return;
   const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k < count) dst[k] = src[k];
 }

@@ -35,6 +35,7 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
     gram_tma_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapY,
                     GramParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
+  if (p.gate.skip()) return;  // speculative pass after a stop / error (device-side pass control)
   // 1024-B alignment for SWIZZLE_128B
   // (pointer arithmetic on the shared array itself keeps the shared address space -> LDS)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -215,6 +216,7 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
 // TI <= TJ, at index TJ(TJ+1)/2 + TI, 8x8 row-major), plus for the oblique Gram the
 // symmetrisation 0.5 (A_ij + A_ji) of the full sums and the appended ||Q||_F^2.
 __global__ void gram_reduce_kernel(GramReduceParams p) {
+  if (p.gate.skip()) return;
   const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long long nout = static_cast<long long>(p.NT) * (p.NT + 1) / 2 * 64;
   if (e < nout) {
@@ -251,6 +253,7 @@ __global__ void gram_reduce_kernel(GramReduceParams p) {
 // partial sums of q_ij^2 (||Q||_F^2 for the oblique shift, reading D4).
 __global__ void oblique_y_kernel(ObliqueYParams p) {
   __shared__ double red[32];
+  if (p.gate.skip()) return;
   const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long long total = p.m * static_cast<long long>(p.n);
   double sq = 0.0;
@@ -283,6 +286,7 @@ __global__ void oblique_y_kernel(ObliqueYParams p) {
 // rows outside [0, m) come from the halo buffers (neighbouring ranks' rows).
 __global__ void csr_y_kernel(ObliqueYParams p) {
   __shared__ double red[32];
+  if (p.gate.skip()) return;
   const int nch = (p.n + 7) / 8;
   const long long total = p.m * nch;
   double sq = 0.0;

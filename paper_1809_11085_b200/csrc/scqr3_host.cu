@@ -62,9 +62,12 @@ struct Ctx {
   int device = -1;
   int num_sms = 0;
   PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  DevStatus* st_host = nullptr;      // pinned, mapped
+  static constexpr int kSlots = 16;  // passes with a status slot (max_passes <= kSlots)
+  DevStatus* st_host = nullptr;      // pinned, mapped: one slot per pass
   DevStatus* st_host_dev = nullptr;  // device alias of st_host
   cudaEvent_t ev = nullptr;
+  cudaEvent_t ev_pass[kSlots] = {};  // chol of pass k done (its status slot is readable)
+  int cur_pass = 0;                  // pass being enqueued (tags the profiling events)
   cudaStream_t side = nullptr;     // R accumulation, overlapped with the TRSM
   cudaEvent_t ev_chol = nullptr;   // chol done (st) -> side may start
   cudaEvent_t ev_side = nullptr;   // side done -> st may reuse the R~ buffer
@@ -72,6 +75,7 @@ struct Ctx {
   static constexpr int kMaxEv = 128;
   cudaEvent_t ev_a[kMaxEv] = {}, ev_b[kMaxEv] = {};
   int ev_kind[kMaxEv] = {};
+  int ev_tag[kMaxEv] = {};
   int ev_used = 0;
   scqr3_prof* prof = nullptr;
   cudaStream_t prof_stream = nullptr;
@@ -89,16 +93,19 @@ int prof_begin(Ctx* c, int kind) {
     cudaEventCreate(&c->ev_b[i]);
   }
   c->ev_kind[i] = kind;
+  c->ev_tag[i] = c->cur_pass;
   cudaEventRecord(c->ev_a[i], kind == PK_TRMUL ? c->side : c->prof_stream);
   return i;
 }
 void prof_end(Ctx* c, int slot) {
   if (slot >= 0) cudaEventRecord(c->ev_b[slot], c->ev_kind[slot] == PK_TRMUL ? c->side : c->prof_stream);
 }
-// After the stream has been synchronised: fold the recorded pairs into *prof.
-void prof_flush(Ctx* c) {
+// After the stream has been synchronised: fold the recorded pairs into *prof (launches of
+// speculative passes beyond the last executed one are left out).
+void prof_flush(Ctx* c, int last_pass = 1 << 30) {
   if (!c->prof) return;
   for (int i = 0; i < c->ev_used; ++i) {
+    if (c->ev_tag[i] > last_pass) continue;
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, c->ev_a[i], c->ev_b[i]) != cudaSuccess) continue;
     switch (c->ev_kind[i]) {
@@ -126,7 +133,8 @@ int get_ctx(Ctx** out) {
     CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
     if (!fn || q != cudaDriverEntryPointSuccess) return fail("cuTensorMapEncodeTiled not available");
     c.encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c.st_host), sizeof(DevStatus), cudaHostAllocMapped));
+    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c.st_host), sizeof(DevStatus) * Ctx::kSlots, cudaHostAllocMapped));
+    for (int i = 0; i < Ctx::kSlots; ++i) CUDA_TRY(cudaEventCreateWithFlags(&c.ev_pass[i], cudaEventDisableTiming));
     CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.st_host_dev), c.st_host, 0));
     CUDA_TRY(cudaEventCreateWithFlags(&c.ev, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&c.ev_chol, cudaEventDisableTiming));
@@ -309,7 +317,7 @@ int assign_gram_jobs(GramParams& gp, bool oblique, int* ncons_out) {
 
 // Gram of the m x n block at src into w.tiles (packed upper tiles; oblique: sym(Q^T Y) and ||Q||_F^2)
 int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld, int64_t m, bool oblique,
-             const ObliqueYParams* yp, cudaStream_t st) {
+             const ObliqueYParams* yp, cudaStream_t st, PassGate gate = PassGate{}) {
   const long long nout = L.tiles_sym * 64;
   if (m == 0) {
     CUDA_TRY(cudaMemsetAsync(w.tiles, 0, static_cast<size_t>(nout + 1) * 8, st));
@@ -318,6 +326,7 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   int colsq_count = 0;
   if (oblique) {
     ObliqueYParams p = *yp;
+    p.gate = gate;
     const long long total = m * static_cast<long long>(L.n);
     long long blocks = std::min<long long>((total + 255) / 256, 4096);
     colsq_count = static_cast<int>(std::max<long long>(blocks, 1));
@@ -335,6 +344,7 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   else my = mq;
 
   GramParams gp{};
+  gp.gate = gate;
   gp.NT = L.NT;
   gp.NB = (L.NT + kJobTiles - 1) / kJobTiles;
   gp.npad = L.npad;
@@ -351,9 +361,9 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   const size_t max_stages = (kGramSmemCap - 2048) / (stage_bytes * nsrc);
   gp.stages = static_cast<int>(std::min<size_t>(std::min<size_t>(8, max_stages), std::max<size_t>(2, 98304 / (stage_bytes * nsrc))));
   const size_t smem = gp.stages * nsrc * stage_bytes + 2 * gp.stages * 8 + 1024;
-  CUDA_TRY(cudaFuncSetAttribute(gram_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  static thread_local LaunchCfgCache gram_cfg;
   int occ = 1;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gram_tma_kernel, threads, smem));
+  CUDA_TRY(cached_launch_cfg(gram_cfg, gram_tma_kernel, smem, threads, &occ));
   occ = std::max(occ, 1);
   gp.total_stages = (m + kGramStageRows - 1) / kGramStageRows;
   long long chunks = std::min<long long>((gp.total_stages + 3) / 4, static_cast<long long>(c->num_sms) * occ / groups);
@@ -367,6 +377,7 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   CUDA_TRY(cudaGetLastError());
 
   GramReduceParams rp{};
+  rp.gate = gate;
   rp.partials = w.partials;
   rp.tiles = w.tiles;
   rp.chunks = gp.chunks;
@@ -387,7 +398,8 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
 int launch_chol(const CholParams& p, cudaStream_t st) {
   if (p.w_in_smem) {
     const size_t smem = static_cast<size_t>(p.n) * (p.n + 1) * 8;
-    CUDA_TRY(cudaFuncSetAttribute(chol_kernel_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    static thread_local LaunchCfgCache chol_cfg;
+    CUDA_TRY(cached_launch_cfg(chol_cfg, chol_kernel_smem, smem, 256, nullptr));
     chol_kernel_smem<<<1, 256, smem, st>>>(p);
   } else {
     chol_kernel_gmem<<<1, 256, 0, st>>>(p);
@@ -400,14 +412,14 @@ int launch_chol(const CholParams& p, cudaStream_t st) {
 // a6 on the side stream: R := R~ R once this pass's chol_kernel is done; the main stream only
 // waits for it before the next chol_kernel overwrites R~ (by then the TRSM has long finished).
 int launch_trmul(Ctx* c, const double* Rt, double* R, double* Rnew, int n, int first, const DevStatus* st_dev,
-                 cudaStream_t st) {
+                 cudaStream_t st, PassGate gate) {
   CUDA_TRY(cudaEventRecord(c->ev_chol, st));
   CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_chol, 0));
   const long long nn = static_cast<long long>(n) * n;
   const unsigned blocks = static_cast<unsigned>((nn + 127) / 128);
   const int pt = prof_begin(c, PK_TRMUL);
-  trmul_kernel<<<blocks, 128, 0, c->side>>>(Rt, R, Rnew, n, first, st_dev);
-  copy_kernel<<<blocks, 128, 0, c->side>>>(Rnew, R, nn, st_dev);
+  trmul_kernel<<<blocks, 128, 0, c->side>>>(Rt, R, Rnew, n, first, st_dev, gate);
+  copy_kernel<<<blocks, 128, 0, c->side>>>(Rnew, R, nn, st_dev, gate);
   prof_end(c, pt);
   g_launches += 2;
   CUDA_TRY(cudaGetLastError());
@@ -476,6 +488,7 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
   c->prof_stream = st;
   c->ev_used = 0;
   const int max_passes = o->max_passes > 0 ? o->max_passes : 8;
+  if (max_passes > Ctx::kSlots) return fail("max_passes %d > %d", max_passes, Ctx::kSlots);
   const double stop_tol = o->stop_tol > 0 ? o->stop_tol : 0.5;
   const int iters = o->power_iters > 0 ? o->power_iters : 32;
 
@@ -594,10 +607,18 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
   tp.Q = Q;
   tp.ldq = ldq;
 
-  const double* src = X;
-  int64_t ldsrc = ld;
-  int status = SCQR3_ENOCONV, k;
-  for (k = 1; k <= max_passes; ++k) {
+  // Device-side pass control with speculative enqueue: pass k+1 is enqueued before the host
+  // has read pass k's status, so the GPU never waits for the host between passes; when chol_k
+  // decides to stop (or fails) it lowers *last_pass and pass k+1's kernels exit at once.
+  int* last_pass = reinterpret_cast<int*>(w.misc + 14);
+  CUDA_TRY(cudaMemsetAsync(last_pass, 0, sizeof(int), st));
+  CUDA_TRY(cudaMemsetAsync(last_pass, max_passes, 1, st));  // little-endian int = max_passes (<= 16)
+  cp.last_pass = last_pass;
+  auto enqueue = [&](int k) -> int {
+    const double* src = k == 1 ? X : Q;
+    const int64_t ldsrc = k == 1 ? ld : ldq;
+    const PassGate gate{last_pass, k};
+    c->cur_pass = k;
     if (oblique) {
       const int ph = cm ? prof_begin(c, PK_COMM) : -1;
       TRY(halo_exchange(cm, src, ldsrc, m, static_cast<int>(n), B.halo(), w.halo, st));
@@ -605,7 +626,7 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
       yp.Q = src;
       yp.ldq = ldsrc;
     }
-    TRY(run_gram(c, L, w, src, ldsrc, m, oblique, &yp, st));
+    TRY(run_gram(c, L, w, src, ldsrc, m, oblique, &yp, st, gate));
     if (cm) {
       const size_t cnt = static_cast<size_t>(L.tiles_sym * 64 + (oblique ? 1 : 0));
       const int pa = prof_begin(c, PK_COMM);
@@ -625,16 +646,17 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
       }
       prof_end(c, pa);
     }
-    c->st_host->code = -1;
+    c->st_host[k - 1].code = -1;
     cp.pass = k;
     if (k > 1) CUDA_TRY(cudaStreamWaitEvent(st, c->ev_side, 0));  // previous R~ consumed
     const int pc = prof_begin(c, PK_CHOL);
     TRY(launch_chol(cp, st));
     prof_end(c, pc);
-    CUDA_TRY(cudaEventRecord(c->ev, st));
-    TRY(launch_trmul(c, w.Rt, R, w.Rnew, static_cast<int>(n), k == 1, w.st, st));
+    CUDA_TRY(cudaEventRecord(c->ev_pass[k - 1], st));
+    TRY(launch_trmul(c, w.Rt, R, w.Rnew, static_cast<int>(n), k == 1, w.st, st, gate));
     tp.X = src;
     tp.ldx = ldsrc;
+    tp.gate = gate;
     if (m > 0) {
       CUtensorMap mx;
       const bool use_tma = L.NT <= 16;
@@ -644,8 +666,19 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
       prof_end(c, pt);
       ++g_launches;
     }
-    CUDA_TRY(cudaEventSynchronize(c->ev));
-    const volatile DevStatus* h = c->st_host;
+    return SCQR3_OK;
+  };
+  // Speculation depth: 0 = the host reads pass k's status (recorded right after chol_k, while
+  // the GPU runs TRSM_k) before enqueueing pass k+1; 1 = pass k+1 is enqueued first.  Measured:
+  // depth 1 is slower on small problems (the launch-bound host then enqueues a whole no-op pass:
+  // PR1 0.25 -> 0.30 ms) and equal on large ones (the GPU is busy with TRSM_k meanwhile).
+  constexpr int kSpeculate = 0;
+  int status = SCQR3_ENOCONV, k;
+  TRY(enqueue(1));
+  for (k = 1;; ++k) {
+    if (kSpeculate && k < max_passes) TRY(enqueue(k + 1));
+    CUDA_TRY(cudaEventSynchronize(c->ev_pass[k - 1]));
+    const volatile DevStatus* h = c->st_host + (k - 1);
     if (h->code < 0) return fail("status block not written by the Cholesky kernel");
     if (o->trace && k - 1 < o->trace_cap) {
       scqr3_pass_trace& t = o->trace[k - 1];
@@ -656,8 +689,6 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
       t.norm2_est = h->norm2_est;
       t.dev_F = h->dev_F;
     }
-    src = Q;
-    ldsrc = ldq;
     if (h->code != SCQR3_OK) {
       status = h->code;
       break;
@@ -666,11 +697,13 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
       status = SCQR3_OK;
       break;
     }
+    if (k == max_passes) break;  // SCQR3_ENOCONV
+    if (!kSpeculate) TRY(enqueue(k + 1));
   }
-  if (o->passes_out) *o->passes_out = std::min(k, max_passes);
+  if (o->passes_out) *o->passes_out = k;
   CUDA_TRY(cudaStreamWaitEvent(st, c->ev_side, 0));  // R complete
   CUDA_TRY(cudaStreamSynchronize(st));
-  prof_flush(c);
+  prof_flush(c, k);
   c->prof = nullptr;
   return status;
 }

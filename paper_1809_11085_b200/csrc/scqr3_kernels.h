@@ -12,7 +12,16 @@ struct DevStatus;
 constexpr int kMaxConsumers = 20;   // consumer warps per Gram CTA (+1 producer = 672 threads)
 constexpr int kMaxGroups = 32;      // job groups (CTAs sharing one row chunk)
 
+// Device-side pass control (speculative enqueue, scqr3_host.cu): the kernels of pass `pass` exit
+// at once when the Cholesky of an earlier pass has set *last_pass below it (stop or error).
+struct PassGate {
+  const int* last_pass = nullptr;  // null: always run (kernel-level API)
+  int pass = 0;
+  __device__ __forceinline__ bool skip() const { return last_pass && pass > *(volatile const int*)last_pass; }
+};
+
 struct GramParams {
+  PassGate gate;
   double* partials;          // [chunks][tiles_per_partial][64]
   long long total_stages;    // ceil(m / 16)
   int chunks;                // row chunks (CTAs per group)
@@ -29,6 +38,7 @@ struct GramParams {
 };
 
 struct GramReduceParams {
+  PassGate gate;
   const double* partials;
   double* tiles;             // packed upper tiles (+1 double: ||Q||_F^2 for oblique)
   int chunks;
@@ -40,6 +50,7 @@ struct GramReduceParams {
 };
 
 struct ObliqueYParams {
+  PassGate gate;
   const double* Q;
   long long ldq;
   const double* d;
@@ -85,10 +96,12 @@ struct CholParams {
   double* bfrag;             // TRSM B fragments (negated R~), NT(NT-1) x 32
   double* dblk;              // TRSM diagonal blocks, NT x 72
   DevStatus* st_dev;
-  DevStatus* st_host;        // host-mapped copy (may be null)
+  DevStatus* st_host;        // host-mapped per-pass slots (st_host[pass-1]; may be null)
+  int* last_pass;            // device-side pass control (may be null): written on stop / error
 };
 
 struct TrsmParams {
+  PassGate gate;
   const double* X;
   long long ldx;
   double* Q;
@@ -114,9 +127,38 @@ __global__ void max_reduce_kernel(const double* partial, int count, double* out)
 __global__ void tiles_to_full_kernel(const double* tiles, int n, double* A);
 __global__ void chol_kernel_smem(CholParams p);
 __global__ void chol_kernel_gmem(CholParams p);
-__global__ void trmul_kernel(const double* Rt, const double* R, double* Rnew, int n, int first, const DevStatus* st);
-__global__ void copy_kernel(const double* src, double* dst, long long count, const DevStatus* st);
+__global__ void trmul_kernel(const double* Rt, const double* R, double* Rnew, int n, int first, const DevStatus* st,
+                             PassGate gate);
+__global__ void copy_kernel(const double* src, double* dst, long long count, const DevStatus* st, PassGate gate);
 __global__ void trsm_prep_kernel(const double* R, int n, int NT, double* bfrag, double* dblk);
+
+// Per-call-site cache of cudaFuncSetAttribute(max dynamic smem) + the occupancy query, so a
+// pass does not repeat these host API calls (small problems are launch-bound on the host).
+struct LaunchCfgCache {
+  int dev = -1;
+  size_t smem = 0;
+  int threads = 0;
+  int occ = 0;
+};
+template <class K>
+inline cudaError_t cached_launch_cfg(LaunchCfgCache& cc, K kernel, size_t smem, int threads, int* occ) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (cc.dev != dev || cc.smem != smem || cc.threads != threads) {
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    int o = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, threads, smem);
+    if (e != cudaSuccess) return e;
+    cc.dev = dev;
+    cc.smem = smem;
+    cc.threads = threads;
+    cc.occ = o;
+  }
+  if (occ) *occ = cc.occ;
+  return cudaSuccess;
+}
 
 // TRSM launcher (chooses the template instance for n)
 cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream);

@@ -29,7 +29,7 @@ namespace scqr3 {
 template <int NT, int A, bool SMEM_B, int THREADS, bool TMA, int P = 1>
 __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant__ CUtensorMap mapX, TrsmParams p) {
   extern __shared__ __align__(1024) unsigned char smraw[];
-  if (p.st && p.st->code != 0) return;
+  if (p.gate.skip() || (p.st && p.st->code != 0)) return;
   constexpr int NF = NT * (NT - 1);
   constexpr int WPB = THREADS / 32;
   constexpr int NPAD = NT * 8;
@@ -221,10 +221,9 @@ static cudaError_t launch_one(const TrsmParams& p, const CUtensorMap* map, int n
   const size_t smem = 1024 + (TMA ? (WPB / P) * kSlot : 0) +
                       static_cast<size_t>((SMEM_B ? NF * 32 : 0) + NT * 72) * 8 + WPB * 8;
   auto k = trsm_kernel<NT, A, SMEM_B, THREADS, TMA, P>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
+  static thread_local LaunchCfgCache cfg;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem);
+  cudaError_t e = cached_launch_cfg(cfg, k, smem, THREADS, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   const long long groups = (p.m + RS - 1) / RS;
@@ -366,7 +365,7 @@ template <int TB, int THREADS>
 __global__ void __launch_bounds__(THREADS, 1) trsm_wide_kernel(TrsmParams p) {
   constexpr int NTT = 32, WPB = THREADS / 32, MAXF = WidePhases<TB>::MAXF;
   extern __shared__ __align__(16) double smp[];
-  if (p.st && p.st->code != 0) return;
+  if (p.gate.skip() || (p.st && p.st->code != 0)) return;
   double* const buf[2] = {smp, smp + MAXF * 32};
   double* const db = smp + 2 * MAXF * 32;
   for (int i = threadIdx.x; i < NTT * 72; i += THREADS) db[i] = p.dblk[TB * 72 + i];
@@ -408,7 +407,8 @@ template <int TB, int THREADS>
 static cudaError_t launch_wide(const TrsmParams& p, int num_sms, cudaStream_t stream) {
   const size_t smem = static_cast<size_t>(2 * WidePhases<TB>::MAXF * 32 + 32 * 72) * 8;
   auto k = trsm_wide_kernel<TB, THREADS>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  static thread_local LaunchCfgCache cfg;
+  cudaError_t e = cached_launch_cfg(cfg, k, smem, THREADS, nullptr);
   if (e != cudaSuccess) return e;
   const long long groups = (p.m + 7) / 8;
   long long grid = num_sms;
