@@ -100,8 +100,10 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
   const bool active = code >= 0;
   const int part = active ? (code & 1) : 0;
   int bi = 0, bj = 0;
-  if (active) decode_job(code >> 1, p.NB, full, bi, bj);
-  const bool diag = !full && bi == bj;
+  // the oblique Gram is also computed on the upper blocks only: A = upper(Q^T (BQ)), mirrored
+  // (reading D22); its diagonal tiles take the A fragments from Q and the B fragments from Y
+  if (active) decode_job(code >> 1, p.NB, false, bi, bj);
+  const bool diag = bi == bj;
   const int NT = p.NT;
   const bool edge = (bi + 1) * kJobTiles > NT || (bj + 1) * kJobTiles > NT;
   const int rr0 = 2 * part;  // first tile row of the part within the block
@@ -149,16 +151,19 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
           for (int b = 0; b < kJobTiles; ++b) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
       }
     } else if (kind == 1) {
-      // diagonal block, tile rows 0-1: tiles (0,0..3), (1,1..3); A fragments are B fragments
+      // diagonal block, tile rows 0-1: tiles (0,0..3), (1,1..3); for Q^T Q the A fragments are
+      // B fragments, for Q^T Y they come from the Q stage
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
-        double fb[kJobTiles];
+        double fb[kJobTiles], fa[2];
 #pragma unroll
         for (int b = 0; b < kJobTiles; ++b) fb[b] = *reinterpret_cast<const double*>(srcB + offB[b] + inner[s]);
 #pragma unroll
+        for (int a = 0; a < 2; ++a) fa[a] = full ? *reinterpret_cast<const double*>(srcA + offB[a] + inner[s]) : fb[a];
+#pragma unroll
         for (int a = 0; a < 2; ++a)
 #pragma unroll
-          for (int b = a; b < kJobTiles; ++b) dmma(acc[a][b][0], acc[a][b][1], fb[a], fb[b]);
+          for (int b = a; b < kJobTiles; ++b) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
       }
     } else if (kind == 2) {
       // diagonal block, tile rows 2-3: tiles (2,2), (2,3), (3,3)
@@ -166,9 +171,11 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
       for (int s = 0; s < 4; ++s) {
         const double f2 = *reinterpret_cast<const double*>(srcB + offB[2] + inner[s]);
         const double f3 = *reinterpret_cast<const double*>(srcB + offB[3] + inner[s]);
-        dmma(acc[0][2][0], acc[0][2][1], f2, f2);
-        dmma(acc[0][3][0], acc[0][3][1], f2, f3);
-        dmma(acc[1][3][0], acc[1][3][1], f3, f3);
+        const double a2 = full ? *reinterpret_cast<const double*>(srcA + offB[2] + inner[s]) : f2;
+        const double a3 = full ? *reinterpret_cast<const double*>(srcA + offB[3] + inner[s]) : f3;
+        dmma(acc[0][2][0], acc[0][2][1], a2, f2);
+        dmma(acc[0][3][0], acc[0][3][1], a2, f3);
+        dmma(acc[1][3][0], acc[1][3][1], a3, f3);
       }
     } else if (kind == 3) {
       // part of a block touching the padded edge (n not a multiple of 32): per-tile validity
@@ -206,41 +213,24 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
       const int TI = bi * kJobTiles + rr0 + a, TJ = bj * kJobTiles + b;
       const bool valid = (TI < NT) && (TJ < NT) && (!diag || rr0 + a <= b);
       if (!valid) continue;
-      const size_t tid = full ? static_cast<size_t>(TI) * NT + TJ : static_cast<size_t>(TJ) * (TJ + 1) / 2 + TI;
+      const size_t tid = static_cast<size_t>(TJ) * (TJ + 1) / 2 + TI;
       double2 v = make_double2(acc[a][b][0], acc[a][b][1]);
       *reinterpret_cast<double2*>(out + tid * 64 + 8 * g + 2 * t) = v;
     }
 }
 
 // Sum the per-chunk partials in chunk order.  Output: packed upper tiles (tile (TI,TJ),
-// TI <= TJ, at index TJ(TJ+1)/2 + TI, 8x8 row-major), plus for the oblique Gram the
-// symmetrisation 0.5 (A_ij + A_ji) of the full sums and the appended ||Q||_F^2.
+// TI <= TJ, at index TJ(TJ+1)/2 + TI, 8x8 row-major), plus for the oblique Gram the appended
+// ||Q||_F^2 (the oblique partials are upper tiles of Q^T (BQ) too, reading D22).
 __global__ void gram_reduce_kernel(GramReduceParams p) {
   if (p.gate.skip()) return;
   const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long long nout = static_cast<long long>(p.NT) * (p.NT + 1) / 2 * 64;
   if (e < nout) {
-    const int tile = static_cast<int>(e >> 6), w = static_cast<int>(e & 63);
-    int TJ = 0;
-    while ((TJ + 1) * (TJ + 2) / 2 <= tile) ++TJ;
-    const int TI = tile - TJ * (TJ + 1) / 2;
-    if (!p.oblique) {
-      double s = 0.0;
-      const double* src = p.partials + e;
-      for (int c = 0; c < p.chunks; ++c) s += src[static_cast<size_t>(c) * p.tiles_per_partial * 64];
-      p.tiles[e] = s;
-    } else {
-      const int r = w >> 3, cc = w & 7;
-      const size_t e1 = (static_cast<size_t>(TI) * p.NT + TJ) * 64 + 8 * r + cc;
-      const size_t e2 = (static_cast<size_t>(TJ) * p.NT + TI) * 64 + 8 * cc + r;
-      double s1 = 0.0, s2 = 0.0;
-      for (int c = 0; c < p.chunks; ++c) {
-        const double* base = p.partials + static_cast<size_t>(c) * p.tiles_per_partial * 64;
-        s1 += base[e1];
-        s2 += base[e2];
-      }
-      p.tiles[e] = (s1 + s2) * 0.5;
-    }
+    double s = 0.0;
+    const double* src = p.partials + e;
+    for (int c = 0; c < p.chunks; ++c) s += src[static_cast<size_t>(c) * p.tiles_per_partial * 64];
+    p.tiles[e] = s;
   } else if (e == nout && p.colsq_partials) {
     double s = 0.0;
     for (int c = 0; c < p.colsq_count; ++c) s += p.colsq_partials[c];

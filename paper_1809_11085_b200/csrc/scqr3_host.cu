@@ -170,11 +170,11 @@ Layout make_layout(int64_t m, int64_t n, int oblique, int64_t halo = 1) {
   L.npad = npad_for(L.n);
   L.NT = L.npad / 8;
   L.tiles_sym = static_cast<long long>(L.NT) * (L.NT + 1) / 2;
-  L.tiles_part = oblique ? static_cast<long long>(L.NT) * L.NT : L.tiles_sym;
+  L.tiles_part = L.tiles_sym;  // upper tiles for the oblique Gram too (reading D22)
   {
     // CTAs per row chunk = job groups (assign_gram_jobs); fewer chunks fit on the GPU when there are more
     const long long nb = (L.NT + kJobTiles - 1) / kJobTiles;
-    const long long codes = 2 * (oblique ? nb * nb : nb * (nb + 1) / 2);
+    const long long codes = 2 * (nb * (nb + 1) / 2);
     const int groups_hi = static_cast<int>(std::max<long long>(1, (codes + kMaxConsumers - 1) / kMaxConsumers));
     L.max_chunks = std::max(1, max_chunks_for_device() / groups_hi);
   }
@@ -261,17 +261,14 @@ int encode_map(Ctx* c, CUtensorMap* map, const double* base, int64_t m, int64_t 
 // the CTA runs on sub-partition w % 4; consumer c is warp c + 1).  Returns the number of groups
 // (CTAs sharing a row chunk) and sets *ncons_out.
 int assign_gram_jobs(GramParams& gp, bool oblique, int* ncons_out) {
-  const int nblocks = oblique ? gp.NB * gp.NB : gp.NB * (gp.NB + 1) / 2;
+  // upper blocks only, also for the oblique Gram (reading D22)
+  (void)oblique;
+  const int nblocks = gp.NB * (gp.NB + 1) / 2;
   auto coords = [&](int j, int& bi, int& bj) {
-    if (oblique) {
-      bi = j / gp.NB;
-      bj = j % gp.NB;
-    } else {
-      int c = 0;
-      while ((c + 1) * (c + 2) / 2 <= j) ++c;
-      bj = c;
-      bi = j - c * (c + 1) / 2;
-    }
+    int c = 0;
+    while ((c + 1) * (c + 2) / 2 <= j) ++c;
+    bj = c;
+    bi = j - c * (c + 1) / 2;
   };
   auto weight = [&](int code) {
     int bi, bj;
@@ -280,7 +277,7 @@ int assign_gram_jobs(GramParams& gp, bool oblique, int* ncons_out) {
     int w = 0;
     for (int a = r0; a < r0 + 2; ++a)
       for (int b = 0; b < kJobTiles; ++b)
-        if (bi * kJobTiles + a < gp.NT && bj * kJobTiles + b < gp.NT && (oblique || bi != bj || a <= b)) ++w;
+        if (bi * kJobTiles + a < gp.NT && bj * kJobTiles + b < gp.NT && (bi != bj || a <= b)) ++w;
     return w;
   };
   std::vector<int> codes;  // job code = 2 * block + part (tile rows 2*part, 2*part+1)

@@ -437,6 +437,10 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
 #if SCQR3_TRSM16_PAIRS
     case 16: return tma ? launch_one<16, 1, true, 512, true, 2>(p, map, num_sms, stream)
                         : launch_one<16, 2, true, 256, false>(p, nullptr, num_sms, stream);
+#elif defined(SCQR3_TRSM16_DIRECT384)
+    case 16: return launch_one<16, 2, true, 384, false>(p, nullptr, num_sms, stream);
+#elif defined(SCQR3_TRSM16_DIRECT512)
+    case 16: return launch_one<16, 1, true, 512, false>(p, nullptr, num_sms, stream);
 #else
     case 16: return tma ? launch_one<16, 2, true, SCQR3_TRSM16_THREADS, true>(p, map, num_sms, stream)
                         : launch_one<16, 2, true, 256, false>(p, nullptr, num_sms, stream);
