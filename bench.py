@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--force-comm", action="store_true",
+                    help="use the NCCL communicator path even at one rank (exercises the multi-GPU code)")
     return ap.parse_args()
 
 
@@ -169,7 +171,8 @@ def run_ours(args):
     import synth
 
     rank, world, local = dist_env()
-    if world > 1:
+    multi = world > 1 or args.force_comm
+    if multi:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -204,7 +207,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
 
-    comm = sq.Comm.create() if world > 1 else None
+    comm = sq.Comm.create() if multi else None
     stream = torch.cuda.Stream(device=dev)
     ws = (sq.workspace(mloc, n, device=dev, csr_halo=csr.halo) if csr is not None
           else sq.workspace(mloc, n, oblique=cfg.oblique, device=dev))
@@ -227,7 +230,7 @@ def run_ours(args):
             res = step()
             assert res.status == 0, f"warm-up step failed with status {res.status}"
     stream.synchronize()
-    if world > 1:
+    if multi:
         dist.barrier()
     torch.cuda.synchronize()
 
@@ -245,7 +248,7 @@ def run_ours(args):
     stream.synchronize()
     clk = clocks.stop()
     launches = sq.launch_count()
-    if world > 1:
+    if multi:
         dist.barrier()
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
@@ -295,7 +298,7 @@ def run_ours(args):
         torch.cuda.empty_cache()
         with torch.cuda.stream(stream):
             sq.scqr3_factor_host(Xh, Q=Qh, R=Rh, ws=wsh, comm=comm, m_global=m, stream=stream)  # warm-up
-            if world > 1:
+            if multi:
                 dist.barrier()
             a0 = torch.cuda.Event(enable_timing=True)
             a1 = torch.cuda.Event(enable_timing=True)
@@ -358,7 +361,7 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.destroy()
-    if world > 1:
+    if multi:
         dist.destroy_process_group()
     return 0
 

@@ -244,20 +244,40 @@ __global__ void gram_reduce_kernel(GramReduceParams p) {
 __global__ void oblique_y_kernel(ObliqueYParams p) {
   __shared__ double red[32];
   if (p.gate.skip()) return;
-  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const long long total = p.m * static_cast<long long>(p.n);
+  // one thread per row (consecutive threads, consecutive rows: every column access coalesced),
+  // the row's band entries in registers, 8 columns in flight per step
   double sq = 0.0;
-  for (long long k = idx; k < total; k += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long i = k % p.m, j = k / p.m;
-    const double* q = p.Q + j * p.ldq;
-    const double qi = q[i];
-    double v = p.d[i] * qi;
-    if (i > 0) v = fma(p.e[i - 1], q[i - 1], v);
-    else if (p.has_prev) v = fma(p.e_prev, p.halo_prev[j], v);
-    if (i + 1 < p.m) v = fma(p.e[i], q[i + 1], v);
-    else if (p.has_next) v = fma(p.e[i], p.halo_next[j], v);
-    p.Y[j * p.ldy + i] = v;
-    sq = fma(qi, qi, sq);
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < p.m;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double di = p.d[i];
+    const bool lo = i > 0, hi = i + 1 < p.m;
+    const double el = lo ? p.e[i - 1] : p.e_prev;
+    const double er = p.e[i];
+    const bool use_l = lo || p.has_prev, use_r = hi || p.has_next;
+    for (int j0 = 0; j0 < p.n; j0 += 8) {
+      double qv[8], ql[8], qr[8];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        const int j = j0 + jj;
+        if (j < p.n) {
+          const double* q = p.Q + j * p.ldq;
+          qv[jj] = __ldcs(q + i);
+          ql[jj] = lo ? q[i - 1] : (p.has_prev ? p.halo_prev[j] : 0.0);
+          qr[jj] = hi ? q[i + 1] : (p.has_next ? p.halo_next[j] : 0.0);
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        const int j = j0 + jj;
+        if (j < p.n) {
+          double v = di * qv[jj];  // the oracle's term order
+          if (use_l) v = fma(el, ql[jj], v);
+          if (use_r) v = fma(er, qr[jj], v);
+          __stcs(p.Y + j * p.ldy + i, v);
+          sq = fma(qv[jj], qv[jj], sq);
+        }
+      }
+    }
   }
   // deterministic block reduction
   for (int o = 16; o > 0; o >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, o);

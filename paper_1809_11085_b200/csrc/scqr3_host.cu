@@ -329,8 +329,13 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
     colsq_count = static_cast<int>(std::max<long long>(blocks, 1));
     p.colsq_partials = w.colsq;
     const int ps = prof_begin(c, PK_REDUCE);
-    if (p.rp) csr_y_kernel<<<colsq_count, 256, 0, st>>>(p);
-    else oblique_y_kernel<<<colsq_count, 256, 0, st>>>(p);
+    if (p.rp) {
+      csr_y_kernel<<<colsq_count, 256, 0, st>>>(p);
+    } else {
+      colsq_count = static_cast<int>(std::max<long long>(1, std::min<long long>((m + 255) / 256, 4096)));
+      p.colsq_partials = w.colsq;
+      oblique_y_kernel<<<colsq_count, 256, 0, st>>>(p);
+    }
     prof_end(c, ps);
     ++g_launches;
     CUDA_TRY(cudaGetLastError());
