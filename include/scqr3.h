@@ -20,7 +20,8 @@
  *     block-column launches).
  *   - All device work is ordered on opts->stream; every call returns only after that
  *     work has finished (the pass count is data dependent).
- *   - Return codes: SCQR3_OK; SCQR3_EINVAL (bad argument, CUDA or NCCL error -- detail in
+ *   - Return codes: SCQR3_OK; SCQR3_EINVAL (bad argument -- including NaN/Inf entries in X,
+ *     detected from the pass-1 Gram -- CUDA or NCCL error; detail in
  *     scqr3_last_error()); SCQR3_EBREAKDOWN (Cholesky broke down even with the shift:
  *     out of the method's regime or rank deficient); SCQR3_ENOCONV (no stop
  *     within max_passes).  On a non-OK return Q and R are unspecified; the trace is valid.

@@ -543,6 +543,15 @@ static int scqr3_impl(int64_t m, int64_t n, const double* X, int64_t ld, const o
         dev = dev + v * v;
       }
     dev = sqrt(dev);
+    if (k == 1) { /* non-finite X is an invalid argument: it reaches the Gram's diagonal */
+      int bad = 0;
+      for (int64_t j = 0; j < n; ++j)
+        if (!isfinite(A[j + j * n])) bad = 1;
+      if (bad) {
+        status = 1;
+        break;
+      }
+    }
     /* norm estimate N2 ~ ||Q||_2^2 (oblique: ||Q||_2^2 via the plain column norms) */
     double N2;
     if (oblique) {

@@ -333,6 +333,27 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
   const double2 dt = block_sum2(loc, tr, red);
   const double dev = sqrt(dt.x), trace = dt.y;
   clk[2] = clock64();
+  if (p.pass == 1 && !isfinite(trace)) {
+    // non-finite entries in X (every NaN / Inf reaches the trace of its Gram): an invalid
+    // argument, reported before any factorisation
+    if (tid == 0) {
+      DevStatus st{};
+      st.code = SCQR3_EINVAL;
+      st.pass = p.pass;
+      st.dev_F = dev;
+      *p.st_dev = st;
+      if (p.last_pass) *(volatile int*)p.last_pass = 0;
+      if (p.st_host) {
+        volatile DevStatus* h = p.st_host;
+        h->pass = st.pass;
+        h->dev_F = st.dev_F;
+        __threadfence_system();
+        h->code = st.code;
+        __threadfence_system();
+      }
+    }
+    return;
+  }
 
   // ---- a3: norm estimate and shift, only when a shift is formed
   const double u = 0x1p-53;

@@ -691,6 +691,10 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
       t.norm2_est = h->norm2_est;
       t.dev_F = h->dev_F;
     }
+    if (h->code == SCQR3_EINVAL) {
+      status = fail("non-finite entries in X (the trace of the pass-1 Gram is not finite)");
+      break;
+    }
     if (h->code != SCQR3_OK) {
       status = h->code;
       break;

@@ -373,3 +373,14 @@ def test_csr_argument_errors():
         sq.scqr3_factor_oblique_csr(X, _csr_dev((rp, ci, cv), halo=2))
     r = sq.scqr3_factor_oblique_csr(X, _csr_dev((rp, ci, cv)))
     assert r.status == 0
+
+
+@gpu
+@pytest.mark.parametrize("bad", [np.nan, np.inf])
+def test_non_finite_input_raises(bad):
+    X = synth.randsvd(3000, 16, 1e3, seed=1)
+    X[1234, 7] = bad
+    with pytest.raises(sq.ScqrError, match="non-finite"):
+        sq.scqr3_factor(dev(X))
+    r = sq.scqr3_factor(dev(synth.randsvd(3000, 16, 1e3, seed=1)))   # the context recovers
+    assert r.status == 0

@@ -286,3 +286,11 @@ def test_csr_laplacian_metric_ceilings():
     Ql = r.Q.astype(np.longdouble)
     G = Ql.T @ (Bd.astype(np.longdouble) @ Ql)
     assert abs(float(np.linalg.norm(G - np.eye(n), "fro")) - orthB) <= 1e-16 + 1e-3 * orthB
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_non_finite_input_is_an_invalid_argument(bad):
+    """entries must be finite; status 1 before any factorisation."""
+    X = synth.randsvd(200, 5, 1e3, seed=1)
+    X[17, 3] = bad
+    assert oracle.scqr3(X).status == 1
