@@ -290,7 +290,9 @@ __device__ __noinline__ void write_outputs(const double* Wg, int ldw, int n, int
 
 template <bool SMEM>
 __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
-  if (p.last_pass && p.pass > *(volatile const int*)p.last_pass) return;  // speculative pass after stop
+  // pass number: a kernel parameter, or (CUDA-graph loop body) a device counter
+  const int pass = p.pass_dev ? *(volatile const int*)p.pass_dev : p.pass;
+  if (p.last_pass && pass > *(volatile const int*)p.last_pass) return;  // a pass after the stop
   __shared__ double red[64];
   __shared__ double ybuf[2][kMaxN];
   __shared__ double rinv[kPanel];
@@ -333,13 +335,13 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
   const double2 dt = block_sum2(loc, tr, red);
   const double dev = sqrt(dt.x), trace = dt.y;
   clk[2] = clock64();
-  if (p.pass == 1 && !isfinite(trace)) {
+  if (pass == 1 && !isfinite(trace)) {
     // non-finite entries in X (every NaN / Inf reaches the trace of its Gram): an invalid
     // argument, reported before any factorisation
     if (tid == 0) {
       DevStatus st{};
       st.code = SCQR3_EINVAL;
-      st.pass = p.pass;
+      st.pass = pass;
       st.dev_F = dev;
       *p.st_dev = st;
       if (p.last_pass) *(volatile int*)p.last_pass = 0;
@@ -360,16 +362,16 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
   const double mg = p.m_global, nn = static_cast<double>(n);
   auto shift_for = [&](double& N2) -> double {
     if (p.oblique) {
-      if (p.pass == 1 && p.norm_mode == SCQR3_NORM_USER) N2 = p.norm2_bound * p.norm2_bound;
+      if (pass == 1 && p.norm_mode == SCQR3_NORM_USER) N2 = p.norm2_bound * p.norm2_bound;
       else N2 = p.tiles[static_cast<size_t>(p.NT) * (p.NT + 1) / 2 * 64];  // ||Q||_F^2 (reading D4)
-    } else if (p.pass == 1 && p.norm_mode == SCQR3_NORM_USER) {
+    } else if (pass == 1 && p.norm_mode == SCQR3_NORM_USER) {
       N2 = p.norm2_bound * p.norm2_bound;
     } else if (p.norm_mode == SCQR3_NORM_FROBENIUS) {
       N2 = trace;
     } else {
       N2 = power_lmax<SMEM>(W, ldw, n, p.power_iters, trace, ybuf, red) * 1.01;
     }
-    if (p.shift_mode == SCQR3_SHIFT_FIXED && p.pass == 1) return p.shift_value;
+    if (p.shift_mode == SCQR3_SHIFT_FIXED && pass == 1) return p.shift_value;
     if (p.oblique) return 11.0 * (2.0 * mg * sqrt(mg * nn) + nn * (nn + 1.0)) * u * N2 * (*p.nb_dev);
     return 11.0 * (mg * nn + nn * (nn + 1.0)) * u * N2;
   };
@@ -381,7 +383,7 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
   int shifted = 0, bpiv = 0, piv = 1;
   double bval = 0.0, pv = 0.0, s = 0.0, N2 = 0.0;
   const bool practical = p.shift_mode == SCQR3_SHIFT_PRACTICAL;
-  const bool shift_first = p.pass == 1 && (p.shift_mode == SCQR3_SHIFT_SAFE || p.shift_mode == SCQR3_SHIFT_FIXED ||
+  const bool shift_first = pass == 1 && (p.shift_mode == SCQR3_SHIFT_SAFE || p.shift_mode == SCQR3_SHIFT_FIXED ||
                                            practical);
   bool w_dirty = false;
   clk[3] = clock64();
@@ -414,7 +416,7 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
     DevStatus st{};
     st.code = code;
     st.stop = (code == SCQR3_OK && !shifted && dev <= p.stop_tol) ? 1 : 0;
-    st.pass = p.pass;
+    st.pass = pass;
     st.shifted = shifted;
     st.shift = shifted ? s : 0.0;
     st.breakdown_pivot = bpiv;
@@ -427,11 +429,11 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
     for (int i = 0; i < 8; ++i) st.clk[i] = clk[i];
     *p.st_dev = st;
     if (p.last_pass) {  // device-side pass control: later (speculative) passes become no-ops
-      if (st.code != SCQR3_OK) *(volatile int*)p.last_pass = p.pass - 1;
-      else if (st.stop) *(volatile int*)p.last_pass = p.pass;
+      if (st.code != SCQR3_OK) *(volatile int*)p.last_pass = pass - 1;
+      else if (st.stop) *(volatile int*)p.last_pass = pass;
     }
     if (p.st_host) {
-      volatile DevStatus* h = p.st_host + (p.mode == CHOL_PASS ? p.pass - 1 : 0);
+      volatile DevStatus* h = p.st_host + (p.mode == CHOL_PASS ? pass - 1 : 0);
       h->stop = st.stop;
       h->pass = st.pass;
       h->shifted = st.shifted;
@@ -507,6 +509,18 @@ __global__ void trsm_prep_kernel(const double* R, int n, int NT, double* bfrag, 
         dblk[k] = 1.0 / rp(8 * J + (w - 64), 8 * J + (w - 64));
       }
     }
+  }
+}
+
+__global__ void pass_advance_kernel(int* pass_dev) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *pass_dev += 1;
+}
+
+__global__ void pass_loop_cond_kernel(const int* pass_dev, const int* last_pass, int max_passes,
+                                      cudaGraphConditionalHandle handle) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const int k = *pass_dev;
+    cudaGraphSetConditional(handle, (k < *last_pass && k < max_passes) ? 1u : 0u);
   }
 }
 

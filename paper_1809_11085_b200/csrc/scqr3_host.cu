@@ -57,6 +57,20 @@ struct Comm {
   int rank, nranks;
 };
 
+struct GraphKey;
+struct GraphPlan {
+  alignas(16) unsigned char key[1024] = {};  // GraphKey bytes
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches_first = 0, launches_body = 0;
+  void reset() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    exec = nullptr;
+    graph = nullptr;
+  }
+};
+
 struct Ctx {
   bool init = false;
   int device = -1;
@@ -68,7 +82,9 @@ struct Ctx {
   cudaEvent_t ev = nullptr;
   cudaEvent_t ev_pass[kSlots] = {};  // chol of pass k done (its status slot is readable)
   int cur_pass = 0;                  // pass being enqueued (tags the profiling events)
+  GraphPlan plan;                    // cached CUDA-graph pass loop (single GPU)
   cudaStream_t side = nullptr;     // R accumulation, overlapped with the TRSM
+  cudaStream_t cap = nullptr;      // graph capture (the caller's stream may be the legacy default)
   cudaEvent_t ev_chol = nullptr;   // chol done (st) -> side may start
   cudaEvent_t ev_side = nullptr;   // side done -> st may reuse the R~ buffer
   // profiling: event pairs recorded around launches when opts->prof is set
@@ -140,6 +156,7 @@ int get_ctx(Ctx** out) {
     CUDA_TRY(cudaEventCreateWithFlags(&c.ev_chol, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&c.ev_side, cudaEventDisableTiming));
     CUDA_TRY(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c.cap, cudaStreamNonBlocking));
     c.init = true;
   }
   *out = &c;
@@ -453,6 +470,95 @@ int halo_exchange(Comm* cm, const double* Qsrc, int64_t ld, int64_t m, int n, in
   return SCQR3_OK;
 }
 
+// ---- CUDA-graph pass loop (device-side pass control)
+// SCQR3_GRAPH=0 selects the host-driven loop for single-GPU calls too (A/B measurement).
+const bool g_use_graph = [] {
+  const char* v = std::getenv("SCQR3_GRAPH");
+  return !(v && v[0] == '0');
+}();
+
+// Everything a captured pass loop bakes in (pointers, sizes, kernel parameter blocks).
+struct GraphKey {
+  const double* X;
+  const double* Q;
+  double* R;
+  int64_t ld, ldq, m, n;
+  void* ws;
+  cudaStream_t st;
+  int max_passes;
+  CholParams cp;
+  TrsmParams tp;
+  ObliqueYParams yp;
+};
+
+// Graph: [control init, pass 1, loop condition] -> WHILE (cond) { pass k = ++counter; condition }
+template <class Init, class Enq>
+int capture_pass_loop(Ctx* c, cudaStream_t st, int max_passes, int* last_pass, int* pass_dev, Init& init,
+                      Enq& enqueue, GraphPlan* out) {
+  cudaGraph_t g = nullptr;
+  CUDA_TRY(cudaGraphCreate(&g, 0));
+  auto bail = [&](int rc) {
+    cudaStreamCaptureStatus cs;
+    if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+      cudaGraph_t tmp = nullptr;
+      cudaStreamEndCapture(st, &tmp);
+    }
+    cudaGetLastError();
+    cudaGraphDestroy(g);
+    return rc;
+  };
+  cudaGraphConditionalHandle h;
+  if (cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault) != cudaSuccess)
+    return bail(fail("cudaGraphConditionalHandleCreate failed"));
+  const int64_t l0 = g_launches;
+  // segment A
+  if (cudaStreamBeginCaptureToGraph(st, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) != cudaSuccess)
+    return bail(fail("cudaStreamBeginCaptureToGraph failed"));
+  int rc = init();
+  if (rc == SCQR3_OK) rc = enqueue(1);
+  if (rc != SCQR3_OK) return bail(rc);
+  if (cudaStreamWaitEvent(st, c->ev_side, 0) != cudaSuccess) return bail(fail("join failed"));
+  pass_loop_cond_kernel<<<1, 32, 0, st>>>(pass_dev, last_pass, max_passes, h);
+  if (cudaGetLastError() != cudaSuccess) return bail(fail("loop condition launch failed"));
+  cudaStreamCaptureStatus cs;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  if (cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &deps, &ndeps) != cudaSuccess)
+    return bail(fail("cudaStreamGetCaptureInfo failed"));
+  std::vector<cudaGraphNode_t> dep(deps, deps + ndeps);
+  cudaGraph_t gA = nullptr;
+  if (cudaStreamEndCapture(st, &gA) != cudaSuccess) return bail(fail("capture of pass 1 failed"));
+  const int64_t l1 = g_launches;
+  // the WHILE node and its body (one generic pass)
+  cudaGraphNodeParams np{};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t wnode;
+  if (cudaGraphAddNode(&wnode, g, dep.data(), dep.size(), &np) != cudaSuccess)
+    return bail(fail("adding the WHILE node failed"));
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  if (cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) != cudaSuccess)
+    return bail(fail("capture of the loop body failed to start"));
+  rc = enqueue(0);
+  if (rc != SCQR3_OK) return bail(rc);
+  if (cudaStreamWaitEvent(st, c->ev_side, 0) != cudaSuccess) return bail(fail("join failed"));
+  pass_loop_cond_kernel<<<1, 32, 0, st>>>(pass_dev, last_pass, max_passes, h);
+  if (cudaGetLastError() != cudaSuccess) return bail(fail("loop condition launch failed"));
+  cudaGraph_t gB = nullptr;
+  if (cudaStreamEndCapture(st, &gB) != cudaSuccess) return bail(fail("capture of the loop body failed"));
+  const int64_t l2 = g_launches;
+  cudaGraphExec_t exec = nullptr;
+  if (cudaGraphInstantiate(&exec, g, 0) != cudaSuccess) return bail(fail("cudaGraphInstantiate failed"));
+  g_launches = l0;  // capture launched nothing; replays are counted per executed pass
+  out->graph = g;
+  out->exec = exec;
+  out->launches_first = l1 - l0 + 1;
+  out->launches_body = l2 - l1 + 1;
+  return SCQR3_OK;
+}
+
 // The oblique metric of a factorisation: none (standard), tridiagonal bands, or CSR.
 struct Metric {
   const double* d = nullptr;
@@ -609,18 +715,29 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
   tp.Q = Q;
   tp.ldq = ldq;
 
-  // Device-side pass control with speculative enqueue: pass k+1 is enqueued before the host
-  // has read pass k's status, so the GPU never waits for the host between passes; when chol_k
-  // decides to stop (or fails) it lowers *last_pass and pass k+1's kernels exit at once.
+  // Device-side pass control: the Cholesky of pass k lowers *last_pass when it stops (or
+  // fails), and every kernel of a later pass exits at once (PassGate).  Two drivers use it:
+  //  * the CUDA-graph loop (single GPU, no profiling): pass 1, then a conditional WHILE node
+  //    whose body is one pass reading its number from a device counter -- no host round trip
+  //    between passes;
+  //  * the host loop (multi-GPU / profiled calls): the host reads pass k's status (recorded
+  //    right after chol_k, while the GPU runs TRSM_k) before enqueueing pass k+1.  (Enqueueing
+  //    pass k+1 speculatively first was measured slower: PR1 0.25 -> 0.30 ms.)
   int* last_pass = reinterpret_cast<int*>(w.misc + 14);
-  CUDA_TRY(cudaMemsetAsync(last_pass, 0, sizeof(int), st));
-  CUDA_TRY(cudaMemsetAsync(last_pass, max_passes, 1, st));  // little-endian int = max_passes (<= 16)
+  int* pass_dev = reinterpret_cast<int*>(w.misc + 15);
   cp.last_pass = last_pass;
+  // k >= 1: pass k with host-known number; k == 0: the generic loop-body pass (number on device)
   auto enqueue = [&](int k) -> int {
+    const bool generic = k == 0;
     const double* src = k == 1 ? X : Q;
     const int64_t ldsrc = k == 1 ? ld : ldq;
-    const PassGate gate{last_pass, k};
+    const PassGate gate{last_pass, k, generic ? pass_dev : nullptr};
     c->cur_pass = k;
+    if (generic) {
+      pass_advance_kernel<<<1, 32, 0, st>>>(pass_dev);
+      ++g_launches;
+      CUDA_TRY(cudaGetLastError());
+    }
     if (oblique) {
       const int ph = cm ? prof_begin(c, PK_COMM) : -1;
       TRY(halo_exchange(cm, src, ldsrc, m, static_cast<int>(n), B.halo(), w.halo, st));
@@ -648,13 +765,14 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
       }
       prof_end(c, pa);
     }
-    c->st_host[k - 1].code = -1;
     cp.pass = k;
-    if (k > 1) CUDA_TRY(cudaStreamWaitEvent(st, c->ev_side, 0));  // previous R~ consumed
+    cp.pass_dev = generic ? pass_dev : nullptr;
+    // previous R~ consumed (a graph segment joins the side stream at its end instead)
+    if (k > 1) CUDA_TRY(cudaStreamWaitEvent(st, c->ev_side, 0));
     const int pc = prof_begin(c, PK_CHOL);
     TRY(launch_chol(cp, st));
     prof_end(c, pc);
-    CUDA_TRY(cudaEventRecord(c->ev_pass[k - 1], st));
+    if (!generic) CUDA_TRY(cudaEventRecord(c->ev_pass[k - 1], st));
     TRY(launch_trmul(c, w.Rt, R, w.Rnew, static_cast<int>(n), k == 1, w.st, st, gate));
     tp.X = src;
     tp.ldx = ldsrc;
@@ -670,44 +788,82 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
     }
     return SCQR3_OK;
   };
-  // Speculation depth: 0 = the host reads pass k's status (recorded right after chol_k, while
-  // the GPU runs TRSM_k) before enqueueing pass k+1; 1 = pass k+1 is enqueued first.  Measured:
-  // depth 1 is slower on small problems (the launch-bound host then enqueues a whole no-op pass:
-  // PR1 0.25 -> 0.30 ms) and equal on large ones (the GPU is busy with TRSM_k meanwhile).
-  constexpr int kSpeculate = 0;
-  int status = SCQR3_ENOCONV, k;
-  TRY(enqueue(1));
-  for (k = 1;; ++k) {
-    if (kSpeculate && k < max_passes) TRY(enqueue(k + 1));
-    CUDA_TRY(cudaEventSynchronize(c->ev_pass[k - 1]));
-    const volatile DevStatus* h = c->st_host + (k - 1);
-    if (h->code < 0) return fail("status block not written by the Cholesky kernel");
-    if (o->trace && k - 1 < o->trace_cap) {
-      scqr3_pass_trace& t = o->trace[k - 1];
-      t.shift = h->shift;
-      t.shifted = h->shifted;
-      t.breakdown_pivot = h->breakdown_pivot;
-      t.pivot_value = h->pivot_value;
-      t.norm2_est = h->norm2_est;
-      t.dev_F = h->dev_F;
+  auto init_control = [&]() -> int {
+    CUDA_TRY(cudaMemsetAsync(last_pass, 0, sizeof(int), st));
+    CUDA_TRY(cudaMemsetAsync(pass_dev, 0, sizeof(int), st));
+    CUDA_TRY(cudaMemsetAsync(last_pass, max_passes, 1, st));       // little-endian int = max_passes (<= 16)
+    CUDA_TRY(cudaMemsetAsync(pass_dev, 1, 1, st));                  // pass 1 is the unrolled one
+    return SCQR3_OK;
+  };
+  // Read back the per-pass status slots; returns the status, sets *kdone.
+  auto collect = [&](int upto, int* kdone) -> int {
+    int status = SCQR3_ENOCONV;
+    *kdone = 0;
+    for (int k = 1; k <= upto; ++k) {
+      const volatile DevStatus* h = c->st_host + (k - 1);
+      if (h->code < 0) break;
+      *kdone = k;
+      if (o->trace && k - 1 < o->trace_cap) {
+        scqr3_pass_trace& t = o->trace[k - 1];
+        t.shift = h->shift;
+        t.shifted = h->shifted;
+        t.breakdown_pivot = h->breakdown_pivot;
+        t.pivot_value = h->pivot_value;
+        t.norm2_est = h->norm2_est;
+        t.dev_F = h->dev_F;
+      }
+      if (h->code == SCQR3_EINVAL) return fail("non-finite entries in X (the trace of the pass-1 Gram is not finite)");
+      if (h->code != SCQR3_OK) return h->code;
+      if (h->stop) return SCQR3_OK;
     }
-    if (h->code == SCQR3_EINVAL) {
-      status = fail("non-finite entries in X (the trace of the pass-1 Gram is not finite)");
-      break;
+    if (*kdone == 0) return fail("status block not written by the Cholesky kernel");
+    return status;
+  };
+  for (int k = 0; k < max_passes; ++k) c->st_host[k].code = -1;
+
+  int status = SCQR3_ENOCONV, k = 0;
+  const bool use_graph = g_use_graph && !cm && !o->prof && m > 0;
+  bool done = false;
+  if (use_graph) {
+    // ---- CUDA-graph pass loop, captured once per argument set and replayed
+    GraphKey key{};
+    key.X = X; key.Q = Q; key.R = R; key.ld = ld; key.ldq = ldq; key.m = m; key.n = n;
+    key.ws = o->workspace; key.st = st; key.max_passes = max_passes; key.cp = cp; key.tp = tp; key.yp = yp;
+    static_assert(sizeof(GraphKey) <= sizeof(GraphPlan::key), "graph key buffer too small");
+    GraphPlan& gpn = c->plan;
+    if (!gpn.exec || std::memcmp(gpn.key, &key, sizeof key) != 0) {
+      gpn.reset();
+      const cudaStream_t user_st = st;
+      st = c->cap;  // the enqueue lambdas capture on the internal stream
+      const int rc = capture_pass_loop(c, st, max_passes, last_pass, pass_dev, init_control, enqueue, &gpn);
+      st = user_st;
+      if (rc == SCQR3_OK) std::memcpy(gpn.key, &key, sizeof key);
+      else gpn.reset();  // fall through to the host loop (same kernels)
     }
-    if (h->code != SCQR3_OK) {
-      status = h->code;
-      break;
+    if (gpn.exec) {
+      CUDA_TRY(cudaGraphLaunch(gpn.exec, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      status = collect(max_passes, &k);
+      g_launches += gpn.launches_first + gpn.launches_body * std::max(0, k - 1);
+      done = true;
     }
-    if (h->stop) {
-      status = SCQR3_OK;
-      break;
+  }
+  if (!done) {
+    TRY(init_control());
+    TRY(enqueue(1));
+    for (k = 1;; ++k) {
+      CUDA_TRY(cudaEventSynchronize(c->ev_pass[k - 1]));
+      const volatile DevStatus* h = c->st_host + (k - 1);
+      if (h->code < 0) return fail("status block not written by the Cholesky kernel");
+      if (h->code != SCQR3_OK || h->stop || k == max_passes) break;
+      TRY(enqueue(k + 1));
     }
-    if (k == max_passes) break;  // SCQR3_ENOCONV
-    if (!kSpeculate) TRY(enqueue(k + 1));
+    int kd = 0;
+    status = collect(k, &kd);
+    k = kd;
   }
   if (o->passes_out) *o->passes_out = k;
-  CUDA_TRY(cudaStreamWaitEvent(st, c->ev_side, 0));  // R complete
+  if (!done) CUDA_TRY(cudaStreamWaitEvent(st, c->ev_side, 0));  // R complete (the graph joins itself)
   CUDA_TRY(cudaStreamSynchronize(st));
   prof_flush(c, k);
   c->prof = nullptr;

@@ -17,7 +17,12 @@ constexpr int kMaxGroups = 32;      // job groups (CTAs sharing one row chunk)
 struct PassGate {
   const int* last_pass = nullptr;  // null: always run (kernel-level API)
   int pass = 0;
-  __device__ __forceinline__ bool skip() const { return last_pass && pass > *(volatile const int*)last_pass; }
+  const int* pass_dev = nullptr;   // CUDA-graph loop body: the pass number lives on the device
+  __device__ __forceinline__ bool skip() const {
+    if (!last_pass) return false;
+    const int k = pass_dev ? *(volatile const int*)pass_dev : pass;
+    return k > *(volatile const int*)last_pass;
+  }
 };
 
 struct GramParams {
@@ -98,6 +103,7 @@ struct CholParams {
   DevStatus* st_dev;
   DevStatus* st_host;        // host-mapped per-pass slots (st_host[pass-1]; may be null)
   int* last_pass;            // device-side pass control (may be null): written on stop / error
+  const int* pass_dev;       // CUDA-graph loop body: pass number on the device (else `pass`)
 };
 
 struct TrsmParams {
@@ -131,6 +137,11 @@ __global__ void trmul_kernel(const double* Rt, const double* R, double* Rnew, in
                              PassGate gate);
 __global__ void copy_kernel(const double* src, double* dst, long long count, const DevStatus* st, PassGate gate);
 __global__ void trsm_prep_kernel(const double* R, int n, int NT, double* bfrag, double* dblk);
+// CUDA-graph pass loop (device-side pass control): the counter advances at the
+// top of each loop-body pass; the loop continues while the Cholesky has not stopped it.
+__global__ void pass_advance_kernel(int* pass_dev);
+__global__ void pass_loop_cond_kernel(const int* pass_dev, const int* last_pass, int max_passes,
+                                      cudaGraphConditionalHandle handle);
 
 // Per-call-site cache of cudaFuncSetAttribute(max dynamic smem) + the occupancy query, so a
 // pass does not repeat these host API calls (small problems are launch-bound on the host).
