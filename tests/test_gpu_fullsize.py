@@ -1,5 +1,6 @@
 """Parity at BASELINE.json's full sizes, in the configuration bench.py times (C3, one GPU) and
-the other single-GPU configs (C2, C5; C4 at reduced m -- its 82 GB input is a 4/8-GPU config).
+the other configs (C2, C5; C4 at reduced m against the oracle, and at its full 82 GB on one GPU
+through properties that hold at any size).
 
 Inputs are generated on the device (synth.randsvd_torch); the oracle runs on the very same
 array copied to the host.  Compared (D14): R within 1e-10 max|R|; the pass pattern;
@@ -93,3 +94,29 @@ def test_c4_shape_reduced_m():
     """C4's n=256, kappa=1e14 cluster spectrum at m=2e6 (the full 4e7 x 256 is a 4/8-GPU config)."""
     rg, ro, orth, res = _run("C4", m=2_000_000)
     assert rg.trace[0]["shifted"]
+
+
+@gpu
+@slow
+def test_c4_full_size_one_gpu_properties():
+    """Full C4 (m=4e7, n=256, kappa=1e14 cluster, 82 GB) on one B200, as `bench.py --config C4`
+    runs it.  The oracle cannot factor 82 GB in test time, so this holds the GPU to properties
+    that pin the result at any size: status OK with Alg. 2's pass pattern (shifted pass 1),
+    R upper triangular with a positive diagonal, B-free orthogonality and the residual within
+    10 n u (compensated chunked metrics), and ||R||_2 = ||X||_2 = 1 (sigma_1 of the recipe).
+    R parity with the oracle at this spectrum is tested at m = 2e6 (test_c4_shape_reduced_m)."""
+    cfg = synth.CONFIGS["C4"]
+    m, n = cfg.m, cfg.n
+    X = synth.randsvd_torch(m, n, cfg.kappa, seed=0, spectrum=cfg.spectrum)
+    Q = sq.colmajor_empty(m, n)
+    rg = sq.scqr3_factor(X, Q=Q)
+    assert rg.status == 0 and rg.trace[0]["shifted"]
+    Rg = rg.R.cpu().numpy()
+    assert np.array_equal(Rg, np.triu(Rg)) and np.all(np.diag(Rg) > 0)
+    # sigma_1 = 1 exactly (D15): ||R||_2 = ||X||_2 = 1 to rounding
+    assert abs(np.linalg.norm(Rg, 2) - 1.0) <= 1e-12
+    orth = gpu_metrics.orth_F(Q)
+    res = gpu_metrics.resid_F(X, Q, rg.R)
+    print(f"C4 full: passes={rg.passes} orth={orth:.2e} resid={res:.2e} (10nu={10 * n * U:.2e})")
+    assert orth <= 10 * n * U, orth
+    assert res <= 10 * n * U, res
