@@ -87,13 +87,30 @@ __device__ __noinline__ double power_lmax(const double* Wg, int ldw, int n, int 
   const int tid = threadIdx.x, part = tid % tpr, rstep = kThreads / tpr;  // rows strided when n > kThreads
   for (int i = tid; i < n; i += kThreads) ybuf[0][i] = 1.0;
   __syncthreads();
+  // this thread's share of (W y)_row: four independent FMA chains, eight loads in flight
+  auto rowdot = [&](int row, const double* y) -> double {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (row >= n) return 0.0;
+    int j = part;
+    if (n < 32 * tpr) {  // short rows (n <= 64): one chain is faster (measured)
+      for (; j < n; j += tpr) a0 = fma(W[j * ldw + row], y[j], a0);
+      return a0;
+    }
+#pragma unroll 2
+    for (; j + 3 * tpr < n; j += 4 * tpr) {
+      a0 = fma(W[j * ldw + row], y[j], a0);
+      a1 = fma(W[(j + tpr) * ldw + row], y[j + tpr], a1);
+      a2 = fma(W[(j + 2 * tpr) * ldw + row], y[j + 2 * tpr], a2);
+      a3 = fma(W[(j + 3 * tpr) * ldw + row], y[j + 3 * tpr], a3);
+    }
+    for (; j < n; j += tpr) a0 = fma(W[j * ldw + row], y[j], a0);
+    return (a0 + a1) + (a2 + a3);
+  };
   int cur = 0;
   for (int it = 0; it < iters; ++it) {
     for (int r0 = 0; r0 < n; r0 += rstep) {
       const int row = r0 + tid / tpr;
-      double acc = 0.0;
-      if (row < n)
-        for (int j = part; j < n; j += tpr) acc = fma(W[j * ldw + row], ybuf[cur][j], acc);
+      double acc = rowdot(row, ybuf[cur]);
       for (int o = 1; o < tpr; o <<= 1) acc += __shfl_xor_sync(kFull, acc, o);
       if (part == 0 && row < n) ybuf[cur ^ 1][row] = acc * sc;
     }
@@ -103,9 +120,7 @@ __device__ __noinline__ double power_lmax(const double* Wg, int ldw, int n, int 
   double num = 0.0, den = 0.0;
   for (int r0 = 0; r0 < n; r0 += rstep) {
     const int row = r0 + tid / tpr;
-    double acc = 0.0;
-    if (row < n)
-      for (int j = part; j < n; j += tpr) acc = fma(W[j * ldw + row], ybuf[cur][j], acc);
+    double acc = rowdot(row, ybuf[cur]);
     for (int o = 1; o < tpr; o <<= 1) acc += __shfl_xor_sync(kFull, acc, o);
     if (part == 0 && row < n) {
       const double y = ybuf[cur][row];
