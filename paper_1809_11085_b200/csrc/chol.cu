@@ -480,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_kernel_gmem(CholParams p) {
 // (side stream, overlapped with the TRSM).  Skipped when the pass broke down.
 __global__ void trmul_kernel(const double* Rt, const double* R, double* Rnew, int n, int first,
                              const DevStatus* st, PassGate gate) {
-  if (gate.skip() || st->code != SCQR3_OK) return;
+  if (SCQR3_GATE_SKIP(gate) || st->code != SCQR3_OK) return;
   const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= static_cast<long long>(n) * n) return;
   const int i = static_cast<int>(k % n), j = static_cast<int>(k / n);
@@ -494,7 +494,7 @@ __global__ void trmul_kernel(const double* Rt, const double* R, double* Rnew, in
 }
 
 __global__ void copy_kernel(const double* src, double* dst, long long count, const DevStatus* st, PassGate gate) {
-  if (gate.skip() || (st && st->code != SCQR3_OK)) return;
+  if (SCQR3_GATE_SKIP(gate) || (st && st->code != SCQR3_OK)) return;
   const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k < count) dst[k] = src[k];
 }

@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
     gram_tma_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapY,
                     GramParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  if (p.gate.skip()) return;  // speculative pass after a stop / error (device-side pass control)
+  if (SCQR3_GATE_SKIP(p.gate)) return;  // speculative pass after a stop / error (device-side pass control)
   // 1024-B alignment for SWIZZLE_128B
   // (pointer arithmetic on the shared array itself keeps the shared address space -> LDS)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -222,19 +222,32 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
 // Sum the per-chunk partials in chunk order.  Output: packed upper tiles (tile (TI,TJ),
 // TI <= TJ, at index TJ(TJ+1)/2 + TI, 8x8 row-major), plus for the oblique Gram the appended
 // ||Q||_F^2 (the oblique partials are upper tiles of Q^T (BQ) too, reading D22).
+// Block = 32 consecutive outputs x 8 chunk classes (c mod 8): coalesced 256-B rows, eight
+// loads in flight per output, then the eight class sums added in class order -- a fixed order,
+// so the result is bitwise reproducible (kReduceThreads threads per block).
 __global__ void gram_reduce_kernel(GramReduceParams p) {
-  if (p.gate.skip()) return;
-  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (SCQR3_GATE_SKIP(p.gate)) return;
+  __shared__ double red[8][33];
+  const int lane = threadIdx.x & 31, cls = threadIdx.x >> 5;
   const long long nout = static_cast<long long>(p.NT) * (p.NT + 1) / 2 * 64;
+  const long long e = static_cast<long long>(blockIdx.x) * 32 + lane;
+  double s = 0.0;
   if (e < nout) {
-    double s = 0.0;
+    const size_t stride = static_cast<size_t>(p.tiles_per_partial) * 64;
     const double* src = p.partials + e;
-    for (int c = 0; c < p.chunks; ++c) s += src[static_cast<size_t>(c) * p.tiles_per_partial * 64];
-    p.tiles[e] = s;
-  } else if (e == nout && p.colsq_partials) {
-    double s = 0.0;
-    for (int c = 0; c < p.colsq_count; ++c) s += p.colsq_partials[c];
-    p.tiles[nout] = s;
+    for (int c = cls; c < p.chunks; c += 8) s += src[static_cast<size_t>(c) * stride];
+  }
+  red[cls][lane] = s;
+  __syncthreads();
+  if (cls == 0 && e < nout) {
+    double t = red[0][lane];
+    for (int k = 1; k < 8; ++k) t += red[k][lane];
+    p.tiles[e] = t;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && p.colsq_partials) {
+    double t = 0.0;
+    for (int c = 0; c < p.colsq_count; ++c) t += p.colsq_partials[c];
+    p.tiles[nout] = t;
   }
 }
 
@@ -243,7 +256,7 @@ __global__ void gram_reduce_kernel(GramReduceParams p) {
 // partial sums of q_ij^2 (||Q||_F^2 for the oblique shift, reading D4).
 __global__ void oblique_y_kernel(ObliqueYParams p) {
   __shared__ double red[32];
-  if (p.gate.skip()) return;
+  if (SCQR3_GATE_SKIP(p.gate)) return;
   // one thread per row (consecutive threads, consecutive rows: every column access coalesced),
   // the row's band entries in registers, 8 columns in flight per step
   double sq = 0.0;
@@ -296,7 +309,7 @@ __global__ void oblique_y_kernel(ObliqueYParams p) {
 // rows outside [0, m) come from the halo buffers (neighbouring ranks' rows).
 __global__ void csr_y_kernel(ObliqueYParams p) {
   __shared__ double red[32];
-  if (p.gate.skip()) return;
+  if (SCQR3_GATE_SKIP(p.gate)) return;
   const int nch = (p.n + 7) / 8;
   const long long total = p.m * nch;
   double sq = 0.0;

@@ -322,11 +322,33 @@ int assign_gram_jobs(GramParams& gp, bool oblique, int* ncons_out) {
       }
       used[best] = true;
       load[(best + 1) & 3] += weight(code);
-      gp.warp_job[g * kMaxConsumers + best] = code;
+      gp.warp_job[g * kMaxConsumers + best] = static_cast<short>(code);
     }
   }
   *ncons_out = ncons;
   return groups;
+}
+
+// Sum `chunks` partials (per-CTA packed upper tiles) into w.tiles in chunk order.
+int launch_gram_reduce(Ctx* c, const Layout& L, const WS& w, int chunks, bool oblique, int colsq_count,
+                       cudaStream_t st, PassGate gate) {
+  GramReduceParams rp{};
+  rp.gate = gate;
+  rp.partials = w.partials;
+  rp.tiles = w.tiles;
+  rp.chunks = chunks;
+  rp.tiles_per_partial = static_cast<int>(L.tiles_part);
+  rp.NT = L.NT;
+  rp.oblique = oblique ? 1 : 0;
+  rp.colsq_partials = oblique ? w.colsq : nullptr;
+  rp.colsq_count = colsq_count;
+  const long long nblocks = (L.tiles_sym * 64 + 31) / 32;  // 32 outputs x 8 chunk classes per block
+  const int pr = prof_begin(c, PK_REDUCE);
+  gram_reduce_kernel<<<static_cast<unsigned>(nblocks), 256, 0, st>>>(rp);
+  prof_end(c, pr);
+  ++g_launches;
+  CUDA_TRY(cudaGetLastError());
+  return SCQR3_OK;
 }
 
 // Gram of the m x n block at src into w.tiles (packed upper tiles; oblique: sym(Q^T Y) and ||Q||_F^2)
@@ -395,23 +417,7 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   ++g_launches;
   CUDA_TRY(cudaGetLastError());
 
-  GramReduceParams rp{};
-  rp.gate = gate;
-  rp.partials = w.partials;
-  rp.tiles = w.tiles;
-  rp.chunks = gp.chunks;
-  rp.tiles_per_partial = gp.tiles_per_partial;
-  rp.NT = L.NT;
-  rp.oblique = gp.oblique;
-  rp.colsq_partials = oblique ? w.colsq : nullptr;
-  rp.colsq_count = colsq_count;
-  const long long nthreads = nout + 1;
-  const int pr = prof_begin(c, PK_REDUCE);
-  gram_reduce_kernel<<<static_cast<unsigned>((nthreads + 255) / 256), 256, 0, st>>>(rp);
-  prof_end(c, pr);
-  ++g_launches;
-  CUDA_TRY(cudaGetLastError());
-  return SCQR3_OK;
+  return launch_gram_reduce(c, L, w, gp.chunks, oblique, colsq_count, st, gate);
 }
 
 int launch_chol(const CholParams& p, cudaStream_t st) {
@@ -472,6 +478,11 @@ int halo_exchange(Comm* cm, const double* Qsrc, int64_t ld, int64_t m, int n, in
 
 // ---- CUDA-graph pass loop (device-side pass control)
 // SCQR3_GRAPH=0 selects the host-driven loop for single-GPU calls too (A/B measurement).
+// SCQR3_FUSE_TG=0 selects the unfused TRSM + Gram pair for n <= 64 (A/B measurement).
+const bool g_fuse_tg = [] {
+  const char* v = std::getenv("SCQR3_FUSE_TG");
+  return !(v && v[0] == '0');
+}();
 const bool g_use_graph = [] {
   const char* v = std::getenv("SCQR3_GRAPH");
   return !(v && v[0] == '0');
@@ -726,6 +737,9 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
   int* last_pass = reinterpret_cast<int*>(w.misc + 14);
   int* pass_dev = reinterpret_cast<int*>(w.misc + 15);
   cp.last_pass = last_pass;
+  // n <= 64, standard inner product: TRSM_k also accumulates Gram_{k+1}
+  const bool fuse_tg = g_fuse_tg && !oblique && trsm_fuses_gram(L.NT) && m > 0;
+  int fused_chunks = 0;
   // k >= 1: pass k with host-known number; k == 0: the generic loop-body pass (number on device)
   auto enqueue = [&](int k) -> int {
     const bool generic = k == 0;
@@ -745,7 +759,12 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
       yp.Q = src;
       yp.ldq = ldsrc;
     }
-    TRY(run_gram(c, L, w, src, ldsrc, m, oblique, &yp, st, gate));
+    if (k == 1 || !fuse_tg) {
+      TRY(run_gram(c, L, w, src, ldsrc, m, oblique, &yp, st, gate));
+    } else {
+      // this pass's Gram was accumulated by the previous pass's fused TRSM (per-CTA partials)
+      TRY(launch_gram_reduce(c, L, w, fused_chunks, false, 0, st, gate));
+    }
     if (cm) {
       const size_t cnt = static_cast<size_t>(L.tiles_sym * 64 + (oblique ? 1 : 0));
       const int pa = prof_begin(c, PK_COMM);
@@ -777,12 +796,13 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
     tp.X = src;
     tp.ldx = ldsrc;
     tp.gate = gate;
+    tp.gram_partials = fuse_tg ? w.partials : nullptr;
     if (m > 0) {
       CUtensorMap mx;
       const bool use_tma = L.NT <= 16;
       if (use_tma) TRY(encode_map(c, &mx, src, m, n, ldsrc, L.npad));
       const int pt = prof_begin(c, PK_TRSM);
-      CUDA_TRY(launch_trsm(tp, use_tma ? &mx : nullptr, c->num_sms, st));
+      CUDA_TRY(launch_trsm(tp, use_tma ? &mx : nullptr, c->num_sms, st, &fused_chunks));
       prof_end(c, pt);
       ++g_launches;
     }

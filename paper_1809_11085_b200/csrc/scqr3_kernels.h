@@ -18,12 +18,15 @@ struct PassGate {
   const int* last_pass = nullptr;  // null: always run (kernel-level API)
   int pass = 0;
   const int* pass_dev = nullptr;   // CUDA-graph loop body: the pass number lives on the device
-  __device__ __forceinline__ bool skip() const {
-    if (!last_pass) return false;
-    const int k = pass_dev ? *(volatile const int*)pass_dev : pass;
-    return k > *(volatile const int*)last_pass;
-  }
 };
+// (scalar arguments: passing or calling on the struct inside a kernel-parameter block makes the
+//  compiler copy the whole block -- 2.6 KB for GramParams -- to local memory; measured)
+__device__ __forceinline__ bool gate_skip3(const int* last_pass, int pass, const int* pass_dev) {
+  if (!last_pass) return false;
+  const int k = pass_dev ? *(volatile const int*)pass_dev : pass;
+  return k > *(volatile const int*)last_pass;
+}
+#define SCQR3_GATE_SKIP(g) gate_skip3((g).last_pass, (g).pass, (g).pass_dev)
 
 struct GramParams {
   PassGate gate;
@@ -39,7 +42,7 @@ struct GramParams {
   int tiles_per_partial;     // NT(NT+1)/2 or NT^2
   // job of consumer warp w in group g: warp_job[g * kMaxConsumers + w] (-1 = idle); the host
   // balances the DMMA work of each group over the SM's four sub-partitions (warp % 4)
-  int warp_job[kMaxGroups * kMaxConsumers];
+  short warp_job[kMaxGroups * kMaxConsumers];  // codes <= 2 * 136 (n <= 512)
 };
 
 struct GramReduceParams {
@@ -117,6 +120,7 @@ struct TrsmParams {
   const double* bfrag;
   const double* dblk;
   const DevStatus* st;       // skip when st->code != 0 (may be null)
+  double* gram_partials;     // fused next-pass Gram (n <= 64): one NT(NT+1)/2-tile partial per CTA
 };
 
 __global__ void gram_tma_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapY,
@@ -172,7 +176,11 @@ inline cudaError_t cached_launch_cfg(LaunchCfgCache& cc, K kernel, size_t smem, 
 }
 
 // TRSM launcher (chooses the template instance for n)
-cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream);
+// With p.gram_partials set (n <= 64 only, see trsm_fuses_gram) the launch also writes the next
+// pass's Gram partials; *grid_out = the number of partials (CTAs).
+cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream,
+                        int* grid_out = nullptr);
+inline bool trsm_fuses_gram(int NT) { return NT <= 8; }
 
 inline int npad_for(int n) {
   // tile counts with a compiled TRSM instance

@@ -26,10 +26,18 @@ namespace scqr3 {
 #endif
 
 // P = warps sharing one TMA slot (P = 2 when a warp owns 8 rows: the slot is one 16-row box).
-template <int NT, int A, bool SMEM_B, int THREADS, bool TMA, int P = 1>
+// GRAM (n <= 64): also accumulate the next pass's Gram Q_k^T Q_k from the
+// solved rows, so the next pass does not read Q from HBM again.  Each warp writes its 16 finished
+// rows to a private swizzled stage and accumulates their Gram (all upper 8x8 tiles) in registers;
+// at the end the CTA sums its warps in a fixed order and writes one partial (gram_reduce_kernel
+// sums the partials of all CTAs, as after gram_tma_kernel).  Skipped when this pass stops.
+template <int NT, int A, bool SMEM_B, int THREADS, bool TMA, int P = 1, bool GRAM = false>
 __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant__ CUtensorMap mapX, TrsmParams p) {
   extern __shared__ __align__(1024) unsigned char smraw[];
-  if (p.gate.skip() || (p.st && p.st->code != 0)) return;
+  if (SCQR3_GATE_SKIP(p.gate) || (p.st && p.st->code != 0)) return;
+  static_assert(!GRAM || (A == 2 && P == 1 && TMA), "fused Gram: 16-row groups per warp");
+  constexpr int NTS = NT * (NT + 1) / 2;  // upper 8x8 tiles of the Gram
+  const bool do_gram = GRAM && p.gram_partials && !(p.st && p.st->stop);
   constexpr int NF = NT * (NT - 1);
   constexpr int WPB = THREADS / 32;
   constexpr int NPAD = NT * 8;
@@ -41,7 +49,8 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
   // (pointer arithmetic on the shared array itself keeps the shared address space -> LDS)
   unsigned char* base = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
   unsigned char* slots = base;
-  double* sm = reinterpret_cast<double*>(base + (TMA ? (WPB / P) * kSlotBytes : 0));
+  unsigned char* ostage = base + (TMA ? (WPB / P) * kSlotBytes : 0);  // GRAM: per-warp Q stages
+  double* sm = reinterpret_cast<double*>(ostage + (GRAM ? WPB * kBoxBytes : 0));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + (SMEM_B ? NF * 32 : 0) + NT * 72);
   const double* bf;
   const double* db;
@@ -86,6 +95,9 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
     issue(rg0);
   }
 
+  double gacc[GRAM ? NTS : 1][2];  // GRAM: this warp's Gram tiles (C fragments)
+#pragma unroll
+  for (int T = 0; T < (GRAM ? NTS : 1); ++T) gacc[T][0] = gacc[T][1] = 0.0;
   for (long long rg = rg0; rg < ngroups; rg += stride) {
     const long long r0 = rg * RS + sub * 8 * A;
     double q[A][NT][2];
@@ -209,18 +221,67 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
       else __syncwarp();
       issue(rg + stride);
     }
+    if constexpr (GRAM) {
+      if (do_gram) {
+        // the 16 solved rows (rows past m and padded columns are exact zeros) -> swizzled stage,
+        // then k-steps over row quads {2s, 2s+1, 2s+8, 2s+9} as in gram_tma_kernel: one
+        // fragment per column block serves as both MMA operands
+        unsigned char* os = ostage + warp * kBoxBytes;
+#pragma unroll
+        for (int a = 0; a < A; ++a)
+#pragma unroll
+          for (int J = 0; J < NT; ++J)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              *reinterpret_cast<double*>(os + swz128_offset(8 * a + g, 8 * J + 2 * t + h)) = q[a][J][h];
+        __syncwarp();
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          const uint32_t inner = ((((s + 4 * (t >> 1)) ^ g) & 7u) << 4) + ((t & 1) << 3);
+          double f[NT];
+#pragma unroll
+          for (int J = 0; J < NT; ++J) f[J] = *reinterpret_cast<const double*>(os + (8 * J + g) * 128u + inner);
+#pragma unroll
+          for (int J = 0; J < NT; ++J)
+#pragma unroll
+            for (int I = 0; I <= J; ++I) dmma(gacc[J * (J + 1) / 2 + I][0], gacc[J * (J + 1) / 2 + I][1], f[I], f[J]);
+        }
+        __syncwarp();
+      }
+    }
+  }
+  if constexpr (GRAM) {
+    if (do_gram) {
+      // CTA partial: warps add their tiles in warp order into shared memory (fixed order)
+      __syncthreads();
+      double* red = reinterpret_cast<double*>(ostage);  // NTS * 64 doubles <= WPB * kBoxBytes
+      for (int w = 0; w < WPB; ++w) {
+        if (warp == w) {
+#pragma unroll
+          for (int T = 0; T < NTS; ++T) {
+            double2* dst = reinterpret_cast<double2*>(red + T * 64 + 8 * g + 2 * t);
+            const double2 old = w == 0 ? make_double2(0.0, 0.0) : *dst;
+            *dst = make_double2(old.x + gacc[T][0], old.y + gacc[T][1]);
+          }
+        }
+        __syncthreads();
+      }
+      double* outp = p.gram_partials + static_cast<size_t>(blockIdx.x) * NTS * 64;
+      for (int i = threadIdx.x; i < NTS * 64; i += THREADS) outp[i] = red[i];
+    }
   }
 }
 
-template <int NT, int A, bool SMEM_B, int THREADS, bool TMA, int P = 1>
-static cudaError_t launch_one(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream) {
+template <int NT, int A, bool SMEM_B, int THREADS, bool TMA, int P = 1, bool GRAM = false>
+static cudaError_t launch_one(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream,
+                              int* grid_out = nullptr) {
   constexpr int NF = NT * (NT - 1);
   constexpr int WPB = THREADS / 32;
   constexpr int RS = 8 * A * P;
   constexpr size_t kSlot = 16u * NT * 8 * 8 * (RS / 16 > 0 ? RS / 16 : 1);
-  const size_t smem = 1024 + (TMA ? (WPB / P) * kSlot : 0) +
+  const size_t smem = 1024 + (TMA ? (WPB / P) * kSlot : 0) + (GRAM ? WPB * 16u * NT * 8 * 8 : 0) +
                       static_cast<size_t>((SMEM_B ? NF * 32 : 0) + NT * 72) * 8 + WPB * 8;
-  auto k = trsm_kernel<NT, A, SMEM_B, THREADS, TMA, P>;
+  auto k = trsm_kernel<NT, A, SMEM_B, THREADS, TMA, P, GRAM>;
   static thread_local LaunchCfgCache cfg;
   int per_sm = 0;
   cudaError_t e = cached_launch_cfg(cfg, k, smem, THREADS, &per_sm);
@@ -233,6 +294,7 @@ static cudaError_t launch_one(const TrsmParams& p, const CUtensorMap* map, int n
   if (grid < 1) grid = 1;
   CUtensorMap dummy{};
   k<<<static_cast<unsigned>(grid), THREADS, smem, stream>>>(map ? *map : dummy, p);
+  if (grid_out) *grid_out = static_cast<int>(grid);
   return cudaGetLastError();
 }
 
@@ -365,7 +427,7 @@ template <int TB, int THREADS>
 __global__ void __launch_bounds__(THREADS, 1) trsm_wide_kernel(TrsmParams p) {
   constexpr int NTT = 32, WPB = THREADS / 32, MAXF = WidePhases<TB>::MAXF;
   extern __shared__ __align__(16) double smp[];
-  if (p.gate.skip() || (p.st && p.st->code != 0)) return;
+  if (SCQR3_GATE_SKIP(p.gate) || (p.st && p.st->code != 0)) return;
   double* const buf[2] = {smp, smp + MAXF * 32};
   double* const db = smp + 2 * MAXF * 32;
   for (int i = threadIdx.x; i < NTT * 72; i += THREADS) db[i] = p.dblk[TB * 72 + i];
@@ -421,9 +483,20 @@ static cudaError_t launch_wide(const TrsmParams& p, int num_sms, cudaStream_t st
 
 // map: TMA descriptor of X with a {16 rows, npad columns} SWIZZLE_128B box (instances with
 // NT <= 16 use it when map != nullptr); the others read X with plain coalesced loads.
-cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream) {
+cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream,
+                        int* grid_out) {
   const int NT = npad_for(p.n) / 8;
   const bool tma = map != nullptr;
+  if (p.gram_partials) {  // fused TRSM + next-pass Gram (A = 2, TMA)
+    if (!tma) return cudaErrorInvalidValue;
+    switch (NT) {
+      case 1: return launch_one<1, 2, true, 256, true, 1, true>(p, map, num_sms, stream, grid_out);
+      case 2: return launch_one<2, 2, true, 256, true, 1, true>(p, map, num_sms, stream, grid_out);
+      case 4: return launch_one<4, 2, true, 256, true, 1, true>(p, map, num_sms, stream, grid_out);
+      case 8: return launch_one<8, 2, true, 256, true, 1, true>(p, map, num_sms, stream, grid_out);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (NT) {
     case 1: return launch_one<1, 4, true, 256, false>(p, nullptr, num_sms, stream);
     case 2: return tma ? launch_one<2, 4, true, 256, true>(p, map, num_sms, stream)
