@@ -63,6 +63,7 @@ struct GraphPlan {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   int64_t launches_first = 0, launches_body = 0;
+  bool failed = false;  // capture not supported here: use the host loop from now on
   void reset() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
@@ -842,7 +843,7 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
   for (int k = 0; k < max_passes; ++k) c->st_host[k].code = -1;
 
   int status = SCQR3_ENOCONV, k = 0;
-  const bool use_graph = g_use_graph && !cm && !o->prof && m > 0;
+  const bool use_graph = g_use_graph && !cm && !o->prof && m > 0 && !c->plan.failed;
   bool done = false;
   if (use_graph) {
     // ---- CUDA-graph pass loop, captured once per argument set and replayed
@@ -857,8 +858,12 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
       st = c->cap;  // the enqueue lambdas capture on the internal stream
       const int rc = capture_pass_loop(c, st, max_passes, last_pass, pass_dev, init_control, enqueue, &gpn);
       st = user_st;
-      if (rc == SCQR3_OK) std::memcpy(gpn.key, &key, sizeof key);
-      else gpn.reset();  // fall through to the host loop (same kernels)
+      if (rc == SCQR3_OK) {
+        std::memcpy(gpn.key, &key, sizeof key);
+      } else {
+        gpn.reset();  // fall through to the host loop (same kernels), and stop trying
+        gpn.failed = true;
+      }
     }
     if (gpn.exec) {
       CUDA_TRY(cudaGraphLaunch(gpn.exec, st));
