@@ -64,10 +64,46 @@ __device__ __forceinline__ double gram_entry(const CholParams& p, int i, int j) 
   return p.tiles[tile * 64 + 8 * (a & 7) + (b & 7)];
 }
 
+// Packed upper tile index -> tile column TJ (tile (TI, TJ) sits at TJ(TJ+1)/2 + TI).
+__device__ __forceinline__ int tile_col(int tile) {
+  int TJ = static_cast<int>((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
+  while ((TJ + 1) * (TJ + 2) / 2 <= tile) ++TJ;
+  while (TJ * (TJ + 1) / 2 > tile) --TJ;
+  return TJ;
+}
+
 __device__ __forceinline__ void load_W(const CholParams& p, double* W, int ldw) {
   const int n = p.n;
-  for (int i = threadIdx.x >> 5; i < n; i += kThreads / 32)
-    for (int j = threadIdx.x & 31; j < n; j += 32) W[i * ldw + j] = gram_entry(p, i, j);
+  if (p.mode == CHOL_ONLY) {
+    for (int i = threadIdx.x >> 5; i < n; i += kThreads / 32)
+      for (int j = threadIdx.x & 31; j < n; j += 32) W[i * ldw + j] = gram_entry(p, i, j);
+  } else {
+    // read the packed tiles linearly (coalesced, all loads independent) and place each upper
+    // element at (i, j) and (j, i): the same values gram_entry gives, without its scattered reads
+    const int ne = p.NT * (p.NT + 1) / 2 * 64;
+    constexpr int kU = 8;  // loads in flight per thread
+    for (int e0 = threadIdx.x; e0 < ne; e0 += kU * kThreads) {
+      double v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int e = e0 + u * kThreads;
+        v[u] = e < ne ? p.tiles[e] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int e = e0 + u * kThreads;
+        if (e >= ne) continue;
+        const int tile = e >> 6, r = (e >> 3) & 7, c = e & 7;
+        const int TJ = tile_col(tile), TI = tile - TJ * (TJ + 1) / 2;
+        if (TI == TJ && r > c) continue;  // a diagonal tile's upper half serves both triangles
+        const int i = 8 * TI + r, j = 8 * TJ + c;
+        if (i < n && j < n) {
+          W[i * ldw + j] = v[u];
+          W[j * ldw + i] = v[u];
+        }
+      }
+    }
+  }
   __syncthreads();
 }
 
@@ -225,6 +261,51 @@ __device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool ad
     // lane keeps a 4x4 register tile.
     const int L = ncols, T4 = (L + 3) >> 2;
     const int base = k0 + kb;
+    if ((n & 7) == 0) {
+      // n a multiple of 8 (kb = 8): 8x8 tiles on the FP64 tensor cores, C_IJ -= P_I^T P_J with
+      // P the panel's 8 rows -- two m8n8k4 steps per tile (A[g][k] = P[k][8I+g], B[k][j] =
+      // -P[k][8J+j]); diagonal tiles are formed whole (their lower half is never read).
+      const int TL = L >> 3, ntiles = TL * (TL + 1) / 2;
+      const int g = lane >> 2, t = lane & 3;
+      constexpr int kU = 4;  // tiles in flight per warp (independent loads and MMAs)
+      constexpr int kW = kThreads / 32;
+      int J = 0, cum = 0;  // tile tau -> (I, J), J-major (tau only grows)
+      for (int tau0 = warp; tau0 < ntiles; tau0 += kU * kW) {
+        double* cp[kU];
+        double c0[kU], c1[kU], a[kU][2], b[kU][2];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int tau = tau0 + u * kW;
+          cp[u] = nullptr;
+          if (tau < ntiles) {
+            while (cum + J + 1 <= tau) cum += ++J;
+            const int I = tau - cum;
+            cp[u] = W + (base + 8 * I + g) * ldw + base + 8 * J + 2 * t;
+            c0[u] = cp[u][0];
+            c1[u] = cp[u][1];
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              const double* pr = W + (k0 + t + 4 * s) * ldw + base;
+              a[u][s] = pr[8 * I + g];
+              b[u][s] = -pr[8 * J + g];
+            }
+          }
+        }
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+          for (int u = 0; u < kU; ++u)
+            if (cp[u]) dmma(c0[u], c1[u], a[u][s], b[u][s]);
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          if (cp[u]) {
+            cp[u][0] = c0[u];
+            cp[u][1] = c1[u];
+          }
+      }
+      __syncthreads();
+      continue;
+    }
     for (int I = warp; I < T4; I += kThreads / 32) {
       const int i0 = 4 * I;
       for (int jc = i0 & ~31; jc < L; jc += 128) {
@@ -283,7 +364,9 @@ __device__ __noinline__ void write_outputs(const double* Wg, int ldw, int n, int
   const int nf = NT * (NT - 1) * 32;
   for (int idx = threadIdx.x; idx < nf; idx += kThreads) {
     const int f = idx >> 5, lane = idx & 31;
-    int J = 1;
+    // target block J of fragment f: the largest J with J(J-1) <= f
+    int J = static_cast<int>((1.0f + sqrtf(1.0f + 4.0f * f)) * 0.5f);
+    while (J * (J - 1) > f) --J;
     while ((J + 1) * J <= f) ++J;
     const int s = f - J * (J - 1);
     const int g = lane >> 2, t = lane & 3;
