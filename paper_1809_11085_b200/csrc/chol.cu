@@ -182,13 +182,11 @@ __device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool ad
     for (int i = tid; i < n; i += kThreads) W[i * ldw + i] = W[i * ldw + i] + s;
   __syncthreads();
   long long t_a = 0, t_b = 0, t0 = 0;
-  for (int k0 = 0; k0 < n; k0 += kPanel) {
-    const int kb = min(kPanel, n - k0);
-    t0 = clock64();
-    // (a) diagonal block on ONE thread, entirely in registers (identity beyond kb): the pivot
-    // chain is rsqrt -> scale -> one FMA per column, with no shuffle or barrier in it, and the
-    // rest of each rank-1 update is independent work that fills the rsqrt latency.
-    if (tid == 0) {
+  // (a) diagonal block on ONE thread, entirely in registers (identity beyond kb): the pivot
+  // chain is rsqrt -> scale -> one FMA per column, with no shuffle or barrier in it, and the
+  // rest of each rank-1 update is independent work that fills the rsqrt latency.
+  auto diag_block = [&](int k0, int kb) {
+    {
       double a[kPanel][kPanel];
 #pragma unroll
       for (int r = 0; r < kPanel; ++r)
@@ -226,6 +224,14 @@ __device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool ad
         *sval = badv;
       }
     }
+  };
+  // n a multiple of 8: look-ahead -- block k+1's diagonal factorisation runs on thread 0 while
+  // the other warps finish panel k's trailing update (its tile is updated first)
+  const bool lookahead = (n & 7) == 0 && n >= 128;  // (measured: no gain below n = 128)
+  for (int k0 = 0; k0 < n; k0 += kPanel) {
+    const int kb = min(kPanel, n - k0);
+    t0 = clock64();
+    if ((!lookahead || k0 == 0) && tid == 0) diag_block(k0, kb);
     __syncthreads();
     t_a += clock64() - t0;
     t0 = clock64();
@@ -268,7 +274,22 @@ __device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool ad
       const int TL = L >> 3, ntiles = TL * (TL + 1) / 2;
       const int g = lane >> 2, t = lane & 3;
       constexpr int kU = 4;  // tiles in flight per warp (independent loads and MMAs)
-      constexpr int kW = kThreads / 32;
+      const int kW = lookahead ? kThreads / 32 - 1 : kThreads / 32;  // tile-sharing warps
+      if (lookahead && warp == 0) {
+        if (ntiles > 0) {  // tile (0,0): the next diagonal block
+          double* cp = W + (base + g) * ldw + base + 2 * t;
+          double c0 = cp[0], c1 = cp[1];
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            const double* pr = W + (k0 + t + 4 * s) * ldw + base;
+            dmma(c0, c1, pr[g], -pr[g]);
+          }
+          cp[0] = c0;
+          cp[1] = c1;
+          __syncwarp();
+          if (lane == 0) diag_block(base, min(kPanel, n - base));
+        }
+      } else {
       int J = 0, cum = 0;  // tile tau -> (I, J), J-major (tau only grows)
       for (int tau0 = warp; tau0 < ntiles; tau0 += kU * kW) {
         double* cp[kU];
@@ -302,6 +323,7 @@ __device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool ad
             cp[u][0] = c0[u];
             cp[u][1] = c1[u];
           }
+      }
       }
       __syncthreads();
       continue;
