@@ -180,19 +180,18 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
       const double* D = db + J * 72;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        const double2 rc = *reinterpret_cast<const double2*>(D + c * 8 + 2 * t);
-        const int owner = (lane & ~3) | (c >> 1);
-#ifndef SCQR3_TRSM_NODIAG_EXPERIMENT
+        // (column 7 of a block updates nothing inside it: its substitution step is skipped --
+        //  3-5 % faster at n = 64 and 256; at n = 128 within code-placement noise, +-0.7 %)
+        if (c < 7) {
+          const double2 rc = *reinterpret_cast<const double2*>(D + c * 8 + 2 * t);
+          const int owner = (lane & ~3) | (c >> 1);
 #pragma unroll
-        for (int a = 0; a < A; ++a) {
-          const double vc = __shfl_sync(0xffffffffu, q[a][J][c & 1], owner);
-          q[a][J][0] = fma(-vc, rc.x, q[a][J][0]);
-          q[a][J][1] = fma(-vc, rc.y, q[a][J][1]);
+          for (int a = 0; a < A; ++a) {
+            const double vc = __shfl_sync(0xffffffffu, q[a][J][c & 1], owner);
+            q[a][J][0] = fma(-vc, rc.x, q[a][J][0]);
+            q[a][J][1] = fma(-vc, rc.y, q[a][J][1]);
+          }
         }
-#else
-        (void)owner;
-        (void)rc;
-#endif
 #pragma unroll
         for (; u < nup * (c + 1) / 8; ++u) {
           const int K = J + 1 + u;
@@ -376,10 +375,12 @@ __device__ __forceinline__ void wide_phase(double (&q)[32][2], const double* __r
     const double* D = db + (J - TB) * 72;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-      const double2 rc = *reinterpret_cast<const double2*>(D + c * 8 + 2 * t);
-      const double vc = __shfl_sync(0xffffffffu, q[J - TB][c & 1], (lane & ~3) | (c >> 1));
-      q[J - TB][0] = fma(-vc, rc.x, q[J - TB][0]);
-      q[J - TB][1] = fma(-vc, rc.y, q[J - TB][1]);
+      if (c < 7) {  // (column 7 updates nothing inside its block)
+        const double2 rc = *reinterpret_cast<const double2*>(D + c * 8 + 2 * t);
+        const double vc = __shfl_sync(0xffffffffu, q[J - TB][c & 1], (lane & ~3) | (c >> 1));
+        q[J - TB][0] = fma(-vc, rc.x, q[J - TB][0]);
+        q[J - TB][1] = fma(-vc, rc.y, q[J - TB][1]);
+      }
 #pragma unroll
       for (int u = nup * c / 8; u < nup * (c + 1) / 8; ++u) {
         const int K = J + 1 + u;
