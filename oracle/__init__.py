@@ -88,6 +88,20 @@ def _load():
         lib.orc_scqr3.argtypes = [i64, i64, P, i64, P, P, P, i64, P, ctypes.POINTER(_Opts),
                                   ctypes.POINTER(_Trace), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
         lib.orc_scqr3.restype = ctypes.c_int
+        lib.orc_zgram.argtypes = [i64, i64, P, i64, P]
+        lib.orc_zcholesky.argtypes = [i64, P, dbl, P, ctypes.POINTER(i64), P]
+        lib.orc_zcholesky.restype = ctypes.c_int
+        lib.orc_ztrsm_rows.argtypes = [i64, i64, P, i64, P, P, i64]
+        lib.orc_ztrmul.argtypes = [i64, P, P]
+        lib.orc_zpower_lmax.argtypes = [i64, P, ctypes.c_int]
+        lib.orc_zpower_lmax.restype = dbl
+        lib.orc_zorth_F.argtypes = [i64, i64, P, i64]
+        lib.orc_zorth_F.restype = dbl
+        lib.orc_zresid_F.argtypes = [i64, i64, P, i64, P, i64, P]
+        lib.orc_zresid_F.restype = dbl
+        lib.orc_zscqr3.argtypes = [i64, i64, P, i64, P, i64, P, ctypes.POINTER(_Opts),
+                                   ctypes.POINTER(_Trace), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+        lib.orc_zscqr3.restype = ctypes.c_int
         lib.orc_num_threads.restype = ctypes.c_int
         lib.orc_set_num_threads.argtypes = [ctypes.c_int]
         _lib = lib
@@ -289,6 +303,90 @@ def scqr3(X, d=None, e=None, *, shift_mode=SHIFT_SAFE, shift_value=0.0, norm_mod
     else:
         st = _load().orc_scqr3(m, n, _p(X), m, _p(d), _p(e), _p(Q), m, _p(R), ctypes.byref(o), tr, cap,
                                ctypes.byref(passes))
+    k = passes.value
+    trace = [PassTrace(t.shift, bool(t.shifted), t.breakdown_pivot, t.pivot_value, t.norm2_est, t.dev_F)
+             for t in list(tr)[:k]]
+    return Result(int(st), Q, R, k, trace)
+
+
+# --------------------------------------------------------------------------- complex (N4)
+def _zcol(X) -> np.ndarray:
+    X = np.asarray(X, dtype=np.complex128)
+    if X.ndim == 1:
+        X = X[:, None]
+    return np.asfortranarray(X)
+
+
+def _zp(a):
+    return None if a is None else a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def zgram(X) -> np.ndarray:
+    """A = X^H X (Hermitian), rows ascending (^T -> ^H)."""
+    X = _zcol(X)
+    m, n = X.shape
+    A = np.zeros((n, n), dtype=np.complex128, order="F")
+    _load().orc_zgram(m, n, _zp(X), m, _zp(A))
+    return A
+
+
+def zcholesky(A, s: float = 0.0):
+    A = np.asfortranarray(np.asarray(A, dtype=np.complex128))
+    n = A.shape[0]
+    R = np.zeros((n, n), dtype=np.complex128, order="F")
+    piv = ctypes.c_int64(0)
+    pv = ctypes.c_double(0)
+    rc = _load().orc_zcholesky(n, _zp(A), float(s), _zp(R), ctypes.byref(piv), ctypes.byref(pv))
+    return Breakdown(int(piv.value), float(pv.value)) if rc else R
+
+
+def ztrsm_rows(X, R) -> np.ndarray:
+    X = _zcol(X)
+    R = np.asfortranarray(np.asarray(R, dtype=np.complex128))
+    m, n = X.shape
+    Q = np.zeros((m, n), dtype=np.complex128, order="F")
+    _load().orc_ztrsm_rows(m, n, _zp(X), m, _zp(R), _zp(Q), m)
+    return Q
+
+
+def ztrmul(Rt, R) -> np.ndarray:
+    Rt = np.asfortranarray(np.asarray(Rt, dtype=np.complex128))
+    out = np.asfortranarray(np.array(R, dtype=np.complex128))
+    _load().orc_ztrmul(Rt.shape[0], _zp(Rt), _zp(out))
+    return out
+
+
+def zpower_lmax(A, iters: int = 32) -> float:
+    A = np.asfortranarray(np.asarray(A, dtype=np.complex128))
+    return float(_load().orc_zpower_lmax(A.shape[0], _zp(A), iters))
+
+
+def zorth_F(Q) -> float:
+    Q = _zcol(Q)
+    m, n = Q.shape
+    return float(_load().orc_zorth_F(m, n, _zp(Q), m))
+
+
+def zresid_F(X, Q, R) -> float:
+    X, Q = _zcol(X), _zcol(Q)
+    R = np.asfortranarray(np.asarray(R, dtype=np.complex128))
+    m, n = X.shape
+    return float(_load().orc_zresid_F(m, n, _zp(X), m, _zp(Q), m, _zp(R)))
+
+
+def zscqr3(X, *, shift_mode=SHIFT_SAFE, shift_value=0.0, norm_mode=NORM_POWER, norm2_bound=0.0,
+           max_passes=8, stop_tol=0.5, power_iters=32, m_global=0) -> Result:
+    """Shifted CholeskyQR3 of a complex X (Alg. 3 + Alg. 2 with ^T -> ^H, reading D23)."""
+    X = _zcol(X)
+    m, n = X.shape
+    Q = np.zeros((m, n), dtype=np.complex128, order="F")
+    R = np.zeros((n, n), dtype=np.complex128, order="F")
+    o = _Opts(shift_mode, shift_value, norm_mode, norm2_bound, 0.0, max_passes, stop_tol, power_iters,
+              float(m_global), 1)
+    cap = max(max_passes, 1)
+    tr = (_Trace * cap)()
+    passes = ctypes.c_int(0)
+    st = _load().orc_zscqr3(m, n, _zp(X), m, _zp(Q), m, _zp(R), ctypes.byref(o), tr, cap, ctypes.byref(passes))
     k = passes.value
     trace = [PassTrace(t.shift, bool(t.shifted), t.breakdown_pivot, t.pivot_value, t.norm2_est, t.dev_F)
              for t in list(tr)[:k]]

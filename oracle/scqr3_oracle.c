@@ -25,6 +25,9 @@
  *   orc_gram_oblique_csr  pinned (CSR of the tridiagonal B in the same term order is
  *                         bitwise orc_gram_oblique; CSR identity = orc_gram; exact integer
  *                         cases against int64 arithmetic)
+ *   orc_z* (complex, N4)  pinned (a real input reproduces the real functions bit for bit;
+ *                         exact Gaussian-integer Gram / Cholesky / TRSM / trmul; numpy complex
+ *                         Householder QR; eigvalsh closed forms; CholeskyQR2 breakdown + target)
  *   orc_scqr3_csr         pinned (CSR-tridiagonal equals orc_scqr3 bitwise; 2-D Laplacian
  *                         B: Q^T B Q = I and X = QR within the T9 ceilings)
  *   orc_cholesky          pinned (exact hand cases, S:69 breakdown, T2 backward error)
@@ -640,6 +643,287 @@ int orc_scqr3_csr(int64_t m, int64_t n, const double* X, int64_t ld, const int64
   if (!rp || !ci || !cv) return 1;
   const orc_metric B = {NULL, NULL, rp, ci, cv};
   return scqr3_impl(m, n, X, ld, &B, Q, ldq, R, o, trace, trace_cap, passes_out);
+}
+
+/* ========================================================================= */
+/* Complex matrices ("everything carries over to complex matrices", P:124-125;
+ * reading D23: transposes become conjugate transposes, u = 2^-53, the shift formula unchanged).
+ * Storage: column-major interleaved complex, element (i, j) at Z[2(i + j ld)] (re), +1 (im).
+ * Complex arithmetic is written out on real parts in a fixed order, so a real input (all
+ * imaginary parts 0) reproduces the real functions above bit for bit (a pin). */
+#define ZRE(Z, i, j, ld) (Z)[2 * ((i) + (j) * (ld))]
+#define ZIM(Z, i, j, ld) (Z)[2 * ((i) + (j) * (ld)) + 1]
+
+/* A = X^H X (n x n, Hermitian, full), rows ascending: A_jl = sum_i conj(x_ij) x_il for j <= l,
+ * A_lj = conj(A_jl) (Alg. 1 line 1 with ^T -> ^H). */
+void orc_zgram(int64_t m, int64_t n, const double* X, int64_t ld, double* A) {
+#pragma omp parallel for schedule(dynamic)
+  for (int64_t jl = 0; jl < n * n; ++jl) {
+    const int64_t j = jl % n, l = jl / n;
+    if (j > l) continue;
+    double re = 0.0, im = 0.0;
+    for (int64_t i = 0; i < m; ++i) {
+      const double a = ZRE(X, i, j, ld), b = ZIM(X, i, j, ld), c = ZRE(X, i, l, ld), d = ZIM(X, i, l, ld);
+      re = re + (a * c + b * d); /* conj(a + ib)(c + id) */
+      im = im + (a * d - b * c);
+    }
+    ZRE(A, j, l, n) = re;
+    ZIM(A, j, l, n) = j == l ? 0.0 : im;
+    ZRE(A, l, j, n) = re;
+    ZIM(A, l, j, n) = j == l ? 0.0 : -im;
+  }
+}
+
+/* R^H R = A + sI (upper R, real positive diagonal), unblocked right-looking; breakdown at the
+ * first pivot (real part of the diagonal) <= 0 or non-finite, as orc_cholesky. */
+int orc_zcholesky(int64_t n, const double* A, double s, double* R, int64_t* piv, double* pivval) {
+  double* W = (double*)malloc((size_t)n * (size_t)n * 2 * sizeof(double));
+  memcpy(W, A, (size_t)n * (size_t)n * 2 * sizeof(double));
+  for (int64_t j = 0; j < n; ++j) ZRE(W, j, j, n) = ZRE(W, j, j, n) + s;
+  memset(R, 0, (size_t)n * (size_t)n * 2 * sizeof(double));
+  int rc = 0;
+  for (int64_t k = 0; k < n; ++k) {
+    const double dkk = ZRE(W, k, k, n);
+    if (!(dkk > 0.0) || !isfinite(dkk) || !isfinite(ZIM(W, k, k, n))) {
+      if (piv) *piv = k + 1;
+      if (pivval) *pivval = dkk;
+      rc = 1;
+      break;
+    }
+    const double rkk = sqrt(dkk);
+    ZRE(R, k, k, n) = rkk;
+    for (int64_t j = k + 1; j < n; ++j) {
+      ZRE(R, k, j, n) = ZRE(W, k, j, n) / rkk;
+      ZIM(R, k, j, n) = ZIM(W, k, j, n) / rkk;
+    }
+    /* W_ij -= conj(r_ki) r_kj, k < i <= j */
+    for (int64_t j = k + 1; j < n; ++j)
+      for (int64_t i = k + 1; i <= j; ++i) {
+        const double a = ZRE(R, k, i, n), b = ZIM(R, k, i, n), c = ZRE(R, k, j, n), d = ZIM(R, k, j, n);
+        ZRE(W, i, j, n) = ZRE(W, i, j, n) - (a * c + b * d);
+        ZIM(W, i, j, n) = ZIM(W, i, j, n) - (a * d - b * c);
+      }
+  }
+  if (rc == 0) {
+    if (piv) *piv = 0;
+    if (pivval) *pivval = 0.0;
+  }
+  free(W);
+  return rc;
+}
+
+/* Q = X R^{-1} row by row: q_ij = (x_ij - sum_{l<j} q_il r_lj) / r_jj (r_jj real). */
+void orc_ztrsm_rows(int64_t m, int64_t n, const double* X, int64_t ldx, const double* R, double* Q, int64_t ldq) {
+#pragma omp parallel
+  {
+    double* q = (double*)malloc((size_t)n * 2 * sizeof(double));
+#pragma omp for schedule(static)
+    for (int64_t i = 0; i < m; ++i) {
+      for (int64_t j = 0; j < n; ++j) {
+        double vr = ZRE(X, i, j, ldx), vi = ZIM(X, i, j, ldx);
+        for (int64_t l = 0; l < j; ++l) {
+          const double a = q[2 * l], b = q[2 * l + 1], c = ZRE(R, l, j, n), d = ZIM(R, l, j, n);
+          vr = vr - (a * c - b * d); /* (a + ib)(c + id) */
+          vi = vi - (a * d + b * c);
+        }
+        const double rjj = ZRE(R, j, j, n);
+        q[2 * j] = vr / rjj;
+        q[2 * j + 1] = vi / rjj;
+      }
+      for (int64_t j = 0; j < n; ++j) {
+        ZRE(Q, i, j, ldq) = q[2 * j];
+        ZIM(Q, i, j, ldq) = q[2 * j + 1];
+      }
+    }
+    free(q);
+  }
+}
+
+/* R := Rt R (upper, complex): (Rt R)_ij = sum_{k=i..j} Rt_ik R_kj, k ascending. */
+void orc_ztrmul(int64_t n, const double* Rt, double* R) {
+  double* P = (double*)calloc((size_t)n * (size_t)n * 2, sizeof(double));
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t i = 0; i <= j; ++i) {
+      double re = 0.0, im = 0.0;
+      for (int64_t k = i; k <= j; ++k) {
+        const double a = ZRE(Rt, i, k, n), b = ZIM(Rt, i, k, n), c = ZRE(R, k, j, n), d = ZIM(R, k, j, n);
+        re = re + (a * c - b * d);
+        im = im + (a * d + b * c);
+      }
+      ZRE(P, i, j, n) = re;
+      ZIM(P, i, j, n) = im;
+    }
+  memcpy(R, P, (size_t)n * (size_t)n * 2 * sizeof(double));
+  free(P);
+}
+
+/* lambda_max of Hermitian A by power iteration from the all-ones vector (as orc_power_lmax),
+ * Rayleigh quotient Re(x^H A x). */
+double orc_zpower_lmax(int64_t n, const double* A, int iters) {
+  double* x = (double*)malloc((size_t)n * 2 * sizeof(double));
+  double* y = (double*)malloc((size_t)n * 2 * sizeof(double));
+  const double nx = sqrt((double)n);
+  for (int64_t i = 0; i < n; ++i) { x[2 * i] = 1.0 / nx; x[2 * i + 1] = 0.0; }
+  for (int it = 0; it < iters; ++it) {
+    double ss = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      double vr = 0.0, vi = 0.0;
+      for (int64_t j = 0; j < n; ++j) {
+        const double a = ZRE(A, i, j, n), b = ZIM(A, i, j, n), c = x[2 * j], d = x[2 * j + 1];
+        vr = vr + (a * c - b * d);
+        vi = vi + (a * d + b * c);
+      }
+      y[2 * i] = vr;
+      y[2 * i + 1] = vi;
+      ss = ss + (vr * vr + vi * vi);
+    }
+    const double ny = sqrt(ss);
+    if (!(ny > 0.0)) break;
+    for (int64_t i = 0; i < 2 * n; ++i) x[i] = y[i] / ny;
+  }
+  double lam = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double vr = 0.0, vi = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+      const double a = ZRE(A, i, j, n), b = ZIM(A, i, j, n), c = x[2 * j], d = x[2 * j + 1];
+      vr = vr + (a * c - b * d);
+      vi = vi + (a * d + b * c);
+    }
+    lam = lam + (x[2 * i] * vr + x[2 * i + 1] * vi); /* Re(conj(x_i) v_i) */
+  }
+  free(x);
+  free(y);
+  return lam;
+}
+
+/* ||Q^H Q - I||_F, every entry accumulated in double-double (Dot2 on real and imaginary parts). */
+double orc_zorth_F(int64_t m, int64_t n, const double* Q, int64_t ld) {
+  double tot = 0.0;
+#pragma omp parallel for schedule(dynamic) reduction(+ : tot)
+  for (int64_t jl = 0; jl < n * n; ++jl) {
+    const int64_t j = jl % n, l = jl / n;
+    if (j > l) continue;
+    double sr = 0, cr = 0, si = 0, ci = 0, p, pe, t, te;
+    for (int64_t i = 0; i < m; ++i) {
+      const double a = ZRE(Q, i, j, ld), b = ZIM(Q, i, j, ld), c = ZRE(Q, i, l, ld), d = ZIM(Q, i, l, ld);
+      two_prod(a, c, &p, &pe); two_sum(sr, p, &t, &te); sr = t; cr += te + pe;
+      two_prod(b, d, &p, &pe); two_sum(sr, p, &t, &te); sr = t; cr += te + pe;
+      two_prod(a, d, &p, &pe); two_sum(si, p, &t, &te); si = t; ci += te + pe;
+      two_prod(-b, c, &p, &pe); two_sum(si, p, &t, &te); si = t; ci += te + pe;
+    }
+    double vr = sr + cr, vi = si + ci;
+    if (j == l) vr = vr - 1.0;
+    tot += (j == l ? 1.0 : 2.0) * (vr * vr + vi * vi);
+  }
+  return sqrt(tot);
+}
+
+/* ||X - Q R||_F / ||X||_F, compensated row products. */
+double orc_zresid_F(int64_t m, int64_t n, const double* X, int64_t ldx, const double* Q, int64_t ldq,
+                    const double* R) {
+  double num = 0.0, den = 0.0;
+#pragma omp parallel for schedule(static) reduction(+ : num, den)
+  for (int64_t i = 0; i < m; ++i) {
+    for (int64_t j = 0; j < n; ++j) {
+      double sr = -ZRE(X, i, j, ldx), si = -ZIM(X, i, j, ldx), cr = 0, ci = 0, p, pe, t, te;
+      for (int64_t l = 0; l <= j; ++l) {
+        const double a = ZRE(Q, i, l, ldq), b = ZIM(Q, i, l, ldq), c = ZRE(R, l, j, n), d = ZIM(R, l, j, n);
+        two_prod(a, c, &p, &pe); two_sum(sr, p, &t, &te); sr = t; cr += te + pe;
+        two_prod(-b, d, &p, &pe); two_sum(sr, p, &t, &te); sr = t; cr += te + pe;
+        two_prod(a, d, &p, &pe); two_sum(si, p, &t, &te); si = t; ci += te + pe;
+        two_prod(b, c, &p, &pe); two_sum(si, p, &t, &te); si = t; ci += te + pe;
+      }
+      const double rr = sr + cr, ri = si + ci;
+      num += rr * rr + ri * ri;
+      den += ZRE(X, i, j, ldx) * ZRE(X, i, j, ldx) + ZIM(X, i, j, ldx) * ZIM(X, i, j, ldx);
+    }
+  }
+  return sqrt(num / den);
+}
+
+/* Shifted CholeskyQR3 for complex X (standard inner product): the pass controller of
+ * scqr3_impl with ^T -> ^H (shift modes, re-shift on breakdown, stop rule D6). */
+int orc_zscqr3(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, int64_t ldq, double* R,
+               const orc_opts* o, orc_trace* trace, int trace_cap, int* passes_out) {
+  if (m < 1 || n < 1 || ld < m || ldq < m) return 1;
+  const int max_passes = o->max_passes > 0 ? o->max_passes : 8;
+  const double stop_tol = o->stop_tol > 0 ? o->stop_tol : 0.5;
+  const int iters = o->power_iters > 0 ? o->power_iters : 32;
+  const double mg = o->m_global > 0 ? o->m_global : (double)m;
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t i = 0; i < m; ++i) {
+      ZRE(Q, i, j, ldq) = ZRE(X, i, j, ld);
+      ZIM(Q, i, j, ldq) = ZIM(X, i, j, ld);
+    }
+  memset(R, 0, (size_t)n * (size_t)n * 2 * sizeof(double));
+  for (int64_t j = 0; j < n; ++j) ZRE(R, j, j, n) = 1.0;
+  double* A = (double*)malloc((size_t)n * (size_t)n * 2 * sizeof(double));
+  double* Rt = (double*)malloc((size_t)n * (size_t)n * 2 * sizeof(double));
+  int status = 3, k = 0;
+  for (k = 1; k <= max_passes; ++k) {
+    orc_zgram(m, n, Q, ldq, A);
+    double dev = 0.0;
+    for (int64_t l = 0; l < n; ++l)
+      for (int64_t j = 0; j < n; ++j) {
+        const double vr = ZRE(A, j, l, n) - (j == l ? 1.0 : 0.0), vi = ZIM(A, j, l, n);
+        dev = dev + (vr * vr + vi * vi);
+      }
+    dev = sqrt(dev);
+    if (k == 1) {
+      int bad = 0;
+      for (int64_t j = 0; j < n; ++j)
+        if (!isfinite(ZRE(A, j, j, n))) bad = 1;
+      if (bad) { status = 1; break; }
+    }
+    double N2;
+    if (k == 1 && o->norm_mode == 2) N2 = o->norm2_bound * o->norm2_bound;
+    else if (o->norm_mode == 1) {
+      N2 = 0.0;
+      for (int64_t j = 0; j < n; ++j) N2 = N2 + ZRE(A, j, j, n);
+    } else {
+      N2 = orc_zpower_lmax(n, A, iters) * 1.01;
+    }
+    const double s = (o->shift_mode == 1 && k == 1) ? o->shift_value : orc_shift(mg, (double)n, N2);
+    const double sp = 0x1p-53 * N2;
+    const int practical = o->shift_mode == 4;
+    int64_t piv = 0;
+    double pv = 0.0, bval = 0.0, s_used = 0.0;
+    int shifted = 0, bpiv = 0, rc;
+    const int shift_first = k == 1 && (o->shift_mode == 0 || o->shift_mode == 1 || practical);
+    if (!shift_first) {
+      rc = orc_zcholesky(n, A, 0.0, Rt, &piv, &pv);
+      if (rc) { bpiv = (int)piv; bval = pv; }
+    } else {
+      rc = 1;
+    }
+    if (rc && o->shift_mode != 2) {
+      shifted = 1;
+      s_used = practical ? sp : s;
+      rc = orc_zcholesky(n, A, s_used, Rt, &piv, &pv);
+      if (rc) { bpiv = (int)piv; bval = pv; }
+      if (rc && practical) {
+        s_used = s;
+        rc = orc_zcholesky(n, A, s_used, Rt, &piv, &pv);
+        if (rc) { bpiv = (int)piv; bval = pv; }
+      }
+    }
+    if (trace && k - 1 < trace_cap) {
+      trace[k - 1].shift = shifted ? s_used : 0.0;
+      trace[k - 1].shifted = shifted;
+      trace[k - 1].breakdown_pivot = bpiv;
+      trace[k - 1].pivot_value = bval;
+      trace[k - 1].norm2_est = N2;
+      trace[k - 1].dev_F = dev;
+    }
+    if (rc) { status = 2; break; }
+    orc_ztrsm_rows(m, n, Q, ldq, Rt, Q, ldq);
+    orc_ztrmul(n, Rt, R);
+    if (!shifted && dev <= stop_tol) { status = 0; break; }
+  }
+  if (passes_out) *passes_out = k > max_passes ? max_passes : k;
+  free(A);
+  free(Rt);
+  return status;
 }
 
 int orc_num_threads(void) {

@@ -95,6 +95,25 @@ def randsvd(m: int, n: int, kappa: float, seed: int = 0, spectrum: str = "geomet
     return np.asfortranarray(X)
 
 
+def _signed_zqr(G: np.ndarray) -> np.ndarray:
+    """Thin unitary Q of a complex G with the phases normalised so diag(R) > 0 (unique)."""
+    Q, R = np.linalg.qr(G, mode="reduced")
+    d = np.diag(R)
+    ph = np.where(np.abs(d) > 0, d / np.abs(d), 1.0)
+    return Q * ph
+
+
+def randsvd_complex(m: int, n: int, kappa: float, seed: int = 0, spectrum: str = "geometric") -> np.ndarray:
+    """Complex X = U diag(sigma) V^H (P:1510-1521 recipe with unitary U, V from complex Gaussians;
+    N4), column-major complex128."""
+    rng_u = np.random.default_rng([seed, TAG_U, 1])
+    rng_v = np.random.default_rng([seed, TAG_V, 1])
+    U = _signed_zqr((rng_u.standard_normal((m, n)) + 1j * rng_u.standard_normal((m, n))) / np.sqrt(2))
+    V = _signed_zqr((rng_v.standard_normal((n, n)) + 1j * rng_v.standard_normal((n, n))) / np.sqrt(2))
+    s = sigma(n, kappa, spectrum, seed)
+    return np.asfortranarray((U * s) @ V.conj().T)
+
+
 def tridiag_b(m: int, seed: int = 0):
     """Bands (d, e) of the SPD tridiagonal metric of BASELINE config 5; e[m-1] = 0 (unused)."""
     rng = np.random.default_rng([seed, TAG_B])
