@@ -13,14 +13,15 @@
 // Breakdown = first pivot <= 0 or non-finite, in pivot order (reading D9).  The norm estimate is
 // only needed when a shift is formed (pass 1, or a pass whose plain Cholesky broke down).
 //
-// Cholesky: right-looking with 32-column panels on a row-major working copy W of A (leading
-// dimension n+1: conflict-free row and column access; shared memory for n <= 159, else an
-// L2-resident global scratch).  Per panel: (a) one warp factors the 32x32 diagonal block in
-// registers (lane j owns column j; the pivot chain is shuffle -> rsqrt -> scale -> one FMA, the
-// rest of the rank-1 updates hang off it); (b) one thread per column forms the panel's rows of R~;
-// (c) all threads apply the rank-32 trailing update in 4x4 register tiles.  Outputs for the TRSM
-// kernel: -R~ in mma B-fragment order, and for each 8x8 diagonal block the strict upper part
-// scaled by its row's reciprocal pivot plus the reciprocal pivots; R~ itself for trmul_kernel.
+// Cholesky: right-looking with 8-column panels on a row-major working copy W of A (leading
+// dimension n+1; shared memory for n <= 159, else an L2-resident global scratch).  Per panel:
+// (a) ONE thread factors the 8x8 diagonal block in registers (pivot chain rsqrt -> scale -> FMA,
+// no shuffle or barrier in it); (b) one thread per column forms the panel's rows of R~; (c) the
+// rank-8 trailing update -- 8x8 tiles on DMMA when n % 8 == 0 (with a look-ahead for n >= 128:
+// the next diagonal block is updated first and factored by one thread while the other warps
+// finish), else 4x4 register tiles.  Outputs for the TRSM kernel: -R~ in mma B-fragment order,
+// and for each 8x8 diagonal block the strict upper part scaled by its row's reciprocal pivot plus
+// the reciprocal pivots; R~ itself for trmul_kernel.
 #include <math.h>
 
 #include "scqr3.h"
