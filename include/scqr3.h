@@ -164,6 +164,19 @@ size_t scqr3_workspace_size_csr(int64_t m, int64_t n, int64_t halo);
 int scqr3_factor_oblique_csr(int64_t m, int64_t n, const double* X, int64_t ld, const scqr3_csr* B,
                              double* Q, int64_t ldq, double* R, const scqr3_opts* opts);
 
+/* Complex X ("everything carries over to complex matrices";
+ * reading D23: X^H X, R~^H R~ = A + sI with a real positive diagonal, the same shift formula).
+ * X, Q: m x n complex double (C99 double complex / cuDoubleComplex: interleaved re, im),
+ * column-major with leading dimensions ld, ldq >= m counted in complex elements, 16-byte
+ * aligned; R: n x n complex, column-major, leading dimension n, upper with a real positive
+ * diagonal.  1 <= n <= 256.  The tall-skinny steps run the real Gram and TRSM kernels on the
+ * m x 2n real "split" matrix (Re x_0, Im x_0, Re x_1, ...), the n x n step is complex.  Same
+ * options, statuses and trace as scqr3_factor; opts->workspace must hold
+ * scqr3_workspace_size_complex(m, n) bytes. */
+size_t scqr3_workspace_size_complex(int64_t m, int64_t n);
+int scqr3_factor_complex(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, int64_t ldq, double* R,
+                         const scqr3_opts* opts);
+
 /* Host-memory variant of scqr3_factor (the end-to-end call): copies X_host to the device
  * (pinned host memory recommended), factors in place, copies Q and R back.  opts->workspace
  * must hold scqr3_host_workspace_size(m, n) bytes. */

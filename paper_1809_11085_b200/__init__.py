@@ -20,7 +20,7 @@ __all__ = [
     "scqr3_factor", "scqr3_factor_oblique", "scqr3_factor_host", "scqr3_gram", "scqr3_gram_oblique",
     "scqr3_cholesky", "scqr3_trsm", "colmajor_empty", "to_colmajor", "workspace", "Comm", "Result",
     "ScqrError", "launch_count", "library_path", "CsrMetric", "scqr3_factor_oblique_csr",
-    "scqr3_gram_oblique_csr",
+    "scqr3_gram_oblique_csr", "scqr3_factor_complex", "colmajor_empty_complex",
 ]
 
 library_path = _abi.LIB_PATH
@@ -243,6 +243,38 @@ def scqr3_gram_oblique_csr(X, B: CsrMetric, *, ws=None, **kw):
     _check(_abi.lib().scqr3_gram_oblique_csr(m, n, X.data_ptr(), _ld(X), ctypes.byref(cb), A.data_ptr(),
                                              cs.data_ptr(), ctypes.byref(o)))
     return A, cs
+
+
+def colmajor_empty_complex(m: int, n: int, ld: int | None = None, device="cuda"):
+    """Column-major complex128 (m, n) tensor (strides (1, ld))."""
+    torch = _torch()
+    ld = ld or m
+    return torch.empty((n, ld), dtype=torch.complex128, device=device).t()[:m]
+
+
+def scqr3_factor_complex(X, *, Q=None, R=None, ws=None, **kw) -> Result:
+    """Shifted CholeskyQR3 of a complex column-major complex128 CUDA tensor (N4, reading D23)."""
+    torch = _torch()
+    if X.dtype != torch.complex128:
+        raise ScqrError("scqr3_factor_complex expects complex128")
+    m, n = X.shape
+    if X.stride(0) != 1:
+        raise ScqrError("X must be column-major")
+    if Q is None:
+        Q = colmajor_empty_complex(m, n, device=X.device)
+    if R is None:
+        R = torch.empty((n, n), dtype=torch.complex128, device=X.device).t()
+    if ws is None:
+        nbytes = _abi.lib().scqr3_workspace_size_complex(m, n)
+        if nbytes == 0:
+            raise ScqrError(f"unsupported size m={m} n={n}")
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=X.device)
+    o, tr, passes = _opts(ws=ws, **kw)
+    ldx = X.stride(1) if n > 1 else max(m, 1)
+    ldq = Q.stride(1) if n > 1 else max(m, 1)
+    rc = _check(_abi.lib().scqr3_factor_complex(m, n, X.data_ptr(), ldx, Q.data_ptr(), ldq, R.data_ptr(),
+                                                ctypes.byref(o)))
+    return Result(rc, Q, R, passes.value, _trace(tr, passes.value))
 
 
 def scqr3_factor_host(X, *, Q=None, R=None, ws=None, **kw) -> Result:

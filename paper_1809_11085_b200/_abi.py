@@ -18,7 +18,8 @@ EXPORTED = [
     "scqr3_host_workspace_size", "scqr3_factor_host", "scqr3_gram", "scqr3_gram_oblique",
     "scqr3_cholesky", "scqr3_trsm", "scqr3_comm_unique_id", "scqr3_comm_init",
     "scqr3_comm_destroy", "scqr3_last_error", "scqr3_launch_count", "scqr3_workspace_size_csr",
-    "scqr3_factor_oblique_csr", "scqr3_gram_oblique_csr",
+    "scqr3_factor_oblique_csr", "scqr3_gram_oblique_csr", "scqr3_workspace_size_complex",
+    "scqr3_factor_complex",
 ]
 
 
@@ -91,6 +92,9 @@ def lib():
         L.scqr3_workspace_size_csr.restype = ctypes.c_size_t
         L.scqr3_factor_oblique_csr.argtypes = [i64, i64, vp, i64, PC, vp, i64, vp, P]
         L.scqr3_gram_oblique_csr.argtypes = [i64, i64, vp, i64, PC, vp, vp, P]
+        L.scqr3_workspace_size_complex.argtypes = [i64, i64]
+        L.scqr3_workspace_size_complex.restype = ctypes.c_size_t
+        L.scqr3_factor_complex.argtypes = [i64, i64, vp, i64, vp, i64, vp, P]
         L.scqr3_cholesky.argtypes = [i64, vp, ctypes.c_double, vp, ctypes.POINTER(ctypes.c_int32),
                                      ctypes.POINTER(ctypes.c_double), P]
         L.scqr3_trsm.argtypes = [i64, i64, vp, i64, vp, vp, i64, P]
@@ -100,7 +104,7 @@ def lib():
         L.scqr3_last_error.restype = ctypes.c_char_p
         L.scqr3_launch_count.argtypes = [ctypes.c_int32]
         L.scqr3_launch_count.restype = ctypes.c_int64
-        for name in ("scqr3_factor_oblique_csr", "scqr3_gram_oblique_csr",
+        for name in ("scqr3_factor_oblique_csr", "scqr3_gram_oblique_csr", "scqr3_factor_complex",
                      "scqr3_factor", "scqr3_factor_oblique", "scqr3_factor_host", "scqr3_gram",
                      "scqr3_gram_oblique", "scqr3_cholesky", "scqr3_trsm", "scqr3_comm_unique_id",
                      "scqr3_comm_init", "scqr3_comm_destroy"):

@@ -895,6 +895,205 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
   return status;
 }
 
+// ---- complex X (reading D23): real kernels on the m x 2n split matrix, complex
+// n x n step (zchol.cu).  Host-driven pass loop (as the multi-GPU path).
+struct ZLayout {
+  Layout L;        // real layout for the 2n-column split matrix
+  int64_t lds;     // split matrix leading dimension (even, >= m)
+  size_t S, A, Rtz, end;
+};
+
+ZLayout make_zlayout(int64_t m, int64_t n) {
+  ZLayout Z{};
+  Z.L = make_layout(m, 2 * n, 0);
+  Z.lds = std::max<int64_t>(2, (m + 1) & ~1LL);
+  size_t off = Z.L.end;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  Z.S = take(static_cast<size_t>(Z.lds) * 2 * n * 8);
+  Z.A = take(static_cast<size_t>(n) * n * 16);
+  Z.Rtz = take(static_cast<size_t>(n) * n * 16);
+  Z.end = off;
+  return Z;
+}
+
+int zfactor_impl(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, int64_t ldq, double* R,
+                 const scqr3_opts* o) {
+  TRY(check_opts(o));
+  if (n < 1 || 2 * n > kMaxN) return fail("complex n=%lld outside [1, %d]", (long long)n, kMaxN / 2);
+  if (m < 0) return fail("m < 0");
+  if (m > 0 && (!X || !Q)) return fail("X or Q is NULL");
+  if (ld < std::max<int64_t>(m, 1) || ldq < std::max<int64_t>(m, 1)) return fail("leading dimension < m");
+  if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Q)) % 16) return fail("X, Q must be 16-byte aligned");
+  if (!R) return fail("R is NULL");
+  Ctx* c;
+  TRY(get_ctx(&c));
+  cudaStream_t st = static_cast<cudaStream_t>(o->stream);
+  Comm* cm = static_cast<Comm*>(o->comm);
+  const ZLayout Z = make_zlayout(m, n);
+  const Layout& L = Z.L;
+  if (!o->workspace || o->workspace_bytes < Z.end) return fail("workspace too small: %zu < %zu bytes", o->workspace_bytes, Z.end);
+  if (reinterpret_cast<uintptr_t>(o->workspace) % 256) return fail("workspace must be 256-byte aligned");
+  WS w;
+  TRY(carve(L, o, &w));
+  char* wb = static_cast<char*>(o->workspace);
+  double* S = reinterpret_cast<double*>(wb + Z.S);
+  double* Az = reinterpret_cast<double*>(wb + Z.A);
+  double* Rtz = reinterpret_cast<double*>(wb + Z.Rtz);
+  c->prof = o->prof;
+  c->prof_stream = st;
+  c->ev_used = 0;
+  const int max_passes = o->max_passes > 0 ? o->max_passes : 8;
+  if (max_passes > Ctx::kSlots) return fail("max_passes %d > %d", max_passes, Ctx::kSlots);
+  int64_t mg = o->m_global;
+  if (mg <= 0) {
+    if (cm) {
+      int64_t* dm = reinterpret_cast<int64_t*>(w.misc + 2);
+      CUDA_TRY(cudaMemcpyAsync(dm, &m, 8, cudaMemcpyHostToDevice, st));
+      NCCL_TRY(ncclAllReduce(dm, dm, 1, ncclInt64, ncclSum, cm->nccl, st));
+      CUDA_TRY(cudaMemcpyAsync(&mg, dm, 8, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+    } else {
+      mg = m;
+    }
+  }
+  if (mg < n) return fail("m_global=%lld < n=%lld", (long long)mg, (long long)n);
+  const int n2 = static_cast<int>(2 * n);
+  if (m > 0) {
+    const long long blocks = std::max<long long>(1, std::min<long long>((m * n + 255) / 256, 8192));
+    z2split_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(X, ld, m, static_cast<int>(n), S, Z.lds);
+    ++g_launches;
+    CUDA_TRY(cudaGetLastError());
+  }
+  int* last_pass = reinterpret_cast<int*>(w.misc + 14);
+  CUDA_TRY(cudaMemsetAsync(last_pass, 0, sizeof(int), st));
+  CUDA_TRY(cudaMemsetAsync(last_pass, max_passes, 1, st));
+  ZCholParams zp{};
+  zp.A = Az;
+  zp.W = w.W;  // the real layout's 2n(2n+1) doubles hold the n x n complex scratch
+  zp.n = static_cast<int>(n);
+  zp.last_pass = last_pass;
+  zp.shift_mode = o->shift_mode;
+  zp.shift_value = o->shift_value;
+  zp.norm_mode = o->norm_mode;
+  zp.norm2_bound = o->norm2_bound;
+  zp.power_iters = o->power_iters > 0 ? o->power_iters : 32;
+  zp.m_global = static_cast<double>(mg);
+  zp.stop_tol = o->stop_tol > 0 ? o->stop_tol : 0.5;
+  zp.Rt = Rtz;
+  zp.M = w.Rt;  // real 2n x 2n
+  zp.st_dev = w.st;
+  zp.st_host = c->st_host_dev;
+  zp.w_in_smem = n <= 128 ? 1 : 0;
+  TrsmParams tp{};
+  tp.m = m;
+  tp.n = n2;
+  tp.bfrag = w.bfrag;
+  tp.dblk = w.dblk;
+  tp.st = w.st;
+  tp.X = S;
+  tp.ldx = Z.lds;
+  tp.Q = S;  // in place on the split matrix
+  tp.ldq = Z.lds;
+  const bool fuse_tg = g_fuse_tg && trsm_fuses_gram(L.NT) && m > 0;
+  int fused_chunks = 0;
+  for (int k = 0; k < max_passes; ++k) c->st_host[k].code = -1;
+  int status = SCQR3_ENOCONV, k;
+  for (k = 1; k <= max_passes; ++k) {
+    const PassGate gate{last_pass, k, nullptr};
+    c->cur_pass = k;
+    if (k == 1 || !fuse_tg) TRY(run_gram(c, L, w, S, Z.lds, m, false, nullptr, st, gate));
+    else TRY(launch_gram_reduce(c, L, w, fused_chunks, false, 0, st, gate));
+    if (cm) {
+      const int pa = prof_begin(c, PK_COMM);
+      NCCL_TRY(ncclAllReduce(w.tiles, w.tiles, L.tiles_sym * 64, ncclDouble, ncclSum, cm->nccl, st));
+      prof_end(c, pa);
+    }
+    const long long nn = n * n;
+    zcombine_kernel<<<static_cast<unsigned>((nn + 255) / 256), 256, 0, st>>>(w.tiles, static_cast<int>(n), Az,
+                                                                              last_pass, k);
+    ++g_launches;
+    CUDA_TRY(cudaGetLastError());
+    zp.pass = k;
+    if (k > 1) CUDA_TRY(cudaStreamWaitEvent(st, c->ev_side, 0));
+    const int pc = prof_begin(c, PK_CHOL);
+    {
+      const size_t zsmem = zp.w_in_smem ? static_cast<size_t>(n) * (n + 1) / 2 * 16 : 0;
+      static thread_local LaunchCfgCache zcfg;
+      if (zsmem) CUDA_TRY(cached_launch_cfg(zcfg, zchol_kernel, zsmem, 256, nullptr));
+      zchol_kernel<<<1, 256, zsmem, st>>>(zp);
+    }
+    ++g_launches;
+    CUDA_TRY(cudaGetLastError());
+    const int tot = L.NT * (L.NT - 1) * 32 + L.NT * 72;
+    trsm_prep_kernel<<<(tot + 255) / 256, 256, 0, st>>>(w.Rt, n2, L.NT, w.bfrag, w.dblk);  // M -> TRSM operands
+    ++g_launches;
+    CUDA_TRY(cudaGetLastError());
+    prof_end(c, pc);
+    CUDA_TRY(cudaEventRecord(c->ev_pass[k - 1], st));
+    // R := R~ R on the side stream
+    CUDA_TRY(cudaEventRecord(c->ev_chol, st));
+    CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_chol, 0));
+    ztrmul_kernel<<<static_cast<unsigned>((nn + 127) / 128), 128, 0, c->side>>>(Rtz, R, w.Rnew, static_cast<int>(n),
+                                                                                 k == 1, w.st, gate);
+    copy_kernel<<<static_cast<unsigned>((2 * nn + 127) / 128), 128, 0, c->side>>>(w.Rnew, R, 2 * nn, w.st, gate);
+    g_launches += 2;
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(c->ev_side, c->side));
+    tp.gate = gate;
+    tp.gram_partials = fuse_tg ? w.partials : nullptr;
+    if (m > 0) {
+      CUtensorMap mx;
+      const bool use_tma = L.NT <= 16;
+      if (use_tma) TRY(encode_map(c, &mx, S, m, n2, Z.lds, L.npad));
+      const int pt = prof_begin(c, PK_TRSM);
+      CUDA_TRY(launch_trsm(tp, use_tma ? &mx : nullptr, c->num_sms, st, &fused_chunks));
+      prof_end(c, pt);
+      ++g_launches;
+    }
+    CUDA_TRY(cudaEventSynchronize(c->ev_pass[k - 1]));
+    const volatile DevStatus* h = c->st_host + (k - 1);
+    if (h->code < 0) return fail("status block not written by the complex Cholesky kernel");
+    if (o->trace && k - 1 < o->trace_cap) {
+      scqr3_pass_trace& t = o->trace[k - 1];
+      t.shift = h->shift;
+      t.shifted = h->shifted;
+      t.breakdown_pivot = h->breakdown_pivot;
+      t.pivot_value = h->pivot_value;
+      t.norm2_est = h->norm2_est;
+      t.dev_F = h->dev_F;
+    }
+    if (h->code == SCQR3_EINVAL) {
+      status = fail("non-finite entries in X (the trace of the pass-1 Gram is not finite)");
+      break;
+    }
+    if (h->code != SCQR3_OK) {
+      status = h->code;
+      break;
+    }
+    if (h->stop) {
+      status = SCQR3_OK;
+      break;
+    }
+  }
+  if (k > max_passes) k = max_passes;
+  if (o->passes_out) *o->passes_out = k;
+  CUDA_TRY(cudaStreamWaitEvent(st, c->ev_side, 0));
+  if (status == SCQR3_OK && m > 0) {
+    const long long blocks = std::max<long long>(1, std::min<long long>((m * n + 255) / 256, 8192));
+    split2z_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(S, Z.lds, m, static_cast<int>(n), Q, ldq);
+    ++g_launches;
+    CUDA_TRY(cudaGetLastError());
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  prof_flush(c, k);
+  c->prof = nullptr;
+  return status;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1167,6 +1366,16 @@ int scqr3_comm_destroy(void* comm) {
 }
 
 const char* scqr3_last_error(void) { return g_err.c_str(); }
+
+size_t scqr3_workspace_size_complex(int64_t m, int64_t n) {
+  if (n < 1 || 2 * n > kMaxN || m < 0) return 0;
+  return make_zlayout(m, n).end;
+}
+
+int scqr3_factor_complex(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, int64_t ldq, double* R,
+                         const scqr3_opts* opts) {
+  return zfactor_impl(m, n, X, ld, Q, ldq, R, opts);
+}
 
 int64_t scqr3_launch_count(int32_t reset) {
   int64_t v = g_launches;

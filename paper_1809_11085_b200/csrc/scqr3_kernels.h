@@ -109,6 +109,28 @@ struct CholParams {
   const int* pass_dev;       // CUDA-graph loop body: pass number on the device (else `pass`)
 };
 
+// complex n x n step (zchol.cu)
+struct ZCholParams {
+  const double* A;           // A = X^H X, n x n complex (column-major interleaved)
+  double* W;                 // n x n complex scratch
+  int n;
+  int pass;
+  const int* pass_dev;
+  int* last_pass;
+  int shift_mode;
+  double shift_value;
+  int norm_mode;
+  double norm2_bound;
+  int power_iters;
+  double m_global;
+  double stop_tol;
+  double* Rt;                // R~ (n x n complex) for ztrmul_kernel
+  double* M;                 // real 2n x 2n upper-triangular image of R~ for the TRSM (column-major)
+  int w_in_smem;             // packed upper working copy in dynamic shared memory (n <= 128)
+  DevStatus* st_dev;
+  DevStatus* st_host;
+};
+
 struct TrsmParams {
   PassGate gate;
   const double* X;
@@ -141,6 +163,12 @@ __global__ void trmul_kernel(const double* Rt, const double* R, double* Rnew, in
                              PassGate gate);
 __global__ void copy_kernel(const double* src, double* dst, long long count, const DevStatus* st, PassGate gate);
 __global__ void trsm_prep_kernel(const double* R, int n, int NT, double* bfrag, double* dblk);
+__global__ void z2split_kernel(const double* Z, long long ldz, long long m, int n, double* S, long long lds);
+__global__ void split2z_kernel(const double* S, long long lds, long long m, int n, double* Z, long long ldz);
+__global__ void zcombine_kernel(const double* tiles, int n, double* A, const int* last_pass, int pass);
+__global__ void zchol_kernel(ZCholParams p);
+__global__ void ztrmul_kernel(const double* Rt, const double* R, double* Rnew, int n, int first, const DevStatus* st,
+                              PassGate gate);
 // CUDA-graph pass loop (device-side pass control): the counter advances at the
 // top of each loop-body pass; the loop continues while the Cholesky has not stopped it.
 __global__ void pass_advance_kernel(int* pass_dev);

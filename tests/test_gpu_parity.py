@@ -384,3 +384,38 @@ def test_non_finite_input_raises(bad):
         sq.scqr3_factor(dev(X))
     r = sq.scqr3_factor(dev(synth.randsvd(3000, 16, 1e3, seed=1)))   # the context recovers
     assert r.status == 0
+
+
+# ------------------------------------------------------------------ complex X (N4)
+def zdev(Z):
+    t = torch.from_numpy(np.asarray(Z, dtype=np.complex128))
+    out = sq.colmajor_empty_complex(t.shape[0], t.shape[1])
+    out.copy_(t)
+    return out
+
+
+@gpu
+@pytest.mark.parametrize("m,n,kappa", [(2000, 16, 1e12), (300, 5, 1e3), (20000, 64, 1e10), (5000, 100, 1e8),
+                                       (3000, 128, 1e12), (1500, 256, 1e6)])
+def test_complex_factor_parity(m, n, kappa):
+    X = synth.randsvd_complex(m, n, kappa, seed=0)
+    rg = sq.scqr3_factor_complex(zdev(X))
+    ro = oracle.zscqr3(X)
+    assert rg.status == 0 and ro.status == 0
+    Rg, Qg = rg.R.cpu().numpy(), rg.Q.cpu().numpy()
+    assert np.max(np.abs(Rg - ro.R)) <= 1e-10 * np.max(np.abs(ro.R))
+    assert np.array_equal(Rg, np.triu(Rg)) and np.all(np.diag(Rg).real > 0) and not np.diag(Rg).imag.any()
+    assert oracle.zorth_F(Qg) <= 10 * n * U
+    assert oracle.zresid_F(X, Qg, Rg) <= 10 * n * U
+    assert rg.trace[0]["shifted"] and ro.trace[0].shifted
+
+
+@gpu
+def test_complex_real_input_matches_real_path():
+    X = synth.randsvd(4000, 24, 1e10, seed=3)
+    a = sq.scqr3_factor(dev(X))
+    b = sq.scqr3_factor_complex(zdev(X.astype(np.complex128)))
+    assert a.status == b.status == 0 and a.passes == b.passes
+    Ra, Rb = host(a.R), b.R.cpu().numpy()
+    assert np.max(np.abs(Rb.imag)) == 0.0
+    assert np.max(np.abs(Ra - Rb.real)) <= 1e-12 * np.max(np.abs(Ra))
