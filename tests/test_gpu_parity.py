@@ -278,6 +278,11 @@ def test_single_rank_nccl_comm_path():
     c3 = sq.scqr3_factor_oblique(dev(X), torch.from_numpy(d).cuda(), torch.from_numpy(e).cuda(), comm=comm,
                                  deterministic=True)
     assert np.array_equal(host(c1.R), host(c3.R))
+    # complex path with the communicator (Gram allreduce of the split matrix)
+    Z = synth.randsvd_complex(3000, 12, 1e9, seed=4)
+    z1 = sq.scqr3_factor_complex(zdev(Z))
+    z2 = sq.scqr3_factor_complex(zdev(Z), comm=comm)
+    assert z1.status == z2.status == 0 and np.array_equal(z1.R.cpu().numpy(), z2.R.cpu().numpy())
     comm.destroy()
 
 
