@@ -264,8 +264,14 @@ def run_ours(args):
     peaks = load_json(FP64_PEAKS) or {}
     peak = peaks.get("roofline_fp64_peak_tflops", 37.1)
     kern = {}
+    # n <= 64, standard inner product: every TRSM launch but a step's last also accumulates the
+    # next pass's Gram (trsm_kernel<..., GRAM>), so its algorithmic work carries that Gram too
+    fused = (not cfg.oblique) and n <= 64 and os.environ.get("SCQR3_FUSE_TG", "1") != "0"
+    fl_trsm = mloc * float(n) * n
+    if fused and passes > 0:
+        fl_trsm += (passes - 1) / passes * mloc * n * (n + 1.0)
     for name, msum, cnt, fl in (("gram", prof.gram_ms, prof.gram_launches, mloc * n * (n + 1.0)),
-                                ("trsm", prof.trsm_ms, prof.trsm_launches, mloc * float(n) * n),
+                                ("trsm", prof.trsm_ms, prof.trsm_launches, fl_trsm),
                                 ("chol", prof.chol_ms, prof.chol_launches, None),
                                 ("reduce", prof.reduce_ms, prof.reduce_launches, None),
                                 ("comm", prof.comm_ms, prof.comm_calls, None)):
@@ -280,10 +286,10 @@ def run_ours(args):
     tr = traffic_tab.get(f"{args.config}:{dom}")
     roofline = {"bound": "tensor", "achieved": kern[dom]["tflops"], "peak": peak, "unit": "TFLOP/s",
                 "frac": kern[dom]["tflops"] / peak, "traffic": tr.get("bytes_per_launch") if tr else None,
-                "kernel": f"{dom}_kernel (FP64 DMMA)",
+                "kernel": f"{dom}_kernel (FP64 DMMA)" + (" + fused next-pass Gram" if dom == "trsm" and fused else ""),
                 "peak_source": "measured FP64 DMMA loop on this pool's B200 (profiles/fp64_peaks.json); "
                                "MEASURED_PEAKS.json has no fp64 entry",
-                "algorithmic_flops_per_launch": mloc * n * (n + 1.0) if dom == "gram" else mloc * float(n) * n}
+                "algorithmic_flops_per_launch": mloc * n * (n + 1.0) if dom == "gram" else fl_trsm}
     step_roof_ms = max(flops_3pass(mloc, n) / (peak * 1e12), (24.0 * mloc * n * 3) / 6536.7e9) * 1e3
 
     # ---- end to end through the C ABI with host buffers (H2D of X, D2H of Q and R inside)
