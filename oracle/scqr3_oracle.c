@@ -536,6 +536,7 @@ static int scqr3_impl(int64_t m, int64_t n, const double* X, int64_t ld, const o
   double* A = (double*)malloc((size_t)n * (size_t)n * sizeof(double));
   double* Rt = (double*)malloc((size_t)n * (size_t)n * sizeof(double));
   double* colsq = (double*)malloc((size_t)n * sizeof(double));
+  double* Pg = (double*)malloc((size_t)n * (size_t)n * sizeof(double)); /* oblique: plain Gram for N2 */
   int status = 3, k = 0;
   for (k = 1; k <= max_passes; ++k) {
     gram_any(m, n, Q, ldq, B, o->nparts, A, colsq);
@@ -555,13 +556,18 @@ static int scqr3_impl(int64_t m, int64_t n, const double* X, int64_t ld, const o
         break;
       }
     }
-    /* norm estimate N2 ~ ||Q||_2^2 (oblique: ||Q||_2^2 via the plain column norms) */
+    /* norm estimate N2 ~ ||Q||_2^2.  Oblique (D4): lambda_max of the plain Gram Q^T Q by power
+     * iteration x 1.01 (the norm estimator of P:660, formed alongside the B-Gram), or ||Q||_F^2
+     * (FROBENIUS), or the user bound on pass 1 */
     double N2;
     if (oblique) {
       if (k == 1 && o->norm_mode == 2) N2 = o->norm2_bound * o->norm2_bound;
-      else {
+      else if (o->norm_mode == 1) {
         N2 = 0.0;
         for (int64_t j = 0; j < n; ++j) N2 = N2 + colsq[j]; /* ||Q||_F^2 >= ||Q||_2^2 */
+      } else {
+        gram_any(m, n, Q, ldq, NULL, o->nparts, Pg, NULL);
+        N2 = orc_power_lmax(n, Pg, iters) * 1.01;
       }
     } else if (k == 1 && o->norm_mode == 2) {
       N2 = o->norm2_bound * o->norm2_bound;
@@ -626,6 +632,7 @@ static int scqr3_impl(int64_t m, int64_t n, const double* X, int64_t ld, const o
   free(A);
   free(Rt);
   free(colsq);
+  free(Pg);
   return status;
 }
 

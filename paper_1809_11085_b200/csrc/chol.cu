@@ -73,8 +73,10 @@ __device__ __forceinline__ int tile_col(int tile) {
   return TJ;
 }
 
-__device__ __forceinline__ void load_W(const CholParams& p, double* W, int ldw) {
+// tiles: packed upper Gram tiles to load (default: the pass's Gram, p.tiles)
+__device__ __forceinline__ void load_W(const CholParams& p, double* W, int ldw, const double* tiles = nullptr) {
   const int n = p.n;
+  if (!tiles) tiles = p.tiles;
   if (p.mode == CHOL_ONLY) {
     for (int i = threadIdx.x >> 5; i < n; i += kThreads / 32)
       for (int j = threadIdx.x & 31; j < n; j += 32) W[i * ldw + j] = gram_entry(p, i, j);
@@ -88,7 +90,7 @@ __device__ __forceinline__ void load_W(const CholParams& p, double* W, int ldw) 
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int e = e0 + u * kThreads;
-        v[u] = e < ne ? p.tiles[e] : 0.0;
+        v[u] = e < ne ? tiles[e] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
@@ -481,10 +483,21 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
   // ---- a3: norm estimate and shift, only when a shift is formed
   const double u = 0x1p-53;
   const double mg = p.m_global, nn = static_cast<double>(n);
+  bool w_plain = false;  // W holds the plain Gram (oblique norm estimate): reload before factoring
   auto shift_for = [&](double& N2) -> double {
     if (p.oblique) {
-      if (pass == 1 && p.norm_mode == SCQR3_NORM_USER) N2 = p.norm2_bound * p.norm2_bound;
-      else N2 = p.tiles[static_cast<size_t>(p.NT) * (p.NT + 1) / 2 * 64];  // ||Q||_F^2 (reading D4)
+      const size_t nout = static_cast<size_t>(p.NT) * (p.NT + 1) / 2 * 64;
+      const double fro = p.tiles[nout];  // ||Q||_F^2, accumulated with the B-Gram
+      if (pass == 1 && p.norm_mode == SCQR3_NORM_USER) {
+        N2 = p.norm2_bound * p.norm2_bound;
+      } else if (p.norm_mode == SCQR3_NORM_FROBENIUS) {
+        N2 = fro;
+      } else {  // lambda_max(Q^T Q) x 1.01 from the plain Gram formed alongside (reading D4)
+        __syncthreads();
+        load_W(p, W, ldw, p.tiles + nout + 1);
+        N2 = power_lmax<SMEM>(W, ldw, n, p.power_iters, fro, ybuf, red) * 1.01;
+        w_plain = true;
+      }
     } else if (pass == 1 && p.norm_mode == SCQR3_NORM_USER) {
       N2 = p.norm2_bound * p.norm2_bound;
     } else if (p.norm_mode == SCQR3_NORM_FROBENIUS) {
@@ -515,6 +528,7 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
   }
   if (piv && p.shift_mode != SCQR3_SHIFT_NONE) {
     const double s_safe = shift_for(N2);
+    if (w_plain) w_dirty = true;
     const double s_p = 0x1p-53 * N2 * (p.oblique ? *p.nb_dev : 1.0);
     clk[3] = clock64();
     for (int attempt = practical ? 0 : 1; attempt < 2 && piv; ++attempt) {

@@ -102,7 +102,10 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
   int bi = 0, bj = 0;
   // the oblique Gram is also computed on the upper blocks only: A = upper(Q^T (BQ)), mirrored
   // (reading D22); its diagonal tiles take the A fragments from Q and the B fragments from Y
-  if (active) decode_job(code >> 1, p.NB, false, bi, bj);
+  // dual (oblique): jobs past the B-Gram's blocks form the plain Gram Q^T Q (B operand from Q)
+  const int nblk = p.NB * (p.NB + 1) / 2;
+  const bool plainjob = full && p.dual && active && (code >> 1) >= nblk;
+  if (active) decode_job((code >> 1) - (plainjob ? nblk : 0), p.NB, false, bi, bj);
   const bool diag = bi == bj;
   const int NT = p.NT;
   const bool edge = (bi + 1) * kJobTiles > NT || (bj + 1) * kJobTiles > NT;
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
   for (int i = 0; i < nst; ++i) {
     mbar_wait(&full_bar[st], ph);
     const unsigned char* srcA = stages + static_cast<size_t>(st) * nsrc * stage_bytes;
-    const unsigned char* srcB = full ? srcA + stage_bytes : srcA;
+    const unsigned char* srcB = (full && !plainjob) ? srcA + stage_bytes : srcA;
     if (kind == 0) {
       // 2 x 4 tiles of an off-diagonal block: 6 fragment loads, 8 DMMA per k-step
 #pragma unroll
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
       const int TI = bi * kJobTiles + rr0 + a, TJ = bj * kJobTiles + b;
       const bool valid = (TI < NT) && (TJ < NT) && (!diag || rr0 + a <= b);
       if (!valid) continue;
-      const size_t tid = static_cast<size_t>(TJ) * (TJ + 1) / 2 + TI;
+      const size_t tid = static_cast<size_t>(TJ) * (TJ + 1) / 2 + TI + (plainjob ? static_cast<size_t>(NT) * (NT + 1) / 2 : 0);
       double2 v = make_double2(acc[a][b][0], acc[a][b][1]);
       *reinterpret_cast<double2*>(out + tid * 64 + 8 * g + 2 * t) = v;
     }
@@ -230,19 +233,20 @@ __global__ void gram_reduce_kernel(GramReduceParams p) {
   __shared__ double red[8][33];
   const int lane = threadIdx.x & 31, cls = threadIdx.x >> 5;
   const long long nout = static_cast<long long>(p.NT) * (p.NT + 1) / 2 * 64;
+  const long long nall = p.dual ? 2 * nout : nout;  // partial entries to reduce
   const long long e = static_cast<long long>(blockIdx.x) * 32 + lane;
   double s = 0.0;
-  if (e < nout) {
+  if (e < nall) {
     const size_t stride = static_cast<size_t>(p.tiles_per_partial) * 64;
     const double* src = p.partials + e;
     for (int c = cls; c < p.chunks; c += 8) s += src[static_cast<size_t>(c) * stride];
   }
   red[cls][lane] = s;
   __syncthreads();
-  if (cls == 0 && e < nout) {
+  if (cls == 0 && e < nall) {
     double t = red[0][lane];
     for (int k = 1; k < 8; ++k) t += red[k][lane];
-    p.tiles[e] = t;
+    p.tiles[e < nout ? e : e + 1] = t;  // (dual: the plain Gram follows the ||Q||_F^2 slot)
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && p.colsq_partials) {
     double t = 0.0;

@@ -188,11 +188,11 @@ Layout make_layout(int64_t m, int64_t n, int oblique, int64_t halo = 1) {
   L.npad = npad_for(L.n);
   L.NT = L.npad / 8;
   L.tiles_sym = static_cast<long long>(L.NT) * (L.NT + 1) / 2;
-  L.tiles_part = L.tiles_sym;  // upper tiles for the oblique Gram too (reading D22)
+  L.tiles_part = oblique ? 2 * L.tiles_sym : L.tiles_sym;  // oblique: [Q^T Y][Q^T Q] upper tiles (D22, D4)
   {
     // CTAs per row chunk = job groups (assign_gram_jobs); fewer chunks fit on the GPU when there are more
     const long long nb = (L.NT + kJobTiles - 1) / kJobTiles;
-    const long long codes = 2 * (nb * (nb + 1) / 2);
+    const long long codes = 2 * (nb * (nb + 1) / 2) * (oblique ? 2 : 1);
     const int groups_hi = static_cast<int>(std::max<long long>(1, (codes + kMaxConsumers - 1) / kMaxConsumers));
     L.max_chunks = std::max(1, max_chunks_for_device() / groups_hi);
   }
@@ -205,7 +205,7 @@ Layout make_layout(int64_t m, int64_t n, int oblique, int64_t halo = 1) {
   };
   L.st = take(sizeof(DevStatus));
   L.partials = take(static_cast<size_t>(L.max_chunks) * L.tiles_part * 64 * 8);
-  L.tiles = take(static_cast<size_t>(L.tiles_sym * 64 + 64) * 8);
+  L.tiles = take(static_cast<size_t>(L.tiles_sym * 64 * (oblique ? 2 : 1) + 64) * 8);
   L.W = take(static_cast<size_t>(n) * (n + 1) * 8);
   L.Rnew = take(static_cast<size_t>(n) * n * 8);
   L.Rt = take(static_cast<size_t>(n) * n * 8);
@@ -279,10 +279,12 @@ int encode_map(Ctx* c, CUtensorMap* map, const double* base, int64_t m, int64_t 
 // the CTA runs on sub-partition w % 4; consumer c is warp c + 1).  Returns the number of groups
 // (CTAs sharing a row chunk) and sets *ncons_out.
 int assign_gram_jobs(GramParams& gp, bool oblique, int* ncons_out) {
-  // upper blocks only, also for the oblique Gram (reading D22)
-  (void)oblique;
-  const int nblocks = gp.NB * (gp.NB + 1) / 2;
+  // upper blocks only, also for the oblique Gram (reading D22); the oblique Gram adds the plain
+  // Gram's blocks (job codes past 2 * nsym) for its norm estimate (reading D4)
+  const int nsym = gp.NB * (gp.NB + 1) / 2;
+  const int nblocks = oblique ? 2 * nsym : nsym;
   auto coords = [&](int j, int& bi, int& bj) {
+    if (j >= nsym) j -= nsym;
     int c = 0;
     while ((c + 1) * (c + 2) / 2 <= j) ++c;
     bj = c;
@@ -343,7 +345,8 @@ int launch_gram_reduce(Ctx* c, const Layout& L, const WS& w, int chunks, bool ob
   rp.oblique = oblique ? 1 : 0;
   rp.colsq_partials = oblique ? w.colsq : nullptr;
   rp.colsq_count = colsq_count;
-  const long long nblocks = (L.tiles_sym * 64 + 31) / 32;  // 32 outputs x 8 chunk classes per block
+  rp.dual = oblique ? 1 : 0;
+  const long long nblocks = (L.tiles_sym * 64 * (oblique ? 2 : 1) + 31) / 32;  // 32 outputs x 8 chunk classes
   const int pr = prof_begin(c, PK_REDUCE);
   gram_reduce_kernel<<<static_cast<unsigned>(nblocks), 256, 0, st>>>(rp);
   prof_end(c, pr);
@@ -391,6 +394,7 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   gp.NB = (L.NT + kJobTiles - 1) / kJobTiles;
   gp.npad = L.npad;
   gp.oblique = oblique ? 1 : 0;
+  gp.dual = oblique ? 1 : 0;
   gp.tiles_per_partial = static_cast<int>(L.tiles_part);
   int ncons = 0;
   const int groups = assign_gram_jobs(gp, oblique, &ncons);
@@ -767,7 +771,8 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
       TRY(launch_gram_reduce(c, L, w, fused_chunks, false, 0, st, gate));
     }
     if (cm) {
-      const size_t cnt = static_cast<size_t>(L.tiles_sym * 64 + (oblique ? 1 : 0));
+      // B-Gram (+ ||Q||_F^2 and the plain Gram for the norm estimate when oblique)
+      const size_t cnt = static_cast<size_t>(L.tiles_sym * 64 + (oblique ? 1 + L.tiles_sym * 64 : 0));
       const int pa = prof_begin(c, PK_COMM);
       if (o->deterministic) {
         // every rank's Gram side by side (the partials area is free once gram_reduce ran), then

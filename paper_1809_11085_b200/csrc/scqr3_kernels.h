@@ -38,8 +38,9 @@ struct GramParams {
   int npad;                  // padded column count (multiple of 8, TMA box width)
   int NT;                    // npad / 8 tiles per side
   int NB;                    // ceil(NT / 4) blocks per side
-  int oblique;               // 1 = full Q^T Y
-  int tiles_per_partial;     // NT(NT+1)/2 or NT^2
+  int oblique;               // 1 = Q^T Y (upper tiles, reading D22)
+  int dual;                  // oblique: also the plain Gram Q^T Q (its norm estimate, reading D4)
+  int tiles_per_partial;     // NT(NT+1)/2, doubled when dual or NT^2
   // job of consumer warp w in group g: warp_job[g * kMaxConsumers + w] (-1 = idle); the host
   // balances the DMMA work of each group over the SM's four sub-partitions (warp % 4)
   short warp_job[kMaxGroups * kMaxConsumers];  // codes <= 2 * 136 (n <= 512)
@@ -47,6 +48,7 @@ struct GramParams {
 
 struct GramReduceParams {
   PassGate gate;
+  int dual;                  // partials hold [Q^T Y tiles][Q^T Q tiles]: output [B-Gram][||Q||_F^2][plain]
   const double* partials;
   double* tiles;             // packed upper tiles (+1 double: ||Q||_F^2 for oblique)
   int chunks;
