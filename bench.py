@@ -270,7 +270,9 @@ def run_ours(args):
     fl_trsm = mloc * float(n) * n
     if fused and passes > 0:
         fl_trsm += (passes - 1) / passes * mloc * n * (n + 1.0)
-    for name, msum, cnt, fl in (("gram", prof.gram_ms, prof.gram_launches, mloc * n * (n + 1.0)),
+    # the oblique Gram kernel also forms the plain Gram (upper tiles) for the norm estimate (D4)
+    fl_gram = mloc * n * (n + 1.0) * (2 if cfg.oblique else 1)
+    for name, msum, cnt, fl in (("gram", prof.gram_ms, prof.gram_launches, fl_gram),
                                 ("trsm", prof.trsm_ms, prof.trsm_launches, fl_trsm),
                                 ("chol", prof.chol_ms, prof.chol_launches, None),
                                 ("reduce", prof.reduce_ms, prof.reduce_launches, None),
@@ -286,10 +288,11 @@ def run_ours(args):
     tr = traffic_tab.get(f"{args.config}:{dom}")
     roofline = {"bound": "tensor", "achieved": kern[dom]["tflops"], "peak": peak, "unit": "TFLOP/s",
                 "frac": kern[dom]["tflops"] / peak, "traffic": tr.get("bytes_per_launch") if tr else None,
-                "kernel": f"{dom}_kernel (FP64 DMMA)" + (" + fused next-pass Gram" if dom == "trsm" and fused else ""),
+                "kernel": f"{dom}_kernel (FP64 DMMA)" + (" + fused next-pass Gram" if dom == "trsm" and fused else "")
+                          + (" (B-Gram + plain Gram)" if dom == "gram" and cfg.oblique else ""),
                 "peak_source": "measured FP64 DMMA loop on this pool's B200 (profiles/fp64_peaks.json); "
                                "MEASURED_PEAKS.json has no fp64 entry",
-                "algorithmic_flops_per_launch": mloc * n * (n + 1.0) if dom == "gram" else fl_trsm}
+                "algorithmic_flops_per_launch": fl_gram if dom == "gram" else fl_trsm}
     step_roof_ms = max(flops_3pass(mloc, n) / (peak * 1e12), (24.0 * mloc * n * 3) / 6536.7e9) * 1e3
 
     # ---- end to end through the C ABI with host buffers (H2D of X, D2H of Q and R inside)
