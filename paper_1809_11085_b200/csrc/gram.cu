@@ -258,12 +258,67 @@ __global__ void gram_reduce_kernel(GramReduceParams p) {
 // Y = B Q for the tridiagonal B (Alg. 4 line 1): y_i = d_i q_i + e_{i-1} q_{i-1} + e_i q_{i+1}
 // (terms in the oracle's order; the halo rows come from the neighbouring ranks), plus per-block
 // partial sums of q_ij^2 (||Q||_F^2 for the oblique shift, reading D4).
+#ifndef SCQR3_Y_COLS
+#define SCQR3_Y_COLS 4  // columns in flight per thread (measured: 4 beats 2, 8, 16)
+#endif
+#ifndef SCQR3_Y_ROWS1
+#define SCQR3_Y_PAIRS  // two rows per thread (measured 5 % faster than one; -DSCQR3_Y_ROWS1 for one)
+#endif
 __global__ void oblique_y_kernel(ObliqueYParams p) {
   __shared__ double red[32];
   if (SCQR3_GATE_SKIP(p.gate)) return;
-  // one thread per row (consecutive threads, consecutive rows: every column access coalesced),
-  // the row's band entries in registers, 8 columns in flight per step
   double sq = 0.0;
+#ifdef SCQR3_Y_PAIRS
+  // two consecutive rows per thread: one 16-byte load and store per column for the pair, the
+  // outer neighbours by two 8-byte loads (L1 hits), SCQR3_Y_COLS columns in flight
+  for (long long i0 = 2 * (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x); i0 < p.m;
+       i0 += 2 * static_cast<long long>(gridDim.x) * blockDim.x) {
+    const bool two = i0 + 1 < p.m;
+    const double d0 = p.d[i0], d1 = two ? p.d[i0 + 1] : 0.0;
+    const double el = i0 > 0 ? p.e[i0 - 1] : p.e_prev, em = p.e[i0], er = two ? p.e[i0 + 1] : 0.0;
+    const bool use_l = i0 > 0 || p.has_prev;
+    const bool use_r = i0 + 2 < p.m || p.has_next;
+    for (int j0 = 0; j0 < p.n; j0 += SCQR3_Y_COLS) {
+      double q0[SCQR3_Y_COLS], q1[SCQR3_Y_COLS], ql[SCQR3_Y_COLS], qr[SCQR3_Y_COLS];
+#pragma unroll
+      for (int jj = 0; jj < SCQR3_Y_COLS; ++jj) {
+        const int j = j0 + jj < p.n ? j0 + jj : p.n - 1;
+        const double* q = p.Q + j * p.ldq;
+        if (two) {
+          const double2 v = __ldcs(reinterpret_cast<const double2*>(q + i0));
+          q0[jj] = v.x;
+          q1[jj] = v.y;
+        } else {
+          q0[jj] = q[i0];
+          q1[jj] = p.has_next ? p.halo_next[j] : 0.0;  // row i0's lower neighbour (i0 = m-1)
+        }
+        ql[jj] = i0 > 0 ? q[i0 - 1] : (p.has_prev ? p.halo_prev[j] : 0.0);
+        qr[jj] = i0 + 2 < p.m ? q[i0 + 2] : (p.has_next && two ? p.halo_next[j] : 0.0);
+      }
+#pragma unroll
+      for (int jj = 0; jj < SCQR3_Y_COLS; ++jj) {
+        const int j = j0 + jj;
+        if (j >= p.n) continue;
+        double y0 = d0 * q0[jj];  // the oracle's term order: d_i q_i + e_{i-1} q_{i-1} + e_i q_{i+1}
+        if (use_l) y0 = fma(el, ql[jj], y0);
+        if (two || p.has_next) y0 = fma(em, q1[jj], y0);
+        sq = fma(q0[jj], q0[jj], sq);
+        double* y = p.Y + j * p.ldy;
+        if (two) {
+          double y1 = d1 * q1[jj];
+          y1 = fma(em, q0[jj], y1);
+          if (use_r) y1 = fma(er, qr[jj], y1);
+          __stcs(reinterpret_cast<double2*>(y + i0), make_double2(y0, y1));
+          sq = fma(q1[jj], q1[jj], sq);
+        } else {
+          y[i0] = y0;
+        }
+      }
+    }
+  }
+#else
+  // one thread per row (consecutive threads, consecutive rows: every column access coalesced),
+  // the row's band entries in registers, SCQR3_Y_COLS columns in flight per step
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < p.m;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const double di = p.d[i];
@@ -271,10 +326,10 @@ __global__ void oblique_y_kernel(ObliqueYParams p) {
     const double el = lo ? p.e[i - 1] : p.e_prev;
     const double er = p.e[i];
     const bool use_l = lo || p.has_prev, use_r = hi || p.has_next;
-    for (int j0 = 0; j0 < p.n; j0 += 8) {
-      double qv[8], ql[8], qr[8];
+    for (int j0 = 0; j0 < p.n; j0 += SCQR3_Y_COLS) {
+      double qv[SCQR3_Y_COLS], ql[SCQR3_Y_COLS], qr[SCQR3_Y_COLS];
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
+      for (int jj = 0; jj < SCQR3_Y_COLS; ++jj) {
         const int j = j0 + jj;
         if (j < p.n) {
           const double* q = p.Q + j * p.ldq;
@@ -284,7 +339,7 @@ __global__ void oblique_y_kernel(ObliqueYParams p) {
         }
       }
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
+      for (int jj = 0; jj < SCQR3_Y_COLS; ++jj) {
         const int j = j0 + jj;
         if (j < p.n) {
           double v = di * qv[jj];  // the oracle's term order
@@ -296,6 +351,7 @@ __global__ void oblique_y_kernel(ObliqueYParams p) {
       }
     }
   }
+#endif
   // deterministic block reduction
   for (int o = 16; o > 0; o >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
