@@ -367,20 +367,24 @@ __global__ void oblique_y_kernel(ObliqueYParams p) {
 // ||Q||_F^2 partials like oblique_y_kernel.  One thread per (row, 8-column chunk): consecutive
 // threads take consecutive rows, so each nonzero's Q reads are coalesced along the column;
 // rows outside [0, m) come from the halo buffers (neighbouring ranks' rows).
+#ifndef SCQR3_CSR_COLS
+#define SCQR3_CSR_COLS 16  // columns per thread (measured on C5L: 16 beats 4, 8, 32, 64)
+#endif
 __global__ void csr_y_kernel(ObliqueYParams p) {
   __shared__ double red[32];
   if (SCQR3_GATE_SKIP(p.gate)) return;
-  const int nch = (p.n + 7) / 8;
+  constexpr int C = SCQR3_CSR_COLS;
+  const int nch = (p.n + C - 1) / C;
   const long long total = p.m * nch;
   double sq = 0.0;
   for (long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; k < total;
        k += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long i = k % p.m;
-    const int c0 = static_cast<int>(k / p.m) * 8;
-    const int cw = min(8, p.n - c0);
-    double acc[8];
+    const int c0 = static_cast<int>(k / p.m) * C;
+    const int cw = min(C, p.n - c0);
+    double acc[C];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+    for (int j = 0; j < C; ++j) acc[j] = 0.0;
     for (long long z = p.rp[i]; z < p.rp[i + 1]; ++z) {
       const long long col = p.ci[z];
       const double v = p.cv[z];
@@ -396,17 +400,19 @@ __global__ void csr_y_kernel(ObliqueYParams p) {
         src = p.Q + col;
         ld = p.ldq;
       }
+      double qv[C];
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j < cw) acc[j] = fma(v, src[(c0 + j) * ld], acc[j]);
+      for (int j = 0; j < C; ++j) qv[j] = j < cw ? src[(c0 + j) * ld] : 0.0;
+#pragma unroll
+      for (int j = 0; j < C; ++j) acc[j] = fma(v, qv[j], acc[j]);
+      if (col == i) {  // the row's own q (SPD: the diagonal is stored) -> ||Q||_F^2 partial
+#pragma unroll
+        for (int j = 0; j < C; ++j) sq = fma(qv[j], qv[j], sq);
+      }
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j < cw) {
-        p.Y[(c0 + j) * p.ldy + i] = acc[j];
-        const double qi = p.Q[i + (c0 + j) * p.ldq];
-        sq = fma(qi, qi, sq);
-      }
+    for (int j = 0; j < C; ++j)
+      if (j < cw) __stcs(p.Y + (c0 + j) * p.ldy + i, acc[j]);
   }
   for (int o = 16; o > 0; o >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
