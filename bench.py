@@ -130,7 +130,7 @@ def run_reference(args):
 
     cfg = synth.CONFIGS[args.config]
     n = cfg.n
-    rows = args.cpu_rows or max(n, int(5e6 * (128 / n) ** 2))
+    rows = args.cpu_rows or max(n, int(2e6 * (128 / n) ** 2))  # ~4 s of oracle work per step (16 cores)
     rows = min(rows, cfg.m)
     kw = {}
     if cfg.oblique:
