@@ -31,7 +31,96 @@ __device__ __forceinline__ void decode_job(int j, int NB, bool full, int& bi, in
   bi = j - c * (c + 1) / 2;
 }
 
-__global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
+// Whole-block jobs (JR = 4): one stage loop per job kind, so only that kind's state is live
+// (18 consumer warps fit 96 registers).  Fragment address of k-step s: the lane's 16-byte chunk
+// is (s + 4*(t>>1)) ^ g = s ^ G, i.e. offset ^ (s << 4) on a 128-byte aligned row base; the
+// block's tile rows / columns sit 8 x 128 B apart (immediate offsets).
+__device__ __forceinline__ void gram_whole_jobs(const GramParams& p, const unsigned char* stages, uint32_t stage_bytes,
+                                                int nsrc, uint64_t* full_bar, uint64_t* empty_bar, int nst, int kind,
+                                                bool b_from_y, bool full, int bi, int bj, bool diag,
+                                                double (&acc)[4][kJobTiles][2], const uint32_t (&offA)[4],
+                                                const uint32_t (&offB)[kJobTiles], const uint32_t (&inner)[4]) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lane_chunk = inner[0];  // chunk G << 4 plus the 8-byte half of this lane's k slot
+  auto frag = [&](uint32_t off) { return *reinterpret_cast<const double*>(stages + off); };
+  auto stage_loop = [&](auto body) {
+    int st = 0;
+    uint32_t ph = 0;
+    for (int i = 0; i < nst; ++i) {
+      mbar_wait(&full_bar[st], ph);
+      const uint32_t oA = static_cast<uint32_t>(st) * nsrc * stage_bytes;
+      body(oA, b_from_y ? oA + stage_bytes : oA);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[st]);
+      if (++st == p.stages) {
+        st = 0;
+        ph ^= 1u;
+      }
+    }
+  };
+  if (kind == 0) {
+    // 4 x 4 tiles of an off-diagonal block: 8 fragment loads, 16 DMMA per k-step
+    const uint32_t a0 = offA[0] + lane_chunk, b0 = offB[0] + lane_chunk;
+    stage_loop([&](uint32_t oA, uint32_t oB) {
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const uint32_t xa = (oA + a0) ^ (s << 4), xb = (oB + b0) ^ (s << 4);
+        double fb[kJobTiles];
+#pragma unroll
+        for (int b = 0; b < kJobTiles; ++b) fb[b] = frag(xb + b * 1024);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const double fa = frag(xa + a * 1024);
+#pragma unroll
+          for (int b = 0; b < kJobTiles; ++b) dmma(acc[a][b][0], acc[a][b][1], fa, fb[b]);
+        }
+      }
+    });
+  } else if (kind == 1) {
+    // diagonal block: its 10 upper tiles (A fragments = B fragments for Q^T Q; from Q for Q^T Y)
+    const uint32_t b0 = offB[0] + lane_chunk;
+    stage_loop([&](uint32_t oA, uint32_t oB) {
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const uint32_t xa = (oA + b0) ^ (s << 4), xb = (oB + b0) ^ (s << 4);
+        double fb[kJobTiles], fa[4];
+#pragma unroll
+        for (int b = 0; b < kJobTiles; ++b) fb[b] = frag(xb + b * 1024);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) fa[a] = full ? frag(xa + a * 1024) : fb[a];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = a; b < kJobTiles; ++b) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+      }
+    });
+  } else if (kind == 3) {
+    // block touching the padded edge (n not a multiple of 32): clamped rows, per-tile validity
+    const int NT = p.NT;
+    stage_loop([&](uint32_t oA, uint32_t oB) {
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        double fa[4], fb[kJobTiles];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) fa[a] = frag(oA + offA[a] + inner[s]);
+#pragma unroll
+        for (int b = 0; b < kJobTiles; ++b) fb[b] = frag(oB + offB[b] + inner[s]);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < kJobTiles; ++b) {
+            const bool valid = (bi * kJobTiles + a < NT) && (bj * kJobTiles + b < NT) && (!diag || a <= b);
+            if (valid) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+          }
+      }
+    });
+  } else {
+    stage_loop([&](uint32_t, uint32_t) {});  // idle warp: release the stages
+  }
+}
+
+template <int JR, int MAXC>
+__global__ void __launch_bounds__(32 * (MAXC + 1), 1)
     gram_tma_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapY,
                     GramParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -91,10 +180,13 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
   }
 
   // ---------------- consumers (job table: host-balanced over the four SM sub-partitions)
-  // Every job is one "part": two tile rows (rows 2*part, 2*part+1 of the 4x4-tile block) by
-  // the block's four tile columns -- 8 DMMA per k-step for an off-diagonal block, 7 (top) or 3
-  // (bottom) for a diagonal block of the symmetric Gram.  Small parts keep the accumulators at
+  // JR = 2: every job is one "part": two tile rows (rows 2*part, 2*part+1 of the 4x4-tile block)
+  // by the block's four tile columns -- 8 DMMA per k-step for an off-diagonal block, 7 (top) or
+  // 3 (bottom) for a diagonal block of the symmetric Gram.  Small parts keep the accumulators at
   // 32 registers and let the host balance the sub-partitions exactly.
+  // JR = 4 (more blocks than one CTA's warps hold as parts, n > 128): every job is a whole
+  // block -- 16 DMMA per 8 fragment loads off the diagonal, 10 on it -- so half as many CTAs
+  // share (and re-read) each row chunk.
   const int cw = warp - 1;
   const int code = p.warp_job[group * kMaxConsumers + cw];  // 2 * block + part, -1 = idle
   const bool active = code >= 0;
@@ -109,19 +201,19 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
   const bool diag = bi == bj;
   const int NT = p.NT;
   const bool edge = (bi + 1) * kJobTiles > NT || (bj + 1) * kJobTiles > NT;
-  const int rr0 = 2 * part;  // first tile row of the part within the block
+  const int rr0 = JR == 2 ? 2 * part : 0;  // first tile row of the job within the block
   const int g = lane >> 2, t = lane & 3;
 
-  double acc[2][kJobTiles][2];
+  double acc[JR][kJobTiles][2];
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < JR; ++a)
 #pragma unroll
     for (int b = 0; b < kJobTiles; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
-  // per-lane smem offsets (without the k-step part) of the part's tile rows / the block's columns
-  uint32_t offA[2], offB[kJobTiles];
+  // per-lane smem offsets (without the k-step part) of the job's tile rows / the block's columns
+  uint32_t offA[JR], offB[kJobTiles];
 #pragma unroll
-  for (int a = 0; a < 2; ++a) offA[a] = static_cast<uint32_t>(8 * min(bi * kJobTiles + rr0 + a, NT - 1) + g) * 128u;
+  for (int a = 0; a < JR; ++a) offA[a] = static_cast<uint32_t>(8 * min(bi * kJobTiles + rr0 + a, NT - 1) + g) * 128u;
 #pragma unroll
   for (int b = 0; b < kJobTiles; ++b) offB[b] = static_cast<uint32_t>(8 * min(bj * kJobTiles + b, NT - 1) + g) * 128u;
   // 16-byte chunk of this lane's k slot per k-step s: rows {2s, 2s+1, 2s+8, 2s+9}[t] -> the
@@ -130,9 +222,14 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
 #pragma unroll
   for (int s = 0; s < 4; ++s)
     inner[s] = ((((s + 4 * (t >> 1)) ^ g) & 7u) << 4) + ((t & 1) << 3);
-  // 0 off-diagonal interior, 1 diagonal top part, 2 diagonal bottom part, 3 edge, 4 idle
+  // 0 off-diagonal interior, 1 diagonal top part (JR = 4: the whole diagonal block), 2 diagonal
+  // bottom part, 3 edge, 4 idle
   const int kind = !active ? 4 : edge ? 3 : diag ? 1 + part : 0;
 
+  if constexpr (JR == 4) {
+    gram_whole_jobs(p, stages, stage_bytes, nsrc, full_bar, empty_bar, nst, kind, full && !plainjob, full,
+                    bi, bj, diag, acc, offA, offB, inner);
+  } else {
   int st = 0;
   uint32_t ph = 0;
   for (int i = 0; i < nst; ++i) {
@@ -206,11 +303,13 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
     }
   }
 
+  }  // JR == 2
+
   if (!active) return;
   // ---------------- write this CTA's partial tiles (8x8 row-major per tile)
   double* out = p.partials + static_cast<size_t>(chunk) * p.tiles_per_partial * 64;
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < JR; ++a)
 #pragma unroll
     for (int b = 0; b < kJobTiles; ++b) {
       const int TI = bi * kJobTiles + rr0 + a, TJ = bj * kJobTiles + b;
@@ -220,6 +319,27 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1)
       double2 v = make_double2(acc[a][b][0], acc[a][b][1]);
       *reinterpret_cast<double2*>(out + tid * 64 + 8 * g + 2 * t) = v;
     }
+}
+
+cudaError_t gram_tma_config(int variant, size_t smem, int threads, int* occ) {
+  static thread_local LaunchCfgCache cfg[3];
+  switch (variant) {
+    case 0: return cached_launch_cfg(cfg[0], gram_tma_kernel<2, kMaxConsumers>, smem, threads, occ);
+    case 1: return cached_launch_cfg(cfg[1], gram_tma_kernel<4, kMaxConsumersWhole>, smem, threads, occ);
+    case 2: return cached_launch_cfg(cfg[2], gram_tma_kernel<4, kMaxConsumersWhole2>, smem, threads, occ);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_gram_tma(int variant, unsigned grid, int threads, size_t smem, cudaStream_t stream,
+                            const CUtensorMap& mapQ, const CUtensorMap& mapY, const GramParams& p) {
+  switch (variant) {
+    case 0: gram_tma_kernel<2, kMaxConsumers><<<grid, threads, smem, stream>>>(mapQ, mapY, p); break;
+    case 1: gram_tma_kernel<4, kMaxConsumersWhole><<<grid, threads, smem, stream>>>(mapQ, mapY, p); break;
+    case 2: gram_tma_kernel<4, kMaxConsumersWhole2><<<grid, threads, smem, stream>>>(mapQ, mapY, p); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
 }
 
 // Sum the per-chunk partials in chunk order.  Output: packed upper tiles (tile (TI,TJ),

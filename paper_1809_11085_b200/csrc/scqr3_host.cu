@@ -274,11 +274,21 @@ int encode_map(Ctx* c, CUtensorMap* map, const double* base, int64_t m, int64_t 
   return SCQR3_OK;
 }
 
-// Gram jobs for the consumer warps.  Job codes: 2*block + part (tile rows 2*part, 2*part+1 of a 4x4-tile block: 8 tiles off the
-// diagonal, 7 / 3 on it), assigned longest first to the least-loaded SM sub-partition (warp w of
-// the CTA runs on sub-partition w % 4; consumer c is warp c + 1).  Returns the number of groups
-// (CTAs sharing a row chunk) and sets *ncons_out.
-int assign_gram_jobs(GramParams& gp, bool oblique, int* ncons_out) {
+// Gram jobs for the consumer warps.  Job codes: 2*block + part.  Three kernel variants:
+//   0: JR = 2, <= 20 consumers -- a job is a part (tile rows 2*part, 2*part+1 of a 4x4-tile
+//      block: 8 tiles off the diagonal, 7 / 3 on it);
+//   1: JR = 4, <= 18 consumers (96 registers) -- a job is a whole block (16 / 10 tiles);
+//   2: JR = 4, <= 15 consumers (128 registers).
+// Within a variant, jobs are split over `groups` CTAs sharing each row chunk and assigned
+// longest first to the least-loaded SM sub-partition (warp w of the CTA runs on sub-partition
+// w % 4; consumer c is warp c + 1).  Each SM runs one CTA and a chunk has total/chunks =
+// total*groups/SMs stages, so the variant with the least
+//     groups x max(64 cycles x (max sub-partition DMMA tiles per stage), stage bytes / 16 B)
+// is taken: 4 k-steps of 16 cycles per tile, and ~16 B/cycle/SM of L2 -> shared memory when every
+// CTA of a chunk streams its own copy (fit to measured times: n = 128 -> 0, 256 -> 2, 512 -> 1).
+// Returns the number of groups; sets *ncons_out and *variant_out.
+int assign_gram_jobs(GramParams& gp, bool oblique, int* ncons_out, int* variant_out) {
+  const long long load_cycles = static_cast<long long>(gp.npad) * 128 * (oblique ? 2 : 1) / 16;
   // upper blocks only, also for the oblique Gram (reading D22); the oblique Gram adds the plain
   // Gram's blocks (job codes past 2 * nsym) for its norm estimate (reading D4)
   const int nsym = gp.NB * (gp.NB + 1) / 2;
@@ -290,46 +300,64 @@ int assign_gram_jobs(GramParams& gp, bool oblique, int* ncons_out) {
     bj = c;
     bi = j - c * (c + 1) / 2;
   };
-  auto weight = [&](int code) {
+  auto weight = [&](int code, int jr) {
     int bi, bj;
     coords(code >> 1, bi, bj);
     const int r0 = 2 * (code & 1);
     int w = 0;
-    for (int a = r0; a < r0 + 2; ++a)
+    for (int a = r0; a < r0 + jr; ++a)
       for (int b = 0; b < kJobTiles; ++b)
         if (bi * kJobTiles + a < gp.NT && bj * kJobTiles + b < gp.NT && (bi != bj || a <= b)) ++w;
     return w;
   };
-  std::vector<int> codes;  // job code = 2 * block + part (tile rows 2*part, 2*part+1)
-  for (int j = 0; j < nblocks; ++j)
-    for (int part = 0; part < 2; ++part) {
-      const int code = 2 * j + part;
-      if (weight(code) > 0) codes.push_back(code);
-    }
-  const int jobs = static_cast<int>(codes.size());
-  const int groups = (jobs + kMaxConsumers - 1) / kMaxConsumers;
-  int ncons = 0;
-  for (int g = 0; g < groups; ++g) ncons = std::max(ncons, jobs * (g + 1) / groups - jobs * g / groups);
-  for (int i = 0; i < kMaxGroups * kMaxConsumers; ++i) gp.warp_job[i] = -1;
-  for (int g = 0; g < groups && g < kMaxGroups; ++g) {
-    const int j0 = jobs * g / groups, j1 = jobs * (g + 1) / groups;
-    std::vector<int> order(codes.begin() + j0, codes.begin() + j1);
-    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return weight(x) > weight(y); });
-    int load[4] = {0, 0, 0, 0};
-    bool used[kMaxConsumers] = {};
-    for (int code : order) {
-      int best = -1;
-      for (int w = 0; w < ncons; ++w) {
-        if (used[w]) continue;
-        if (best < 0 || load[(w + 1) & 3] < load[(best + 1) & 3]) best = w;
+  static const int kVariant[3][2] = {{2, kMaxConsumers}, {4, kMaxConsumersWhole}, {4, kMaxConsumersWhole2}};
+  long long best_cost = -1;
+  int best = 0, best_groups = 1, best_ncons = 0;
+  std::vector<short> best_job;
+  for (int v = 0; v < 3; ++v) {
+    const int jr = kVariant[v][0], maxc = kVariant[v][1];
+    std::vector<int> codes;
+    for (int j = 0; j < nblocks; ++j)
+      for (int part = 0; part < (jr == 2 ? 2 : 1); ++part)
+        if (weight(2 * j + part, jr) > 0) codes.push_back(2 * j + part);
+    const int jobs = static_cast<int>(codes.size());
+    const int groups = std::max(1, (jobs + maxc - 1) / maxc);
+    if (groups > kMaxGroups) continue;
+    int ncons = 0;
+    for (int g = 0; g < groups; ++g) ncons = std::max(ncons, jobs * (g + 1) / groups - jobs * g / groups);
+    std::vector<short> job(kMaxGroups * kMaxConsumers, -1);
+    int maxload = 0;
+    for (int g = 0; g < groups; ++g) {
+      const int j0 = jobs * g / groups, j1 = jobs * (g + 1) / groups;
+      std::vector<int> order(codes.begin() + j0, codes.begin() + j1);
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return weight(x, jr) > weight(y, jr); });
+      int load[4] = {0, 0, 0, 0};
+      bool used[kMaxConsumers] = {};
+      for (int code : order) {
+        int bw = -1;
+        for (int w = 0; w < ncons; ++w) {
+          if (used[w]) continue;
+          if (bw < 0 || load[(w + 1) & 3] < load[(bw + 1) & 3]) bw = w;
+        }
+        used[bw] = true;
+        load[(bw + 1) & 3] += weight(code, jr);
+        job[g * kMaxConsumers + bw] = static_cast<short>(code);
       }
-      used[best] = true;
-      load[(best + 1) & 3] += weight(code);
-      gp.warp_job[g * kMaxConsumers + best] = static_cast<short>(code);
+      for (int q = 0; q < 4; ++q) maxload = std::max(maxload, load[q]);
+    }
+    const long long cost = static_cast<long long>(groups) * std::max<long long>(64LL * maxload, load_cycles);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = v;
+      best_groups = groups;
+      best_ncons = ncons;
+      best_job = job;
     }
   }
-  *ncons_out = ncons;
-  return groups;
+  for (int i = 0; i < kMaxGroups * kMaxConsumers; ++i) gp.warp_job[i] = best_job[i];
+  *ncons_out = best_ncons;
+  *variant_out = best;
+  return best_groups;
 }
 
 // Sum `chunks` partials (per-CTA packed upper tiles) into w.tiles in chunk order.
@@ -396,8 +424,8 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   gp.oblique = oblique ? 1 : 0;
   gp.dual = oblique ? 1 : 0;
   gp.tiles_per_partial = static_cast<int>(L.tiles_part);
-  int ncons = 0;
-  const int groups = assign_gram_jobs(gp, oblique, &ncons);
+  int ncons = 0, variant = 0;
+  const int groups = assign_gram_jobs(gp, oblique, &ncons, &variant);
   if (groups > kMaxGroups) return fail("internal: too many Gram job groups");
   gp.groups = groups;
   const int threads = 32 * (1 + ncons);
@@ -407,9 +435,8 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   const size_t max_stages = (kGramSmemCap - 2048) / (stage_bytes * nsrc);
   gp.stages = static_cast<int>(std::min<size_t>(std::min<size_t>(8, max_stages), std::max<size_t>(2, 98304 / (stage_bytes * nsrc))));
   const size_t smem = gp.stages * nsrc * stage_bytes + 2 * gp.stages * 8 + 1024;
-  static thread_local LaunchCfgCache gram_cfg;
   int occ = 1;
-  CUDA_TRY(cached_launch_cfg(gram_cfg, gram_tma_kernel, smem, threads, &occ));
+  CUDA_TRY(gram_tma_config(variant, smem, threads, &occ));
   occ = std::max(occ, 1);
   gp.total_stages = (m + kGramStageRows - 1) / kGramStageRows;
   long long chunks = std::min<long long>((gp.total_stages + 3) / 4, static_cast<long long>(c->num_sms) * occ / groups);
@@ -417,10 +444,10 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   gp.chunks = static_cast<int>(chunks);
   gp.partials = w.partials;
   const int pg = prof_begin(c, PK_GRAM);
-  gram_tma_kernel<<<static_cast<unsigned>(chunks * groups), threads, smem, st>>>(mq, my, gp);
+  const cudaError_t le = launch_gram_tma(variant, static_cast<unsigned>(chunks * groups), threads, smem, st, mq, my, gp);
   prof_end(c, pg);
   ++g_launches;
-  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(le);
 
   return launch_gram_reduce(c, L, w, gp.chunks, oblique, colsq_count, st, gate);
 }

@@ -10,6 +10,8 @@ namespace scqr3 {
 struct DevStatus;
 
 constexpr int kMaxConsumers = 20;   // consumer warps per Gram CTA (+1 producer = 672 threads)
+constexpr int kMaxConsumersWhole = 18;   // whole-block Gram jobs, 19 warps x 96 registers
+constexpr int kMaxConsumersWhole2 = 15;  // whole-block Gram jobs, 16 warps x 128 registers
 constexpr int kMaxGroups = 32;      // job groups (CTAs sharing one row chunk)
 
 // Device-side pass control (speculative enqueue, scqr3_host.cu): the kernels of pass `pass` exit
@@ -147,8 +149,12 @@ struct TrsmParams {
   double* gram_partials;     // fused next-pass Gram (n <= 64): one NT(NT+1)/2-tile partial per CTA
 };
 
-__global__ void gram_tma_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapY,
-                                GramParams p);
+// gram_tma_kernel<JR, MAXC> (gram.cu): JR = tile rows per consumer-warp job, 2 (half 4x4-tile
+// blocks) or 4 (whole blocks); MAXC = consumer warps it is compiled for.  Variant v of
+// assign_gram_jobs: 0 = <2, 20>, 1 = <4, 18>, 2 = <4, 15>.
+cudaError_t gram_tma_config(int variant, size_t smem, int threads, int* occ);  // smem attribute + occupancy (cached)
+cudaError_t launch_gram_tma(int variant, unsigned grid, int threads, size_t smem, cudaStream_t stream,
+                            const CUtensorMap& mapQ, const CUtensorMap& mapY, const GramParams& p);
 __global__ void gram_reduce_kernel(GramReduceParams p);
 __global__ void csr_y_kernel(ObliqueYParams p);
 __global__ void csr_gershgorin_kernel(const long long* rp, const double* cv, long long m, double* partial);
