@@ -162,6 +162,18 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- our arm
+def host_mem_available():
+    """MemAvailable of /proc/meminfo in bytes (0 if unreadable)."""
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return 1024.0 * float(line.split()[1])
+    except OSError:
+        pass
+    return 0.0
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -297,7 +309,20 @@ def run_ours(args):
 
     # ---- end to end through the C ABI with host buffers (H2D of X, D2H of Q and R inside)
     e2e = None
-    if not args.no_e2e and not cfg.oblique:
+    e2e_note = None
+    want_e2e = not args.no_e2e and not cfg.oblique
+    if want_e2e:
+        # pinned host X and Q of every rank on this node (C4: 164 GB) must fit in host memory;
+        # rank 0 decides for all ranks so that they stay in step
+        need = 16.0 * m * n
+        ok = torch.tensor([1.0 if need < 0.5 * host_mem_available() else 0.0], dtype=torch.float64, device=dev)
+        if multi:
+            dist.broadcast(ok, src=0)
+        if ok.item() == 0.0:
+            want_e2e = False
+            e2e_note = (f"e2e skipped: pinned host X and Q need {need / 1e9:.0f} GB, more than half of the "
+                        f"host's available memory ({host_mem_available() / 1e9:.0f} GB)")
+    if want_e2e:
         Xh = torch.empty((n, mloc), dtype=torch.float64, pin_memory=True).t()
         Xh.copy_(X)
         Qh = torch.empty((n, mloc), dtype=torch.float64, pin_memory=True).t()
@@ -364,6 +389,7 @@ def run_ours(args):
             "kernels": kern,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            **({"e2e_note": e2e_note} if e2e_note else {}),
             "gpu_launches": launches,
             "clocks": clk,
         }

@@ -359,11 +359,13 @@ __device__ __forceinline__ void wide_phase(double (&q)[32][2], const double* __r
       for (int i = 0; i < 8; ++i) a[i] = b[i];
     }
   }
-  // (i-b) updates from the blocks of earlier phases of this launch, targets interleaved
+  // (i-b) updates from the blocks of earlier phases of this launch: target K0's here; target
+  // J+1's run inside block J's diagonal chain below (a dependency-free DMMA stream that hides the
+  // chain's shuffle / DFMA latency; one accumulator chain per warp keeps the pipe ~94 % busy at
+  // two warps per sub-partition, tools/dmma_pattern.cu)
+  constexpr int NS = 2 * (K0 - TB);  // k-steps per target from earlier phases
 #pragma unroll
-  for (int s = 2 * TB; s < 2 * K0; ++s)
-#pragma unroll
-    for (int K = K0; K < K1; ++K) dmma(q[K - TB][0], q[K - TB][1], q[(s >> 1) - TB][s & 1], frag(K, s));
+  for (int s = 2 * TB; s < 2 * K0; ++s) dmma(q[K0 - TB][0], q[K0 - TB][1], q[(s >> 1) - TB][s & 1], frag(K0, s));
   // (ii) triangular part inside the phase (right-looking, as in trsm_kernel)
 #pragma unroll
   for (int J = K0; J < K1; ++J) {
@@ -386,6 +388,11 @@ __device__ __forceinline__ void wide_phase(double (&q)[32][2], const double* __r
         const int K = J + 1 + u;
 #pragma unroll
         for (int s = 2 * (J - 1); s < 2 * J; ++s) dmma(q[K - TB][0], q[K - TB][1], q[J - 1 - TB][s & 1], frag(K, s));
+      }
+      if (J + 1 < K1) {
+#pragma unroll
+        for (int v = 2 * TB + NS * c / 8; v < 2 * TB + NS * (c + 1) / 8; ++v)
+          dmma(q[J + 1 - TB][0], q[J + 1 - TB][1], q[(v >> 1) - TB][v & 1], frag(J + 1, v));
       }
     }
     const double2 ri = *reinterpret_cast<const double2*>(D + 64 + 2 * t);
