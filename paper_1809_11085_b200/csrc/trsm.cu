@@ -172,26 +172,13 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
           for (int a = 0; a < A; ++a) dmma(q[a][J][0], q[a][J][1], q[a][J - 1][s & 1], b);
         }
       }
-      // (ii) diagonal block J: right-looking substitution inside each quad on the unscaled
-      // values v (v_j -= v_c * (r_cj / r_cc), strict upper only, zeros elsewhere), interleaved
-      // with the updates C_K += Q_{J-1} (-R~_{J-1,K}) of the later blocks K = J+1..NT-1
+      // (ii) diagonal block J: right-looking substitution on the unscaled values v
+      // (v_j -= v_c * (r_cj / r_cc), strict upper only, zeros elsewhere), interleaved with the
+      // updates C_K += Q_{J-1} (-R~_{J-1,K}) of the later blocks K = J+1..NT-1
       const int nup = J >= 1 ? NT - 1 - J : 0;
       int u = 0;
       const double* D = db + J * 72;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        // (column 7 of a block updates nothing inside it: its substitution step is skipped --
-        //  3-5 % faster at n = 64 and 256; at n = 128 within code-placement noise, +-0.7 %)
-        if (c < 7) {
-          const double2 rc = *reinterpret_cast<const double2*>(D + c * 8 + 2 * t);
-          const int owner = (lane & ~3) | (c >> 1);
-#pragma unroll
-          for (int a = 0; a < A; ++a) {
-            const double vc = __shfl_sync(0xffffffffu, q[a][J][c & 1], owner);
-            q[a][J][0] = fma(-vc, rc.x, q[a][J][0]);
-            q[a][J][1] = fma(-vc, rc.y, q[a][J][1]);
-          }
-        }
+      auto later_updates = [&](int c) {
 #pragma unroll
         for (; u < nup * (c + 1) / 8; ++u) {
           const int K = J + 1 + u;
@@ -202,13 +189,87 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
             for (int a = 0; a < A; ++a) dmma(q[a][K][0], q[a][K][1], q[a][J - 1][s & 1], b);
           }
         }
-      }
-      // (iii) q_j = v_j / r_jj as a multiply by the reciprocal (reading D11)
-      const double2 ri = *reinterpret_cast<const double2*>(D + 64 + 2 * t);
+      };
+      if constexpr (A % 2 == 0) {
+        // Fragment pairs (a, a+1) = rows g and g+8 of the quad.  Lanes t^2 swap halves so that
+        // lanes t = 0,1 hold row g and lanes t = 2,3 row g+8, four columns each: lane u = t&1
+        // holds columns {2u, 2u+1, 2u+4, 2u+5} (P[0..3]).  Step c then updates only the
+        // registers whose column can exceed c for some lane: 18 DFMA per pair instead of 28, and
+        // the pivot comes from the partner lane (same substitution order, same rounding).
+        const int uu = t & 1;
+        const bool lo = t < 2;
+        double P[A / 2][4];
 #pragma unroll
-      for (int a = 0; a < A; ++a) {
-        q[a][J][0] *= ri.x;
-        q[a][J][1] *= ri.y;
+        for (int a = 0; a < A; a += 2) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const double snd = lo ? q[a + 1][J][h] : q[a][J][h];
+            const double rcv = __shfl_xor_sync(0xffffffffu, snd, 2);
+            P[a / 2][h] = lo ? q[a][J][h] : rcv;
+            P[a / 2][2 + h] = lo ? rcv : q[a + 1][J][h];
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (c < 7) {
+            const double2 r01 = *reinterpret_cast<const double2*>(D + c * 8 + 2 * uu);
+            const double2 r23 = *reinterpret_cast<const double2*>(D + c * 8 + 4 + 2 * uu);
+            const int owner = (lane & ~1) | ((c >> 1) & 1);
+            constexpr int kmax[4] = {2, 3, 6, 7};  // register k can still change while c < kmax[k]
+#pragma unroll
+            for (int b = 0; b < A / 2; ++b) {
+              const double vc = __shfl_sync(0xffffffffu, P[b][(c & 1) + 2 * (c >> 2)], owner);
+              if (c < kmax[0]) P[b][0] = fma(-vc, r01.x, P[b][0]);
+              if (c < kmax[1]) P[b][1] = fma(-vc, r01.y, P[b][1]);
+              if (c < kmax[2]) P[b][2] = fma(-vc, r23.x, P[b][2]);
+              if (c < kmax[3]) P[b][3] = fma(-vc, r23.y, P[b][3]);
+            }
+          }
+          later_updates(c);
+        }
+        // (iii) q_j = v_j / r_jj as a multiply by the reciprocal (reading D11), then back to
+        // the C-fragment layout
+        const double2 i01 = *reinterpret_cast<const double2*>(D + 64 + 2 * uu);
+        const double2 i23 = *reinterpret_cast<const double2*>(D + 64 + 4 + 2 * uu);
+#pragma unroll
+        for (int a = 0; a < A; a += 2) {
+          double* Pb = P[a / 2];
+          Pb[0] *= i01.x;
+          Pb[1] *= i01.y;
+          Pb[2] *= i23.x;
+          Pb[3] *= i23.y;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const double snd = lo ? Pb[2 + h] : Pb[h];
+            const double rcv = __shfl_xor_sync(0xffffffffu, snd, 2);
+            q[a][J][h] = lo ? Pb[h] : rcv;
+            q[a + 1][J][h] = lo ? rcv : Pb[2 + h];
+          }
+        }
+      } else {
+        // (odd A: inside each quad, lane t holds columns 2t, 2t+1 of its row)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          // (column 7 of a block updates nothing inside it: its substitution step is skipped)
+          if (c < 7) {
+            const double2 rc = *reinterpret_cast<const double2*>(D + c * 8 + 2 * t);
+            const int owner = (lane & ~3) | (c >> 1);
+#pragma unroll
+            for (int a = 0; a < A; ++a) {
+              const double vc = __shfl_sync(0xffffffffu, q[a][J][c & 1], owner);
+              q[a][J][0] = fma(-vc, rc.x, q[a][J][0]);
+              q[a][J][1] = fma(-vc, rc.y, q[a][J][1]);
+            }
+          }
+          later_updates(c);
+        }
+        // (iii) q_j = v_j / r_jj as a multiply by the reciprocal (reading D11)
+        const double2 ri = *reinterpret_cast<const double2*>(D + 64 + 2 * t);
+#pragma unroll
+        for (int a = 0; a < A; ++a) {
+          q[a][J][0] *= ri.x;
+          q[a][J][1] *= ri.y;
+        }
       }
       // block J-1 had its last use above: store it now (spreads the stores over the solve
       // instead of one burst per row group that fills the LSU queue)
