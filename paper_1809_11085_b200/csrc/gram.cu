@@ -381,16 +381,13 @@ __global__ void gram_reduce_kernel(GramReduceParams p) {
 #ifndef SCQR3_Y_COLS
 #define SCQR3_Y_COLS 4  // columns in flight per thread (measured: 4 beats 2, 8, 16)
 #endif
-#ifndef SCQR3_Y_ROWS1
-#define SCQR3_Y_PAIRS  // two rows per thread (measured 5 % faster than one; -DSCQR3_Y_ROWS1 for one)
-#endif
 __global__ void oblique_y_kernel(ObliqueYParams p) {
   __shared__ double red[32];
   if (SCQR3_GATE_SKIP(p.gate)) return;
   double sq = 0.0;
-#ifdef SCQR3_Y_PAIRS
-  // two consecutive rows per thread: one 16-byte load and store per column for the pair, the
-  // outer neighbours by two 8-byte loads (L1 hits), SCQR3_Y_COLS columns in flight
+  // two consecutive rows per thread (measured 5 % faster than one row per thread): one 16-byte
+  // load and store per column for the pair, the outer neighbours by two 8-byte loads (L1 hits),
+  // SCQR3_Y_COLS columns in flight
   for (long long i0 = 2 * (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x); i0 < p.m;
        i0 += 2 * static_cast<long long>(gridDim.x) * blockDim.x) {
     const bool two = i0 + 1 < p.m;
@@ -436,42 +433,6 @@ __global__ void oblique_y_kernel(ObliqueYParams p) {
       }
     }
   }
-#else
-  // one thread per row (consecutive threads, consecutive rows: every column access coalesced),
-  // the row's band entries in registers, SCQR3_Y_COLS columns in flight per step
-  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < p.m;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const double di = p.d[i];
-    const bool lo = i > 0, hi = i + 1 < p.m;
-    const double el = lo ? p.e[i - 1] : p.e_prev;
-    const double er = p.e[i];
-    const bool use_l = lo || p.has_prev, use_r = hi || p.has_next;
-    for (int j0 = 0; j0 < p.n; j0 += SCQR3_Y_COLS) {
-      double qv[SCQR3_Y_COLS], ql[SCQR3_Y_COLS], qr[SCQR3_Y_COLS];
-#pragma unroll
-      for (int jj = 0; jj < SCQR3_Y_COLS; ++jj) {
-        const int j = j0 + jj;
-        if (j < p.n) {
-          const double* q = p.Q + j * p.ldq;
-          qv[jj] = __ldcs(q + i);
-          ql[jj] = lo ? q[i - 1] : (p.has_prev ? p.halo_prev[j] : 0.0);
-          qr[jj] = hi ? q[i + 1] : (p.has_next ? p.halo_next[j] : 0.0);
-        }
-      }
-#pragma unroll
-      for (int jj = 0; jj < SCQR3_Y_COLS; ++jj) {
-        const int j = j0 + jj;
-        if (j < p.n) {
-          double v = di * qv[jj];  // the oracle's term order
-          if (use_l) v = fma(el, ql[jj], v);
-          if (use_r) v = fma(er, qr[jj], v);
-          __stcs(p.Y + j * p.ldy + i, v);
-          sq = fma(qv[jj], qv[jj], sq);
-        }
-      }
-    }
-  }
-#endif
   // deterministic block reduction
   for (int o = 16; o > 0; o >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;

@@ -21,27 +21,22 @@
 
 namespace scqr3 {
 
-#ifndef SCQR3_TRSM16_THREADS
-#define SCQR3_TRSM16_THREADS 256
-#endif
-
-// P = warps sharing one TMA slot (P = 2 when a warp owns 8 rows: the slot is one 16-row box).
 // GRAM (n <= 64): also accumulate the next pass's Gram Q_k^T Q_k from the
 // solved rows, so the next pass does not read Q from HBM again.  Each warp writes its 16 finished
 // rows to a private swizzled stage and accumulates their Gram (all upper 8x8 tiles) in registers;
 // at the end the CTA sums its warps in a fixed order and writes one partial (gram_reduce_kernel
 // sums the partials of all CTAs, as after gram_tma_kernel).  Skipped when this pass stops.
-template <int NT, int A, bool SMEM_B, int THREADS, bool TMA, int P = 1, bool GRAM = false>
+template <int NT, int A, bool SMEM_B, int THREADS, bool TMA, bool GRAM = false>
 __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant__ CUtensorMap mapX, TrsmParams p) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   if (SCQR3_GATE_SKIP(p.gate) || (p.st && p.st->code != 0)) return;
-  static_assert(!GRAM || (A == 2 && P == 1 && TMA), "fused Gram: 16-row groups per warp");
+  static_assert(!GRAM || (A == 2 && TMA), "fused Gram: 16-row groups per warp");
   constexpr int NTS = NT * (NT + 1) / 2;  // upper 8x8 tiles of the Gram
   const bool do_gram = GRAM && p.gram_partials && !(p.st && p.st->stop);
   constexpr int NF = NT * (NT - 1);
   constexpr int WPB = THREADS / 32;
   constexpr int NPAD = NT * 8;
-  constexpr int RS = 8 * A * P;                            // rows per slot (multiple of 16)
+  constexpr int RS = 8 * A;                                // rows per warp slot (multiple of 16)
   constexpr uint32_t kBoxBytes = 16u * NPAD * 8u;         // one 16-row TMA box
   constexpr uint32_t kSlotBytes = kBoxBytes * (RS / 16);
   static_assert(!TMA || RS % 16 == 0, "TMA slots hold whole 16-row boxes");
@@ -49,7 +44,7 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
   // (pointer arithmetic on the shared array itself keeps the shared address space -> LDS)
   unsigned char* base = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
   unsigned char* slots = base;
-  unsigned char* ostage = base + (TMA ? (WPB / P) * kSlotBytes : 0);  // GRAM: per-warp Q stages
+  unsigned char* ostage = base + (TMA ? WPB * kSlotBytes : 0);  // GRAM: per-warp Q stages
   double* sm = reinterpret_cast<double*>(ostage + (GRAM ? WPB * kBoxBytes : 0));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + (SMEM_B ? NF * 32 : 0) + NT * 72);
   const double* bf;
@@ -66,22 +61,21 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   if (TMA && threadIdx.x == 0) {
-    for (int w = 0; w < WPB / P; ++w) mbar_init(&bars[w], 1);
+    for (int w = 0; w < WPB; ++w) mbar_init(&bars[w], 1);
     fence_barrier_init();
   }
   __syncthreads();
 
   const long long m = p.m;
   const int n = p.n;
-  // work unit = one slot group of RS rows (P warps, 8A rows each)
+  // work unit = one row group of RS = 8A rows per warp
   const long long ngroups = (m + RS - 1) / RS;
-  const long long stride = static_cast<long long>(gridDim.x) * (WPB / P);
-  const int sidx = warp / P, sub = warp % P;
-  unsigned char* slot = slots + sidx * kSlotBytes;
-  uint64_t* bar = bars + sidx;
+  const long long stride = static_cast<long long>(gridDim.x) * WPB;
+  unsigned char* slot = slots + warp * kSlotBytes;
+  uint64_t* bar = bars + warp;
   uint32_t phase = 0;
   auto issue = [&](long long rg) {  // elected lane: TMA of slot group rg into this slot
-    if (TMA && sub == 0 && lane == 0 && rg < ngroups) {
+    if (TMA && lane == 0 && rg < ngroups) {
       fence_proxy_async();
       mbar_arrive_expect_tx(bar, kSlotBytes);
 #pragma unroll
@@ -89,7 +83,7 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
         tma_load_2d(slot + b * kBoxBytes, &mapX, static_cast<int>(rg * RS + 16 * b), 0, bar);
     }
   };
-  const long long rg0 = static_cast<long long>(blockIdx.x) * (WPB / P) + sidx;
+  const long long rg0 = static_cast<long long>(blockIdx.x) * WPB + warp;
   if (TMA) {
     if (lane == 0) tma_prefetch_desc(&mapX);
     issue(rg0);
@@ -99,7 +93,7 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
 #pragma unroll
   for (int T = 0; T < (GRAM ? NTS : 1); ++T) gacc[T][0] = gacc[T][1] = 0.0;
   for (long long rg = rg0; rg < ngroups; rg += stride) {
-    const long long r0 = rg * RS + sub * 8 * A;
+    const long long r0 = rg * RS;
     double q[A][NT][2];
     auto store_block = [&](double (&qq)[A][NT][2], int J) {
 #pragma unroll
@@ -119,7 +113,7 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
       phase ^= 1u;
 #pragma unroll
       for (int a = 0; a < A; ++a) {
-        const int r = sub * 8 * A + 8 * a + g;  // row inside the slot
+        const int r = 8 * a + g;  // row inside the slot
         const unsigned char* box = slot + (r >> 4) * kBoxBytes;
 #pragma unroll
         for (int J = 0; J < NT; ++J)
@@ -147,20 +141,14 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
     // (Right-looking order: block K receives one k-step pair per iteration, so no DMMA
     //  accumulator chain is longer than two, and the updates from block J-1 to blocks > J are
     //  independent MMAs that fill the pipe while block J's shuffle chain runs.)
-#ifdef SCQR3_TRSM_NOLDS_EXPERIMENT
-    const double bfake = bf[lane];
-    auto bfrag = [&](int K, int s) -> double { return bfake * (K + s); };
-#else
     auto bfrag = [&](int K, int s) -> double {  // -R~ fragment of k-step s for target block K
       return SMEM_B ? bf[(K * (K - 1) + s) * 32 + lane] : __ldg(bf + (K * (K - 1) + s) * 32 + lane);
     };
-#endif
 #pragma unroll
     for (int J = 0; J < NT; ++J) {
       if (TMA && J == (NT > 1 ? 1 : 0)) {
         // every lane's slot reads have been consumed by now: refill the slot with the next group
-        if (P > 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + sidx), "r"(32 * P) : "memory");
-        else __syncwarp();
+        __syncwarp();
         issue(rg + stride);
       }
       // (i) block J's last update, from block J-1 (final since the previous iteration)
@@ -193,20 +181,20 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
       if constexpr (A % 2 == 0) {
         // Fragment pairs (a, a+1) = rows g and g+8 of the quad.  Lanes t^2 swap halves so that
         // lanes t = 0,1 hold row g and lanes t = 2,3 row g+8, four columns each: lane u = t&1
-        // holds columns {2u, 2u+1, 2u+4, 2u+5} (P[0..3]).  Step c then updates only the
+        // holds columns {2u, 2u+1, 2u+4, 2u+5} (V[0..3]).  Step c then updates only the
         // registers whose column can exceed c for some lane: 18 DFMA per pair instead of 28, and
         // the pivot comes from the partner lane (same substitution order, same rounding).
         const int uu = t & 1;
         const bool lo = t < 2;
-        double P[A / 2][4];
+        double V[A / 2][4];
 #pragma unroll
         for (int a = 0; a < A; a += 2) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const double snd = lo ? q[a + 1][J][h] : q[a][J][h];
             const double rcv = __shfl_xor_sync(0xffffffffu, snd, 2);
-            P[a / 2][h] = lo ? q[a][J][h] : rcv;
-            P[a / 2][2 + h] = lo ? rcv : q[a + 1][J][h];
+            V[a / 2][h] = lo ? q[a][J][h] : rcv;
+            V[a / 2][2 + h] = lo ? rcv : q[a + 1][J][h];
           }
         }
 #pragma unroll
@@ -218,11 +206,11 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
             constexpr int kmax[4] = {2, 3, 6, 7};  // register k can still change while c < kmax[k]
 #pragma unroll
             for (int b = 0; b < A / 2; ++b) {
-              const double vc = __shfl_sync(0xffffffffu, P[b][(c & 1) + 2 * (c >> 2)], owner);
-              if (c < kmax[0]) P[b][0] = fma(-vc, r01.x, P[b][0]);
-              if (c < kmax[1]) P[b][1] = fma(-vc, r01.y, P[b][1]);
-              if (c < kmax[2]) P[b][2] = fma(-vc, r23.x, P[b][2]);
-              if (c < kmax[3]) P[b][3] = fma(-vc, r23.y, P[b][3]);
+              const double vc = __shfl_sync(0xffffffffu, V[b][(c & 1) + 2 * (c >> 2)], owner);
+              if (c < kmax[0]) V[b][0] = fma(-vc, r01.x, V[b][0]);
+              if (c < kmax[1]) V[b][1] = fma(-vc, r01.y, V[b][1]);
+              if (c < kmax[2]) V[b][2] = fma(-vc, r23.x, V[b][2]);
+              if (c < kmax[3]) V[b][3] = fma(-vc, r23.y, V[b][3]);
             }
           }
           later_updates(c);
@@ -233,17 +221,17 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
         const double2 i23 = *reinterpret_cast<const double2*>(D + 64 + 4 + 2 * uu);
 #pragma unroll
         for (int a = 0; a < A; a += 2) {
-          double* Pb = P[a / 2];
-          Pb[0] *= i01.x;
-          Pb[1] *= i01.y;
-          Pb[2] *= i23.x;
-          Pb[3] *= i23.y;
+          double* Vb = V[a / 2];
+          Vb[0] *= i01.x;
+          Vb[1] *= i01.y;
+          Vb[2] *= i23.x;
+          Vb[3] *= i23.y;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const double snd = lo ? Pb[2 + h] : Pb[h];
+            const double snd = lo ? Vb[2 + h] : Vb[h];
             const double rcv = __shfl_xor_sync(0xffffffffu, snd, 2);
-            q[a][J][h] = lo ? Pb[h] : rcv;
-            q[a + 1][J][h] = lo ? rcv : Pb[2 + h];
+            q[a][J][h] = lo ? Vb[h] : rcv;
+            q[a + 1][J][h] = lo ? rcv : Vb[2 + h];
           }
         }
       } else {
@@ -277,8 +265,7 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
     }
     store_block(q, NT - 1);
     if (TMA && NT <= 1) {
-      if (P > 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + sidx), "r"(32 * P) : "memory");
-      else __syncwarp();
+      __syncwarp();
       issue(rg + stride);
     }
     if constexpr (GRAM) {
@@ -332,16 +319,16 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
   }
 }
 
-template <int NT, int A, bool SMEM_B, int THREADS, bool TMA, int P = 1, bool GRAM = false>
+template <int NT, int A, bool SMEM_B, int THREADS, bool TMA, bool GRAM = false>
 static cudaError_t launch_one(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream,
                               int* grid_out = nullptr) {
   constexpr int NF = NT * (NT - 1);
   constexpr int WPB = THREADS / 32;
-  constexpr int RS = 8 * A * P;
+  constexpr int RS = 8 * A;
   constexpr size_t kSlot = 16u * NT * 8 * 8 * (RS / 16 > 0 ? RS / 16 : 1);
-  const size_t smem = 1024 + (TMA ? (WPB / P) * kSlot : 0) + (GRAM ? WPB * 16u * NT * 8 * 8 : 0) +
+  const size_t smem = 1024 + (TMA ? WPB * kSlot : 0) + (GRAM ? WPB * 16u * NT * 8 * 8 : 0) +
                       static_cast<size_t>((SMEM_B ? NF * 32 : 0) + NT * 72) * 8 + WPB * 8;
-  auto k = trsm_kernel<NT, A, SMEM_B, THREADS, TMA, P, GRAM>;
+  auto k = trsm_kernel<NT, A, SMEM_B, THREADS, TMA, GRAM>;
   static thread_local LaunchCfgCache cfg;
   int per_sm = 0;
   cudaError_t e = cached_launch_cfg(cfg, k, smem, THREADS, &per_sm);
@@ -349,7 +336,7 @@ static cudaError_t launch_one(const TrsmParams& p, const CUtensorMap* map, int n
   if (per_sm < 1) per_sm = 1;
   const long long groups = (p.m + RS - 1) / RS;
   long long grid = static_cast<long long>(num_sms) * per_sm;
-  const long long need = (groups + WPB / P - 1) / (WPB / P);
+  const long long need = (groups + WPB - 1) / WPB;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
   CUtensorMap dummy{};
@@ -559,10 +546,10 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
   if (p.gram_partials) {  // fused TRSM + next-pass Gram (A = 2, TMA)
     if (!tma) return cudaErrorInvalidValue;
     switch (NT) {
-      case 1: return launch_one<1, 2, true, 256, true, 1, true>(p, map, num_sms, stream, grid_out);
-      case 2: return launch_one<2, 2, true, 256, true, 1, true>(p, map, num_sms, stream, grid_out);
-      case 4: return launch_one<4, 2, true, 256, true, 1, true>(p, map, num_sms, stream, grid_out);
-      case 8: return launch_one<8, 2, true, 256, true, 1, true>(p, map, num_sms, stream, grid_out);
+      case 1: return launch_one<1, 2, true, 256, true, true>(p, map, num_sms, stream, grid_out);
+      case 2: return launch_one<2, 2, true, 256, true, true>(p, map, num_sms, stream, grid_out);
+      case 4: return launch_one<4, 2, true, 256, true, true>(p, map, num_sms, stream, grid_out);
+      case 8: return launch_one<8, 2, true, 256, true, true>(p, map, num_sms, stream, grid_out);
       default: return cudaErrorInvalidValue;
     }
   }
@@ -576,17 +563,8 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
                        : launch_one<8, 4, true, 256, false>(p, nullptr, num_sms, stream);
     case 12: return tma ? launch_one<12, 2, true, 256, true>(p, map, num_sms, stream)
                         : launch_one<12, 2, true, 256, false>(p, nullptr, num_sms, stream);
-#if SCQR3_TRSM16_PAIRS
-    case 16: return tma ? launch_one<16, 1, true, 512, true, 2>(p, map, num_sms, stream)
+    case 16: return tma ? launch_one<16, 2, true, 256, true>(p, map, num_sms, stream)
                         : launch_one<16, 2, true, 256, false>(p, nullptr, num_sms, stream);
-#elif defined(SCQR3_TRSM16_DIRECT384)
-    case 16: return launch_one<16, 2, true, 384, false>(p, nullptr, num_sms, stream);
-#elif defined(SCQR3_TRSM16_DIRECT512)
-    case 16: return launch_one<16, 1, true, 512, false>(p, nullptr, num_sms, stream);
-#else
-    case 16: return tma ? launch_one<16, 2, true, SCQR3_TRSM16_THREADS, true>(p, map, num_sms, stream)
-                        : launch_one<16, 2, true, 256, false>(p, nullptr, num_sms, stream);
-#endif
     case 24: return launch_one<24, 1, true, 256, false>(p, nullptr, num_sms, stream);
     case 32: return launch_wide<0, 256>(p, num_sms, stream);
     case 64: {
