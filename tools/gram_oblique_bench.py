@@ -19,5 +19,4 @@ for _ in range(5):
     sq.scqr3_gram_oblique(X, d, e, ws=ws)
 e1.record()
 torch.cuda.synchronize()
-print(f"oblique gram m={m} n={n}: {e0.elapsed_time(e1) / 5:.3f} ms per call (Y + Gram + reduce)"
-      f" fuse_y={'off' if os.environ.get('SCQR3_FUSE_Y') == '0' else 'on'}")
+print(f"oblique gram m={m} n={n}: {e0.elapsed_time(e1) / 5:.3f} ms per call (Y + Gram + reduce)")
