@@ -171,6 +171,77 @@ __device__ __noinline__ double power_lmax(const double* Wg, int ldw, int n, int 
   return nd.y > 0.0 ? nd.x / nd.y : 0.0;
 }
 
+// n <= 128 (W in shared memory): the same iteration with this thread's share of W -- row
+// tid / TPR, columns part + TPR * k, k < CPP -- held in registers for all iterations, so an
+// iteration reads only y (the TPR parts of a warp read TPR consecutive entries: one wavefront).  Shared-memory traffic bounded the version above
+// (64 W loads + 64 y loads per thread and iteration at n = 128).  TPR threads per row as above
+// (the largest power of two <= 32 with TPR * n <= 256); CPP >= ceil(n / TPR) a compile-time
+// power of two, so the iteration has no branches; columns past n carry zeros.
+template <int TPR, int CPP>
+__device__ __noinline__ double power_lmax_reg(int ldw, int n, int iters, double trace, double (*ybuf)[kMaxN],
+                                              double* red) {
+  extern __shared__ double smdyn[];
+  const double* W = smdyn;
+  if (!(trace > 0.0) || !isfinite(trace)) return 0.0;
+  const double sc = ldexp(1.0, -(ilogb(trace) + 1));
+  const int tid = threadIdx.x, part = tid % TPR, row = tid / TPR;
+  double w[CPP];
+#pragma unroll
+  for (int k = 0; k < CPP; ++k) {
+    const int j = part + TPR * k;
+    w[k] = (j < n && row < n) ? W[j * ldw + row] : 0.0;
+  }
+  for (int i = tid; i < TPR * CPP; i += kThreads) {  // y past n stays 0
+    ybuf[0][i] = i < n ? 1.0 : 0.0;
+    ybuf[1][i] = 0.0;
+  }
+  __syncthreads();
+  auto rowdot = [&](const double* y) -> double {
+    constexpr int NC = CPP < 4 ? CPP : 4;  // independent FMA chains
+    double a[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) a[c] = 0.0;
+#pragma unroll
+    for (int k = 0; k < CPP; ++k) a[k % NC] = fma(w[k], y[part + TPR * k], a[k % NC]);
+    double acc = a[0];
+#pragma unroll
+    for (int c = 1; c < NC; ++c) acc += a[c];
+#pragma unroll
+    for (int o = 1; o < TPR; o <<= 1) acc += __shfl_xor_sync(kFull, acc, o);
+    return acc;
+  };
+  int cur = 0;
+  for (int it = 0; it < iters; ++it) {
+    const double acc = rowdot(ybuf[cur]);
+    if (part == 0 && row < n) ybuf[cur ^ 1][row] = acc * sc;
+    __syncthreads();
+    cur ^= 1;
+  }
+  double num = 0.0, den = 0.0;
+  const double acc = rowdot(ybuf[cur]);
+  if (part == 0 && row < n) {
+    const double y = ybuf[cur][row];
+    num = fma(y, acc, num);
+    den = fma(y, y, den);
+  }
+  const double2 nd = block_sum2(num, den, red);
+  return nd.y > 0.0 ? nd.x / nd.y : 0.0;
+}
+
+// lambda_max estimate of the n x n Gram in W (reading D2): register version for n <= 128
+template <bool SMEM>
+__device__ double power_lmax_any(const double* W, int ldw, int n, int iters, double trace, double (*ybuf)[kMaxN],
+                                 double* red) {
+  if (SMEM && n <= 128) {
+    if (n > 64) return power_lmax_reg<2, 64>(ldw, n, iters, trace, ybuf, red);
+    if (n > 32) return power_lmax_reg<4, 16>(ldw, n, iters, trace, ybuf, red);
+    if (n > 16) return power_lmax_reg<8, 4>(ldw, n, iters, trace, ybuf, red);
+    if (n > 8) return power_lmax_reg<16, 1>(ldw, n, iters, trace, ybuf, red);
+    return power_lmax_reg<32, 1>(ldw, n, iters, trace, ybuf, red);
+  }
+  return power_lmax<SMEM>(W, ldw, n, iters, trace, ybuf, red);
+}
+
 // Blocked right-looking Cholesky of W (+ s on the diagonal).  Returns 0, or the 1-based
 // breakdown pivot (value in *pv_out).  On success the upper triangle of W holds R~.
 // (__noinline__: one copy of this heavily unrolled code instead of one per call site keeps the
@@ -495,7 +566,7 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
       } else {  // lambda_max(Q^T Q) x 1.01 from the plain Gram formed alongside (reading D4)
         __syncthreads();
         load_W(p, W, ldw, p.tiles + nout + 1);
-        N2 = power_lmax<SMEM>(W, ldw, n, p.power_iters, fro, ybuf, red) * 1.01;
+        N2 = power_lmax_any<SMEM>(W, ldw, n, p.power_iters, fro, ybuf, red) * 1.01;
         w_plain = true;
       }
     } else if (pass == 1 && p.norm_mode == SCQR3_NORM_USER) {
@@ -503,7 +574,7 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
     } else if (p.norm_mode == SCQR3_NORM_FROBENIUS) {
       N2 = trace;
     } else {
-      N2 = power_lmax<SMEM>(W, ldw, n, p.power_iters, trace, ybuf, red) * 1.01;
+      N2 = power_lmax_any<SMEM>(W, ldw, n, p.power_iters, trace, ybuf, red) * 1.01;
     }
     if (p.shift_mode == SCQR3_SHIFT_FIXED && pass == 1) return p.shift_value;
     if (p.oblique) return 11.0 * (2.0 * mg * sqrt(mg * nn) + nn * (nn + 1.0)) * u * N2 * (*p.nb_dev);

@@ -15,7 +15,8 @@ for n in (16, 64, 128, 256):
     X = synth.randsvd_torch(m, n, 1e10, seed=0)
     ws = sq.workspace(m, n)
     for rep in range(2):
-        r = sq.scqr3_factor(X, ws=ws, max_passes=int(os.environ.get("MAXP", "2")))
+        r = sq.scqr3_factor(X, ws=ws, max_passes=int(os.environ.get("MAXP", "2")),
+                            power_iters=int(os.environ.get("PITERS", "32")))
     st = ws[:160].cpu().numpy().view(np.int64)
     clk = st[56 // 8: 56 // 8 + 8]
     d = np.diff(clk[:6])
