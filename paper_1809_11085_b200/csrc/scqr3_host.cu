@@ -834,8 +834,10 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
       CUtensorMap mx;
       const bool use_tma = L.NT <= 16;
       if (use_tma) TRY(encode_map(c, &mx, src, m, n, ldsrc, L.npad));
+      CUtensorMap mq;  // fused TRSM + Gram: bulk stores of Q
+      if (fuse_tg) TRY(encode_map(c, &mq, Q, m, n, ldq, L.npad));
       const int pt = prof_begin(c, PK_TRSM);
-      CUDA_TRY(launch_trsm(tp, use_tma ? &mx : nullptr, c->num_sms, st, &fused_chunks));
+      CUDA_TRY(launch_trsm(tp, use_tma ? &mx : nullptr, c->num_sms, st, &fused_chunks, fuse_tg ? &mq : nullptr));
       prof_end(c, pt);
       ++g_launches;
     }
@@ -1082,7 +1084,9 @@ int zfactor_impl(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, i
       const bool use_tma = L.NT <= 16;
       if (use_tma) TRY(encode_map(c, &mx, S, m, n2, Z.lds, L.npad));
       const int pt = prof_begin(c, PK_TRSM);
-      CUDA_TRY(launch_trsm(tp, use_tma ? &mx : nullptr, c->num_sms, st, &fused_chunks));
+      // (in place on the split matrix: the bulk stores of Q use the same descriptor)
+      CUDA_TRY(launch_trsm(tp, use_tma ? &mx : nullptr, c->num_sms, st, &fused_chunks,
+                           fuse_tg && use_tma ? &mx : nullptr));
       prof_end(c, pt);
       ++g_launches;
     }

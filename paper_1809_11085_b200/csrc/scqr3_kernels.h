@@ -213,9 +213,10 @@ inline cudaError_t cached_launch_cfg(LaunchCfgCache& cc, K kernel, size_t smem, 
 
 // TRSM launcher (chooses the template instance for n)
 // With p.gram_partials set (n <= 64 only, see trsm_fuses_gram) the launch also writes the next
-// pass's Gram partials; *grid_out = the number of partials (CTAs).
+// pass's Gram partials; *grid_out = the number of partials (CTAs).  mapQ (required then): TMA
+// descriptor of Q (same box as map) for the bulk stores of the solved rows.
 cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream,
-                        int* grid_out = nullptr);
+                        int* grid_out = nullptr, const CUtensorMap* mapQ = nullptr);
 inline bool trsm_fuses_gram(int NT) { return NT <= 8; }
 
 inline int npad_for(int n) {

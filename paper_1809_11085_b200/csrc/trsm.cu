@@ -27,12 +27,16 @@ namespace scqr3 {
 // at the end the CTA sums its warps in a fixed order and writes one partial (gram_reduce_kernel
 // sums the partials of all CTAs, as after gram_tma_kernel).  Skipped when this pass stops.
 template <int NT, int A, bool SMEM_B, int THREADS, bool TMA, bool GRAM = false>
-__global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant__ CUtensorMap mapX, TrsmParams p) {
+__global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant__ CUtensorMap mapX,
+                                                          const __grid_constant__ CUtensorMap mapQ, TrsmParams p) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   if (SCQR3_GATE_SKIP(p.gate) || (p.st && p.st->code != 0)) return;
   static_assert(!GRAM || (A == 2 && TMA), "fused Gram: 16-row groups per warp");
   constexpr int NTS = NT * (NT + 1) / 2;  // upper 8x8 tiles of the Gram
   const bool do_gram = GRAM && p.gram_partials && !(p.st && p.st->stop);
+  // fused Gram: the solved rows go through the per-warp stage anyway, so Q leaves by one bulk
+  // tensor store per 16 rows instead of 8-byte stores from the registers
+  const bool bulk_q = GRAM && do_gram;
   constexpr int NF = NT * (NT - 1);
   constexpr int WPB = THREADS / 32;
   constexpr int NPAD = NT * 8;
@@ -261,9 +265,9 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
       }
       // block J-1 had its last use above: store it now (spreads the stores over the solve
       // instead of one burst per row group that fills the LSU queue)
-      if (J >= 1) store_block(q, J - 1);
+      if (J >= 1 && !bulk_q) store_block(q, J - 1);
     }
-    store_block(q, NT - 1);
+    if (!bulk_q) store_block(q, NT - 1);
     if (TMA && NT <= 1) {
       __syncwarp();
       issue(rg + stride);
@@ -274,6 +278,8 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
         // then k-steps over row quads {2s, 2s+1, 2s+8, 2s+9} as in gram_tma_kernel: one
         // fragment per column block serves as both MMA operands
         unsigned char* os = ostage + warp * kBoxBytes;
+        if (lane == 0) bulk_wait_read_all();  // the previous group's bulk store has read the stage
+        __syncwarp();
 #pragma unroll
         for (int a = 0; a < A; ++a)
 #pragma unroll
@@ -281,7 +287,12 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
 #pragma unroll
             for (int h = 0; h < 2; ++h)
               *reinterpret_cast<double*>(os + swz128_offset(8 * a + g, 8 * J + 2 * t + h)) = q[a][J][h];
+        fence_proxy_async();  // the stage writes, visible to the bulk copy
         __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&mapQ, static_cast<int>(r0), 0, os);  // rows past m / columns past n are clipped
+          bulk_commit();
+        }
 #pragma unroll
         for (int s = 0; s < 4; ++s) {
           const uint32_t inner = ((((s + 4 * (t >> 1)) ^ g) & 7u) << 4) + ((t & 1) << 3);
@@ -299,7 +310,9 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
   }
   if constexpr (GRAM) {
     if (do_gram) {
-      // CTA partial: warps add their tiles in warp order into shared memory (fixed order)
+      // CTA partial: warps add their tiles in warp order into shared memory (fixed order); the
+      // stages become the reduction buffer once every warp's last bulk store has read its stage
+      if (lane == 0) bulk_wait_read_all();
       __syncthreads();
       double* red = reinterpret_cast<double*>(ostage);  // NTS * 64 doubles <= WPB * kBoxBytes
       for (int w = 0; w < WPB; ++w) {
@@ -315,13 +328,14 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
       }
       double* outp = p.gram_partials + static_cast<size_t>(blockIdx.x) * NTS * 64;
       for (int i = threadIdx.x; i < NTS * 64; i += THREADS) outp[i] = red[i];
+      if (lane == 0) bulk_wait_all();  // this warp's bulk stores of Q complete before the CTA exits
     }
   }
 }
 
 template <int NT, int A, bool SMEM_B, int THREADS, bool TMA, bool GRAM = false>
 static cudaError_t launch_one(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream,
-                              int* grid_out = nullptr) {
+                              int* grid_out = nullptr, const CUtensorMap* mapQ = nullptr) {
   constexpr int NF = NT * (NT - 1);
   constexpr int WPB = THREADS / 32;
   constexpr int RS = 8 * A;
@@ -340,7 +354,7 @@ static cudaError_t launch_one(const TrsmParams& p, const CUtensorMap* map, int n
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
   CUtensorMap dummy{};
-  k<<<static_cast<unsigned>(grid), THREADS, smem, stream>>>(map ? *map : dummy, p);
+  k<<<static_cast<unsigned>(grid), THREADS, smem, stream>>>(map ? *map : dummy, mapQ ? *mapQ : dummy, p);
   if (grid_out) *grid_out = static_cast<int>(grid);
   return cudaGetLastError();
 }
@@ -540,16 +554,16 @@ static cudaError_t launch_wide(const TrsmParams& p, int num_sms, cudaStream_t st
 // map: TMA descriptor of X with a {16 rows, npad columns} SWIZZLE_128B box (instances with
 // NT <= 16 use it when map != nullptr); the others read X with plain coalesced loads.
 cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream,
-                        int* grid_out) {
+                        int* grid_out, const CUtensorMap* mapQ) {
   const int NT = npad_for(p.n) / 8;
   const bool tma = map != nullptr;
   if (p.gram_partials) {  // fused TRSM + next-pass Gram (A = 2, TMA)
-    if (!tma) return cudaErrorInvalidValue;
+    if (!tma || !mapQ) return cudaErrorInvalidValue;
     switch (NT) {
-      case 1: return launch_one<1, 2, true, 256, true, true>(p, map, num_sms, stream, grid_out);
-      case 2: return launch_one<2, 2, true, 256, true, true>(p, map, num_sms, stream, grid_out);
-      case 4: return launch_one<4, 2, true, 256, true, true>(p, map, num_sms, stream, grid_out);
-      case 8: return launch_one<8, 2, true, 256, true, true>(p, map, num_sms, stream, grid_out);
+      case 1: return launch_one<1, 2, true, 256, true, true>(p, map, num_sms, stream, grid_out, mapQ);
+      case 2: return launch_one<2, 2, true, 256, true, true>(p, map, num_sms, stream, grid_out, mapQ);
+      case 4: return launch_one<4, 2, true, 256, true, true>(p, map, num_sms, stream, grid_out, mapQ);
+      case 8: return launch_one<8, 2, true, 256, true, true>(p, map, num_sms, stream, grid_out, mapQ);
       default: return cudaErrorInvalidValue;
     }
   }
