@@ -38,8 +38,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
-        with open(os.path.join(BUILD, src + ".ptxas.txt"), "w") as f:
-            f.write(r.stderr)
+        with open(os.path.join(BUILD, src + ".ptxas.txt"), "w") as f:  # (without the timing lines)
+            f.write("".join(l for l in r.stderr.splitlines(True) if "Compile time" not in l))
         return obj
 
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
