@@ -71,7 +71,7 @@ def test_gram_ld_padding_and_determinism():
 
 
 @gpu
-@pytest.mark.parametrize("m,n", [(2, 1), (999, 16), (20000, 64), (3001, 128), (1500, 300)])
+@pytest.mark.parametrize("m,n", [(2, 1), (999, 16), (20000, 64), (3001, 128), (2500, 200), (1500, 300)])
 def test_gram_oblique_parity(m, n):
     X = synth.random_rows(m, n, seed=n)
     d, e = synth.tridiag_b(m, seed=n)
