@@ -207,8 +207,8 @@ def test_fixed_shift_first_pass_matches_oracle():
 
 
 @gpu
-def test_inplace_and_ragged_and_determinism():
-    m, n = 40003, 72
+@pytest.mark.parametrize("m,n", [(40003, 72), (10007, 40)])   # (n = 40: fused TRSM + Gram, bulk Q stores)
+def test_inplace_and_ragged_and_determinism(m, n):
     X = synth.randsvd(m, n, 1e9, seed=8)
     Xd = dev(X)
     r1 = sq.scqr3_factor(Xd)
