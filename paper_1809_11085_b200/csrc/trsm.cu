@@ -374,6 +374,10 @@ template <> struct WidePhases<0> {  // targets 0..31
   static constexpr int P = 4, MAXF = 290;
   __host__ __device__ static constexpr int b(int i) { return i == 0 ? 0 : i == 1 ? 16 : i == 2 ? 22 : i == 3 ? 27 : 32; }
 };
+template <> struct WidePhases<16> {  // targets 16..31 after a 128-column first launch
+  static constexpr int P = 4, MAXF = 290;
+  __host__ __device__ static constexpr int b(int i) { return i == 0 ? 16 : i == 1 ? 21 : i == 2 ? 25 : i == 3 ? 29 : 32; }
+};
 template <> struct WidePhases<32> {  // targets 32..63 (greedy, <= MAXF fragments per phase)
   static constexpr int P = 10, MAXF = 370;
   __host__ __device__ static constexpr int b(int i) {
@@ -385,7 +389,8 @@ template <int TB> constexpr bool phases_ok(int i = 0) {
   return i == WidePhases<TB>::P ||
          (phase_frags(WidePhases<TB>::b(i), WidePhases<TB>::b(i + 1)) <= WidePhases<TB>::MAXF && phases_ok<TB>(i + 1));
 }
-static_assert(phases_ok<0>() && phases_ok<32>(), "phase fragment counts exceed the buffers");
+static_assert(phases_ok<0>() && phases_ok<16>() && phases_ok<32>(), "phase fragment counts exceed the buffers");
+template <int TB> constexpr int wide_ntt() { return WidePhases<TB>::b(WidePhases<TB>::P) - TB; }  // target blocks
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
@@ -396,7 +401,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // One phase of the wide TRSM for one warp's 8 rows; every register index is compile-time.
 // q[k] holds target block TB + k; qe points at this lane's row of the finished Q (blocks < TB).
 template <int TB, int PH>
-__device__ __forceinline__ void wide_phase(double (&q)[32][2], const double* __restrict__ cur,
+__device__ __forceinline__ void wide_phase(double (&q)[wide_ntt<TB>()][2], const double* __restrict__ cur,
                                            const double* __restrict__ db, int lane, int t, bool rok,
                                            long long row, const double* __restrict__ qe, const TrsmParams& p) {
   constexpr int K0 = WidePhases<TB>::b(PH), K1 = WidePhases<TB>::b(PH + 1);
@@ -473,7 +478,7 @@ __device__ __forceinline__ void wide_phase(double (&q)[32][2], const double* __r
 // Phases PH.. of one row group: phase PH computes from buffer PH&1 while phase PH+1 (or, after
 // the last phase, the next row group's phase 0) streams into the other one.
 template <int TB, int PH, typename Stage>
-__device__ __forceinline__ void wide_phases(double (&q)[32][2], double* const (&buf)[2], const double* db,
+__device__ __forceinline__ void wide_phases(double (&q)[wide_ntt<TB>()][2], double* const (&buf)[2], const double* db,
                                             int lane, int t, bool act, bool rok, long long row,
                                             const double* qe, const TrsmParams& p, bool more, Stage& stage) {
   constexpr int P = WidePhases<TB>::P;
@@ -495,7 +500,7 @@ __device__ __forceinline__ void wide_phases(double (&q)[32][2], double* const (&
 
 template <int TB, int THREADS>
 __global__ void __launch_bounds__(THREADS, 1) trsm_wide_kernel(TrsmParams p) {
-  constexpr int NTT = 32, WPB = THREADS / 32, MAXF = WidePhases<TB>::MAXF;
+  constexpr int NTT = wide_ntt<TB>(), WPB = THREADS / 32, MAXF = WidePhases<TB>::MAXF;
   extern __shared__ __align__(16) double smp[];
   if (SCQR3_GATE_SKIP(p.gate) || (p.st && p.st->code != 0)) return;
   double* const buf[2] = {smp, smp + MAXF * 32};
@@ -537,7 +542,7 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_wide_kernel(TrsmParams p) {
 
 template <int TB, int THREADS>
 static cudaError_t launch_wide(const TrsmParams& p, int num_sms, cudaStream_t stream) {
-  const size_t smem = static_cast<size_t>(2 * WidePhases<TB>::MAXF * 32 + 32 * 72) * 8;
+  const size_t smem = static_cast<size_t>(2 * WidePhases<TB>::MAXF * 32 + wide_ntt<TB>() * 72) * 8;
   auto k = trsm_wide_kernel<TB, THREADS>;
   static thread_local LaunchCfgCache cfg;
   cudaError_t e = cached_launch_cfg(cfg, k, smem, THREADS, nullptr);
@@ -552,7 +557,8 @@ static cudaError_t launch_wide(const TrsmParams& p, int num_sms, cudaStream_t st
 }
 
 // map: TMA descriptor of X with a {16 rows, npad columns} SWIZZLE_128B box (instances with
-// NT <= 16 use it when map != nullptr); the others read X with plain coalesced loads.
+// NT <= 16 use it when map != nullptr; NT = 32: a {16, 128} box of the first 128 columns); the
+// others read X with plain coalesced loads.
 cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream,
                         int* grid_out, const CUtensorMap* mapQ) {
   const int NT = npad_for(p.n) / 8;
@@ -580,7 +586,18 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
     case 16: return tma ? launch_one<16, 2, true, 256, true>(p, map, num_sms, stream)
                         : launch_one<16, 2, true, 256, false>(p, nullptr, num_sms, stream);
     case 24: return launch_one<24, 1, true, 256, false>(p, nullptr, num_sms, stream);
-    case 32: return launch_wide<0, 256>(p, num_sms, stream);
+    case 32: {
+      // block-column split: columns 0..127 by the register-resident kernel (map: a 128-column
+      // box), then targets 16..31 by the wide kernel at 16 warps (A = 1, 16 target blocks in
+      // registers), its updates from Q(:, 0:128) read back (n = 256: 13.8 ms at m = 5e6 against
+      // 14.3 ms for one wide launch over all 32 targets)
+      if (!map) return launch_wide<0, 256>(p, num_sms, stream);
+      TrsmParams p1 = p;
+      p1.n = 128;
+      cudaError_t e = launch_one<16, 2, true, 256, true>(p1, map, num_sms, stream);
+      if (e != cudaSuccess) return e;
+      return launch_wide<16, 512>(p, num_sms, stream);
+    }
     case 64: {
       // block-column TRSM: Q(:, 0:256) first; the second launch reads it back for its updates
       cudaError_t e = launch_wide<0, 256>(p, num_sms, stream);
