@@ -599,8 +599,18 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
       return launch_wide<16, 512>(p, num_sms, stream);
     }
     case 64: {
-      // block-column TRSM: Q(:, 0:256) first; the second launch reads it back for its updates
-      cudaError_t e = launch_wide<0, 256>(p, num_sms, stream);
+      // block-column TRSM: Q(:, 0:256) first (split as for NT = 32); the last launch reads it
+      // back for its updates
+      cudaError_t e;
+      if (map) {
+        TrsmParams p1 = p;
+        p1.n = 128;
+        e = launch_one<16, 2, true, 256, true>(p1, map, num_sms, stream);
+        if (e != cudaSuccess) return e;
+        e = launch_wide<16, 512>(p, num_sms, stream);
+      } else {
+        e = launch_wide<0, 256>(p, num_sms, stream);
+      }
       if (e != cudaSuccess) return e;
       return launch_wide<32, 256>(p, num_sms, stream);
     }
