@@ -398,78 +398,141 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-// One phase of the wide TRSM for one warp's 8 rows; every register index is compile-time.
-// q[k] holds target block TB + k; qe points at this lane's row of the finished Q (blocks < TB).
-template <int TB, int PH>
-__device__ __forceinline__ void wide_phase(double (&q)[wide_ntt<TB>()][2], const double* __restrict__ cur,
-                                           const double* __restrict__ db, int lane, int t, bool rok,
-                                           long long row, const double* __restrict__ qe, const TrsmParams& p) {
+// One phase of the wide TRSM for one warp's 8A rows (fragment a: rows 8a + g); every register
+// index is compile-time.  q[a][k] holds target block TB + k; qe[a] points at this lane's row of
+// the finished Q (blocks < TB).
+template <int TB, int PH, int A>
+__device__ __forceinline__ void wide_phase(double (&q)[A][wide_ntt<TB>()][2], const double* __restrict__ cur,
+                                           const double* __restrict__ db, int lane, int t, const bool (&rok)[A],
+                                           const long long (&row)[A], const double* const (&qe)[A],
+                                           const TrsmParams& p) {
   constexpr int K0 = WidePhases<TB>::b(PH), K1 = WidePhases<TB>::b(PH + 1);
   auto frag = [&](int K, int s) { return cur[(K * (K - 1) - K0 * (K0 - 1) + s) * 32 + lane]; };
   // (i-a) updates from the blocks of the previous launch (finished Q columns, read back)
   if (TB > 0) {
-    double a[8];
+    double av[A][8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) a[i] = __ldg(qe + static_cast<long long>(8 * (i >> 1) + 2 * t + (i & 1)) * p.ldq);
+    for (int a = 0; a < A; ++a)
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        av[a][i] = __ldg(qe[a] + static_cast<long long>(8 * (i >> 1) + 2 * t + (i & 1)) * p.ldq);
 #pragma unroll 1
     for (int sb = 0; sb < 2 * TB; sb += 8) {
-      double b[8];
+      double bv[A][8];
       const int sn = sb + 8 < 2 * TB ? sb + 8 : sb;  // (last batch reloads itself, harmless)
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        b[i] = __ldg(qe + static_cast<long long>(8 * ((sn + i) >> 1) + 2 * t + (i & 1)) * p.ldq);
+      for (int a = 0; a < A; ++a)
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          bv[a][i] = __ldg(qe[a] + static_cast<long long>(8 * ((sn + i) >> 1) + 2 * t + (i & 1)) * p.ldq);
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int K = K0; K < K1; ++K) dmma(q[K - TB][0], q[K - TB][1], a[i], frag(K, sb + i));
+        for (int K = K0; K < K1; ++K) {
+          const double b = frag(K, sb + i);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = b[i];
+          for (int a = 0; a < A; ++a) dmma(q[a][K - TB][0], q[a][K - TB][1], av[a][i], b);
+        }
+#pragma unroll
+      for (int a = 0; a < A; ++a)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) av[a][i] = bv[a][i];
     }
   }
+  auto upd = [&](int K, int src, int s) {  // C_K += Q_src(k-step s) (-R~ fragment), all fragments
+    const double b = frag(K, s);
+#pragma unroll
+    for (int a = 0; a < A; ++a) dmma(q[a][K - TB][0], q[a][K - TB][1], q[a][src - TB][s & 1], b);
+  };
   // (i-b) updates from the blocks of earlier phases of this launch: target K0's here; target
   // J+1's run inside block J's diagonal chain below (a dependency-free DMMA stream that hides the
   // chain's shuffle / DFMA latency; one accumulator chain per warp keeps the pipe ~94 % busy at
   // two warps per sub-partition, tools/dmma_pattern.cu)
   constexpr int NS = 2 * (K0 - TB);  // k-steps per target from earlier phases
 #pragma unroll
-  for (int s = 2 * TB; s < 2 * K0; ++s) dmma(q[K0 - TB][0], q[K0 - TB][1], q[(s >> 1) - TB][s & 1], frag(K0, s));
+  for (int s = 2 * TB; s < 2 * K0; ++s) upd(K0, s >> 1, s);
   // (ii) triangular part inside the phase (right-looking, as in trsm_kernel)
 #pragma unroll
   for (int J = K0; J < K1; ++J) {
     if (J > K0) {
 #pragma unroll
-      for (int s = 2 * (J - 1); s < 2 * J; ++s) dmma(q[J - TB][0], q[J - TB][1], q[J - 1 - TB][s & 1], frag(J, s));
+      for (int s = 2 * (J - 1); s < 2 * J; ++s) upd(J, J - 1, s);
     }
     const int nup = J > K0 ? K1 - 1 - J : 0;
     const double* D = db + (J - TB) * 72;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      if (c < 7) {  // (column 7 updates nothing inside its block)
-        const double2 rc = *reinterpret_cast<const double2*>(D + c * 8 + 2 * t);
-        const double vc = __shfl_sync(0xffffffffu, q[J - TB][c & 1], (lane & ~3) | (c >> 1));
-        q[J - TB][0] = fma(-vc, rc.x, q[J - TB][0]);
-        q[J - TB][1] = fma(-vc, rc.y, q[J - TB][1]);
-      }
+    auto interleave = [&](int c) {
 #pragma unroll
       for (int u = nup * c / 8; u < nup * (c + 1) / 8; ++u) {
-        const int K = J + 1 + u;
 #pragma unroll
-        for (int s = 2 * (J - 1); s < 2 * J; ++s) dmma(q[K - TB][0], q[K - TB][1], q[J - 1 - TB][s & 1], frag(K, s));
+        for (int s = 2 * (J - 1); s < 2 * J; ++s) upd(J + 1 + u, J - 1, s);
       }
       if (J + 1 < K1) {
 #pragma unroll
-        for (int v = 2 * TB + NS * c / 8; v < 2 * TB + NS * (c + 1) / 8; ++v)
-          dmma(q[J + 1 - TB][0], q[J + 1 - TB][1], q[(v >> 1) - TB][v & 1], frag(J + 1, v));
+        for (int v = 2 * TB + NS * c / 8; v < 2 * TB + NS * (c + 1) / 8; ++v) upd(J + 1, v >> 1, v);
       }
-    }
-    const double2 ri = *reinterpret_cast<const double2*>(D + 64 + 2 * t);
-    q[J - TB][0] *= ri.x;
-    q[J - TB][1] *= ri.y;
-    if (rok) {
+    };
+    if constexpr (A == 2) {
+      // rows g and g+8: the pair swap of trsm_kernel (lane u = t&1 of each half-quad holds
+      // columns {2u, 2u+1, 2u+4, 2u+5} of one row; 18 DFMA per block instead of 28)
+      const int uu = t & 1;
+      const bool lo = t < 2;
+      double V[4];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int col = 8 * J + 2 * t + h;
-        if (col < p.n) __stcs(p.Q + row + static_cast<long long>(col) * p.ldq, q[J - TB][h]);
+        const double snd = lo ? q[1][J - TB][h] : q[0][J - TB][h];
+        const double rcv = __shfl_xor_sync(0xffffffffu, snd, 2);
+        V[h] = lo ? q[0][J - TB][h] : rcv;
+        V[2 + h] = lo ? rcv : q[1][J - TB][h];
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c < 7) {
+          const double2 r01 = *reinterpret_cast<const double2*>(D + c * 8 + 2 * uu);
+          const double2 r23 = *reinterpret_cast<const double2*>(D + c * 8 + 4 + 2 * uu);
+          const double vc = __shfl_sync(0xffffffffu, V[(c & 1) + 2 * (c >> 2)], (lane & ~1) | ((c >> 1) & 1));
+          if (c < 2) V[0] = fma(-vc, r01.x, V[0]);
+          if (c < 3) V[1] = fma(-vc, r01.y, V[1]);
+          if (c < 6) V[2] = fma(-vc, r23.x, V[2]);
+          V[3] = fma(-vc, r23.y, V[3]);
+        }
+        interleave(c);
+      }
+      const double2 i01 = *reinterpret_cast<const double2*>(D + 64 + 2 * uu);
+      const double2 i23 = *reinterpret_cast<const double2*>(D + 64 + 4 + 2 * uu);
+      V[0] *= i01.x;
+      V[1] *= i01.y;
+      V[2] *= i23.x;
+      V[3] *= i23.y;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double snd = lo ? V[2 + h] : V[h];
+        const double rcv = __shfl_xor_sync(0xffffffffu, snd, 2);
+        q[0][J - TB][h] = lo ? V[h] : rcv;
+        q[1][J - TB][h] = lo ? rcv : V[2 + h];
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c < 7) {  // (column 7 updates nothing inside its block)
+          const double2 rc = *reinterpret_cast<const double2*>(D + c * 8 + 2 * t);
+          const double vc = __shfl_sync(0xffffffffu, q[0][J - TB][c & 1], (lane & ~3) | (c >> 1));
+          q[0][J - TB][0] = fma(-vc, rc.x, q[0][J - TB][0]);
+          q[0][J - TB][1] = fma(-vc, rc.y, q[0][J - TB][1]);
+        }
+        interleave(c);
+      }
+      const double2 ri = *reinterpret_cast<const double2*>(D + 64 + 2 * t);
+      q[0][J - TB][0] *= ri.x;
+      q[0][J - TB][1] *= ri.y;
+    }
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+      if (rok[a]) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = 8 * J + 2 * t + h;
+          if (col < p.n) __stcs(p.Q + row[a] + static_cast<long long>(col) * p.ldq, q[a][J - TB][h]);
+        }
       }
     }
   }
@@ -477,18 +540,19 @@ __device__ __forceinline__ void wide_phase(double (&q)[wide_ntt<TB>()][2], const
 
 // Phases PH.. of one row group: phase PH computes from buffer PH&1 while phase PH+1 (or, after
 // the last phase, the next row group's phase 0) streams into the other one.
-template <int TB, int PH, typename Stage>
-__device__ __forceinline__ void wide_phases(double (&q)[wide_ntt<TB>()][2], double* const (&buf)[2], const double* db,
-                                            int lane, int t, bool act, bool rok, long long row,
-                                            const double* qe, const TrsmParams& p, bool more, Stage& stage) {
+template <int TB, int PH, int A, typename Stage>
+__device__ __forceinline__ void wide_phases(double (&q)[A][wide_ntt<TB>()][2], double* const (&buf)[2],
+                                            const double* db, int lane, int t, bool act, const bool (&rok)[A],
+                                            const long long (&row)[A], const double* const (&qe)[A],
+                                            const TrsmParams& p, bool more, Stage& stage) {
   constexpr int P = WidePhases<TB>::P;
   if constexpr (PH + 1 < P) stage(PH + 1, buf[(PH + 1) & 1]);
   else if ((P - 1) & 1) { if (more) stage(0, buf[0]); }  // buf[0] is free during an odd last phase
-  if (act) wide_phase<TB, PH>(q, buf[PH & 1], db, lane, t, rok, row, qe, p);
+  if (act) wide_phase<TB, PH, A>(q, buf[PH & 1], db, lane, t, rok, row, qe, p);
   cp_async_wait_all();
   __syncthreads();
   if constexpr (PH + 1 < P) {
-    wide_phases<TB, PH + 1>(q, buf, db, lane, t, act, rok, row, qe, p, more, stage);
+    wide_phases<TB, PH + 1, A>(q, buf, db, lane, t, act, rok, row, qe, p, more, stage);
   } else if (!((P - 1) & 1)) {  // even last phase used buf[0]: stage the next phase 0 now
     if (more) {
       stage(0, buf[0]);
@@ -498,7 +562,7 @@ __device__ __forceinline__ void wide_phases(double (&q)[wide_ntt<TB>()][2], doub
   }
 }
 
-template <int TB, int THREADS>
+template <int TB, int THREADS, int A>
 __global__ void __launch_bounds__(THREADS, 1) trsm_wide_kernel(TrsmParams p) {
   constexpr int NTT = wide_ntt<TB>(), WPB = THREADS / 32, MAXF = WidePhases<TB>::MAXF;
   extern __shared__ __align__(16) double smp[];
@@ -520,34 +584,42 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_wide_kernel(TrsmParams p) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const long long m = p.m;
   const int n = p.n;
-  const long long ngroups = (m + 7) / 8;
+  const long long ngroups = (m + 8 * A - 1) / (8 * A);
   const long long stride = static_cast<long long>(gridDim.x) * WPB;
   for (long long base = static_cast<long long>(blockIdx.x) * WPB; base < ngroups; base += stride) {
     const long long rg = base + warp;
     const bool act = rg < ngroups;
-    const long long row = rg * 8 + g;
-    const bool rok = act && row < m;
-    const double* qe = p.Q + (rok ? row : 0);
-    double q[NTT][2];
+    long long row[A];
+    bool rok[A];
+    const double* qe[A];
 #pragma unroll
-    for (int J = 0; J < NTT; ++J)
+    for (int a = 0; a < A; ++a) {
+      row[a] = rg * 8 * A + 8 * a + g;
+      rok[a] = act && row[a] < m;
+      qe[a] = p.Q + (rok[a] ? row[a] : 0);
+    }
+    double q[A][NTT][2];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int col = 8 * (TB + J) + 2 * t + h;
-        q[J][h] = (rok && col < n) ? __ldcs(p.X + row + static_cast<long long>(col) * p.ldx) : 0.0;
-      }
-    wide_phases<TB, 0>(q, buf, db, lane, t, act, rok, row, qe, p, base + stride < ngroups, stage);
+    for (int a = 0; a < A; ++a)
+#pragma unroll
+      for (int J = 0; J < NTT; ++J)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = 8 * (TB + J) + 2 * t + h;
+          q[a][J][h] = (rok[a] && col < n) ? __ldcs(p.X + row[a] + static_cast<long long>(col) * p.ldx) : 0.0;
+        }
+    wide_phases<TB, 0, A>(q, buf, db, lane, t, act, rok, row, qe, p, base + stride < ngroups, stage);
   }
 }
 
-template <int TB, int THREADS>
+template <int TB, int THREADS, int A = 1>
 static cudaError_t launch_wide(const TrsmParams& p, int num_sms, cudaStream_t stream) {
   const size_t smem = static_cast<size_t>(2 * WidePhases<TB>::MAXF * 32 + wide_ntt<TB>() * 72) * 8;
-  auto k = trsm_wide_kernel<TB, THREADS>;
+  auto k = trsm_wide_kernel<TB, THREADS, A>;
   static thread_local LaunchCfgCache cfg;
   cudaError_t e = cached_launch_cfg(cfg, k, smem, THREADS, nullptr);
   if (e != cudaSuccess) return e;
-  const long long groups = (p.m + 7) / 8;
+  const long long groups = (p.m + 8 * A - 1) / (8 * A);
   long long grid = num_sms;
   const long long need = (groups + THREADS / 32 - 1) / (THREADS / 32);
   if (grid > need) grid = need;
@@ -588,15 +660,16 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
     case 24: return launch_one<24, 1, true, 256, false>(p, nullptr, num_sms, stream);
     case 32: {
       // block-column split: columns 0..127 by the register-resident kernel (map: a 128-column
-      // box), then targets 16..31 by the wide kernel at 16 warps (A = 1, 16 target blocks in
-      // registers), its updates from Q(:, 0:128) read back (n = 256: 13.8 ms at m = 5e6 against
-      // 14.3 ms for one wide launch over all 32 targets)
+      // box), then targets 16..31 by the wide kernel with 16 rows per warp (A = 2: 16 target
+      // blocks x 2 fragments in registers, the pair-swap diagonal solve), its updates from
+      // Q(:, 0:128) read back.  n = 256 at m = 5e6: 13.45 ms, against 13.84 ms with A = 1 at 16
+      // warps and 14.3 ms for one wide launch over all 32 targets.
       if (!map) return launch_wide<0, 256>(p, num_sms, stream);
       TrsmParams p1 = p;
       p1.n = 128;
       cudaError_t e = launch_one<16, 2, true, 256, true>(p1, map, num_sms, stream);
       if (e != cudaSuccess) return e;
-      return launch_wide<16, 512>(p, num_sms, stream);
+      return launch_wide<16, 256, 2>(p, num_sms, stream);
     }
     case 64: {
       // block-column TRSM: Q(:, 0:256) first (split as for NT = 32); the last launch reads it
@@ -607,7 +680,7 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
         p1.n = 128;
         e = launch_one<16, 2, true, 256, true>(p1, map, num_sms, stream);
         if (e != cudaSuccess) return e;
-        e = launch_wide<16, 512>(p, num_sms, stream);
+        e = launch_wide<16, 256, 2>(p, num_sms, stream);
       } else {
         e = launch_wide<0, 256>(p, num_sms, stream);
       }
