@@ -368,10 +368,27 @@ __global__ void gram_reduce_kernel(GramReduceParams p) {
     for (int k = 1; k < 8; ++k) t += red[k][lane];
     p.tiles[e < nout ? e : e + 1] = t;  // (dual: the plain Gram follows the ||Q||_F^2 slot)
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0 && p.colsq_partials) {
-    double t = 0.0;
-    for (int c = 0; c < p.colsq_count; ++c) t += p.colsq_partials[c];
-    p.tiles[nout] = t;
+  if (blockIdx.x == 0 && p.colsq_partials) {
+    // ||Q||_F^2 from the Y kernel's per-block partials: thread i sums partials i, i + 256, ...
+    // (eight loads in flight), then a fixed-order tree -- deterministic, and ~3 us instead of a
+    // 4096-long dependent chain on one thread (~160 us, measured)
+    __shared__ double cs[256];
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+    int c = threadIdx.x;
+    for (; c + 768 < p.colsq_count; c += 1024) {
+      t0 += p.colsq_partials[c];
+      t1 += p.colsq_partials[c + 256];
+      t2 += p.colsq_partials[c + 512];
+      t3 += p.colsq_partials[c + 768];
+    }
+    for (; c < p.colsq_count; c += 256) t0 += p.colsq_partials[c];
+    cs[threadIdx.x] = (t0 + t1) + (t2 + t3);
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+      if (threadIdx.x < o) cs[threadIdx.x] += cs[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) p.tiles[nout] = cs[0];
   }
 }
 
@@ -564,11 +581,12 @@ __global__ void gershgorin_kernel(const double* d, const double* e, long long m,
 }
 
 __global__ void max_reduce_kernel(const double* partial, int count, double* out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double v = 0.0;
-    for (int i = 0; i < count; ++i) v = fmax(v, partial[i]);
-    *out = v;
-  }
+  // one warp (max is order independent, so the result is still exact and reproducible)
+  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+  double v = 0.0;
+  for (int i = threadIdx.x; i < count; i += 32) v = fmax(v, partial[i]);
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+  if (threadIdx.x == 0) *out = v;
 }
 
 // packed upper tiles -> full symmetric n x n column-major matrix (kernel-level API only)
