@@ -24,6 +24,8 @@
 // the reciprocal pivots; R~ itself for trmul_kernel.
 #include <math.h>
 
+#include <type_traits>
+
 #include "scqr3.h"
 #include "scqr3_dev.cuh"
 #include "scqr3_kernels.h"
@@ -259,7 +261,10 @@ __device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool ad
   // (a) diagonal block on ONE thread, entirely in registers (identity beyond kb): the pivot
   // chain is rsqrt -> scale -> one FMA per column, with no shuffle or barrier in it, and the
   // rest of each rank-1 update is independent work that fills the rsqrt latency.
-  auto diag_block = [&](int k0, int kb) {
+  // (FULL: kb == 8 known at compile time, so the per-entry kb guards vanish from the chain)
+  auto diag_block_t = [&](int k0, int kb_rt, auto full_tag) {
+    constexpr bool FULL = decltype(full_tag)::value;
+    const int kb = FULL ? kPanel : kb_rt;
     {
       double a[kPanel][kPanel];
 #pragma unroll
@@ -298,6 +303,10 @@ __device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool ad
         *sval = badv;
       }
     }
+  };
+  auto diag_block = [&](int k0, int kb) {
+    if (kb == kPanel) diag_block_t(k0, kb, std::integral_constant<bool, true>{});
+    else diag_block_t(k0, kb, std::integral_constant<bool, false>{});
   };
   // n a multiple of 8: look-ahead -- block k+1's diagonal factorisation runs on thread 0 while
   // the other warps finish panel k's trailing update (its tile is updated first)
