@@ -68,7 +68,9 @@ if __name__ == "__main__":
     ap.add_argument("--config", default="C3")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
-    summary = {"config": a.config, "round": a.round}
+    out_path = os.path.join(PROF, f"ncu_{a.round}_{a.config}.json")
+    summary = json.load(open(out_path)) if os.path.exists(out_path) else {}  # keep the other part
+    summary.update({"config": a.config, "round": a.round})
     if a.launches:
         summary["launch_list"] = launches(a.launches)
         summary["launch_list_note"] = ("ncu --metrics gpu__time_duration.sum --clock-control none: per-launch "
@@ -84,5 +86,5 @@ if __name__ == "__main__":
                 "bytes_per_launch": gbytes(d["dram__bytes_read.sum"]) + gbytes(d["dram__bytes_write.sum"]),
                 "source": f"profiles/ncu_{a.round}_{a.config}.json (ncu --set full, one launch)"}
         json.dump(traffic, open(traffic_path, "w"), indent=1)
-    json.dump(summary, open(os.path.join(PROF, f"ncu_{a.round}_{a.config}.json"), "w"), indent=1)
+    json.dump(summary, open(out_path, "w"), indent=1)
     print(json.dumps(summary, indent=1)[:3000])
