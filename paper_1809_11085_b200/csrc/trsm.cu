@@ -11,11 +11,14 @@
 // block s/2, element s%2 (the k-index of the step is mapped to columns {8(s/2)+2t+(s%2)}), so
 // the solved rows never leave the registers; the B operand (-R~ rows in fragment order,
 // written by chol_kernel) is read from shared memory, conflict free.  The 8x8 diagonal block
-// is then solved by right-looking substitution inside each quad (shuffle of each pivot
-// column).  The loop is software-pipelined: the (latency-bound) diagonal solve of block J-1 is
-// interleaved with block J's tensor-core updates from blocks 0..J-2.
+// is then solved by right-looking substitution inside each quad; with two fragments (rows g and
+// g+8) the quad's lanes first swap halves so that each lane holds four columns of one row, and
+// each step issues only the DFMAs whose column can still change (18 per pair instead of 28).
+// The loop is software-pipelined: the (latency-bound) diagonal solve of block J is interleaved
+// with block J-1's tensor-core updates to the later blocks.
 // X is read once (TMA into a per-warp shared-memory slot, one row group ahead, so the HBM
-// latency is off the critical path) and Q written once per pass.
+// latency is off the critical path) and Q written once per pass.  n > 192: block-column launches
+// (trsm_wide_kernel below).
 #include "scqr3_dev.cuh"
 #include "scqr3_kernels.h"
 
