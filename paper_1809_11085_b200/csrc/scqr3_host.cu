@@ -832,9 +832,9 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
     tp.gram_partials = fuse_tg ? w.partials : nullptr;
     if (m > 0) {
       CUtensorMap mx;
-      const bool use_tma = L.NT <= 16 || L.NT >= 32;
-      // (NT >= 32: the map of the first 128 columns, for the split TRSM)
-      if (use_tma) TRY(encode_map(c, &mx, src, m, L.NT >= 32 ? 128 : n, ldsrc, L.NT >= 32 ? 128 : L.npad));
+      const bool use_tma = L.NT <= 16 || L.NT >= 24;
+      // (NT >= 24: the map of the first 128 columns, for the split TRSM)
+      if (use_tma) TRY(encode_map(c, &mx, src, m, L.NT >= 24 ? 128 : n, ldsrc, L.NT >= 24 ? 128 : L.npad));
       CUtensorMap mq;  // fused TRSM + Gram: bulk stores of Q
       if (fuse_tg) TRY(encode_map(c, &mq, Q, m, n, ldq, L.npad));
       const int pt = prof_begin(c, PK_TRSM);
@@ -1082,8 +1082,8 @@ int zfactor_impl(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, i
     tp.gram_partials = fuse_tg ? w.partials : nullptr;
     if (m > 0) {
       CUtensorMap mx;
-      const bool use_tma = L.NT <= 16 || L.NT >= 32;
-      if (use_tma) TRY(encode_map(c, &mx, S, m, L.NT >= 32 ? 128 : n2, Z.lds, L.NT >= 32 ? 128 : L.npad));
+      const bool use_tma = L.NT <= 16 || L.NT >= 24;
+      if (use_tma) TRY(encode_map(c, &mx, S, m, L.NT >= 24 ? 128 : n2, Z.lds, L.NT >= 24 ? 128 : L.npad));
       const int pt = prof_begin(c, PK_TRSM);
       // (in place on the split matrix: the bulk stores of Q use the same descriptor)
       CUDA_TRY(launch_trsm(tp, use_tma ? &mx : nullptr, c->num_sms, st, &fused_chunks,
@@ -1359,8 +1359,8 @@ int scqr3_trsm(int64_t m, int64_t n, const double* X, int64_t ld, const double* 
   tp.st = nullptr;
   if (m > 0) {
     CUtensorMap mx;
-    const bool use_tma = L.NT <= 16 || L.NT >= 32;
-    if (use_tma) TRY(encode_map(c, &mx, X, m, L.NT >= 32 ? 128 : n, ld, L.NT >= 32 ? 128 : L.npad));
+    const bool use_tma = L.NT <= 16 || L.NT >= 24;
+    if (use_tma) TRY(encode_map(c, &mx, X, m, L.NT >= 24 ? 128 : n, ld, L.NT >= 24 ? 128 : L.npad));
     CUDA_TRY(launch_trsm(tp, use_tma ? &mx : nullptr, c->num_sms, st));
     ++g_launches;
   }

@@ -17,8 +17,8 @@
 // The loop is software-pipelined: the (latency-bound) diagonal solve of block J is interleaved
 // with block J-1's tensor-core updates to the later blocks.
 // X is read once (TMA into a per-warp shared-memory slot, one row group ahead, so the HBM
-// latency is off the critical path) and Q written once per pass.  n > 192: block-column launches
-// (trsm_wide_kernel below).
+// latency is off the critical path) and Q written once per pass.  Block-column launches
+// (trsm_wide_kernel below) for n > 128.
 #include "scqr3_dev.cuh"
 #include "scqr3_kernels.h"
 
@@ -372,28 +372,32 @@ static cudaError_t launch_one(const TrsmParams& p, const CUtensorMap* map, int n
 // phase, as in trsm_kernel.  n > 256 runs as two launches (block-column TRSM): targets 0..31,
 // then targets 32..63, whose updates from blocks 0..31 read the finished Q columns back.
 constexpr int phase_frags(int k0, int k1) { return k1 * (k1 - 1) - k0 * (k0 - 1); }
-template <int TB> struct WidePhases;
-template <> struct WidePhases<0> {  // targets 0..31
+template <int TB, int TE> struct WidePhases;  // targets TB..TE-1
+template <> struct WidePhases<0, 32> {  // targets 0..31
   static constexpr int P = 4, MAXF = 290;
   __host__ __device__ static constexpr int b(int i) { return i == 0 ? 0 : i == 1 ? 16 : i == 2 ? 22 : i == 3 ? 27 : 32; }
 };
-template <> struct WidePhases<16> {  // targets 16..31 after a 128-column first launch
+template <> struct WidePhases<16, 24> {  // targets 16..23 after a 128-column first launch (n <= 192)
+  static constexpr int P = 2, MAXF = 290;
+  __host__ __device__ static constexpr int b(int i) { return i == 0 ? 16 : i == 1 ? 20 : 24; }
+};
+template <> struct WidePhases<16, 32> {  // targets 16..31 after a 128-column first launch
   static constexpr int P = 4, MAXF = 290;
   __host__ __device__ static constexpr int b(int i) { return i == 0 ? 16 : i == 1 ? 21 : i == 2 ? 25 : i == 3 ? 29 : 32; }
 };
-template <> struct WidePhases<32> {  // targets 32..63 (greedy, <= MAXF fragments per phase)
+template <> struct WidePhases<32, 64> {  // targets 32..63 (greedy, <= MAXF fragments per phase)
   static constexpr int P = 10, MAXF = 370;
   __host__ __device__ static constexpr int b(int i) {
     return i == 0 ? 32 : i == 1 ? 37 : i == 2 ? 41 : i == 3 ? 45 : i == 4 ? 48 : i == 5 ? 51
          : i == 6 ? 54 : i == 7 ? 57 : i == 8 ? 60 : i == 9 ? 62 : 64;
   }
 };
-template <int TB> constexpr bool phases_ok(int i = 0) {
-  return i == WidePhases<TB>::P ||
-         (phase_frags(WidePhases<TB>::b(i), WidePhases<TB>::b(i + 1)) <= WidePhases<TB>::MAXF && phases_ok<TB>(i + 1));
+template <int TB, int TE> constexpr bool phases_ok(int i = 0) {
+  using W = WidePhases<TB, TE>;
+  return i == W::P || (phase_frags(W::b(i), W::b(i + 1)) <= W::MAXF && W::b(W::P) == TE && phases_ok<TB, TE>(i + 1));
 }
-static_assert(phases_ok<0>() && phases_ok<16>() && phases_ok<32>(), "phase fragment counts exceed the buffers");
-template <int TB> constexpr int wide_ntt() { return WidePhases<TB>::b(WidePhases<TB>::P) - TB; }  // target blocks
+static_assert(phases_ok<0, 32>() && phases_ok<16, 24>() && phases_ok<16, 32>() && phases_ok<32, 64>(),
+              "phase fragment counts exceed the buffers");
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
@@ -404,12 +408,12 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // One phase of the wide TRSM for one warp's 8A rows (fragment a: rows 8a + g); every register
 // index is compile-time.  q[a][k] holds target block TB + k; qe[a] points at this lane's row of
 // the finished Q (blocks < TB).
-template <int TB, int PH, int A>
-__device__ __forceinline__ void wide_phase(double (&q)[A][wide_ntt<TB>()][2], const double* __restrict__ cur,
+template <int TB, int TE, int PH, int A>
+__device__ __forceinline__ void wide_phase(double (&q)[A][TE - TB][2], const double* __restrict__ cur,
                                            const double* __restrict__ db, int lane, int t, const bool (&rok)[A],
                                            const long long (&row)[A], const double* const (&qe)[A],
                                            const TrsmParams& p) {
-  constexpr int K0 = WidePhases<TB>::b(PH), K1 = WidePhases<TB>::b(PH + 1);
+  constexpr int K0 = WidePhases<TB, TE>::b(PH), K1 = WidePhases<TB, TE>::b(PH + 1);
   auto frag = [&](int K, int s) { return cur[(K * (K - 1) - K0 * (K0 - 1) + s) * 32 + lane]; };
   // (i-a) updates from the blocks of the previous launch (finished Q columns, read back)
   if (TB > 0) {
@@ -543,19 +547,19 @@ __device__ __forceinline__ void wide_phase(double (&q)[A][wide_ntt<TB>()][2], co
 
 // Phases PH.. of one row group: phase PH computes from buffer PH&1 while phase PH+1 (or, after
 // the last phase, the next row group's phase 0) streams into the other one.
-template <int TB, int PH, int A, typename Stage>
-__device__ __forceinline__ void wide_phases(double (&q)[A][wide_ntt<TB>()][2], double* const (&buf)[2],
+template <int TB, int TE, int PH, int A, typename Stage>
+__device__ __forceinline__ void wide_phases(double (&q)[A][TE - TB][2], double* const (&buf)[2],
                                             const double* db, int lane, int t, bool act, const bool (&rok)[A],
                                             const long long (&row)[A], const double* const (&qe)[A],
                                             const TrsmParams& p, bool more, Stage& stage) {
-  constexpr int P = WidePhases<TB>::P;
+  constexpr int P = WidePhases<TB, TE>::P;
   if constexpr (PH + 1 < P) stage(PH + 1, buf[(PH + 1) & 1]);
   else if ((P - 1) & 1) { if (more) stage(0, buf[0]); }  // buf[0] is free during an odd last phase
-  if (act) wide_phase<TB, PH, A>(q, buf[PH & 1], db, lane, t, rok, row, qe, p);
+  if (act) wide_phase<TB, TE, PH, A>(q, buf[PH & 1], db, lane, t, rok, row, qe, p);
   cp_async_wait_all();
   __syncthreads();
   if constexpr (PH + 1 < P) {
-    wide_phases<TB, PH + 1, A>(q, buf, db, lane, t, act, rok, row, qe, p, more, stage);
+    wide_phases<TB, TE, PH + 1, A>(q, buf, db, lane, t, act, rok, row, qe, p, more, stage);
   } else if (!((P - 1) & 1)) {  // even last phase used buf[0]: stage the next phase 0 now
     if (more) {
       stage(0, buf[0]);
@@ -565,16 +569,16 @@ __device__ __forceinline__ void wide_phases(double (&q)[A][wide_ntt<TB>()][2], d
   }
 }
 
-template <int TB, int THREADS, int A>
+template <int TB, int TE, int THREADS, int A>
 __global__ void __launch_bounds__(THREADS, 1) trsm_wide_kernel(TrsmParams p) {
-  constexpr int NTT = wide_ntt<TB>(), WPB = THREADS / 32, MAXF = WidePhases<TB>::MAXF;
+  constexpr int NTT = TE - TB, WPB = THREADS / 32, MAXF = WidePhases<TB, TE>::MAXF;
   extern __shared__ __align__(16) double smp[];
   if (SCQR3_GATE_SKIP(p.gate) || (p.st && p.st->code != 0)) return;
   double* const buf[2] = {smp, smp + MAXF * 32};
   double* const db = smp + 2 * MAXF * 32;
   for (int i = threadIdx.x; i < NTT * 72; i += THREADS) db[i] = p.dblk[TB * 72 + i];
   auto stage = [&](int ph, double* dst) {  // cooperative cp.async of phase ph's fragments
-    const int k0 = WidePhases<TB>::b(ph), k1 = WidePhases<TB>::b(ph + 1);
+    const int k0 = WidePhases<TB, TE>::b(ph), k1 = WidePhases<TB, TE>::b(ph + 1);
     const double* src = p.bfrag + static_cast<size_t>(k0) * (k0 - 1) * 32;
     const int chunks = phase_frags(k0, k1) * 32 / 2;  // 16-byte chunks
     for (int c = threadIdx.x; c < chunks; c += THREADS) cp_async16(dst + 2 * c, src + 2 * c);
@@ -611,14 +615,14 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_wide_kernel(TrsmParams p) {
           const int col = 8 * (TB + J) + 2 * t + h;
           q[a][J][h] = (rok[a] && col < n) ? __ldcs(p.X + row[a] + static_cast<long long>(col) * p.ldx) : 0.0;
         }
-    wide_phases<TB, 0, A>(q, buf, db, lane, t, act, rok, row, qe, p, base + stride < ngroups, stage);
+    wide_phases<TB, TE, 0, A>(q, buf, db, lane, t, act, rok, row, qe, p, base + stride < ngroups, stage);
   }
 }
 
-template <int TB, int THREADS, int A = 1>
+template <int TB, int TE, int THREADS, int A = 1>
 static cudaError_t launch_wide(const TrsmParams& p, int num_sms, cudaStream_t stream) {
-  const size_t smem = static_cast<size_t>(2 * WidePhases<TB>::MAXF * 32 + wide_ntt<TB>() * 72) * 8;
-  auto k = trsm_wide_kernel<TB, THREADS, A>;
+  const size_t smem = static_cast<size_t>(2 * WidePhases<TB, TE>::MAXF * 32 + (TE - TB) * 72) * 8;
+  auto k = trsm_wide_kernel<TB, TE, THREADS, A>;
   static thread_local LaunchCfgCache cfg;
   cudaError_t e = cached_launch_cfg(cfg, k, smem, THREADS, nullptr);
   if (e != cudaSuccess) return e;
@@ -632,7 +636,7 @@ static cudaError_t launch_wide(const TrsmParams& p, int num_sms, cudaStream_t st
 }
 
 // map: TMA descriptor of X with a {16 rows, npad columns} SWIZZLE_128B box (instances with
-// NT <= 16 use it when map != nullptr; NT = 32: a {16, 128} box of the first 128 columns); the
+// NT <= 16 use it when map != nullptr; NT >= 24: a {16, 128} box of the first 128 columns); the
 // others read X with plain coalesced loads.
 cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream,
                         int* grid_out, const CUtensorMap* mapQ) {
@@ -660,19 +664,27 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
                         : launch_one<12, 2, true, 256, false>(p, nullptr, num_sms, stream);
     case 16: return tma ? launch_one<16, 2, true, 256, true>(p, map, num_sms, stream)
                         : launch_one<16, 2, true, 256, false>(p, nullptr, num_sms, stream);
-    case 24: return launch_one<24, 1, true, 256, false>(p, nullptr, num_sms, stream);
+    case 24: {
+      // split as for NT = 32: columns 0..127, then targets 16..23 (A = 2)
+      if (!map) return launch_one<24, 1, true, 256, false>(p, nullptr, num_sms, stream);
+      TrsmParams p1 = p;
+      p1.n = 128;
+      cudaError_t e = launch_one<16, 2, true, 256, true>(p1, map, num_sms, stream);
+      if (e != cudaSuccess) return e;
+      return launch_wide<16, 24, 256, 2>(p, num_sms, stream);
+    }
     case 32: {
       // block-column split: columns 0..127 by the register-resident kernel (map: a 128-column
       // box), then targets 16..31 by the wide kernel with 16 rows per warp (A = 2: 16 target
       // blocks x 2 fragments in registers, the pair-swap diagonal solve), its updates from
       // Q(:, 0:128) read back.  n = 256 at m = 5e6: 13.45 ms, against 13.84 ms with A = 1 at 16
       // warps and 14.3 ms for one wide launch over all 32 targets.
-      if (!map) return launch_wide<0, 256>(p, num_sms, stream);
+      if (!map) return launch_wide<0, 32, 256>(p, num_sms, stream);
       TrsmParams p1 = p;
       p1.n = 128;
       cudaError_t e = launch_one<16, 2, true, 256, true>(p1, map, num_sms, stream);
       if (e != cudaSuccess) return e;
-      return launch_wide<16, 256, 2>(p, num_sms, stream);
+      return launch_wide<16, 32, 256, 2>(p, num_sms, stream);
     }
     case 64: {
       // block-column TRSM: Q(:, 0:256) first (split as for NT = 32); the last launch reads it
@@ -683,12 +695,12 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
         p1.n = 128;
         e = launch_one<16, 2, true, 256, true>(p1, map, num_sms, stream);
         if (e != cudaSuccess) return e;
-        e = launch_wide<16, 256, 2>(p, num_sms, stream);
+        e = launch_wide<16, 32, 256, 2>(p, num_sms, stream);
       } else {
-        e = launch_wide<0, 256>(p, num_sms, stream);
+        e = launch_wide<0, 32, 256>(p, num_sms, stream);
       }
       if (e != cudaSuccess) return e;
-      return launch_wide<32, 256>(p, num_sms, stream);
+      return launch_wide<32, 64, 256>(p, num_sms, stream);
     }
     default: return cudaErrorInvalidValue;
   }

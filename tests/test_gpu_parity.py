@@ -118,8 +118,8 @@ def test_cholesky_breakdown_matches_oracle():
 
 # ------------------------------------------------------------------ TRSM
 @gpu
-@pytest.mark.parametrize("m,n", [(1, 1), (31, 5), (1000, 16), (4097, 64), (10007, 128), (3000, 200), (2049, 256),
-                                 (2001, 264), (1800, 512)])
+@pytest.mark.parametrize("m,n", [(1, 1), (31, 5), (1000, 16), (4097, 64), (10007, 128), (3001, 160), (3000, 200),
+                                 (2049, 256), (2001, 264), (1800, 512)])
 def test_trsm_integer_exact(m, n):
     rng = np.random.default_rng(m)
     Q = rng.integers(-9, 10, size=(m, n)).astype(float)
@@ -163,7 +163,8 @@ def _compare(X, rg, ro, kappa, d=None, e=None):
 
 @gpu
 @pytest.mark.parametrize("m,n,kappa", [(2000, 16, 1e12), (300, 10, 1e15), (1000, 30, 1e12), (100, 100, 1e13),
-                                       (5001, 64, 1e4), (20000, 128, 1e10), (8000, 100, 1e6), (4000, 256, 1e8), (3000, 512, 1e10),
+                                       (5001, 64, 1e4), (20000, 128, 1e10), (8000, 100, 1e6), (4000, 150, 1e9), (4000, 256, 1e8),
+                                       (3000, 512, 1e10),
                                        (3000, 1, 1.0), (17, 17, 1e3)])
 def test_factor_parity(m, n, kappa):
     X = synth.randsvd(m, n, kappa, seed=0)
