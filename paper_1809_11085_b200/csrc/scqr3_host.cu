@@ -285,7 +285,9 @@ int encode_map(Ctx* c, CUtensorMap* map, const double* base, int64_t m, int64_t 
 // total*groups/SMs stages, so the variant with the least
 //     groups x max(64 cycles x (max sub-partition DMMA tiles per stage), stage bytes / 16 B)
 // is taken: 4 k-steps of 16 cycles per tile, and ~16 B/cycle/SM of L2 -> shared memory when every
-// CTA of a chunk streams its own copy (fit to measured times: n = 128 -> 0, 256 -> 2, 512 -> 1).
+// CTA of a chunk streams its own copy (fit to measured times of all three variants, forced, at
+// n = 96, 128, 192, 256, 384, 512 and the oblique n = 64, 128: the model picks the fastest --
+// 0 up to n = 128, a whole-block variant above: 1 at n = 192 (2 within 1 %), 2 at 256, 1 at 512).
 // Returns the number of groups; sets *ncons_out and *variant_out.
 int assign_gram_jobs(GramParams& gp, bool oblique, int* ncons_out, int* variant_out) {
   const long long load_cycles = static_cast<long long>(gp.npad) * 128 * (oblique ? 2 : 1) / 16;
@@ -345,7 +347,10 @@ int assign_gram_jobs(GramParams& gp, bool oblique, int* ncons_out, int* variant_
       }
       for (int q = 0; q < 4; ++q) maxload = std::max(maxload, load[q]);
     }
-    const long long cost = static_cast<long long>(groups) * std::max<long long>(64LL * maxload, load_cycles);
+    // (parts load 6 fragments per 8 DMMA against 8 per 16 for whole blocks: 69 instead of 64
+    //  cycles per tile and k-step, fitted so n = 192 takes a whole-block variant, measured 4 % faster)
+    const long long tile_cycles = jr == 2 ? 69 : 64;
+    const long long cost = static_cast<long long>(groups) * std::max<long long>(tile_cycles * maxload, load_cycles);
     if (best_cost < 0 || cost < best_cost) {
       best_cost = cost;
       best = v;
