@@ -387,6 +387,18 @@ template <> struct WidePhases<16, 32> {  // targets 16..31 after a 128-column fi
   static constexpr int P = 1, MAXF = 752;
   __host__ __device__ static constexpr int b(int i) { return i == 0 ? 16 : 32; }
 };
+// n in (256, 512]: targets 32..63 in launches whose fragments stay resident (<= 206 KB each)
+#define SCQR3_RESIDENT_RANGE(B0, B1)                                                            \
+  template <> struct WidePhases<B0, B1> {                                                       \
+    static constexpr int P = 1, MAXF = B1 * (B1 - 1) - B0 * (B0 - 1);                           \
+    __host__ __device__ static constexpr int b(int i) { return i == 0 ? B0 : B1; }              \
+  };
+SCQR3_RESIDENT_RANGE(32, 40)
+SCQR3_RESIDENT_RANGE(40, 48)
+SCQR3_RESIDENT_RANGE(48, 56)
+SCQR3_RESIDENT_RANGE(56, 60)
+SCQR3_RESIDENT_RANGE(60, 64)
+#undef SCQR3_RESIDENT_RANGE
 template <> struct WidePhases<32, 64> {  // targets 32..63 (greedy, <= MAXF fragments per phase)
   static constexpr int P = 10, MAXF = 370;
   __host__ __device__ static constexpr int b(int i) {
@@ -398,7 +410,9 @@ template <int TB, int TE> constexpr bool phases_ok(int i = 0) {
   using W = WidePhases<TB, TE>;
   return i == W::P || (phase_frags(W::b(i), W::b(i + 1)) <= W::MAXF && W::b(W::P) == TE && phases_ok<TB, TE>(i + 1));
 }
-static_assert(phases_ok<0, 32>() && phases_ok<16, 24>() && phases_ok<16, 32>() && phases_ok<32, 64>(),
+static_assert(phases_ok<0, 32>() && phases_ok<16, 24>() && phases_ok<16, 32>() && phases_ok<32, 64>() &&
+                  phases_ok<32, 40>() && phases_ok<40, 48>() && phases_ok<48, 56>() && phases_ok<56, 60>() &&
+                  phases_ok<60, 64>(),
               "phase fragment counts exceed the buffers");
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -708,7 +722,20 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
         e = launch_wide<0, 32, 256>(p, num_sms, stream);
       }
       if (e != cudaSuccess) return e;
+#ifdef SCQR3_WIDE512_PHASED
       return launch_wide<32, 64, 256>(p, num_sms, stream);
+#else
+      // targets 32..63 in five launches with resident fragments, each reading Q(:, 0:8 TB) back;
+      // launches whose targets lie wholly in the padding past n are skipped (so every column
+      // read back is < n: TB < ceil(n / 8) gives 8 TB < n)
+      const int nb = (p.n + 7) / 8;
+      if ((e = launch_wide<32, 40, 256, 2>(p, num_sms, stream)) != cudaSuccess) return e;
+      if (nb > 40 && (e = launch_wide<40, 48, 256, 2>(p, num_sms, stream)) != cudaSuccess) return e;
+      if (nb > 48 && (e = launch_wide<48, 56, 256, 2>(p, num_sms, stream)) != cudaSuccess) return e;
+      if (nb > 56 && (e = launch_wide<56, 60, 256, 2>(p, num_sms, stream)) != cudaSuccess) return e;
+      if (nb > 60) return launch_wide<60, 64, 256, 2>(p, num_sms, stream);
+      return cudaSuccess;
+#endif
     }
     default: return cudaErrorInvalidValue;
   }

@@ -119,7 +119,7 @@ def test_cholesky_breakdown_matches_oracle():
 # ------------------------------------------------------------------ TRSM
 @gpu
 @pytest.mark.parametrize("m,n", [(1, 1), (31, 5), (1000, 16), (4097, 64), (10007, 128), (3001, 160), (3000, 200),
-                                 (2049, 256), (2001, 264), (1800, 512)])
+                                 (2049, 256), (2001, 264), (3001, 300), (1500, 321), (1800, 512)])
 def test_trsm_integer_exact(m, n):
     rng = np.random.default_rng(m)
     Q = rng.integers(-9, 10, size=(m, n)).astype(float)
