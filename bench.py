@@ -301,6 +301,8 @@ def run_ours(args):
     roofline = {"bound": "tensor", "achieved": kern[dom]["tflops"], "peak": peak, "unit": "TFLOP/s",
                 "frac": kern[dom]["tflops"] / peak, "traffic": tr.get("bytes_per_launch") if tr else None,
                 "kernel": f"{dom}_kernel (FP64 DMMA)" + (" + fused next-pass Gram" if dom == "trsm" and fused else "")
+                          + (" + trsm_wide_kernel (block-column launches, one timed unit)" if dom == "trsm" and n > 128
+                             else "")
                           + (" (B-Gram + plain Gram)" if dom == "gram" and cfg.oblique else ""),
                 "peak_source": "measured FP64 DMMA loop on this pool's B200 (profiles/fp64_peaks.json); "
                                "MEASURED_PEAKS.json has no fp64 entry",
