@@ -16,8 +16,14 @@
  *     device (it keeps a small pinned host status block and two events per thread).
  *   - TMA requirements: X, Q 16-byte aligned and ld, ldq even (8*ld % 16 == 0).
  *   - Supported sizes: 1 <= n <= 512 (SURVEY 8(b) contract), m_global >= n, m >= 0 on
- *     every rank.  n in (256, 512] is padded to 512 internally (its TRSM runs as two
- *     block-column launches).
+ *     every rank (an oblique metric across ranks needs m >= its halo rows on every rank).
+ *     n in (128, 512] is padded to the next compiled width (192, 256 or 512) and its TRSM runs
+ *     as block-column launches: columns 0..127 by the register-resident kernel, then the
+ *     targets 16..31 (16..23 for n <= 192), then for n > 256 up to five launches for the
+ *     targets 32..40, 40..48, 48..56, 56..60, 60..64 (8-column tiles), each skipped when its
+ *     targets lie wholly past n.
+ *   - With opts->comm, argument errors are agreed collectively: if any rank's arguments are
+ *     invalid, every rank returns SCQR3_EINVAL before the first exchange.
  *   - All device work is ordered on opts->stream; every call returns only after that
  *     work has finished (the pass count is data dependent).
  *   - Return codes: SCQR3_OK; SCQR3_EINVAL (bad argument -- including NaN/Inf entries in X,
@@ -211,6 +217,19 @@ int scqr3_comm_unique_id(void* id_out);
 /* Creates this rank's communicator on the current CUDA device; *comm_out is passed in
  * scqr3_opts.comm.  Collective over all nranks. */
 int scqr3_comm_init(void** comm_out, int32_t nranks, const void* id, int32_t rank);
+/* In-process "loopback" communicator group (validation of the multi-rank protocol on one GPU):
+ * writes nranks handles to comms_out[0..nranks-1], 1 <= nranks <= 16.  Rank r's handle is
+ * passed in scqr3_opts.comm by the host thread that drives rank r; the nranks threads call the
+ * same entry point concurrently, each on its own stream and rows, on the SAME current device.
+ * The exchanges run the same protocol as NCCL (Gram sum, halo rows, b_off coupling, global m,
+ * ||B|| bound): a rank publishes a device buffer and an event, a host barrier, then each rank's
+ * stream waits on its peers' events and reads their buffers with its own copies / kernels
+ * (rank-ordered sum, so R is bitwise identical on every rank).  No kernel waits on another.
+ * If a rank fails after the exchanges began, the group is marked failed and its peers return
+ * SCQR3_EINVAL; a group whose ranks stop calling times out after 600 s.  Every handle is
+ * released with scqr3_comm_destroy (the shared state with the last one). */
+int scqr3_comm_init_loopback(void** comms_out, int32_t nranks);
+/* Releases a communicator (NCCL or loopback). */
 int scqr3_comm_destroy(void* comm);
 
 /* Thread-local description of the last SCQR3_EINVAL. */

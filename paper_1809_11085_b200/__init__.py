@@ -127,6 +127,15 @@ class Comm:
         _check(_abi.lib().scqr3_comm_init(ctypes.byref(h), world, raw, rank))
         return cls(h, rank, world)
 
+    @classmethod
+    def loopback(cls, world: int):
+        """`world` in-process ranks on the current GPU (scqr3_comm_init_loopback): rank r's
+        calls must be made by a host thread of its own, concurrently with the other ranks'
+        (see ``paper_1809_11085_b200.dist.run_ranks``)."""
+        hs = (ctypes.c_void_p * world)()
+        _check(_abi.lib().scqr3_comm_init_loopback(hs, world))
+        return [cls(ctypes.c_void_p(hs[r]), r, world) for r in range(world)]
+
     def destroy(self):
         if self.handle:
             _abi.lib().scqr3_comm_destroy(self.handle)

@@ -19,7 +19,7 @@ EXPORTED = [
     "scqr3_cholesky", "scqr3_trsm", "scqr3_comm_unique_id", "scqr3_comm_init",
     "scqr3_comm_destroy", "scqr3_last_error", "scqr3_launch_count", "scqr3_workspace_size_csr",
     "scqr3_factor_oblique_csr", "scqr3_gram_oblique_csr", "scqr3_workspace_size_complex",
-    "scqr3_factor_complex",
+    "scqr3_factor_complex", "scqr3_comm_init_loopback",
 ]
 
 
@@ -101,13 +101,14 @@ def lib():
         L.scqr3_comm_unique_id.argtypes = [vp]
         L.scqr3_comm_init.argtypes = [ctypes.POINTER(vp), ctypes.c_int32, vp, ctypes.c_int32]
         L.scqr3_comm_destroy.argtypes = [vp]
+        L.scqr3_comm_init_loopback.argtypes = [ctypes.POINTER(vp), ctypes.c_int32]
         L.scqr3_last_error.restype = ctypes.c_char_p
         L.scqr3_launch_count.argtypes = [ctypes.c_int32]
         L.scqr3_launch_count.restype = ctypes.c_int64
         for name in ("scqr3_factor_oblique_csr", "scqr3_gram_oblique_csr", "scqr3_factor_complex",
                      "scqr3_factor", "scqr3_factor_oblique", "scqr3_factor_host", "scqr3_gram",
                      "scqr3_gram_oblique", "scqr3_cholesky", "scqr3_trsm", "scqr3_comm_unique_id",
-                     "scqr3_comm_init", "scqr3_comm_destroy"):
+                     "scqr3_comm_init", "scqr3_comm_destroy", "scqr3_comm_init_loopback"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib

@@ -544,7 +544,10 @@ __global__ void csr_gershgorin_kernel(const long long* rp, const double* cv, lon
 
 // Argument check of a CSR metric on the device: row_ptr non-decreasing from 0, every column
 // index inside [-halo, m + halo).  *bad is set to 1 on any violation.
-__global__ void csr_check_kernel(const long long* rp, const int* ci, long long m, long long halo, int* bad) {
+__global__ void csr_check_kernel(const long long* rp, const int* ci, long long m, long long halo, int has_prev,
+                                 int has_next, int* bad) {
+  // halo rows exist only towards neighbouring ranks: none before rank 0, none after the last
+  const long long lo = has_prev ? -halo : 0, hi = has_next ? m + halo : m;
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long a = rp[i], b = rp[i + 1];
@@ -553,7 +556,7 @@ __global__ void csr_check_kernel(const long long* rp, const int* ci, long long m
       continue;
     }
     for (long long z = a; z < b; ++z)
-      if (ci[z] < -halo || ci[z] >= m + halo) *bad = 1;
+      if (ci[z] < lo || ci[z] >= hi) *bad = 1;
   }
 }
 

@@ -16,17 +16,19 @@
 #include <vector>
 
 #include "scqr3.h"
+#include "scqr3_comm.h"
 #include "scqr3_dev.cuh"
 #include "scqr3_kernels.h"
 
 using namespace scqr3;
 
 namespace {
-
 thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
+}  // namespace
 
-int fail(const char* fmt, ...) {
+namespace scqr3 {
+int set_error(const char* fmt, ...) {
   char buf[512];
   va_list ap;
   va_start(ap, fmt);
@@ -35,6 +37,11 @@ int fail(const char* fmt, ...) {
   g_err = buf;
   return SCQR3_EINVAL;
 }
+}  // namespace scqr3
+
+namespace {
+
+#define fail set_error
 
 #define CUDA_TRY(expr)                                                                      \
   do {                                                                                      \
@@ -51,11 +58,6 @@ int fail(const char* fmt, ...) {
     int rc_ = (expr);          \
     if (rc_ != SCQR3_OK) return rc_; \
   } while (0)
-
-struct Comm {
-  ncclComm_t nccl;
-  int rank, nranks;
-};
 
 struct GraphKey;
 struct GraphPlan {
@@ -391,9 +393,11 @@ int launch_gram_reduce(Ctx* c, const Layout& L, const WS& w, int chunks, bool ob
 // Gram of the m x n block at src into w.tiles (packed upper tiles; oblique: sym(Q^T Y) and ||Q||_F^2)
 int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld, int64_t m, bool oblique,
              const ObliqueYParams* yp, cudaStream_t st, PassGate gate = PassGate{}) {
-  const long long nout = L.tiles_sym * 64;
   if (m == 0) {
-    CUDA_TRY(cudaMemsetAsync(w.tiles, 0, static_cast<size_t>(nout + 1) * 8, st));
+    // an empty shard contributes zeros to every summed entry: the (B-)Gram, ||Q||_F^2 and, for
+    // the oblique layout, the plain Gram behind them
+    const long long nout = L.tiles_sym * 64 * (oblique ? 2 : 1) + 1;
+    CUDA_TRY(cudaMemsetAsync(w.tiles, 0, static_cast<size_t>(nout) * 8, st));
     return SCQR3_OK;
   }
   int colsq_count = 0;
@@ -490,28 +494,6 @@ int launch_trmul(Ctx* c, const double* Rt, double* R, double* Rnew, int n, int f
 }
 
 bool w_fits_smem(int n) { return static_cast<size_t>(n) * (n + 1) * 8 <= 200 * 1024; }
-
-int halo_exchange(Comm* cm, const double* Qsrc, int64_t ld, int64_t m, int n, int64_t h, double* halo,
-                  cudaStream_t st) {
-  // halo layout, each block h x n column-major (ld h): [0] my first h rows, [1] my last h rows,
-  // [2] the previous rank's last h rows, [3] the next rank's first h rows
-  if (!cm || h <= 0) return SCQR3_OK;
-  if (m < h) return fail("halo of %lld rows exceeds this rank's %lld rows", (long long)h, (long long)m);
-  const size_t blk = static_cast<size_t>(h) * n;
-  CUDA_TRY(cudaMemcpy2DAsync(halo, h * 8, Qsrc, ld * 8, h * 8, n, cudaMemcpyDeviceToDevice, st));
-  CUDA_TRY(cudaMemcpy2DAsync(halo + blk, h * 8, Qsrc + (m - h), ld * 8, h * 8, n, cudaMemcpyDeviceToDevice, st));
-  NCCL_TRY(ncclGroupStart());
-  if (cm->rank > 0) {
-    NCCL_TRY(ncclSend(halo, blk, ncclDouble, cm->rank - 1, cm->nccl, st));
-    NCCL_TRY(ncclRecv(halo + 2 * blk, blk, ncclDouble, cm->rank - 1, cm->nccl, st));
-  }
-  if (cm->rank + 1 < cm->nranks) {
-    NCCL_TRY(ncclSend(halo + blk, blk, ncclDouble, cm->rank + 1, cm->nccl, st));
-    NCCL_TRY(ncclRecv(halo + 3 * blk, blk, ncclDouble, cm->rank + 1, cm->nccl, st));
-  }
-  NCCL_TRY(ncclGroupEnd());
-  return SCQR3_OK;
-}
 
 // ---- CUDA-graph pass loop (device-side pass control)
 // SCQR3_GRAPH=0 selects the host-driven loop for single-GPU calls too (A/B measurement).
@@ -616,52 +598,68 @@ struct Metric {
   int64_t halo() const { return csr ? csr->halo : 1; }
 };
 
-int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric& B, double* Q, int64_t ldq,
-                double* R, const scqr3_opts* o) {
+// Local argument checks of factor_impl (everything that can fail before the first exchange).
+int factor_checks(int64_t m, int64_t n, const double* X, int64_t ld, const Metric& B, const double* Q, int64_t ldq,
+                  const double* R, const scqr3_opts* o, Ctx** c, Layout* L, WS* w) {
+  const Comm* cm = static_cast<const Comm*>(o->comm);
   TRY(check_opts(o));
-  const bool oblique = B.oblique();
-  const double* bd = B.d;
-  const double* be = B.e;
   if (n < 1 || n > kMaxN) return fail("n=%lld outside [1, %d]", (long long)n, kMaxN);
   if (m < 0) return fail("m < 0");
   TRY(check_matrix("X", X, m, ld));
   TRY(check_matrix("Q", Q, m, ldq));
   if (!R) return fail("R is NULL");
-  if (B.d && m > 0 && !be) return fail("b_off is NULL");
+  if (B.d && m > 0 && !B.e) return fail("b_off is NULL");
   if (B.csr) {
     if (m > 0 && (!B.csr->row_ptr || !B.csr->col_idx || !B.csr->vals)) return fail("CSR metric has a NULL array");
     if (B.csr->halo < 0) return fail("CSR halo < 0");
-    if (!o->comm && B.csr->halo != 0) return fail("CSR halo must be 0 without a communicator");
+    if (!cm && B.csr->halo != 0) return fail("CSR halo must be 0 without a communicator");
   }
-  Ctx* c;
-  TRY(get_ctx(&c));
-  cudaStream_t st = static_cast<cudaStream_t>(o->stream);
+  // a rank of an oblique factorisation must own at least its halo rows (its neighbours read them)
+  if (cm && B.oblique() && cm->nranks > 1 && m < std::max<int64_t>(B.halo(), 1))
+    return fail("oblique metric across ranks: this rank owns %lld rows, fewer than the halo (%lld)", (long long)m,
+                (long long)std::max<int64_t>(B.halo(), 1));
+  const int max_passes = o->max_passes > 0 ? o->max_passes : 8;
+  if (max_passes > Ctx::kSlots) return fail("max_passes %d > %d", max_passes, Ctx::kSlots);
+  TRY(get_ctx(c));
+  *L = make_layout(m, n, B.oblique(), B.halo());
+  TRY(carve(*L, o, w));
+  return SCQR3_OK;
+}
+
+int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric& B, double* Q, int64_t ldq,
+                double* R, const scqr3_opts* o, bool* in_protocol) {
+  if (!o) return fail("opts is NULL");
   Comm* cm = static_cast<Comm*>(o->comm);
-  const Layout L = make_layout(m, n, oblique, B.halo());
-  WS w;
-  TRY(carve(L, o, &w));
+  cudaStream_t st = static_cast<cudaStream_t>(o->stream);
+  Ctx* c = nullptr;
+  Layout L{};
+  WS w{};
+  const int rc_local = factor_checks(m, n, X, ld, B, Q, ldq, R, o, &c, &L, &w);
+  // every rank returns SCQR3_EINVAL together when any rank's arguments are bad (no rank is left
+  // waiting in an exchange)
+  if (cm) TRY(comm_agree(cm, rc_local == SCQR3_OK, st));
+  else TRY(rc_local);
+  *in_protocol = cm != nullptr;
+  const bool oblique = B.oblique();
+  const double* bd = B.d;
+  const double* be = B.e;
   c->prof = o->prof;
   c->prof_stream = st;
   c->ev_used = 0;
   const int max_passes = o->max_passes > 0 ? o->max_passes : 8;
-  if (max_passes > Ctx::kSlots) return fail("max_passes %d > %d", max_passes, Ctx::kSlots);
   const double stop_tol = o->stop_tol > 0 ? o->stop_tol : 0.5;
   const int iters = o->power_iters > 0 ? o->power_iters : 32;
 
   // global m (the shift uses the global m)
   int64_t mg = o->m_global;
   if (mg <= 0) {
-    if (cm) {
-      int64_t* dm = reinterpret_cast<int64_t*>(w.misc + 2);
-      CUDA_TRY(cudaMemcpyAsync(dm, &m, 8, cudaMemcpyHostToDevice, st));
-      NCCL_TRY(ncclAllReduce(dm, dm, 1, ncclInt64, ncclSum, cm->nccl, st));
-      CUDA_TRY(cudaMemcpyAsync(&mg, dm, 8, cudaMemcpyDeviceToHost, st));
-      CUDA_TRY(cudaStreamSynchronize(st));
-    } else {
-      mg = m;
-    }
+    if (cm) TRY(comm_host_allreduce(cm, m, COMM_SUM, &mg, st));
+    else mg = m;
   }
-  if (mg < n) return fail("m_global=%lld < n=%lld", (long long)mg, (long long)n);
+  if (mg < n) {
+    *in_protocol = false;  // the same decision on every rank
+    return fail("m_global=%lld < n=%lld", (long long)mg, (long long)n);
+  }
 
   ObliqueYParams yp{};
   double* nb_dev = w.misc;
@@ -684,28 +682,33 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
       yp.ci = B.csr->col_idx;
       yp.cv = B.csr->vals;
       yp.halo = B.csr->halo;
-      if (m > 0) {  // argument check on the device (indices inside this rank's rows + halo)
+      // argument check on the device: row_ptr monotone from 0, indices inside this rank's rows
+      // plus the halo rows that exist (none before rank 0, none after the last rank)
+      int hbad = 0;
+      if (m > 0) {
         int* bad = reinterpret_cast<int*>(w.misc + 12);
         CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), st));
         const int blocks = static_cast<int>(std::max<long long>(1, std::min<long long>((m + 255) / 256, 1024)));
-        csr_check_kernel<<<blocks, 256, 0, st>>>(yp.rp, yp.ci, m, yp.halo, bad);
+        csr_check_kernel<<<blocks, 256, 0, st>>>(yp.rp, yp.ci, m, yp.halo, yp.has_prev, yp.has_next, bad);
         ++g_launches;
         CUDA_TRY(cudaGetLastError());
-        int hbad = 0;
         CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaStreamSynchronize(st));
-        if (hbad) return fail("CSR metric: row_ptr not monotone from 0 or a column index outside [-halo, m+halo)");
+        if (hbad) fail("CSR metric: row_ptr not monotone from 0 or a column index outside this rank's rows and halo");
+      }
+      if (cm) {
+        const int rc = comm_agree(cm, hbad == 0, st);
+        if (rc != SCQR3_OK) *in_protocol = false;  // every rank returns EINVAL together
+        TRY(rc);
+      } else if (hbad) {
+        return SCQR3_EINVAL;
       }
     }
     // e_prev = previous rank's b_off[m_prev - 1]
     double e_prev = 0.0;
     if (multi && B.d) {
       double* ebuf = w.misc + 8;  // [8] send, [9] recv
-      if (m > 0) CUDA_TRY(cudaMemcpyAsync(ebuf, be + (m - 1), 8, cudaMemcpyDeviceToDevice, st));
-      NCCL_TRY(ncclGroupStart());
-      if (rank + 1 < nranks) NCCL_TRY(ncclSend(ebuf, 1, ncclDouble, rank + 1, cm->nccl, st));
-      if (rank > 0) NCCL_TRY(ncclRecv(ebuf + 1, 1, ncclDouble, rank - 1, cm->nccl, st));
-      NCCL_TRY(ncclGroupEnd());
+      TRY(comm_shift_right1(cm, m > 0 ? be + (m - 1) : nullptr, ebuf, ebuf + 1, st));
       CUDA_TRY(cudaMemcpyAsync(&e_prev, ebuf + 1, 8, cudaMemcpyDeviceToHost, st));
       CUDA_TRY(cudaStreamSynchronize(st));
       if (rank == 0) e_prev = 0.0;
@@ -727,7 +730,7 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
       max_reduce_kernel<<<1, 32, 0, st>>>(part, m > 0 ? blocks : 1, nb_dev);
       ++g_launches;
       CUDA_TRY(cudaGetLastError());
-      if (multi) NCCL_TRY(ncclAllReduce(nb_dev, nb_dev, 1, ncclDouble, ncclMax, cm->nccl, st));
+      if (multi) TRY(comm_allreduce_max1(cm, nb_dev, st));
     }
   }
 
@@ -790,9 +793,11 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
       CUDA_TRY(cudaGetLastError());
     }
     if (oblique) {
-      const int ph = cm ? prof_begin(c, PK_COMM) : -1;
-      TRY(halo_exchange(cm, src, ldsrc, m, static_cast<int>(n), B.halo(), w.halo, st));
-      prof_end(c, ph);
+      if (cm) {
+        const int ph = prof_begin(c, PK_COMM);
+        TRY(comm_halo(cm, src, ldsrc, m, static_cast<int>(n), B.halo(), w.halo, st));
+        prof_end(c, ph);
+      }
       yp.Q = src;
       yp.ldq = ldsrc;
     }
@@ -806,20 +811,9 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
       // B-Gram (+ ||Q||_F^2 and the plain Gram for the norm estimate when oblique)
       const size_t cnt = static_cast<size_t>(L.tiles_sym * 64 + (oblique ? 1 + L.tiles_sym * 64 : 0));
       const int pa = prof_begin(c, PK_COMM);
-      if (o->deterministic) {
-        // every rank's Gram side by side (the partials area is free once gram_reduce ran), then
-        // one fixed-order sum: the same bits on every rank and every run
-        if (static_cast<long long>(cm->nranks) * static_cast<long long>(cnt) >
-            static_cast<long long>(L.max_chunks) * L.tiles_part * 64)
-          return fail("deterministic mode: %d ranks exceed the workspace's Gram slots", cm->nranks);
-        NCCL_TRY(ncclAllGather(w.tiles, w.partials, cnt, ncclDouble, cm->nccl, st));
-        rank_sum_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, st>>>(w.partials, cm->nranks,
-                                                                                   static_cast<long long>(cnt), w.tiles);
-        ++g_launches;
-        CUDA_TRY(cudaGetLastError());
-      } else {
-        NCCL_TRY(ncclAllReduce(w.tiles, w.tiles, cnt, ncclDouble, ncclSum, cm->nccl, st));
-      }
+      // (deterministic NCCL mode gathers into the partials area, free once gram_reduce ran)
+      TRY(comm_allreduce_sum(cm, w.tiles, cnt, o->deterministic != 0, w.partials,
+                             static_cast<size_t>(L.max_chunks) * L.tiles_part * 64, st));
       prof_end(c, pa);
     }
     cp.pass = k;
@@ -935,6 +929,16 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
   return status;
 }
 
+int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric& B, double* Q, int64_t ldq,
+                double* R, const scqr3_opts* o) {
+  bool in_protocol = false;
+  const int rc = factor_body(m, n, X, ld, B, Q, ldq, R, o, &in_protocol);
+  // an error after the ranks started exchanging (CUDA / NCCL failure on this rank): a loopback
+  // group is marked failed so that the peers return instead of waiting at the next exchange
+  if (rc == SCQR3_EINVAL && in_protocol) comm_abort(static_cast<Comm*>(o->comm), g_err.c_str());
+  return rc;
+}
+
 // ---- complex X (reading D23): real kernels on the m x 2n split matrix, complex
 // n x n step (zchol.cu).  Host-driven pass loop (as the multi-GPU path).
 struct ZLayout {
@@ -960,8 +964,8 @@ ZLayout make_zlayout(int64_t m, int64_t n) {
   return Z;
 }
 
-int zfactor_impl(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, int64_t ldq, double* R,
-                 const scqr3_opts* o) {
+int zfactor_checks(int64_t m, int64_t n, const double* X, int64_t ld, const double* Q, int64_t ldq, const double* R,
+                   const scqr3_opts* o, Ctx** c, ZLayout* Z, WS* w) {
   TRY(check_opts(o));
   if (n < 1 || 2 * n > kMaxN) return fail("complex n=%lld outside [1, %d]", (long long)n, kMaxN / 2);
   if (m < 0) return fail("m < 0");
@@ -969,16 +973,28 @@ int zfactor_impl(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, i
   if (ld < std::max<int64_t>(m, 1) || ldq < std::max<int64_t>(m, 1)) return fail("leading dimension < m");
   if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Q)) % 16) return fail("X, Q must be 16-byte aligned");
   if (!R) return fail("R is NULL");
-  Ctx* c;
-  TRY(get_ctx(&c));
+  const int max_passes = o->max_passes > 0 ? o->max_passes : 8;
+  if (max_passes > Ctx::kSlots) return fail("max_passes %d > %d", max_passes, Ctx::kSlots);
+  TRY(get_ctx(c));
+  *Z = make_zlayout(m, n);
+  if (!o->workspace || o->workspace_bytes < Z->end) return fail("workspace too small: %zu < %zu bytes", o->workspace_bytes, Z->end);
+  if (reinterpret_cast<uintptr_t>(o->workspace) % 256) return fail("workspace must be 256-byte aligned");
+  TRY(carve(Z->L, o, w));
+  return SCQR3_OK;
+}
+
+int zfactor_impl(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, int64_t ldq, double* R,
+                 const scqr3_opts* o) {
+  if (!o) return fail("opts is NULL");
   cudaStream_t st = static_cast<cudaStream_t>(o->stream);
   Comm* cm = static_cast<Comm*>(o->comm);
-  const ZLayout Z = make_zlayout(m, n);
+  Ctx* c = nullptr;
+  ZLayout Z{};
+  WS w{};
+  const int rc_local = zfactor_checks(m, n, X, ld, Q, ldq, R, o, &c, &Z, &w);
+  if (cm) TRY(comm_agree(cm, rc_local == SCQR3_OK, st));
+  else TRY(rc_local);
   const Layout& L = Z.L;
-  if (!o->workspace || o->workspace_bytes < Z.end) return fail("workspace too small: %zu < %zu bytes", o->workspace_bytes, Z.end);
-  if (reinterpret_cast<uintptr_t>(o->workspace) % 256) return fail("workspace must be 256-byte aligned");
-  WS w;
-  TRY(carve(L, o, &w));
   char* wb = static_cast<char*>(o->workspace);
   double* S = reinterpret_cast<double*>(wb + Z.S);
   double* Az = reinterpret_cast<double*>(wb + Z.A);
@@ -987,18 +1003,10 @@ int zfactor_impl(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, i
   c->prof_stream = st;
   c->ev_used = 0;
   const int max_passes = o->max_passes > 0 ? o->max_passes : 8;
-  if (max_passes > Ctx::kSlots) return fail("max_passes %d > %d", max_passes, Ctx::kSlots);
   int64_t mg = o->m_global;
   if (mg <= 0) {
-    if (cm) {
-      int64_t* dm = reinterpret_cast<int64_t*>(w.misc + 2);
-      CUDA_TRY(cudaMemcpyAsync(dm, &m, 8, cudaMemcpyHostToDevice, st));
-      NCCL_TRY(ncclAllReduce(dm, dm, 1, ncclInt64, ncclSum, cm->nccl, st));
-      CUDA_TRY(cudaMemcpyAsync(&mg, dm, 8, cudaMemcpyDeviceToHost, st));
-      CUDA_TRY(cudaStreamSynchronize(st));
-    } else {
-      mg = m;
-    }
+    if (cm) TRY(comm_host_allreduce(cm, m, COMM_SUM, &mg, st));
+    else mg = m;
   }
   if (mg < n) return fail("m_global=%lld < n=%lld", (long long)mg, (long long)n);
   const int n2 = static_cast<int>(2 * n);
@@ -1049,7 +1057,8 @@ int zfactor_impl(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, i
     else TRY(launch_gram_reduce(c, L, w, fused_chunks, false, 0, st, gate));
     if (cm) {
       const int pa = prof_begin(c, PK_COMM);
-      NCCL_TRY(ncclAllReduce(w.tiles, w.tiles, L.tiles_sym * 64, ncclDouble, ncclSum, cm->nccl, st));
+      TRY(comm_allreduce_sum(cm, w.tiles, static_cast<size_t>(L.tiles_sym * 64), o->deterministic != 0, w.partials,
+                             static_cast<size_t>(L.max_chunks) * L.tiles_part * 64, st));
       prof_end(c, pa);
     }
     const long long nn = n * n;
@@ -1231,7 +1240,8 @@ int scqr3_gram(int64_t m, int64_t n, const double* X, int64_t ld, double* A, con
   TRY(run_gram(c, L, w, X, ld, m, false, nullptr, st));
   Comm* cm = static_cast<Comm*>(opts->comm);
   if (cm)
-    NCCL_TRY(ncclAllReduce(w.tiles, w.tiles, L.tiles_sym * 64, ncclDouble, ncclSum, cm->nccl, st));
+    TRY(comm_allreduce_sum(cm, w.tiles, static_cast<size_t>(L.tiles_sym * 64), opts->deterministic != 0, w.partials,
+                           static_cast<size_t>(L.max_chunks) * L.tiles_part * 64, st));
   const long long nn = n * n;
   tiles_to_full_kernel<<<static_cast<unsigned>((nn + 255) / 256), 256, 0, st>>>(w.tiles, static_cast<int>(n), A);
   ++g_launches;
@@ -1388,10 +1398,17 @@ int scqr3_comm_init(void** comm_out, int32_t nranks, const void* id, int32_t ran
   ncclUniqueId uid;
   std::memcpy(&uid, id, sizeof uid);
   Comm* c = new Comm{};
+  c->kind = COMM_NCCL;
   c->rank = rank;
   c->nranks = nranks;
+  if (cudaMalloc(&c->dscratch, 64) != cudaSuccess) {
+    cudaGetLastError();
+    delete c;
+    return fail("cudaMalloc of the communicator scratch failed");
+  }
   ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, uid, rank);
   if (r != ncclSuccess) {
+    cudaFree(c->dscratch);
     delete c;
     return fail("ncclCommInitRank: %s", ncclGetErrorString(r));
   }
@@ -1399,13 +1416,15 @@ int scqr3_comm_init(void** comm_out, int32_t nranks, const void* id, int32_t ran
   return SCQR3_OK;
 }
 
-int scqr3_comm_destroy(void* comm) {
-  if (!comm) return SCQR3_OK;
-  Comm* c = static_cast<Comm*>(comm);
-  ncclCommDestroy(c->nccl);
-  delete c;
+int scqr3_comm_init_loopback(void** comms_out, int32_t nranks) {
+  if (!comms_out) return fail("comms_out is NULL");
+  std::vector<Comm*> cs(std::max(nranks, 1));
+  TRY(comm_create_loopback(cs.data(), nranks));
+  for (int r = 0; r < nranks; ++r) comms_out[r] = cs[r];
   return SCQR3_OK;
 }
+
+int scqr3_comm_destroy(void* comm) { return comm_destroy(static_cast<Comm*>(comm)); }
 
 const char* scqr3_last_error(void) { return g_err.c_str(); }
 

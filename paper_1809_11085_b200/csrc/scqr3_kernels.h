@@ -158,7 +158,8 @@ cudaError_t launch_gram_tma(int variant, unsigned grid, int threads, size_t smem
 __global__ void gram_reduce_kernel(GramReduceParams p);
 __global__ void csr_y_kernel(ObliqueYParams p);
 __global__ void csr_gershgorin_kernel(const long long* rp, const double* cv, long long m, double* partial);
-__global__ void csr_check_kernel(const long long* rp, const int* ci, long long m, long long halo, int* bad);
+__global__ void csr_check_kernel(const long long* rp, const int* ci, long long m, long long halo, int has_prev,
+                                 int has_next, int* bad);
 __global__ void rank_sum_kernel(const double* parts, int nparts, long long count, double* out);
 __global__ void oblique_y_kernel(ObliqueYParams p);
 __global__ void gershgorin_kernel(const double* d, const double* e, long long m, int has_prev, double e_prev,

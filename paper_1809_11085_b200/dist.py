@@ -29,3 +29,29 @@ def max_over_ranks(value: float, group=None, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+_POOL = None
+
+
+def run_ranks(fns):
+    """Run fns[r]() for every rank r concurrently, one host thread per rank (the loopback
+    communicator's ranks, scqr3_comm_init_loopback), and return their results in rank order.
+    The threads are reused across calls (each thread keeps the library's per-thread state).
+    An exception in any rank is re-raised after all ranks have returned."""
+    import concurrent.futures as cf
+
+    global _POOL
+    if _POOL is None or _POOL._max_workers < len(fns):
+        _POOL = cf.ThreadPoolExecutor(max_workers=max(16, len(fns)), thread_name_prefix="scqr3-rank")
+    futs = [_POOL.submit(f) for f in fns]
+    out, err = [], None
+    for f in futs:
+        try:
+            out.append(f.result())
+        except BaseException as e:  # noqa: BLE001 -- re-raised below after every rank returned
+            out.append(None)
+            err = err or e
+    if err is not None:
+        raise err
+    return out
