@@ -68,6 +68,48 @@ def load_json(path):
         return None
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def executed_roofline_ms(cfg, m, n, passes, peak_tflops, fused, nnz=0, hbm_gbs=6536.7):
+    """Roofline time of the work a factorisation executed on this rank: the sum over its kernels
+    (which run one after another) of max(algorithmic flops / FP64 peak, algorithmic bytes / HBM
+    bandwidth), for the executed pass count.  Per pass: Gram m n(n+1) flop, 8mn B (oblique: the
+    dual B-Gram + plain Gram, 2 m n(n+1) flop, 16mn B, after Y = BQ: tridiagonal 5mn flop,
+    16mn + 16m B; CSR 2 nnz n flop, 16mn + 12 nnz ceil(n/16) B); TRSM m n^2 flop, 16mn B; the
+    fused n <= 64 TRSM also carries the next pass's Gram (no 8mn re-read).  The n x n steps
+    (reduce, Cholesky) are latency and not in the model."""
+    P, BW = peak_tflops * 1e12, hbm_gbs * 1e9
+    t = lambda fl, by: max(fl / P, by / BW)  # noqa: E731
+    tot = 0.0
+    for k in range(1, passes + 1):
+        if cfg.oblique:
+            if cfg.metric == "laplacian":
+                tot += t(2.0 * nnz * n, 16.0 * m * n + 12.0 * nnz * -(-n // 16))
+            else:
+                tot += t(5.0 * m * n, 16.0 * m * n + 16.0 * m)
+            tot += t(2.0 * m * n * (n + 1), 16.0 * m * n)
+            tot += t(1.0 * m * n * n, 16.0 * m * n)
+        elif fused:
+            if k == 1:
+                tot += t(1.0 * m * n * (n + 1), 8.0 * m * n)
+            fl = m * n * n + (m * n * (n + 1) if k < passes else 0)
+            tot += t(fl, 16.0 * m * n)
+        else:
+            tot += t(1.0 * m * n * (n + 1), 8.0 * m * n) + t(1.0 * m * n * n, 16.0 * m * n)
+    model = ("sum over the executed kernels of max(flops / fp64 peak, bytes / 6536.7 GB/s), "
+             f"{passes} passes, per GPU")
+    return tot * 1e3, model
+
+
 class Clocks:
     """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
 
@@ -199,14 +241,10 @@ def run_ours(args):
     r0, r1 = row_block(m, rank, world)
     mloc = r1 - r0
 
-    # ---- input: the same global X on every rank (same seed), keep this rank's row block
-    Xg = synth.randsvd_torch(m, n, cfg.kappa, seed=0, spectrum=cfg.spectrum, device=dev)
-    if world == 1:
-        X = Xg
-    else:
-        X = sq.colmajor_empty(mloc, n, device=dev)
-        X.copy_(Xg[r0:r1])
-        del Xg
+    # ---- input: each rank generates only its own rows of the global X (per-chunk seeded TSQR
+    # generator: the stitched X is the same for every rank count; synth.randsvd_torch_rows)
+    X = synth.randsvd_torch_rows(m, n, cfg.kappa, r0, r1, seed=0, spectrum=cfg.spectrum, device=dev,
+                                 allreduce=(dist.all_reduce if world > 1 else None))
     d = e = csr = None
     if cfg.oblique and cfg.metric == "laplacian":
         Bg = synth.laplacian2d(cfg.grid_nx, m // cfg.grid_nx, seed=0, wmax=1e4)
@@ -252,10 +290,12 @@ def run_ours(args):
     ev1 = torch.cuda.Event(enable_timing=True)
     clocks.start()
     time.sleep(0.3)
+    # timed region: the default call path (single GPU: the cached CUDA-graph pass loop; with a
+    # communicator: the host-driven pass loop), no profiling events
     with torch.cuda.stream(stream):
         ev0.record(stream)
         for _ in range(args.steps):
-            res = step(with_prof=True)
+            res = step()
         ev1.record(stream)
     stream.synchronize()
     clk = clocks.stop()
@@ -271,6 +311,19 @@ def run_ours(args):
     value = flops_3pass(m, n) / (ms * 1e-3) / 1e12
     passes = res.passes
     actual = passes * m * (2.0 * n * n + n) / (ms * 1e-3) / 1e12
+
+    # ---- profiled replay of the same steps right after the timed region: CUDA events recorded
+    # by the library on `stream` around every launch (host-driven pass loop) give each kernel's
+    # duration; its step time is reported beside the headline
+    with torch.cuda.stream(stream):
+        p0 = torch.cuda.Event(enable_timing=True)
+        p1 = torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        for _ in range(args.steps):
+            step(with_prof=True)
+        p1.record(stream)
+    stream.synchronize()
+    ms_prof = p0.elapsed_time(p1) / args.steps
 
     # ---- per-kernel device time measured live during the timed steps (events on `stream`)
     peaks = load_json(FP64_PEAKS) or {}
@@ -291,7 +344,7 @@ def run_ours(args):
                                 ("comm", prof.comm_ms, prof.comm_calls, None)):
         if cnt:
             avg = msum / cnt
-            kern[name] = {"avg_ms": avg, "launches": int(cnt), "share_of_step": msum / (ms * args.steps)}
+            kern[name] = {"avg_ms": avg, "launches": int(cnt), "share_of_step": msum / (ms_prof * args.steps)}
             if fl:
                 kern[name]["tflops"] = fl / (avg * 1e-3) / 1e12
                 kern[name]["frac_of_peak"] = kern[name]["tflops"] / peak
@@ -307,7 +360,8 @@ def run_ours(args):
                 "peak_source": "measured FP64 DMMA loop on this pool's B200 (profiles/fp64_peaks.json); "
                                "MEASURED_PEAKS.json has no fp64 entry",
                 "algorithmic_flops_per_launch": fl_gram if dom == "gram" else fl_trsm}
-    step_roof_ms = max(flops_3pass(mloc, n) / (peak * 1e12), (24.0 * mloc * n * 3) / 6536.7e9) * 1e3
+    step_roof_ms, step_model = executed_roofline_ms(cfg, mloc, n, passes, peak, fused,
+                                                    nnz=(int(csr.vals.numel()) if csr is not None else 0))
 
     # ---- end to end through the C ABI with host buffers (H2D of X, D2H of Q and R inside)
     e2e = None
@@ -372,6 +426,8 @@ def run_ours(args):
         tc = time.perf_counter() - t0
         cpu = {"value": flops_3pass(rows, n) / tc / 1e12, "unit": "TFLOP/s", "cores": oracle.num_threads(),
                "kind": "oracle", "seconds": tc, "passes": ro.passes, "status": ro.status,
+               "tflops_actual_passes": ro.passes * rows * (2.0 * n * n + n) / tc / 1e12,
+               "cpu_model": cpu_model(),
                "sample": f"first {rows} of {m} rows of the same device-generated X ({args.config}), one factorisation"}
 
     if rank == 0:
@@ -385,8 +441,9 @@ def run_ours(args):
                        "shifted": [t["shifted"] for t in res.trace], "parallelism": f"row-block x{world}",
                        "l2": f"no flush: X and Q ({8 * mloc * n / 1e9:.2f} GB each per GPU) >> 126 MB L2"},
             "roofline": roofline,
-            "roofline_step": {"ms": step_roof_ms, "frac": step_roof_ms / ms,
-                              "model": "max(6mn^2 / fp64 peak, 72mn bytes / 6536.7 GB/s) per GPU"},
+            "roofline_step": {"ms": step_roof_ms, "frac": step_roof_ms / ms, "passes": passes,
+                              "model": step_model},
+            "ms_per_step_profiled": ms_prof,
             "tflops_actual_passes": actual,
             "kernels": kern,
             "cpu_baseline": cpu,

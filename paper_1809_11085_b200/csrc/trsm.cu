@@ -21,8 +21,18 @@
 // (trsm_wide_kernel below) for n > 128.
 #include "scqr3_dev.cuh"
 #include "scqr3_kernels.h"
+#ifdef SCQR3_TRSM_CLOCK
+#include <cstdio>
+#endif
 
 namespace scqr3 {
+
+#ifndef SCQR3_TRSM_PIPE
+#define SCQR3_TRSM_PIPE 1  // 0: both k-steps of each later target back to back (A/B builds)
+#endif
+#ifndef SCQR3_TRSM_RED_FROM
+#define SCQR3_TRSM_RED_FROM 1000  // first column block solved in the full-row form (A even)
+#endif
 
 // GRAM (n <= 64): also accumulate the next pass's Gram Q_k^T Q_k from the
 // solved rows, so the next pass does not read Q from HBM again.  Each warp writes its 16 finished
@@ -96,6 +106,11 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
     issue(rg0);
   }
 
+#ifdef SCQR3_TRSM_STAGGER_NS
+  // (experiment) offset the two warps of each SM sub-partition (w, w + 4) by part of a row
+  // group, so that one warp's DMMA-dense head meets the other's latency-bound tail
+  if (warp >= 4) __nanosleep(SCQR3_TRSM_STAGGER_NS);
+#endif
   double gacc[GRAM ? NTS : 1][2];  // GRAM: this warp's Gram tiles (C fragments)
 #pragma unroll
   for (int T = 0; T < (GRAM ? NTS : 1); ++T) gacc[T][0] = gacc[T][1] = 0.0;
@@ -151,8 +166,14 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
     auto bfrag = [&](int K, int s) -> double {  // -R~ fragment of k-step s for target block K
       return SMEM_B ? bf[(K * (K - 1) + s) * 32 + lane] : __ldg(bf + (K * (K - 1) + s) * 32 + lane);
     };
+#ifdef SCQR3_TRSM_CLOCK
+    long long tclk[NT + 1];
+#endif
 #pragma unroll
     for (int J = 0; J < NT; ++J) {
+#ifdef SCQR3_TRSM_CLOCK
+      tclk[J] = clock64();
+#endif
       if (TMA && J == (NT > 1 ? 1 : 0)) {
         // every lane's slot reads have been consumed by now: refill the slot with the next group
         __syncwarp();
@@ -171,21 +192,100 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
       // (v_j -= v_c * (r_cj / r_cc), strict upper only, zeros elsewhere), interleaved with the
       // updates C_K += Q_{J-1} (-R~_{J-1,K}) of the later blocks K = J+1..NT-1
       const int nup = J >= 1 ? NT - 1 - J : 0;
+#if !SCQR3_TRSM_PIPE
       int u = 0;
+#endif
       const double* D = db + J * 72;
+      auto upd = [&](int K, int s) {
+        const double b = bfrag(K, s);
+#pragma unroll
+        for (int a = 0; a < A; ++a) dmma(q[a][K][0], q[a][K][1], q[a][J - 1][s & 1], b);
+      };
+      // The two k-steps of a target's update are a dependent DMMA pair; step c of the chain
+      // issues the first k-step of its targets and the second k-step of step c-1's, so that
+      // the dependent DMMAs sit a whole chain step apart (adjacent dependent DMMAs get a NOP
+      // and a fixed-latency wait in between).
       auto later_updates = [&](int c) {
+#if SCQR3_TRSM_PIPE
+#pragma unroll
+        for (int v = nup * c / 8; v < nup * (c + 1) / 8; ++v) upd(J + 1 + v, 2 * (J - 1));
+        if (c >= 1) {
+#pragma unroll
+          for (int v = nup * (c - 1) / 8; v < nup * c / 8; ++v) upd(J + 1 + v, 2 * J - 1);
+        }
+        if (c == 7) {
+#pragma unroll
+          for (int v = nup * 7 / 8; v < nup; ++v) upd(J + 1 + v, 2 * J - 1);
+        }
+#else
 #pragma unroll
         for (; u < nup * (c + 1) / 8; ++u) {
           const int K = J + 1 + u;
 #pragma unroll
-          for (int s = 2 * (J - 1); s < 2 * J; ++s) {
-            const double b = bfrag(K, s);
-#pragma unroll
-            for (int a = 0; a < A; ++a) dmma(q[a][K][0], q[a][K][1], q[a][J - 1][s & 1], b);
-          }
+          for (int s = 2 * (J - 1); s < 2 * J; ++s) upd(K, s);
         }
+#endif
       };
       if constexpr (A % 2 == 0) {
+       if (J >= SCQR3_TRSM_RED_FROM) {
+        // Full-row solve (late blocks, whose few later updates cannot hide a shuffle per step):
+        // lanes t = 0,1 both hold all 8 columns of row g, lanes t = 2,3 those of row g+8, so the
+        // pivot of every step is local and the chain is one DFMA per step instead of a shuffle
+        // plus a DFMA (28 DFMA per lane and block instead of 18; same operations in the same
+        // order on every value, so the same rounding as the split form below).
+        const bool lo = t < 2;
+        const int qb = lane & ~3;
+        double v[A / 2][8];
+#pragma unroll
+        for (int b = 0; b < A / 2; ++b)
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const double x0 = __shfl_sync(0xffffffffu, q[2 * b][J][h], qb | e);
+              const double x1 = __shfl_sync(0xffffffffu, q[2 * b + 1][J][h], qb | e);
+              v[b][2 * e + h] = lo ? x0 : x1;
+            }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (c < 7) {
+            double r[8];
+#pragma unroll
+            for (int k = 2 * ((c + 1) / 2); k < 8; k += 2) {
+              const double2 rr = *reinterpret_cast<const double2*>(D + c * 8 + k);
+              r[k] = rr.x;
+              r[k + 1] = rr.y;
+            }
+#pragma unroll
+            for (int b = 0; b < A / 2; ++b)
+#pragma unroll
+              for (int j = c + 1; j < 8; ++j) v[b][j] = fma(-v[b][c], r[j], v[b][j]);
+          }
+          later_updates(c);
+        }
+        double ri[8];
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) {
+          const double2 rr = *reinterpret_cast<const double2*>(D + 64 + k);
+          ri[k] = rr.x;
+          ri[k + 1] = rr.y;
+        }
+        const bool t1 = t & 1, t2 = t & 2;
+#pragma unroll
+        for (int b = 0; b < A / 2; ++b) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[b][j] *= ri[j];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            // own row's column 2t+h, and for the other half the column 2(t^2)+h of this row
+            const double own = t2 ? (t1 ? v[b][6 + h] : v[b][4 + h]) : (t1 ? v[b][2 + h] : v[b][h]);
+            const double snd = t2 ? (t1 ? v[b][2 + h] : v[b][h]) : (t1 ? v[b][6 + h] : v[b][4 + h]);
+            const double oth = __shfl_xor_sync(0xffffffffu, snd, 2);
+            q[2 * b][J][h] = lo ? own : oth;
+            q[2 * b + 1][J][h] = lo ? oth : own;
+          }
+        }
+       } else {
         // Fragment pairs (a, a+1) = rows g and g+8 of the quad.  Lanes t^2 swap halves so that
         // lanes t = 0,1 hold row g and lanes t = 2,3 row g+8, four columns each: lane u = t&1
         // holds columns {2u, 2u+1, 2u+4, 2u+5} (V[0..3]).  Step c then updates only the
@@ -241,6 +341,7 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
             q[a + 1][J][h] = lo ? rcv : Vb[2 + h];
           }
         }
+       }
       } else {
         // (odd A: inside each quad, lane t holds columns 2t, 2t+1 of its row)
 #pragma unroll
@@ -271,6 +372,16 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
       if (J >= 1 && !bulk_q) store_block(q, J - 1);
     }
     if (!bulk_q) store_block(q, NT - 1);
+#ifdef SCQR3_TRSM_CLOCK
+    tclk[NT] = clock64();
+    if (lane == 0 && blockIdx.x == 7 && (warp == 1 || warp == 5) && rg / stride == 2) {
+      long long d[16] = {};
+      for (int J = 0; J < NT && J < 16; ++J) d[J] = tclk[J + 1] - tclk[J];
+      printf("w%d %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld tot %lld\n", warp,
+             d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], d[8], d[9], d[10], d[11], d[12], d[13], d[14], d[15],
+             tclk[NT] - tclk[0]);
+    }
+#endif
     if (TMA && NT <= 1) {
       __syncwarp();
       issue(rg + stride);
@@ -369,8 +480,11 @@ static cudaError_t launch_one(const TrsmParams& p, const CUtensorMap* map, int n
 // computes.  Each warp owns 8 rows and 32 target blocks in registers (q: 64 doubles).  Per
 // phase [K0, K1): (i) the updates of its targets from all earlier blocks (a dependency-free
 // DMMA stream, targets interleaved), then (ii) the right-looking triangular part inside the
-// phase, as in trsm_kernel.  n > 256 runs as two launches (block-column TRSM): targets 0..31,
-// then targets 32..63, whose updates from blocks 0..31 read the finished Q columns back.
+// phase, as in trsm_kernel.  n > 128 runs as block-column launches (launch_trsm below): columns
+// 0..127 by trsm_kernel, targets 16..31 (16..23 for n <= 192) with resident fragments, and for
+// n > 256 up to five resident launches for targets 32..40, 40..48, 48..56, 56..60, 60..64 (each
+// reads the finished Q columns back; launches wholly past n are skipped).  The phased form
+// (fragments re-streamed per row group) remains for the targets 0..31 / 32..63 fallbacks.
 constexpr int phase_frags(int k0, int k1) { return k1 * (k1 - 1) - k0 * (k0 - 1); }
 template <int TB, int TE> struct WidePhases;  // targets TB..TE-1
 template <> struct WidePhases<0, 32> {  // targets 0..31
@@ -684,8 +798,15 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
                        : launch_one<8, 4, true, 256, false>(p, nullptr, num_sms, stream);
     case 12: return tma ? launch_one<12, 2, true, 256, true>(p, map, num_sms, stream)
                         : launch_one<12, 2, true, 256, false>(p, nullptr, num_sms, stream);
-    case 16: return tma ? launch_one<16, 2, true, 256, true>(p, map, num_sms, stream)
+#ifndef SCQR3_TRSM16_THREADS
+#define SCQR3_TRSM16_THREADS 256
+#endif
+#ifdef SCQR3_TRSM16_A1
+    case 16: return launch_one<16, 1, true, SCQR3_TRSM16_A1, false>(p, nullptr, num_sms, stream);
+#else
+    case 16: return tma ? launch_one<16, 2, true, SCQR3_TRSM16_THREADS, true>(p, map, num_sms, stream)
                         : launch_one<16, 2, true, 256, false>(p, nullptr, num_sms, stream);
+#endif
     case 24: {
       // split as for NT = 32: columns 0..127, then targets 16..23 (A = 2)
       if (!map) return launch_one<24, 1, true, 256, false>(p, nullptr, num_sms, stream);

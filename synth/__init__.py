@@ -7,8 +7,9 @@ BASELINE.json tridiagonal SPD metric B.  Both the oracle and the CUDA path consu
 it returns; neither is imported here.
 
 Recipes (DESIGN.md "Inputs"):
-  * U (m x n) and V (n x n): Householder QR (LAPACK geqrf/orgqr via numpy, or cuSOLVER via
-    torch on the device; above 16 GB a chunked Householder TSQR, reading D17) of i.i.d. N(0,1)
+  * U (m x n) and V (n x n): Householder QR (LAPACK geqrf/orgqr via numpy on the host; on the
+    device a Householder TSQR over fixed 2^20-row chunks, each drawn from its own seeded
+    generator, so a rank can generate just its own rows -- reading D17) of i.i.d. N(0,1)
     matrices, columns sign-normalised so diag(R) > 0.
   * sigma geometric: sigma_i = kappa^{-(i-1)/(n-1)}, i = 1..n (||X||_2 = 1, kappa_2 = kappa).
   * sigma "cluster" (BASELINE config 4, reading D15): sigma_1 = 1, sigma_2..sigma_{n-8}
@@ -183,44 +184,58 @@ def random_rows(m: int, n: int, seed: int = 0) -> np.ndarray:
 
 
 # --------------------------------------------------------------------------- device side
+CHUNK_ROWS = 1 << 20  # device generator: rows per seeded Gaussian chunk (independent of the GPU count)
+
+
 def randsvd_torch(m: int, n: int, kappa: float, seed: int = 0, spectrum: str = "geometric",
                   device="cuda", ld: int | None = None):
-    """Same recipe on the device (torch RNG + cuSOLVER Householder QR); returns an (m, n)
-    torch view with column-major strides (1, ld)."""
+    """Same recipe on the device; returns the whole (m, n) X with column-major strides (1, ld).
+    (randsvd_torch_rows with one rank.)"""
+    return randsvd_torch_rows(m, n, kappa, 0, m, seed=seed, spectrum=spectrum, device=device, ld=ld)
+
+
+def randsvd_torch_rows(m: int, n: int, kappa: float, r0: int, r1: int, seed: int = 0, spectrum: str = "geometric",
+                       device="cuda", ld: int | None = None, allreduce=None):
+    """Rows [r0, r1) of X = U diag(sigma) V^T generated on the device without
+    forming the other rows, so each rank of a multi-GPU run makes only its own block.
+
+    U is the thin Q factor of an m x n N(0,1) matrix G, by Householder TSQR (reading D17): G's
+    fixed 2^20-row chunks are drawn from generators seeded per chunk (seed, chunk), each chunk
+    is QR-factorised (cuSOLVER), the chunks' R factors are stacked and QR-factorised again, and
+    chunk c's rows of U are Q_c times block c of that second Q, signs normalised so the
+    overall R has a positive diagonal.  The result does not depend on how the rows are split
+    over ranks.  `allreduce(t)` sums a tensor over the ranks in place (None: one rank); each
+    chunk's R is contributed by the rank holding the chunk's first row (others add zeros).
+    Returns an (r1 - r0, n) view with strides (1, ld)."""
     import torch
 
-    ld = ld or m
-    g = torch.Generator(device=device)
-    g.manual_seed(int(seed) * 1000003 + TAG_U)
-    chunk = 1 << 20
-    if m * n * 8 <= (16 << 30):
-        G = torch.randn((n, m), generator=g, dtype=torch.float64, device=device).t()  # col-major (m, n)
-        Uq, Ur = torch.linalg.qr(G, mode="reduced")
-        del G
-        sgn = torch.sign(torch.diagonal(Ur))
-        sgn[sgn == 0] = 1.0
-        del Ur
-    else:
-        # Too large for one device Householder QR next to X and Q (C4: 82 GB): Householder TSQR
-        # in place (reading D17) -- per-chunk QR, QR of the stacked chunk R's, then each chunk's
-        # Q times its block of the second Q.  Same thin Q factor up to rounding.
-        buf = torch.empty((n, ld), dtype=torch.float64, device=device)
-        Uq = buf.t()[:m]
-        Rs = []
-        for r0 in range(0, m, chunk):
-            r1 = min(m, r0 + chunk)
-            Gc = torch.randn((n, r1 - r0), generator=g, dtype=torch.float64, device=device).t()
-            Qc, Rc = torch.linalg.qr(Gc, mode="reduced")
-            Uq[r0:r1].copy_(Qc)
-            Rs.append(Rc)
-            del Gc, Qc
-        Q2, R2 = torch.linalg.qr(torch.cat(Rs, 0), mode="reduced")
-        for i, r0 in enumerate(range(0, m, chunk)):
-            r1 = min(m, r0 + chunk)
-            Uq[r0:r1].copy_(Uq[r0:r1] @ Q2[i * n:(i + 1) * n])
-        sgn = torch.sign(torch.diagonal(R2))
-        sgn[sgn == 0] = 1.0
-        del Rs, Q2, R2
+    if not (0 <= r0 <= r1 <= m):
+        raise ValueError("bad row range")
+    mr = r1 - r0
+    ld = ld or max(mr, 1)
+    C = CHUNK_ROWS
+    nch = (m + C - 1) // C
+    mine = [c for c in range(nch) if c * C < r1 and min(m, (c + 1) * C) > r0] if mr > 0 else []
+
+    def chunk_qr(c):
+        g = torch.Generator(device=device)
+        g.manual_seed((int(seed) * 1000003 + TAG_U) * 65537 + c)
+        rows = min(m, (c + 1) * C) - c * C
+        Gc = torch.randn((n, rows), generator=g, dtype=torch.float64, device=device).t()
+        return torch.linalg.qr(Gc, mode="reduced")
+
+    Rs = torch.zeros((nch, n, n), dtype=torch.float64, device=device)
+    Qc = {}
+    for c in mine:
+        Qm, Rm = chunk_qr(c)
+        Qc[c] = Qm
+        if r0 <= c * C:  # this rank holds the chunk's first row: it contributes R_c
+            Rs[c].copy_(Rm)
+    if allreduce is not None:
+        allreduce(Rs)
+    Q2, R2 = torch.linalg.qr(Rs.reshape(nch * n, n), mode="reduced")
+    sgn = torch.sign(torch.diagonal(R2))
+    sgn[sgn == 0] = 1.0
     gv = torch.Generator(device=device)
     gv.manual_seed(int(seed) * 1000003 + TAG_V)
     Gv = torch.randn((n, n), generator=gv, dtype=torch.float64, device=device)
@@ -228,16 +243,14 @@ def randsvd_torch(m: int, n: int, kappa: float, seed: int = 0, spectrum: str = "
     Vq = Vq * torch.sign(torch.diagonal(Vr))
     s = torch.as_tensor(sigma(n, kappa, spectrum, seed), dtype=torch.float64, device=device)
     W = (sgn * s)[:, None] * Vq.t()                       # diag(sgn*sigma) V^T, n x n
-    if m * n * 8 > (16 << 30):
-        Xc = Uq                                             # overwrite U in place, row chunk by chunk
-    else:
-        out = torch.empty((n, ld), dtype=torch.float64, device=device)
-        Xc = out.t()[:m]                                    # (m, n), strides (1, ld)
-    for r0 in range(0, m, chunk):
-        r1 = min(m, r0 + chunk)
-        Xc[r0:r1].copy_(Uq[r0:r1] @ W)
-    del Uq
-    return Xc
+    out = torch.empty((n, ld), dtype=torch.float64, device=device)
+    X = out.t()[:mr]
+    for c in mine:
+        a, b = max(r0, c * C), min(r1, (c + 1) * C)
+        Mc = Q2[c * n:(c + 1) * n] @ W                      # block c of the second Q, times diag(sigma) V^T
+        X[a - r0:b - r0].copy_(Qc[c][a - c * C:b - c * C] @ Mc)
+        del Qc[c]
+    return X
 
 
 def tridiag_b_torch(m: int, seed: int = 0, device="cuda"):

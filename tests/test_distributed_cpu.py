@@ -153,3 +153,46 @@ def test_two_rank_gloo_decomposition_matches_single_process():
     G = out[0]["Gcsr"]
     assert np.array_equal(G, out[1]["Gcsr"])
     assert np.max(np.abs((G + G.T) / 2 - Ac)) <= 1e-12 * np.max(np.abs(Ac))
+
+
+def _gen_worker(rank, world, port, q):
+    import synth
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        synth.CHUNK_ROWS = 1 << 12           # several chunks, some split between ranks
+        m, n = 20_000, 6
+        r0, r1 = pdist.row_block(m, rank, world)
+        X = synth.randsvd_torch_rows(m, n, 1e8, r0, r1, seed=3, device="cpu", allreduce=dist.all_reduce)
+        q.put((rank, (r0, X.numpy().copy())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_row_sharded_generator_matches_one_rank():
+    """bench.py's multi-GPU input: each rank generates only its rows (per-chunk seeded Gaussian
+    chunks, Householder TSQR with the chunk R factors summed over ranks); the stitched X is
+    bitwise the one-rank X, with the requested spectrum."""
+    import synth
+
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gen_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    synth.CHUNK_ROWS = 1 << 12
+    try:
+        ref = synth.randsvd_torch(20_000, 6, 1e8, seed=3, device="cpu").numpy()
+    finally:
+        synth.CHUNK_ROWS = 1 << 20
+    X = np.concatenate([out[r][1] for r in range(world)], axis=0)
+    assert np.array_equal(X, ref)
+    s = np.linalg.svd(X, compute_uv=False)
+    assert abs(s[0] - 1.0) < 1e-12 and abs(s[0] / s[-1] / 1e8 - 1.0) < 1e-6
