@@ -66,6 +66,7 @@ def _load():
         lib.orc_gram_oblique.argtypes = [i64, i64, P, i64, P, P, P, P]
         PI64, PI32 = ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int32)
         lib.orc_gram_oblique_csr.argtypes = [i64, i64, P, i64, PI64, PI32, P, P, P]
+        lib.orc_gram_parts.argtypes = [i64, i64, P, i64, P, P, PI64, PI32, P, ctypes.c_int, P, P]
         lib.orc_orth_F_csr.argtypes = [i64, i64, P, i64, PI64, PI32, P]
         lib.orc_orth_F_csr.restype = dbl
         lib.orc_scqr3_csr.argtypes = [i64, i64, P, i64, PI64, PI32, P, P, i64, P, ctypes.POINTER(_Opts),
@@ -169,6 +170,26 @@ def gram_oblique_csr(X, B):
     A = np.zeros((n, n), order="F")
     cs = np.zeros(n)
     _load().orc_gram_oblique_csr(m, n, _p(X), m, prp, pci, pcv, _p(A), _p(cs))
+    del keep
+    return A, cs
+
+
+def gram_parts(X, nparts: int, d=None, e=None, csr=None):
+    """The pass Gram of scqr3(..., nparts=P): contiguous row blocks' Grams summed in rank order
+    (oblique: each block's X_p^T (B X)_p with the halo rows of its neighbours, symmetrised after
+    the sum).  Returns (A, colsq) -- colsq (diag(X^T X)) only for an oblique metric."""
+    X = _colmajor(X)
+    m, n = X.shape
+    A = np.zeros((n, n), order="F")
+    cs = np.zeros(n)
+    if d is not None:
+        d = np.ascontiguousarray(d, dtype=np.float64)
+        e = np.ascontiguousarray(e, dtype=np.float64)
+    if csr is not None:
+        prp, pci, pcv, keep = _csr(csr)
+    else:
+        prp = pci = pcv = keep = None
+    _load().orc_gram_parts(m, n, _p(X), m, _p(d), _p(e), prp, pci, pcv, int(nparts), _p(A), _p(cs))
     del keep
     return A, cs
 

@@ -514,6 +514,18 @@ static void gram_any(int64_t m, int64_t n, const double* Q, int64_t ld, const or
   free(cp);
 }
 
+/* The Gram of one pass as gram_any forms it (exported for pins): nparts contiguous row blocks,
+ * each block's (oblique: X_p^T (B X)_p with the neighbours' boundary rows as halo) Gram summed
+ * in rank order; oblique results symmetrised after the sum.  d/e (tridiagonal) or rp/ci/cv
+ * (CSR, global column indices) select the metric; all NULL = the plain Gram. */
+void orc_gram_parts(int64_t m, int64_t n, const double* X, int64_t ld, const double* d, const double* e,
+                    const int64_t* rp, const int32_t* ci, const double* cv, int nparts, double* A,
+                    double* colsq) {
+  const orc_metric B = {d, e, rp, ci, cv};
+  const int oblique = d != NULL || rp != NULL;
+  gram_any(m, n, X, ld, oblique ? &B : NULL, nparts, A, colsq);
+}
+
 /* Returns 0 ok, 2 breakdown even with the shift, 3 not converged, 1 bad argument. */
 static int scqr3_impl(int64_t m, int64_t n, const double* X, int64_t ld, const orc_metric* B,
                       double* Q, int64_t ldq, double* R, const orc_opts* o, orc_trace* trace, int trace_cap,
