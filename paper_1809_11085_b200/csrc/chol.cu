@@ -75,40 +75,65 @@ __device__ __forceinline__ int tile_col(int tile) {
   return TJ;
 }
 
-// tiles: packed upper Gram tiles to load (default: the pass's Gram, p.tiles)
-__device__ __forceinline__ void load_W(const CholParams& p, double* W, int ldw, const double* tiles = nullptr) {
+// tiles: packed upper Gram tiles to load (default: the pass's Gram, p.tiles).  With acc set,
+// also returns this thread's share of the stop-test sums: sum over all (i, j) of (A_ij - delta_ij)^2
+// (off-diagonal entries counted twice, once per triangle) and of the diagonal (the trace).
+__device__ __forceinline__ void load_W(const CholParams& p, double* W, int ldw, const double* tiles = nullptr,
+                                       double* acc_dev = nullptr, double* acc_tr = nullptr) {
   const int n = p.n;
   if (!tiles) tiles = p.tiles;
+  double dv = 0.0, tr = 0.0;
   if (p.mode == CHOL_ONLY) {
     for (int i = threadIdx.x >> 5; i < n; i += kThreads / 32)
       for (int j = threadIdx.x & 31; j < n; j += 32) W[i * ldw + j] = gram_entry(p, i, j);
   } else {
-    // read the packed tiles linearly (coalesced, all loads independent) and place each upper
-    // element at (i, j) and (j, i): the same values gram_entry gives, without its scattered reads
-    const int ne = p.NT * (p.NT + 1) / 2 * 64;
-    constexpr int kU = 8;  // loads in flight per thread
-    for (int e0 = threadIdx.x; e0 < ne; e0 += kU * kThreads) {
-      double v[kU];
+    // read the packed tiles linearly, 16 bytes per load (two columns of one tile row) and eight
+    // loads in flight per thread, and place each upper element at (i, j) and (j, i): the same
+    // values gram_entry gives, without its scattered reads.  A thread's pair index e2 walks the
+    // tiles in order, so its tile column follows from the previous one (no sqrt per element).
+    const int ne2 = p.NT * (p.NT + 1) / 2 * 32;  // element pairs
+    constexpr int kU = 8;
+    // (the oblique plain Gram follows the B-Gram and ||Q||_F^2: 8-byte aligned only)
+    const bool al16 = (reinterpret_cast<uintptr_t>(tiles) & 15) == 0;
+    int TJ = 0, tbase = 0;  // tile column of the current tile and index of its first tile
+    for (int e0 = threadIdx.x; e0 < ne2; e0 += kU * kThreads) {
+      double2 v[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        const int e = e0 + u * kThreads;
-        v[u] = e < ne ? tiles[e] : 0.0;
+        const int e2 = e0 + u * kThreads;
+        if (e2 >= ne2) v[u] = make_double2(0.0, 0.0);
+        else if (al16) v[u] = reinterpret_cast<const double2*>(tiles)[e2];
+        else v[u] = make_double2(tiles[2 * e2], tiles[2 * e2 + 1]);
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        const int e = e0 + u * kThreads;
-        if (e >= ne) continue;
-        const int tile = e >> 6, r = (e >> 3) & 7, c = e & 7;
-        const int TJ = tile_col(tile), TI = tile - TJ * (TJ + 1) / 2;
-        if (TI == TJ && r > c) continue;  // a diagonal tile's upper half serves both triangles
-        const int i = 8 * TI + r, j = 8 * TJ + c;
-        if (i < n && j < n) {
-          W[i * ldw + j] = v[u];
-          W[j * ldw + i] = v[u];
+        const int e2 = e0 + u * kThreads;
+        if (e2 >= ne2) continue;
+        const int tile = e2 >> 5, r = (e2 >> 2) & 7, c = 2 * (e2 & 3);
+        while (tbase + TJ + 1 <= tile) tbase += ++TJ;  // tiles only grow along a thread's walk
+        const int TI = tile - tbase;
+        const int i = 8 * TI + r, j0 = 8 * TJ + c;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int j = j0 + h;
+          const double x = h ? v[u].y : v[u].x;
+          if (TI == TJ && r > c + h) continue;  // a diagonal tile's upper half serves both triangles
+          if (i < n && j < n) {
+            W[i * ldw + j] = x;
+            W[j * ldw + i] = x;
+            if (i == j) {
+              tr += x;
+              dv = fma(x - 1.0, x - 1.0, dv);
+            } else {
+              dv = fma(2.0 * x, x, dv);
+            }
+          }
         }
       }
     }
   }
+  if (acc_dev) *acc_dev = dv;
+  if (acc_tr) *acc_tr = tr;
   __syncthreads();
 }
 
@@ -308,9 +333,161 @@ __device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool ad
     if (kb == kPanel) diag_block_t(k0, kb, std::integral_constant<bool, true>{});
     else diag_block_t(k0, kb, std::integral_constant<bool, false>{});
   };
-  // n a multiple of 8: look-ahead -- block k+1's diagonal factorisation runs on thread 0 while
-  // the other warps finish panel k's trailing update (its tile is updated first)
-  const bool lookahead = (n & 7) == 0 && n >= 128;  // (measured: no gain below n = 128)
+  // (b) rows k0..k0+7 of R~ right of the diagonal block: forward substitution per column, for
+  // the columns jj = start, start + stride, ... (full 8-column panel)
+  auto panel_rows = [&](int k0, int start, int stride) {
+    const int ncols = n - k0 - kPanel;
+    for (int jj = start; jj < ncols; jj += stride) {
+      const int j = k0 + kPanel + jj;
+      double w[kPanel];
+#pragma unroll
+      for (int r = 0; r < kPanel; ++r) w[r] = W[(k0 + r) * ldw + j];
+#pragma unroll
+      for (int r = 0; r < kPanel; ++r) {
+        const double v = w[r] * rinv[r];
+        w[r] = v;
+#pragma unroll
+        for (int l = r + 1; l < kPanel; ++l) w[l] = fma(-W[(k0 + r) * ldw + k0 + l], v, w[l]);
+      }
+#pragma unroll
+      for (int r = 0; r < kPanel; ++r) W[(k0 + r) * ldw + j] = w[r];
+    }
+  };
+  // n a multiple of 8: one barrier per panel.  While warps 1..7 apply panel k's rank-8 update to
+  // the trailing tiles below the next row block, warp 0 updates that row block (tiles (k+1, J)),
+  // lane 0 factors its diagonal block, and the warp's lanes form its rows of R~ -- so panel k+1
+  // is complete when the barrier releases the update by panel k+1.  (Same operations in the
+  // same order on every entry as the three-barrier form below.)
+  if ((n & 7) == 0) {
+    if (tid == 0) diag_block(0, kPanel);
+    __syncthreads();
+    if (*sflag) {
+      *pv_out = *sval;
+      return *sflag;
+    }
+    panel_rows(0, tid, kThreads);
+    __syncthreads();
+    const int g = lane >> 2, t = lane & 3;
+    long long ph[4] = {0, 0, 0, 0}, tq = 0;  // diagnostics (warp 0: diag tile + block, rows; warp 1: row block; warp 2: update)
+    // roles per panel (warp w runs on SM sub-partition w % 4): warp 0 (alone on sub-partition 0
+    // with the idle warp 4, so no tensor-core work delays its pivot chain) updates the next
+    // diagonal tile and lane 0 factors it; warp 1 updates the rest of the next row block; warps
+    // 0, 1, 4 then form that row block's rows of R~; warps 2, 3, 5, 6, 7 update the other tiles
+    auto update_tile = [&](int k0, int base, int I, int J) {  // C_IJ -= P_I^T P_J (trailing coords)
+      double* cp = W + (base + 8 * I + g) * ldw + base + 8 * J + 2 * t;
+      double c0 = cp[0], c1 = cp[1], a[2], b[2];
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2) {
+        const double* pr = W + (k0 + t + 4 * s2) * ldw + base;
+        a[s2] = pr[8 * I + g];
+        b[s2] = -pr[8 * J + g];
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2) dmma(c0, c1, a[s2], b[s2]);
+      cp[0] = c0;
+      cp[1] = c1;
+    };
+    for (int k0 = 0; k0 + kPanel < n; k0 += kPanel) {
+      const int base = k0 + kPanel, TL = (n - base) >> 3;
+      tq = clock64();
+      if (warp == 0 || warp == 1 || warp == 4) {
+        if (warp == 0) {
+          update_tile(k0, base, 0, 0);
+          __syncwarp();
+          if (lane == 0) diag_block(base, kPanel);
+          __syncwarp();
+        } else if (warp == 1) {
+          // row block tiles (0, J), J >= 1: 4 in flight
+          double a[2];
+#pragma unroll
+          for (int s2 = 0; s2 < 2; ++s2) a[s2] = W[(k0 + t + 4 * s2) * ldw + base + g];
+          for (int J0 = 1; J0 < TL; J0 += 4) {
+            double c0[4], c1[4], b[4][2];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int J = min(J0 + u, TL - 1);
+              const double* cp = W + (base + g) * ldw + base + 8 * J + 2 * t;
+              c0[u] = cp[0];
+              c1[u] = cp[1];
+#pragma unroll
+              for (int s2 = 0; s2 < 2; ++s2) b[u][s2] = -W[(k0 + t + 4 * s2) * ldw + base + 8 * J + g];
+            }
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+              for (int u = 0; u < 4; ++u) dmma(c0[u], c1[u], a[s2], b[u][s2]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (J0 + u < TL) {
+                double* cp = W + (base + g) * ldw + base + 8 * (J0 + u) + 2 * t;
+                cp[0] = c0[u];
+                cp[1] = c1[u];
+              }
+            }
+          }
+        }
+        asm volatile("bar.sync 1, 96;" ::: "memory");  // warps 0, 1, 4: the row block is updated
+        if (warp == 0) ph[0] += clock64() - tq;
+        if (warp == 1) ph[1] += clock64() - tq;
+        tq = clock64();
+        if (!*sflag) panel_rows(base, warp == 0 ? lane : warp == 1 ? 32 + lane : 64 + lane, 96);
+        if (warp == 0) ph[2] += clock64() - tq;
+      } else {
+        // the other trailing tiles (I, J), 1 <= I <= J < TL, J-major; 4 in flight per warp
+        constexpr int kU = 4, kW = 5;
+        const int wi = warp < 4 ? warp - 2 : warp - 3;  // 2, 3, 5, 6, 7 -> 0..4
+        const int ntiles = TL * (TL - 1) / 2;
+        int J = 1, cum = 0;  // tiles of columns < J: cum = J(J-1)/2
+        for (int tau0 = wi; tau0 < ntiles; tau0 += kU * kW) {
+          double c0[kU], c1[kU], a[kU][2], b[kU][2];
+          int off[kU];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int tau = min(tau0 + u * kW, ntiles - 1);
+            while (cum + J <= tau) cum += J++;
+            const int I = 1 + tau - cum;
+            off[u] = (base + 8 * I + g) * ldw + base + 8 * J + 2 * t;
+            c0[u] = W[off[u]];
+            c1[u] = W[off[u] + 1];
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+              const double* pr = W + (k0 + t + 4 * s2) * ldw + base;
+              a[u][s2] = pr[8 * I + g];
+              b[u][s2] = -pr[8 * J + g];
+            }
+          }
+#pragma unroll
+          for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+            for (int u = 0; u < kU; ++u) dmma(c0[u], c1[u], a[u][s2], b[u][s2]);
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            if (tau0 + u * kW < ntiles) {
+              W[off[u]] = c0[u];
+              W[off[u] + 1] = c1[u];
+            }
+          }
+        }
+        if (warp == 2) ph[3] += clock64() - tq;
+      }
+      __syncthreads();
+      if (*sflag) {
+        *pv_out = *sval;
+        return *sflag;
+      }
+    }
+    __shared__ long long sph[4];
+    if (threadIdx.x == 0) { sph[0] = ph[0]; sph[2] = ph[2]; }
+    if (threadIdx.x == 32) sph[1] = ph[1];
+    if (threadIdx.x == 64) sph[3] = ph[3];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      g_phase[0] = sph[0] + (sph[1] << 32);
+      g_phase[1] = sph[3] + (sph[2] << 32);
+    }
+    return 0;
+  }
+  const bool lookahead = false;
   for (int k0 = 0; k0 < n; k0 += kPanel) {
     const int kb = min(kPanel, n - k0);
     t0 = clock64();
@@ -455,40 +632,80 @@ __device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool ad
   return 0;
 }
 
-__device__ __forceinline__ double rpad(const double* W, int ldw, int n, int i, int j) {
-  if (i < n && j < n) return i <= j ? W[i * ldw + j] : 0.0;
-  return i == j ? 1.0 : 0.0;
+
+// Upper-triangular entry (i, j) of R~ padded with the identity past n, read without a branch:
+// the (clamped) load is unconditional and the select comes after it, so a loop can keep all its
+// loads in flight (a load inside a branch serialises on its latency).
+__device__ __forceinline__ double rload(const double* W, int ldw, int n, int i, int j) {
+  const int ic = i < n ? i : n - 1, jc = j < n ? j : n - 1;
+  const double x = W[ic * ldw + jc];
+  return (i < n && j < n) ? (i <= j ? x : 0.0) : (i == j ? 1.0 : 0.0);
 }
 
 // TRSM layout (trsm.cu): B fragments of -R~ and scaled diagonal blocks; R~ (column-major) for trmul.
+// Latency-bound on one CTA: each thread walks a flat index with kU independent reads in flight
+// before its (coalesced) global stores.
 template <bool SMEM>
 __device__ __noinline__ void write_outputs(const double* Wg, int ldw, int n, int NT, double* bfrag,
                                               double* dblk, double* Rt) {
   extern __shared__ double smdyn[];
   const double* W = SMEM ? smdyn : Wg;
-  const int nf = NT * (NT - 1) * 32;
-  for (int idx = threadIdx.x; idx < nf; idx += kThreads) {
-    const int f = idx >> 5, lane = idx & 31;
-    // target block J of fragment f: the largest J with J(J-1) <= f
-    int J = static_cast<int>((1.0f + sqrtf(1.0f + 4.0f * f)) * 0.5f);
-    while (J * (J - 1) > f) --J;
-    while ((J + 1) * J <= f) ++J;
-    const int s = f - J * (J - 1);
-    const int g = lane >> 2, t = lane & 3;
-    bfrag[idx] = -rpad(W, ldw, n, 8 * (s >> 1) + 2 * t + (s & 1), 8 * J + g);
+  constexpr int kU = 8;
+  const int nf = NT * (NT - 1) * 32;  // fragment f = idx / 32: target block J >= 1, k-step s < 2J
+#ifdef SCQR3_CHOL_OUTCLK
+  long long o0 = clock64();
+#endif
+  for (int i0 = threadIdx.x; i0 < nf; i0 += kU * kThreads) {
+    double v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int idx = min(i0 + u * kThreads, nf - 1);
+      const int f = idx >> 5, lane = idx & 31;
+      int J = static_cast<int>((1.0f + sqrtf(1.0f + 4.0f * f)) * 0.5f);  // largest J with J(J-1) <= f
+      J -= J * (J - 1) > f ? 1 : 0;
+      J += (J + 1) * J <= f ? 1 : 0;
+      const int s = f - J * (J - 1);
+      v[u] = -rload(W, ldw, n, 8 * (s >> 1) + 2 * (lane & 3) + (s & 1), 8 * J + (lane >> 2));
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (i0 + u * kThreads < nf) bfrag[i0 + u * kThreads] = v[u];
   }
+#ifdef SCQR3_CHOL_OUTCLK
+  long long o1 = clock64();
+#endif
   for (int idx = threadIdx.x; idx < NT * 72; idx += kThreads) {
     const int J = idx / 72, w = idx % 72;
-    if (w < 64) {
-      const int c = 8 * J + (w >> 3), j = 8 * J + (w & 7);
-      dblk[idx] = j > c ? rpad(W, ldw, n, c, j) / rpad(W, ldw, n, c, c) : 0.0;
-    } else {
-      dblk[idx] = 1.0 / rpad(W, ldw, n, 8 * J + (w - 64), 8 * J + (w - 64));
+    const int c = 8 * J + (w < 64 ? (w >> 3) : w - 64), j = 8 * J + (w < 64 ? (w & 7) : w - 64);
+    const double rcj = rload(W, ldw, n, c, j), rcc = rload(W, ldw, n, c, c);
+    dblk[idx] = w < 64 ? (j > c ? rcj / rcc : 0.0) : 1.0 / rcc;
+  }
+#ifdef SCQR3_CHOL_OUTCLK
+  long long o2 = clock64();
+#endif
+  if (Rt) {
+    const int nn = n * n;
+    for (int i0 = threadIdx.x; i0 < nn; i0 += kU * kThreads) {
+      double v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int idx = min(i0 + u * kThreads, nn - 1);
+        const int i = idx % n, j = idx / n;
+        const double x = W[i * ldw + j];
+        v[u] = i <= j ? x : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (i0 + u * kThreads < nn) Rt[i0 + u * kThreads] = v[u];
     }
   }
-  if (Rt)
-    for (int j = threadIdx.x >> 5; j < n; j += kThreads / 32)
-      for (int i = threadIdx.x & 31; i < n; i += 32) Rt[i + static_cast<size_t>(j) * n] = i <= j ? W[i * ldw + j] : 0.0;
+#ifdef SCQR3_CHOL_OUTCLK
+  long long o3 = clock64();
+  if (threadIdx.x == 0) {
+    g_phase[0] = (o1 - o0) + ((o2 - o1) << 32);
+    g_phase[1] = o3 - o2;
+  }
+#endif
 }
 
 template <bool SMEM>
@@ -507,7 +724,8 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
   long long clk[8] = {};
   clk[0] = clock64();
   if (tid == 0) sflag = 0;
-  load_W(p, W, ldw);
+  double loc = 0.0, tr = 0.0;  // a7 input: ||A - I||_F^2 and trace(A) shares (stop test, reading D6)
+  load_W(p, W, ldw, nullptr, &loc, &tr);
   clk[1] = clock64();
 
   if (p.mode == CHOL_ONLY) {
@@ -527,14 +745,6 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
     return;
   }
 
-  // ---- a7 input: distance of the Gram from I (stop test, reading D6) and its trace
-  double loc = 0.0, tr = 0.0;
-  for (int i = tid >> 5; i < n; i += kThreads / 32)
-    for (int j = tid & 31; j < n; j += 32) {
-      const double v = W[i * ldw + j] - (i == j ? 1.0 : 0.0);
-      loc = fma(v, v, loc);
-      if (i == j) tr += W[i * ldw + j];
-    }
   const double2 dt = block_sum2(loc, tr, red);
   const double dev = sqrt(dt.x), trace = dt.y;
   clk[2] = clock64();
@@ -552,9 +762,7 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
         volatile DevStatus* h = p.st_host;
         h->pass = st.pass;
         h->dev_F = st.dev_F;
-        __threadfence_system();
         h->code = st.code;
-        __threadfence_system();
       }
     }
     return;
@@ -647,6 +855,9 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
       if (st.code != SCQR3_OK) *(volatile int*)p.last_pass = pass - 1;
       else if (st.stop) *(volatile int*)p.last_pass = pass;
     }
+    // (host-mapped status slot: the host reads it only after an event recorded behind this
+    // kernel has completed, which orders these writes -- no system-scope fence, which cost
+    // ~6 us per pass)
     if (p.st_host) {
       volatile DevStatus* h = p.st_host + (p.mode == CHOL_PASS ? pass - 1 : 0);
       h->stop = st.stop;
@@ -657,9 +868,7 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
       h->pivot_value = st.pivot_value;
       h->norm2_est = st.norm2_est;
       h->dev_F = st.dev_F;
-      __threadfence_system();
       h->code = st.code;
-      __threadfence_system();
     }
   }
 }

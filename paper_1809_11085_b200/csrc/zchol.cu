@@ -156,9 +156,7 @@ __global__ void __launch_bounds__(kZThreads, 1) zchol_kernel(ZCholParams p) {
       h->pivot_value = st.pivot_value;
       h->norm2_est = st.norm2_est;
       h->dev_F = st.dev_F;
-      __threadfence_system();
       h->code = st.code;
-      __threadfence_system();
     }
   };
   if (pass == 1 && !isfinite(trace)) {  // NaN / Inf in X
