@@ -143,7 +143,7 @@ __device__ __forceinline__ void load_W(const CholParams& p, double* W, int ldw, 
 // (SMEM: W is the dynamic shared-memory array -- addressed as such so loads are LDS.)
 template <bool SMEM>
 __device__ __noinline__ double power_lmax(const double* Wg, int ldw, int n, int iters, double trace,
-                                          double (*ybuf)[kMaxN], double* red) {
+                                          double (*ybuf)[kMaxN + 64], double* red) {
   extern __shared__ double smdyn[];
   const double* W = SMEM ? smdyn : Wg;
   if (!(trace > 0.0) || !isfinite(trace)) return 0.0;
@@ -199,28 +199,34 @@ __device__ __noinline__ double power_lmax(const double* Wg, int ldw, int n, int 
 }
 
 // n <= 128 (W in shared memory): the same iteration with this thread's share of W -- row
-// tid / TPR, columns part + TPR * k, k < CPP -- held in registers for all iterations, so an
-// iteration reads only y (the TPR parts of a warp read TPR consecutive entries: one wavefront).  Shared-memory traffic bounded the version above
-// (64 W loads + 64 y loads per thread and iteration at n = 128).  TPR threads per row as above
-// (the largest power of two <= 32 with TPR * n <= 256); CPP >= ceil(n / TPR) a compile-time
-// power of two, so the iteration has no branches; columns past n carry zeros.
+// tid / TPR, the CPP contiguous columns part * CPP + k -- held in registers for all iterations,
+// so an iteration reads only y: 16-byte loads of consecutive y entries, the TPR parts of a warp
+// on different banks (y stored with 2 doubles of skew per part), i.e. one wavefront per load
+// (shared-memory wavefronts of the y reads bound the iteration: ~750 cycles with 8-byte loads of
+// strided columns at n = 128).  TPR threads per row (the largest power of two <= 32 with
+// TPR * n <= 256); CPP >= ceil(n / TPR) a compile-time power of two, so the iteration has no
+// branches; columns past n carry zeros.
 template <int TPR, int CPP>
-__device__ __noinline__ double power_lmax_reg(int ldw, int n, int iters, double trace, double (*ybuf)[kMaxN],
+__device__ __noinline__ double power_lmax_reg(int ldw, int n, int iters, double trace, double (*ybuf)[kMaxN + 64],
                                               double* red) {
   extern __shared__ double smdyn[];
   const double* W = smdyn;
   if (!(trace > 0.0) || !isfinite(trace)) return 0.0;
   const double sc = ldexp(1.0, -(ilogb(trace) + 1));
   const int tid = threadIdx.x, part = tid % TPR, row = tid / TPR;
+  constexpr int kSkew = CPP >= 2 ? 2 : 0;
+  auto yix = [](int j) { return j + kSkew * (j / CPP); };  // skewed position of y_j
   double w[CPP];
+  const int rc = row < n ? row : n - 1;
 #pragma unroll
-  for (int k = 0; k < CPP; ++k) {
-    const int j = part + TPR * k;
-    w[k] = (j < n && row < n) ? W[j * ldw + row] : 0.0;
+  for (int k = 0; k < CPP; ++k) {  // (clamped unconditional loads: no branch per element)
+    const int j = part * CPP + k;
+    const double x = W[(j < n ? j : n - 1) * ldw + rc];
+    w[k] = (j < n && row < n) ? x : 0.0;
   }
   for (int i = tid; i < TPR * CPP; i += kThreads) {  // y past n stays 0
-    ybuf[0][i] = i < n ? 1.0 : 0.0;
-    ybuf[1][i] = 0.0;
+    ybuf[0][yix(i)] = i < n ? 1.0 : 0.0;
+    ybuf[1][yix(i)] = 0.0;
   }
   __syncthreads();
   auto rowdot = [&](const double* y) -> double {
@@ -228,8 +234,18 @@ __device__ __noinline__ double power_lmax_reg(int ldw, int n, int iters, double 
     double a[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) a[c] = 0.0;
+    const double* yp = y + part * (CPP + kSkew);
+    if constexpr (CPP >= 2) {
 #pragma unroll
-    for (int k = 0; k < CPP; ++k) a[k % NC] = fma(w[k], y[part + TPR * k], a[k % NC]);
+      for (int k = 0; k < CPP; k += 2) {
+        const double2 yy = *reinterpret_cast<const double2*>(yp + k);
+        a[k % NC] = fma(w[k], yy.x, a[k % NC]);
+        a[(k + 1) % NC] = fma(w[k + 1], yy.y, a[(k + 1) % NC]);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < CPP; ++k) a[k % NC] = fma(w[k], yp[k], a[k % NC]);
+    }
     double acc = a[0];
 #pragma unroll
     for (int c = 1; c < NC; ++c) acc += a[c];
@@ -240,14 +256,14 @@ __device__ __noinline__ double power_lmax_reg(int ldw, int n, int iters, double 
   int cur = 0;
   for (int it = 0; it < iters; ++it) {
     const double acc = rowdot(ybuf[cur]);
-    if (part == 0 && row < n) ybuf[cur ^ 1][row] = acc * sc;
+    if (part == 0 && row < n) ybuf[cur ^ 1][yix(row)] = acc * sc;
     __syncthreads();
     cur ^= 1;
   }
   double num = 0.0, den = 0.0;
   const double acc = rowdot(ybuf[cur]);
   if (part == 0 && row < n) {
-    const double y = ybuf[cur][row];
+    const double y = ybuf[cur][yix(row)];
     num = fma(y, acc, num);
     den = fma(y, y, den);
   }
@@ -257,7 +273,7 @@ __device__ __noinline__ double power_lmax_reg(int ldw, int n, int iters, double 
 
 // lambda_max estimate of the n x n Gram in W (reading D2): register version for n <= 128
 template <bool SMEM>
-__device__ double power_lmax_any(const double* W, int ldw, int n, int iters, double trace, double (*ybuf)[kMaxN],
+__device__ double power_lmax_any(const double* W, int ldw, int n, int iters, double trace, double (*ybuf)[kMaxN + 64],
                                  double* red) {
   if (SMEM && n <= 128) {
     if (n > 64) return power_lmax_reg<2, 64>(ldw, n, iters, trace, ybuf, red);
@@ -714,7 +730,7 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
   const int pass = p.pass_dev ? *(volatile const int*)p.pass_dev : p.pass;
   if (p.last_pass && pass > *(volatile const int*)p.last_pass) return;  // a pass after the stop
   __shared__ double red[64];
-  __shared__ double ybuf[2][kMaxN];
+  __shared__ __align__(16) double ybuf[2][kMaxN + 64];
   __shared__ double rinv[kPanel];
   __shared__ int sflag;
   __shared__ double sval;
