@@ -833,7 +833,7 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
       CUtensorMap mx;
       const bool use_tma = L.NT <= 16 || L.NT >= 24;
       // (NT >= 24: the map of the first 128 columns, for the split TRSM)
-      if (use_tma) TRY(encode_map(c, &mx, src, m, L.NT >= 24 ? 128 : n, ldsrc, L.NT >= 24 ? 128 : L.npad));
+      if (use_tma) TRY(encode_map(c, &mx, src, m, L.NT >= 24 ? 128 : n, ldsrc, trsm_x_box_cols(L.NT)));
       CUtensorMap mq;  // fused TRSM + Gram: bulk stores of Q
       if (fuse_tg) TRY(encode_map(c, &mq, Q, m, n, ldq, L.npad));
       const int pt = prof_begin(c, PK_TRSM);
@@ -1097,7 +1097,7 @@ int zfactor_impl(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, i
     if (m > 0) {
       CUtensorMap mx;
       const bool use_tma = L.NT <= 16 || L.NT >= 24;
-      if (use_tma) TRY(encode_map(c, &mx, S, m, L.NT >= 24 ? 128 : n2, Z.lds, L.NT >= 24 ? 128 : L.npad));
+      if (use_tma) TRY(encode_map(c, &mx, S, m, L.NT >= 24 ? 128 : n2, Z.lds, trsm_x_box_cols(L.NT)));
       const int pt = prof_begin(c, PK_TRSM);
       // (in place on the split matrix: the bulk stores of Q use the same descriptor)
       CUDA_TRY(launch_trsm(tp, use_tma ? &mx : nullptr, c->num_sms, st, &fused_chunks,
@@ -1375,7 +1375,7 @@ int scqr3_trsm(int64_t m, int64_t n, const double* X, int64_t ld, const double* 
   if (m > 0) {
     CUtensorMap mx;
     const bool use_tma = L.NT <= 16 || L.NT >= 24;
-    if (use_tma) TRY(encode_map(c, &mx, X, m, L.NT >= 24 ? 128 : n, ld, L.NT >= 24 ? 128 : L.npad));
+    if (use_tma) TRY(encode_map(c, &mx, X, m, L.NT >= 24 ? 128 : n, ld, trsm_x_box_cols(L.NT)));
     CUDA_TRY(launch_trsm(tp, use_tma ? &mx : nullptr, c->num_sms, st));
     ++g_launches;
   }

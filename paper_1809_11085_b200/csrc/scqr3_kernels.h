@@ -219,6 +219,9 @@ inline cudaError_t cached_launch_cfg(LaunchCfgCache& cc, K kernel, size_t smem, 
 cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream,
                         int* grid_out = nullptr, const CUtensorMap* mapQ = nullptr);
 inline bool trsm_fuses_gram(int NT) { return NT <= 8; }
+// width of the TMA box of X the TRSM launcher expects (the map of the first 128 columns for
+// NT >= 24; a narrower box where the kernel reads the later columns from global memory)
+int trsm_x_box_cols(int NT);
 
 inline int npad_for(int n) {
   // tile counts with a compiled TRSM instance

@@ -30,9 +30,6 @@ namespace scqr3 {
 #ifndef SCQR3_TRSM_PIPE
 #define SCQR3_TRSM_PIPE 1  // 0: both k-steps of each later target back to back (A/B builds)
 #endif
-#ifndef SCQR3_TRSM_RED_FROM
-#define SCQR3_TRSM_RED_FROM 1000  // first column block solved in the full-row form (A even)
-#endif
 
 // GRAM (n <= 64): also accumulate the next pass's Gram Q_k^T Q_k from the
 // solved rows, so the next pass does not read Q from HBM again.  Each warp writes its 16 finished
@@ -106,11 +103,6 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
     issue(rg0);
   }
 
-#ifdef SCQR3_TRSM_STAGGER_NS
-  // (experiment) offset the two warps of each SM sub-partition (w, w + 4) by part of a row
-  // group, so that one warp's DMMA-dense head meets the other's latency-bound tail
-  if (warp >= 4) __nanosleep(SCQR3_TRSM_STAGGER_NS);
-#endif
   double gacc[GRAM ? NTS : 1][2];  // GRAM: this warp's Gram tiles (C fragments)
 #pragma unroll
   for (int T = 0; T < (GRAM ? NTS : 1); ++T) gacc[T][0] = gacc[T][1] = 0.0;
@@ -227,65 +219,6 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
 #endif
       };
       if constexpr (A % 2 == 0) {
-       if (J >= SCQR3_TRSM_RED_FROM) {
-        // Full-row solve (late blocks, whose few later updates cannot hide a shuffle per step):
-        // lanes t = 0,1 both hold all 8 columns of row g, lanes t = 2,3 those of row g+8, so the
-        // pivot of every step is local and the chain is one DFMA per step instead of a shuffle
-        // plus a DFMA (28 DFMA per lane and block instead of 18; same operations in the same
-        // order on every value, so the same rounding as the split form below).
-        const bool lo = t < 2;
-        const int qb = lane & ~3;
-        double v[A / 2][8];
-#pragma unroll
-        for (int b = 0; b < A / 2; ++b)
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const double x0 = __shfl_sync(0xffffffffu, q[2 * b][J][h], qb | e);
-              const double x1 = __shfl_sync(0xffffffffu, q[2 * b + 1][J][h], qb | e);
-              v[b][2 * e + h] = lo ? x0 : x1;
-            }
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          if (c < 7) {
-            double r[8];
-#pragma unroll
-            for (int k = 2 * ((c + 1) / 2); k < 8; k += 2) {
-              const double2 rr = *reinterpret_cast<const double2*>(D + c * 8 + k);
-              r[k] = rr.x;
-              r[k + 1] = rr.y;
-            }
-#pragma unroll
-            for (int b = 0; b < A / 2; ++b)
-#pragma unroll
-              for (int j = c + 1; j < 8; ++j) v[b][j] = fma(-v[b][c], r[j], v[b][j]);
-          }
-          later_updates(c);
-        }
-        double ri[8];
-#pragma unroll
-        for (int k = 0; k < 8; k += 2) {
-          const double2 rr = *reinterpret_cast<const double2*>(D + 64 + k);
-          ri[k] = rr.x;
-          ri[k + 1] = rr.y;
-        }
-        const bool t1 = t & 1, t2 = t & 2;
-#pragma unroll
-        for (int b = 0; b < A / 2; ++b) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) v[b][j] *= ri[j];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            // own row's column 2t+h, and for the other half the column 2(t^2)+h of this row
-            const double own = t2 ? (t1 ? v[b][6 + h] : v[b][4 + h]) : (t1 ? v[b][2 + h] : v[b][h]);
-            const double snd = t2 ? (t1 ? v[b][2 + h] : v[b][h]) : (t1 ? v[b][6 + h] : v[b][4 + h]);
-            const double oth = __shfl_xor_sync(0xffffffffu, snd, 2);
-            q[2 * b][J][h] = lo ? own : oth;
-            q[2 * b + 1][J][h] = lo ? oth : own;
-          }
-        }
-       } else {
         // Fragment pairs (a, a+1) = rows g and g+8 of the quad.  Lanes t^2 swap halves so that
         // lanes t = 0,1 hold row g and lanes t = 2,3 row g+8, four columns each: lane u = t&1
         // holds columns {2u, 2u+1, 2u+4, 2u+5} (V[0..3]).  Step c then updates only the
@@ -341,7 +274,6 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
             q[a + 1][J][h] = lo ? rcv : Vb[2 + h];
           }
         }
-       }
       } else {
         // (odd A: inside each quad, lane t holds columns 2t, 2t+1 of its row)
 #pragma unroll
@@ -771,6 +703,9 @@ static cudaError_t launch_wide(const TrsmParams& p, int num_sms, cudaStream_t st
   return cudaGetLastError();
 }
 
+// Width of the TMA box of X that launch_trsm expects for NT column tiles (host: encode_map).
+int trsm_x_box_cols(int NT) { return NT >= 24 ? 128 : NT * 8; }
+
 // map: TMA descriptor of X with a {16 rows, npad columns} SWIZZLE_128B box (instances with
 // NT <= 16 use it when map != nullptr; NT >= 24: a {16, 128} box of the first 128 columns); the
 // others read X with plain coalesced loads.
@@ -798,15 +733,8 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
                        : launch_one<8, 4, true, 256, false>(p, nullptr, num_sms, stream);
     case 12: return tma ? launch_one<12, 2, true, 256, true>(p, map, num_sms, stream)
                         : launch_one<12, 2, true, 256, false>(p, nullptr, num_sms, stream);
-#ifndef SCQR3_TRSM16_THREADS
-#define SCQR3_TRSM16_THREADS 256
-#endif
-#ifdef SCQR3_TRSM16_A1
-    case 16: return launch_one<16, 1, true, SCQR3_TRSM16_A1, false>(p, nullptr, num_sms, stream);
-#else
-    case 16: return tma ? launch_one<16, 2, true, SCQR3_TRSM16_THREADS, true>(p, map, num_sms, stream)
+    case 16: return tma ? launch_one<16, 2, true, 256, true>(p, map, num_sms, stream)
                         : launch_one<16, 2, true, 256, false>(p, nullptr, num_sms, stream);
-#endif
     case 24: {
       // split as for NT = 32: columns 0..127, then targets 16..23 (A = 2)
       if (!map) return launch_one<24, 1, true, 256, false>(p, nullptr, num_sms, stream);
