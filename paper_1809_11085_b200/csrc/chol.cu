@@ -412,6 +412,7 @@ __device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool ad
           __syncwarp();
           if (lane == 0) diag_block(base, kPanel);
           __syncwarp();
+          ph[2] += clock64() - tq;  // (diagnostics: diagonal tile + block, before the wait)
         } else if (warp == 1) {
           // row block tiles (0, J), J >= 1: 4 in flight
           double a[2];
@@ -447,7 +448,6 @@ __device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool ad
         if (warp == 1) ph[1] += clock64() - tq;
         tq = clock64();
         if (!*sflag) panel_rows(base, warp == 0 ? lane : warp == 1 ? 32 + lane : 64 + lane, 96);
-        if (warp == 0) ph[2] += clock64() - tq;
       } else {
         // the other trailing tiles (I, J), 1 <= I <= J < TL, J-major; 4 in flight per warp
         constexpr int kU = 4, kW = 5;
@@ -735,7 +735,7 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
   __shared__ int sflag;
   __shared__ double sval;
   const int n = p.n, tid = threadIdx.x;
-  const int ldw = n + 1;
+  const int ldw = chol_ldw(n);
   double* W = SMEM ? smW : p.W;
   long long clk[8] = {};
   clk[0] = clock64();

@@ -208,7 +208,7 @@ Layout make_layout(int64_t m, int64_t n, int oblique, int64_t halo = 1) {
   L.st = take(sizeof(DevStatus));
   L.partials = take(static_cast<size_t>(L.max_chunks) * L.tiles_part * 64 * 8);
   L.tiles = take(static_cast<size_t>(L.tiles_sym * 64 * (oblique ? 2 : 1) + 64) * 8);
-  L.W = take(static_cast<size_t>(n) * (n + 1) * 8);
+  L.W = take(static_cast<size_t>(n) * chol_ldw(static_cast<int>(n)) * 8);
   L.Rnew = take(static_cast<size_t>(n) * n * 8);
   L.Rt = take(static_cast<size_t>(n) * n * 8);
   L.bfrag = take(static_cast<size_t>(L.NT) * (L.NT - 1) * 32 * 8 + 8);
@@ -463,7 +463,7 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
 
 int launch_chol(const CholParams& p, cudaStream_t st) {
   if (p.w_in_smem) {
-    const size_t smem = static_cast<size_t>(p.n) * (p.n + 1) * 8;
+    const size_t smem = static_cast<size_t>(p.n) * chol_ldw(p.n) * 8;
     static thread_local LaunchCfgCache chol_cfg;
     CUDA_TRY(cached_launch_cfg(chol_cfg, chol_kernel_smem, smem, 256, nullptr));
     chol_kernel_smem<<<1, 256, smem, st>>>(p);
@@ -493,7 +493,7 @@ int launch_trmul(Ctx* c, const double* Rt, double* R, double* Rnew, int n, int f
   return SCQR3_OK;
 }
 
-bool w_fits_smem(int n) { return static_cast<size_t>(n) * (n + 1) * 8 <= 200 * 1024; }
+bool w_fits_smem(int n) { return static_cast<size_t>(n) * chol_ldw(n) * 8 <= 200 * 1024; }
 
 // ---- CUDA-graph pass loop (device-side pass control)
 // SCQR3_GRAPH=0 selects the host-driven loop for single-GPU calls too (A/B measurement).

@@ -86,6 +86,12 @@ struct ObliqueYParams {
 
 enum CholMode { CHOL_PASS = 0, CHOL_ONLY = 1 };
 
+// Leading dimension of the Cholesky kernel's working copy W (row-major n x n): n + 4 puts the
+// mma fragment loads of the panel rows (lanes t, g -> W[(k + t) * ldw + 8 I + g]) on 16 distinct
+// bank pairs per half-warp (n + 1 gave 4-way conflicts: the trailing update was bound by
+// shared-memory wavefronts).
+inline __host__ __device__ int chol_ldw(int n) { return n + 4; }
+
 struct CholParams {
   const double* tiles;       // packed upper tiles of the Gram (CHOL_PASS)
   const double* Afull;       // or a full column-major n x n matrix (CHOL_ONLY)
