@@ -226,6 +226,9 @@ def run_ours(args):
 
     rank, world, local = dist_env()
     multi = world > 1 or args.force_comm
+    if multi and "RANK" not in os.environ:  # --force-comm without a launcher: a one-rank group
+        os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                          MASTER_PORT=os.environ.get("MASTER_PORT", "29541"))
     if multi:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))

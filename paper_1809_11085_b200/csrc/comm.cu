@@ -160,6 +160,7 @@ int comm_destroy(Comm* c) {
   if (c->kind == COMM_NCCL) {
     if (c->nccl) ncclCommDestroy(c->nccl);
     if (c->dscratch) cudaFree(c->dscratch);
+    if (c->hscratch) cudaFreeHost(c->hscratch);
   } else {
     LoopGroup* g = c->lg;
     bool last = false;
@@ -193,10 +194,13 @@ void comm_abort(Comm* c, const char* why) {
 int comm_host_allreduce(Comm* c, int64_t v, int op, int64_t* out, cudaStream_t st) {
   if (c->kind == COMM_NCCL) {
     const ncclRedOp_t nop = op == COMM_SUM ? ncclSum : op == COMM_MIN ? ncclMin : ncclMax;
-    CTRY(cudaMemcpyAsync(c->dscratch, &v, 8, cudaMemcpyHostToDevice, st));
+    // (pinned staging: both copies stay asynchronous, one stream synchronisation in total)
+    c->hscratch[0] = v;
+    CTRY(cudaMemcpyAsync(c->dscratch, c->hscratch, 8, cudaMemcpyHostToDevice, st));
     NTRY(ncclAllReduce(c->dscratch, c->dscratch, 1, ncclInt64, nop, c->nccl, st));
-    CTRY(cudaMemcpyAsync(out, c->dscratch, 8, cudaMemcpyDeviceToHost, st));
+    CTRY(cudaMemcpyAsync(c->hscratch + 1, c->dscratch, 8, cudaMemcpyDeviceToHost, st));
     CTRY(cudaStreamSynchronize(st));
+    *out = c->hscratch[1];
     return SCQR3_OK;
   }
   LoopGroup* g = c->lg;

@@ -32,6 +32,7 @@ struct Comm {
   int rank = 0, nranks = 1;
   ncclComm_t nccl = nullptr;
   int64_t* dscratch = nullptr;  // NCCL: a few int64 of device scratch for host-level reductions
+  int64_t* hscratch = nullptr;  // NCCL: pinned host staging of those values (async copies)
   LoopGroup* lg = nullptr;      // LOOPBACK: shared by the group's ranks
 };
 

@@ -1401,14 +1401,17 @@ int scqr3_comm_init(void** comm_out, int32_t nranks, const void* id, int32_t ran
   c->kind = COMM_NCCL;
   c->rank = rank;
   c->nranks = nranks;
-  if (cudaMalloc(&c->dscratch, 64) != cudaSuccess) {
+  if (cudaMalloc(&c->dscratch, 64) != cudaSuccess ||
+      cudaHostAlloc(reinterpret_cast<void**>(&c->hscratch), 64, cudaHostAllocDefault) != cudaSuccess) {
     cudaGetLastError();
+    if (c->dscratch) cudaFree(c->dscratch);
     delete c;
-    return fail("cudaMalloc of the communicator scratch failed");
+    return fail("allocation of the communicator scratch failed");
   }
   ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, uid, rank);
   if (r != ncclSuccess) {
     cudaFree(c->dscratch);
+    cudaFreeHost(c->hscratch);
     delete c;
     return fail("ncclCommInitRank: %s", ncclGetErrorString(r));
   }
