@@ -42,6 +42,13 @@ __device__ __forceinline__ void gram_whole_jobs(const GramParams& p, const unsig
                                                 const uint32_t (&offB)[kJobTiles], const uint32_t (&inner)[4]) {
   const int lane = threadIdx.x & 31;
   const uint32_t lane_chunk = inner[0];  // chunk G << 4 plus the 8-byte half of this lane's k slot
+  auto release = [&](uint64_t* bar) {  // this stage consumed: in every CTA of the cluster (multicast)
+    if (p.mc > 1) {
+      for (int j = 0; j < p.mc; ++j) mbar_arrive_cluster(bar, static_cast<uint32_t>(j));
+    } else {
+      mbar_arrive(bar);
+    }
+  };
   auto frag = [&](uint32_t off) { return *reinterpret_cast<const double*>(stages + off); };
   auto stage_loop = [&](auto body) {
     int st = 0;
@@ -51,7 +58,7 @@ __device__ __forceinline__ void gram_whole_jobs(const GramParams& p, const unsig
       const uint32_t oA = static_cast<uint32_t>(st) * nsrc * stage_bytes;
       body(oA, b_from_y ? oA + stage_bytes : oA);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[st]);
+      if (lane == 0) release(&empty_bar[st]);
       if (++st == p.stages) {
         st = 0;
         ph ^= 1u;
@@ -144,20 +151,27 @@ __global__ void __launch_bounds__(32 * (MAXC + 1), 1)
   const long long s_end = (long long)p.total_stages * (chunk + 1) / p.chunks;
   const int nst = static_cast<int>(s_end - s_begin);
 
+  // multicast (p.mc > 1): the CTAs of a chunk form a cluster; every stage lands in all of them
+  // from one L2 read (each CTA issues 1 / mc of the stage's boxes to the whole cluster), and a
+  // stage is refilled only after the consumers of every CTA released it (remote arrivals)
+  const bool mc = p.mc > 1;
+  const uint32_t crank = mc ? cluster_ctarank() : 0;
   if (threadIdx.x == 0) {
     for (int i = 0; i < p.stages; ++i) {
       mbar_init(&full_bar[i], 1);
-      mbar_init(&empty_bar[i], ncons);
+      mbar_init(&empty_bar[i], ncons * (mc ? p.mc : 1));
     }
     fence_barrier_init();
   }
   __syncthreads();
+  if (mc) cluster_sync();  // every CTA's barriers are initialised before any remote use
 
   if (warp == 0) {
     // ---------------- producer: TMA stream of this chunk's rows
     if (lane == 0) {
       tma_prefetch_desc(&mapQ);
       if (full) tma_prefetch_desc(&mapY);
+      const uint16_t mask = static_cast<uint16_t>((1u << p.mc) - 1u);
       int st = 0;
       uint32_t ph = 0;
       for (int i = 0; i < nst; ++i, ++st) {
@@ -165,16 +179,30 @@ __global__ void __launch_bounds__(32 * (MAXC + 1), 1)
           st = 0;
           ph ^= 1u;
         }
-        if (i >= p.stages) mbar_wait(&empty_bar[st], ph ^ 1);
+        if (i >= p.stages) {
+          if (mc) mbar_wait_cluster(&empty_bar[st], ph ^ 1);
+          else mbar_wait(&empty_bar[st], ph ^ 1);
+        }
         mbar_arrive_expect_tx(&full_bar[st], stage_bytes * nsrc);
         const int row = static_cast<int>((s_begin + i) * kGramStageRows);
         unsigned char* dst = stages + static_cast<size_t>(st) * nsrc * stage_bytes;
         // a TMA box spans at most 256 columns: wider stages take several boxes (npad 512)
-        for (int c0 = 0; c0 < p.npad; c0 += kTmaBoxCols) {
-          tma_load_2d(dst + c0 * 128u, &mapQ, row, c0, &full_bar[st]);
-          if (full) tma_load_2d(dst + stage_bytes + c0 * 128u, &mapY, row, c0, &full_bar[st]);
+        if (mc) {
+          for (int c0 = static_cast<int>(crank) * p.box_cols; c0 < p.npad; c0 += p.mc * p.box_cols) {
+            tma_load_2d_multicast(dst + c0 * 128u, &mapQ, row, c0, &full_bar[st], mask);
+            if (full) tma_load_2d_multicast(dst + stage_bytes + c0 * 128u, &mapY, row, c0, &full_bar[st], mask);
+          }
+        } else {
+          for (int c0 = 0; c0 < p.npad; c0 += p.box_cols) {
+            tma_load_2d(dst + c0 * 128u, &mapQ, row, c0, &full_bar[st]);
+            if (full) tma_load_2d(dst + stage_bytes + c0 * 128u, &mapY, row, c0, &full_bar[st]);
+          }
         }
       }
+    }
+    if (mc) {
+      __syncwarp();
+      cluster_sync();  // (matches the consumers' final cluster barrier)
     }
     return;
   }
@@ -296,7 +324,13 @@ __global__ void __launch_bounds__(32 * (MAXC + 1), 1)
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[st]);
+    if (lane == 0) {
+      if (mc) {
+        for (int j = 0; j < p.mc; ++j) mbar_arrive_cluster(&empty_bar[st], static_cast<uint32_t>(j));
+      } else {
+        mbar_arrive(&empty_bar[st]);
+      }
+    }
     if (++st == p.stages) {
       st = 0;
       ph ^= 1u;
@@ -305,6 +339,8 @@ __global__ void __launch_bounds__(32 * (MAXC + 1), 1)
 
   }  // JR == 2
 
+  // no CTA of a cluster exits while a peer may still arrive on its barriers
+  if (mc) cluster_sync();
   if (!active) return;
   // ---------------- write this CTA's partial tiles (8x8 row-major per tile)
   double* out = p.partials + static_cast<size_t>(chunk) * p.tiles_per_partial * 64;
@@ -331,8 +367,54 @@ cudaError_t gram_tma_config(int variant, size_t smem, int threads, int* occ) {
   }
 }
 
+template <class K>
+static cudaError_t launch_cluster(K kernel, unsigned grid, int threads, size_t smem, cudaStream_t stream, int mc,
+                                  const CUtensorMap& mapQ, const CUtensorMap& mapY, const GramParams& p) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = mc;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, mapQ, mapY, p);
+}
+
+cudaError_t gram_tma_max_clusters(int variant, size_t smem, int threads, int mc, int* nclusters) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(mc);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = mc;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  switch (variant) {
+    case 0: return cudaOccupancyMaxActiveClusters(nclusters, gram_tma_kernel<2, kMaxConsumers>, &cfg);
+    case 1: return cudaOccupancyMaxActiveClusters(nclusters, gram_tma_kernel<4, kMaxConsumersWhole>, &cfg);
+    case 2: return cudaOccupancyMaxActiveClusters(nclusters, gram_tma_kernel<4, kMaxConsumersWhole2>, &cfg);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 cudaError_t launch_gram_tma(int variant, unsigned grid, int threads, size_t smem, cudaStream_t stream,
                             const CUtensorMap& mapQ, const CUtensorMap& mapY, const GramParams& p) {
+  if (p.mc > 1) {
+    switch (variant) {
+      case 0: return launch_cluster(gram_tma_kernel<2, kMaxConsumers>, grid, threads, smem, stream, p.mc, mapQ, mapY, p);
+      case 1: return launch_cluster(gram_tma_kernel<4, kMaxConsumersWhole>, grid, threads, smem, stream, p.mc, mapQ, mapY, p);
+      case 2: return launch_cluster(gram_tma_kernel<4, kMaxConsumersWhole2>, grid, threads, smem, stream, p.mc, mapQ, mapY, p);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (variant) {
     case 0: gram_tma_kernel<2, kMaxConsumers><<<grid, threads, smem, stream>>>(mapQ, mapY, p); break;
     case 1: gram_tma_kernel<4, kMaxConsumersWhole><<<grid, threads, smem, stream>>>(mapQ, mapY, p); break;

@@ -276,6 +276,13 @@ int encode_map(Ctx* c, CUtensorMap* map, const double* base, int64_t m, int64_t 
   return SCQR3_OK;
 }
 
+const bool g_gram_debug = std::getenv("SCQR3_GRAM_DEBUG") != nullptr;
+const int g_gram_force_groups = std::getenv("SCQR3_GRAM_GROUPS") ? std::atoi(std::getenv("SCQR3_GRAM_GROUPS")) : 0;
+const bool g_gram_mc = [] {
+  const char* v = std::getenv("SCQR3_GRAM_MC");
+  return !(v && v[0] == '0');
+}();
+
 // Gram jobs for the consumer warps.  Job codes: 2*block + part.  Three kernel variants:
 //   0: JR = 2, <= 20 consumers -- a job is a part (tile rows 2*part, 2*part+1 of a 4x4-tile
 //      block: 8 tiles off the diagonal, 7 / 3 on it);
@@ -326,7 +333,7 @@ int assign_gram_jobs(GramParams& gp, bool oblique, int* ncons_out, int* variant_
         if (weight(2 * j + part, jr) > 0) codes.push_back(2 * j + part);
     const int jobs = static_cast<int>(codes.size());
     const int groups = std::max(1, (jobs + maxc - 1) / maxc);
-    if (groups > kMaxGroups) continue;
+    if (groups > kMaxGroups || (g_gram_force_groups > 0 && groups != g_gram_force_groups)) continue;
     int ncons = 0;
     for (int g = 0; g < groups; ++g) ncons = std::max(ncons, jobs * (g + 1) / groups - jobs * g / groups);
     std::vector<short> job(kMaxGroups * kMaxConsumers, -1);
@@ -420,11 +427,6 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
     ++g_launches;
     CUDA_TRY(cudaGetLastError());
   }
-  CUtensorMap mq, my;
-  TRY(encode_map(c, &mq, src, m, L.n, ld, L.npad));
-  if (oblique) TRY(encode_map(c, &my, w.y, m, L.n, L.ldy, L.npad));
-  else my = mq;
-
   GramParams gp{};
   gp.gate = gate;
   gp.NT = L.NT;
@@ -443,13 +445,41 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   // 2..8 stages within ~96 KB; a single (serialising) stage only where two do not fit (oblique, npad 512)
   const size_t max_stages = (kGramSmemCap - 2048) / (stage_bytes * nsrc);
   gp.stages = static_cast<int>(std::min<size_t>(std::min<size_t>(8, max_stages), std::max<size_t>(2, 98304 / (stage_bytes * nsrc))));
-  const size_t smem = gp.stages * nsrc * stage_bytes + 2 * gp.stages * 8 + 1024;
+  size_t smem = gp.stages * nsrc * stage_bytes + 2 * gp.stages * 8 + 1024;
   int occ = 1;
   CUDA_TRY(gram_tma_config(variant, smem, threads, &occ));
   occ = std::max(occ, 1);
   gp.total_stages = (m + kGramStageRows - 1) / kGramStageRows;
   long long chunks = std::min<long long>((gp.total_stages + 3) / 4, static_cast<long long>(c->num_sms) * occ / groups);
   chunks = std::max<long long>(1, std::min<long long>(chunks, L.max_chunks));
+  // Several CTAs per row chunk (n > 128): make them a thread-block cluster and multicast each
+  // stage (one L2 read per stage instead of one per CTA: DRAM reads 8mn instead of ~2x), with a
+  // deeper stage ring (a cluster advances at the pace of its slowest CTA).  Taken only when as
+  // many clusters fit at once as there are row chunks -- GPC granularity can leave SMs idle
+  // (n = 256: 45 clusters of 3 against 49 chunks, 10 % slower).  n = 192: 5.56 ms either way at
+  // m = 4e6 with half the DRAM traffic.  SCQR3_GRAM_MC=0 turns it off (A/B measurement).
+  gp.mc = 1;
+  int ncl = 0;
+  if (groups > 1 && groups <= 8 && L.npad % 32 == 0 && g_gram_mc) {
+    const int st_mc = static_cast<int>(std::min<size_t>(8, max_stages));
+    const size_t smem_mc = st_mc * nsrc * stage_bytes + 2 * st_mc * 8 + 1024;
+    int occ_mc = 0;
+    CUDA_TRY(gram_tma_config(variant, smem_mc, threads, &occ_mc));
+    CUDA_TRY(gram_tma_max_clusters(variant, smem_mc, threads, groups, &ncl));
+    if (ncl >= chunks) {
+      gp.mc = groups;
+      gp.stages = st_mc;
+      smem = smem_mc;
+    }
+  }
+  if (g_gram_debug)
+    fprintf(stderr, "gram: n=%d variant=%d groups=%d ncons=%d stages=%d smem=%zu occ=%d mc=%d clusters=%d chunks=%lld\n",
+            L.n, variant, groups, ncons, gp.stages, smem, occ, gp.mc, ncl, chunks);
+  gp.box_cols = gp.mc > 1 ? 32 : std::min(L.npad, kTmaBoxCols);
+  CUtensorMap mq, my;
+  TRY(encode_map(c, &mq, src, m, L.n, ld, gp.box_cols));
+  if (oblique) TRY(encode_map(c, &my, w.y, m, L.n, L.ldy, gp.box_cols));
+  else my = mq;
   gp.chunks = static_cast<int>(chunks);
   gp.partials = w.partials;
   const int pg = prof_begin(c, PK_GRAM);

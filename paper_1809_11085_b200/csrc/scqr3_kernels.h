@@ -43,6 +43,9 @@ struct GramParams {
   int oblique;               // 1 = Q^T Y (upper tiles, reading D22)
   int dual;                  // oblique: also the plain Gram Q^T Q (its norm estimate, reading D4)
   int tiles_per_partial;     // NT(NT+1)/2, doubled when dual or NT^2
+  int mc;                    // > 1: the `groups` CTAs of a row chunk form a cluster and each stage
+                             //   is multicast to all of them (each CTA loads 1 / mc of its boxes)
+  int box_cols;              // columns per TMA box of the stage (the map's box width)
   // job of consumer warp w in group g: warp_job[g * kMaxConsumers + w] (-1 = idle); the host
   // balances the DMMA work of each group over the SM's four sub-partitions (warp % 4)
   short warp_job[kMaxGroups * kMaxConsumers];  // codes <= 2 * 136 (n <= 512)
@@ -159,6 +162,8 @@ struct TrsmParams {
 // blocks) or 4 (whole blocks); MAXC = consumer warps it is compiled for.  Variant v of
 // assign_gram_jobs: 0 = <2, 20>, 1 = <4, 18>, 2 = <4, 15>.
 cudaError_t gram_tma_config(int variant, size_t smem, int threads, int* occ);  // smem attribute + occupancy (cached)
+// clusters of mc CTAs that fit at once (multicast launch)
+cudaError_t gram_tma_max_clusters(int variant, size_t smem, int threads, int mc, int* nclusters);
 cudaError_t launch_gram_tma(int variant, unsigned grid, int threads, size_t smem, cudaStream_t stream,
                             const CUtensorMap& mapQ, const CUtensorMap& mapY, const GramParams& p);
 __global__ void gram_reduce_kernel(GramReduceParams p);
