@@ -351,6 +351,15 @@ __device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool ad
   };
   // (b) rows k0..k0+7 of R~ right of the diagonal block: forward substitution per column, for
   // the columns jj = start, start + stride, ... (full 8-column panel)
+  // Rows k0..k0+7 of R~ as read by the rank-8 updates: W itself when W is in shared memory;
+  // with W in global memory, a shared-memory copy written by panel_rows (two buffers: panel k's
+  // rows are read by the trailing update while panel k+1's are formed), so the mma fragment loads
+  // of the updates do not go to L2.
+  extern __shared__ double smdyn_p[];
+  auto prow = [&](int k0, int r) -> double* {
+    if constexpr (SMEM) return W + (k0 + r) * ldw;
+    else return smdyn_p + (((k0 / kPanel) & 1) * kPanel + r) * ldw;
+  };
   auto panel_rows = [&](int k0, int start, int stride) {
     const int ncols = n - k0 - kPanel;
     for (int jj = start; jj < ncols; jj += stride) {
@@ -367,6 +376,10 @@ __device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool ad
       }
 #pragma unroll
       for (int r = 0; r < kPanel; ++r) W[(k0 + r) * ldw + j] = w[r];
+      if constexpr (!SMEM) {
+#pragma unroll
+        for (int r = 0; r < kPanel; ++r) prow(k0, r)[j] = w[r];
+      }
     }
   };
   // n a multiple of 8: one barrier per panel.  While warps 1..7 apply panel k's rank-8 update to
@@ -394,7 +407,7 @@ __device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool ad
       double c0 = cp[0], c1 = cp[1], a[2], b[2];
 #pragma unroll
       for (int s2 = 0; s2 < 2; ++s2) {
-        const double* pr = W + (k0 + t + 4 * s2) * ldw + base;
+        const double* pr = prow(k0, t + 4 * s2) + base;
         a[s2] = pr[8 * I + g];
         b[s2] = -pr[8 * J + g];
       }
@@ -417,7 +430,7 @@ __device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool ad
           // row block tiles (0, J), J >= 1: 4 in flight
           double a[2];
 #pragma unroll
-          for (int s2 = 0; s2 < 2; ++s2) a[s2] = W[(k0 + t + 4 * s2) * ldw + base + g];
+          for (int s2 = 0; s2 < 2; ++s2) a[s2] = prow(k0, t + 4 * s2)[base + g];
           for (int J0 = 1; J0 < TL; J0 += 4) {
             double c0[4], c1[4], b[4][2];
 #pragma unroll
@@ -427,7 +440,7 @@ __device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool ad
               c0[u] = cp[0];
               c1[u] = cp[1];
 #pragma unroll
-              for (int s2 = 0; s2 < 2; ++s2) b[u][s2] = -W[(k0 + t + 4 * s2) * ldw + base + 8 * J + g];
+              for (int s2 = 0; s2 < 2; ++s2) b[u][s2] = -prow(k0, t + 4 * s2)[base + 8 * J + g];
             }
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2)
@@ -449,8 +462,9 @@ __device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool ad
         tq = clock64();
         if (!*sflag) panel_rows(base, warp == 0 ? lane : warp == 1 ? 32 + lane : 64 + lane, 96);
       } else {
-        // the other trailing tiles (I, J), 1 <= I <= J < TL, J-major; 4 in flight per warp
-        constexpr int kU = 4, kW = 5;
+        // the other trailing tiles (I, J), 1 <= I <= J < TL, J-major; 4 in flight per warp (8
+        // with W in global memory: L2 latency)
+        constexpr int kU = SMEM ? 4 : 8, kW = 5;
         const int wi = warp < 4 ? warp - 2 : warp - 3;  // 2, 3, 5, 6, 7 -> 0..4
         const int ntiles = TL * (TL - 1) / 2;
         int J = 1, cum = 0;  // tiles of columns < J: cum = J(J-1)/2
@@ -467,7 +481,7 @@ __device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool ad
             c1[u] = W[off[u] + 1];
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) {
-              const double* pr = W + (k0 + t + 4 * s2) * ldw + base;
+              const double* pr = prow(k0, t + 4 * s2) + base;
               a[u][s2] = pr[8 * I + g];
               b[u][s2] = -pr[8 * J + g];
             }
@@ -796,6 +810,8 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
         N2 = p.norm2_bound * p.norm2_bound;
       } else if (p.norm_mode == SCQR3_NORM_FROBENIUS) {
         N2 = fro;
+      } else if (p.lmax_dev && pass == 1) {  // computed by power_cluster_kernel before this kernel
+        N2 = *p.lmax_dev * 1.01;
       } else {  // lambda_max(Q^T Q) x 1.01 from the plain Gram formed alongside (reading D4)
         __syncthreads();
         load_W(p, W, ldw, p.tiles + nout + 1);
@@ -806,6 +822,8 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
       N2 = p.norm2_bound * p.norm2_bound;
     } else if (p.norm_mode == SCQR3_NORM_FROBENIUS) {
       N2 = trace;
+    } else if (p.lmax_dev && pass == 1) {  // computed by power_cluster_kernel before this kernel
+      N2 = *p.lmax_dev * 1.01;
     } else {
       N2 = power_lmax_any<SMEM>(W, ldw, n, p.power_iters, trace, ybuf, red) * 1.01;
     }
@@ -889,6 +907,129 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
   }
 }
 }  // namespace
+
+// ---- power iteration for n in (128, 256] on a cluster of 8 CTAs (reading D2): the one-CTA
+// kernel keeps W in global memory there (it does not fit one SM's shared memory), and its
+// power iteration re-read W from L2 every step (~9 us per step at n = 256).  Here CTA r holds
+// rows [32 r, 32 r + 32) of the Gram in its shared memory; each step every CTA forms its rows of
+// sc * W y and stores them into every CTA's copy of the next y (distributed shared memory),
+// then one cluster barrier.  Same iteration as power_lmax (all-ones start, unnormalised
+// iterates scaled by the exact power of two sc, Rayleigh quotient) -- the summation order of
+// the dot products differs, so the estimate agrees to rounding.
+constexpr int kPowCl = 8, kPowRows = 32, kPowThreads = 256;
+
+__device__ __forceinline__ void st_cluster_f64(double* local_addr, uint32_t cta, double v) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(smem_u32(local_addr)), "r"(cta));
+  asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(remote), "d"(v) : "memory");
+}
+
+__global__ void __cluster_dims__(kPowCl, 1, 1) __launch_bounds__(kPowThreads, 1) power_cluster_kernel(PowerParams p) {
+  extern __shared__ __align__(16) double psm[];
+  const int pass = p.pass_dev ? *(volatile const int*)p.pass_dev : p.pass;
+  if (p.last_pass && pass > *(volatile const int*)p.last_pass) return;  // (every CTA of the cluster alike)
+  const int n = p.n, tid = threadIdx.x;
+  const int ldl = ((n + 7) / 16) * 16 + 8;  // = 8 (mod 16): two rows of 8 parts on distinct banks
+  const uint32_t r = cluster_ctarank();
+  const int row0 = static_cast<int>(r) * kPowRows;
+  double* Wl = psm;                                  // [kPowRows][ldl]
+  double* y[2] = {Wl + kPowRows * ldl, Wl + kPowRows * ldl + kMaxN};
+  double* slots = y[1] + kMaxN;                      // [2][kPowCl]: per-CTA partial sums
+  // my rows of the symmetric Gram from its packed upper tiles
+  for (int idx = tid; idx < kPowRows * n; idx += kPowThreads) {
+    const int ir = idx / n, c = idx % n, i = row0 + ir;
+    double v = 0.0;
+    if (i < n) {
+      const int a = i <= c ? i : c, b = i <= c ? c : i;
+      const size_t tile = static_cast<size_t>(b >> 3) * ((b >> 3) + 1) / 2 + (a >> 3);
+      v = p.tiles[tile * 64 + 8 * (a & 7) + (b & 7)];
+    }
+    Wl[ir * ldl + c] = v;
+  }
+  for (int c = tid; c < kMaxN; c += kPowThreads) y[0][c] = c < n ? 1.0 : 0.0;
+  __syncthreads();
+  // trace (for the scale sc): every CTA gets all partials, summed in rank order
+  if (tid < 32) {
+    double t = 0.0;
+    for (int ir = tid; ir < kPowRows; ir += 32)
+      if (row0 + ir < n) t += Wl[ir * ldl + row0 + ir];
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+    if (tid == 0)
+      for (int j = 0; j < kPowCl; ++j) st_cluster_f64(slots + r, static_cast<uint32_t>(j), t);
+  }
+  cluster_sync();
+  double trace = 0.0;
+  for (int j = 0; j < kPowCl; ++j) trace += slots[j];
+  const bool ok = trace > 0.0 && isfinite(trace);
+  const double sc = ok ? ldexp(1.0, -(ilogb(trace) + 1)) : 1.0;
+  const int ir = tid / 8, part = tid % 8, i = row0 + ir;
+  auto rowdot = [&](const double* yv) -> double {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const double* w = Wl + ir * ldl;
+    int c = part;
+    for (; c + 24 < n; c += 32) {
+      a0 = fma(w[c], yv[c], a0);
+      a1 = fma(w[c + 8], yv[c + 8], a1);
+      a2 = fma(w[c + 16], yv[c + 16], a2);
+      a3 = fma(w[c + 24], yv[c + 24], a3);
+    }
+    for (; c < n; c += 8) a0 = fma(w[c], yv[c], a0);
+    double acc = (a0 + a1) + (a2 + a3);
+    for (int o = 1; o < 8; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    return acc;
+  };
+  int cur = 0;
+  for (int it = 0; it < p.iters; ++it) {
+    const double acc = rowdot(y[cur]);
+    if (part == 0 && i < n) {
+      const double v = acc * sc;
+      for (int j = 0; j < kPowCl; ++j) st_cluster_f64(y[cur ^ 1] + i, static_cast<uint32_t>(j), v);
+    }
+    cluster_sync();  // every CTA's next y is complete (and nobody still reads this one)
+    cur ^= 1;
+  }
+  const double acc = rowdot(y[cur]);
+  double num = 0.0, den = 0.0;
+  if (part == 0 && i < n) {
+    const double yi = y[cur][i];
+    num = yi * acc;
+    den = yi * yi;
+  }
+  // CTA partials (fixed order) -> CTA 0, which sums them in rank order
+  for (int o = 8; o < 32; o <<= 1) {
+    num += __shfl_xor_sync(0xffffffffu, num, o);
+    den += __shfl_xor_sync(0xffffffffu, den, o);
+  }
+  __shared__ double wsum[2][kPowThreads / 32];
+  if ((tid & 31) == 0) {
+    wsum[0][tid >> 5] = num;
+    wsum[1][tid >> 5] = den;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double sn = 0.0, sd = 0.0;
+    for (int w = 0; w < kPowThreads / 32; ++w) {
+      sn += wsum[0][w];
+      sd += wsum[1][w];
+    }
+    st_cluster_f64(slots + kPowCl + r, 0u, sn);
+    st_cluster_f64(slots + 2 * kPowCl + r, 0u, sd);
+  }
+  cluster_sync();
+  if (r == 0 && tid == 0) {
+    double sn = 0.0, sd = 0.0;
+    for (int j = 0; j < kPowCl; ++j) {
+      sn += slots[kPowCl + j];
+      sd += slots[2 * kPowCl + j];
+    }
+    *p.out = (ok && sd > 0.0) ? sn / sd : 0.0;
+  }
+}
+
+size_t power_cluster_smem(int n) {
+  const int ldl = ((n + 7) / 16) * 16 + 8;
+  return (static_cast<size_t>(kPowRows) * ldl + 2 * kMaxN + 3 * kPowCl) * sizeof(double);
+}
 
 __global__ void __launch_bounds__(kThreads, 1) chol_kernel_smem(CholParams p) {
   extern __shared__ double smW[];

@@ -498,7 +498,11 @@ int launch_chol(const CholParams& p, cudaStream_t st) {
     CUDA_TRY(cached_launch_cfg(chol_cfg, chol_kernel_smem, smem, 256, nullptr));
     chol_kernel_smem<<<1, 256, smem, st>>>(p);
   } else {
-    chol_kernel_gmem<<<1, 256, 0, st>>>(p);
+    // (W in global memory; shared memory holds two copies of the panel rows, chol.cu)
+    const size_t smem = static_cast<size_t>(2 * 8) * chol_ldw(p.n) * 8;
+    static thread_local LaunchCfgCache chol_cfg_g;
+    CUDA_TRY(cached_launch_cfg(chol_cfg_g, chol_kernel_gmem, smem, 256, nullptr));
+    chol_kernel_gmem<<<1, 256, smem, st>>>(p);
   }
   ++g_launches;
   CUDA_TRY(cudaGetLastError());
@@ -851,6 +855,31 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
     // previous R~ consumed (a graph segment joins the side stream at its end instead)
     if (k > 1) CUDA_TRY(cudaStreamWaitEvent(st, c->ev_side, 0));
     const int pc = prof_begin(c, PK_CHOL);
+    // pass 1's norm estimate for n in (128, 256] (W does not fit one SM's shared memory): the
+    // power iteration runs on a cluster of 8 CTAs first (reading D2 / D4)
+    const bool pow_needs = k == 1 && n > 128 && n <= 256 && o->norm_mode == SCQR3_NORM_POWER &&
+                           (o->shift_mode == SCQR3_SHIFT_SAFE || o->shift_mode == SCQR3_SHIFT_PRACTICAL);
+    cp.lmax_dev = nullptr;
+    if (pow_needs) {
+      PowerParams pp{};
+      pp.tiles = oblique ? w.tiles + L.tiles_sym * 64 + 1 : w.tiles;
+      pp.n = static_cast<int>(n);
+      pp.iters = iters;
+      pp.out = w.misc + 24;
+      pp.pass = 1;
+      pp.last_pass = last_pass;
+      const size_t psmem = power_cluster_smem(static_cast<int>(n));
+      static thread_local int pow_dev = -1;  // (a cluster kernel: only the shared-memory attribute)
+      if (pow_dev != c->device) {
+        CUDA_TRY(cudaFuncSetAttribute(power_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(power_cluster_smem(256))));
+        pow_dev = c->device;
+      }
+      power_cluster_kernel<<<8, 256, psmem, st>>>(pp);
+      ++g_launches;
+      CUDA_TRY(cudaGetLastError());
+      cp.lmax_dev = w.misc + 24;
+    }
     TRY(launch_chol(cp, st));
     prof_end(c, pc);
     if (!generic) CUDA_TRY(cudaEventRecord(c->ev_pass[k - 1], st));

@@ -109,6 +109,7 @@ struct CholParams {
   int power_iters;
   double m_global;
   const double* nb_dev;      // oblique: ||B||_2 bound (device scalar)
+  const double* lmax_dev;    // pass 1: lambda_max estimate from power_cluster_kernel (null: in-kernel)
   double stop_tol;
   double* W;                 // n x n scratch (global) when it does not fit in shared memory
   int w_in_smem;
@@ -121,6 +122,19 @@ struct CholParams {
   int* last_pass;            // device-side pass control (may be null): written on stop / error
   const int* pass_dev;       // CUDA-graph loop body: pass number on the device (else `pass`)
 };
+
+// power iteration on a cluster of 8 CTAs (n in (128, 256]): Rayleigh quotient -> *out
+struct PowerParams {
+  const double* tiles;       // packed upper tiles of the Gram to iterate on
+  int n;
+  int iters;
+  double* out;
+  int pass;                  // gate as the chol kernel's: skipped after a stop
+  const int* pass_dev;
+  const int* last_pass;
+};
+__global__ void power_cluster_kernel(PowerParams p);
+size_t power_cluster_smem(int n);
 
 // complex n x n step (zchol.cu)
 struct ZCholParams {
