@@ -453,3 +453,35 @@ def test_factor_parity_full_sweeps(n, kappa):
     rg = sq.scqr3_factor(dev(X))
     ro = oracle.scqr3(X)
     _compare(X, rg, ro, kappa)
+
+
+# ------------------------------------------------------------------ round-2 paths
+@gpu
+@pytest.mark.parametrize("m,n", [(60_001, 150), (40_000, 192), (33_333, 176)])
+def test_gram_parity_cluster_multicast(m, n):
+    """n in (128, 192]: two CTAs share each row chunk and run as a thread-block cluster whose
+    stages arrive by TMA multicast (gram.cu); T1 bound against the oracle, exact symmetry."""
+    X = synth.random_rows(m, n, seed=n)
+    A = host(sq.scqr3_gram(dev(X)))
+    Ao = oracle.gram(X)
+    bound = 2 * gamma(m) * (np.abs(X).T @ np.abs(X))
+    assert np.all(np.abs(A - Ao) <= bound + 1e-300)
+    assert np.array_equal(A, A.T)
+    Xi = np.random.default_rng(n).integers(-30, 31, size=(m, n)).astype(float)
+    Ai = host(sq.scqr3_gram(dev(Xi)))
+    assert np.array_equal(Ai, (Xi.astype(np.int64).T @ Xi.astype(np.int64)).astype(float))
+
+
+@gpu
+@pytest.mark.parametrize("n", [136, 200, 256])
+def test_cluster_power_iteration_shift(n):
+    """n in (128, 256]: pass 1's norm estimate comes from power_cluster_kernel (8 CTAs); the
+    shift equals the oracle's (the same 32-step power iteration, reading D2) to rounding."""
+    m = 20_000
+    X = synth.randsvd(m, n, 1e10, seed=n)
+    rg = sq.scqr3_factor(dev(X))
+    ro = oracle.scqr3(X)
+    assert rg.status == 0 and ro.status == 0
+    assert rg.trace[0]["norm2_est"] == pytest.approx(ro.trace[0].norm2_est, rel=1e-12)
+    assert rg.trace[0]["shift"] == pytest.approx(ro.trace[0].shift, rel=1e-12)
+    _compare(X, rg, ro, 1e10)
