@@ -217,14 +217,29 @@ struct LaunchCfgCache {
   int threads = 0;
   int occ = 0;
 };
+// The dynamic shared-memory limit is a process-wide attribute of the kernel while this cache is
+// per thread, and the host threads of a loopback group (or of any multi-threaded caller) launch
+// the same kernel with different sizes (e.g. Gram ring depths that depend on the rank's m): so
+// the limit is raised once to the most the kernel can take, never set to one call's size -- a
+// later, smaller setting by another thread would make this thread's launch fail.
 template <class K>
 inline cudaError_t cached_launch_cfg(LaunchCfgCache& cc, K kernel, size_t smem, int threads, int* occ) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (cc.dev != dev || cc.smem != smem || cc.threads != threads) {
-    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncAttributes fa{};
+    e = cudaFuncGetAttributes(&fa, kernel);
     if (e != cudaSuccess) return e;
+    int optin = 0;
+    e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e != cudaSuccess) return e;
+    const int lim = optin - static_cast<int>(fa.sharedSizeBytes);
+    if (static_cast<size_t>(lim) < smem) return cudaErrorInvalidValue;
+    if (fa.maxDynamicSharedSizeBytes != lim) {
+      e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+      if (e != cudaSuccess) return e;
+    }
     int o = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, threads, smem);
     if (e != cudaSuccess) return e;
