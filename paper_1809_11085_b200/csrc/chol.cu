@@ -14,14 +14,18 @@
 // only needed when a shift is formed (pass 1, or a pass whose plain Cholesky broke down).
 //
 // Cholesky: right-looking with 8-column panels on a row-major working copy W of A (leading
-// dimension n+1; shared memory for n <= 159, else an L2-resident global scratch).  Per panel:
-// (a) ONE thread factors the 8x8 diagonal block in registers (pivot chain rsqrt -> scale -> FMA,
-// no shuffle or barrier in it); (b) one thread per column forms the panel's rows of R~; (c) the
-// rank-8 trailing update -- 8x8 tiles on DMMA when n % 8 == 0 (with a look-ahead for n >= 128:
-// the next diagonal block is updated first and factored by one thread while the other warps
-// finish), else 4x4 register tiles.  Outputs for the TRSM kernel: -R~ in mma B-fragment order,
-// and for each 8x8 diagonal block the strict upper part scaled by its row's reciprocal pivot plus
-// the reciprocal pivots; R~ itself for trmul_kernel.
+// dimension n + 4; shared memory for n <= 157, else an L2-resident global scratch).  Per panel:
+// ONE thread factors the 8x8 diagonal block in registers (pivot chain rsqrt -> scale -> FMA, no
+// shuffle or barrier in it); the panel's rows of R~ by forward substitution, one thread per
+// column; the rank-8 trailing update.  n % 8 == 0: the update as 8x8 tiles on DMMA, and one
+// barrier per panel -- warp 1 updates the next row block, warp 0 the next diagonal tile, whose
+// block lane 0 factors, warps 0, 1, 4 form the next panel's rows behind a named barrier, while
+// warps 2, 3, 5, 6, 7 update the rest (panel k+1 is ready when the barrier releases panel k's
+// update).  Otherwise three barriers per panel and scalar 4x4 register tiles.  Outputs for the
+// TRSM kernel: -R~ in mma B-fragment order, and for each 8x8 diagonal block the strict upper part
+// scaled by its row's reciprocal pivot plus the reciprocal pivots; R~ itself for trmul_kernel.
+// n in (128, 256]: pass 1's power iteration runs before this kernel on a cluster of 8 CTAs
+// (power_cluster_kernel).
 #include <math.h>
 
 #include <type_traits>
@@ -517,11 +521,11 @@ __device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool ad
     }
     return 0;
   }
-  const bool lookahead = false;
+  // n not a multiple of 8: three barriers per panel, scalar 4x4 register tiles for the update
   for (int k0 = 0; k0 < n; k0 += kPanel) {
     const int kb = min(kPanel, n - k0);
     t0 = clock64();
-    if ((!lookahead || k0 == 0) && tid == 0) diag_block(k0, kb);
+    if (tid == 0) diag_block(k0, kb);
     __syncthreads();
     t_a += clock64() - t0;
     t0 = clock64();
@@ -557,67 +561,6 @@ __device__ __noinline__ int factor(double* Wg, int ldw, int n, double s, bool ad
     // lane keeps a 4x4 register tile.
     const int L = ncols, T4 = (L + 3) >> 2;
     const int base = k0 + kb;
-    if ((n & 7) == 0) {
-      // n a multiple of 8 (kb = 8): 8x8 tiles on the FP64 tensor cores, C_IJ -= P_I^T P_J with
-      // P the panel's 8 rows -- two m8n8k4 steps per tile (A[g][k] = P[k][8I+g], B[k][j] =
-      // -P[k][8J+j]); diagonal tiles are formed whole (their lower half is never read).
-      const int TL = L >> 3, ntiles = TL * (TL + 1) / 2;
-      const int g = lane >> 2, t = lane & 3;
-      constexpr int kU = 4;  // tiles in flight per warp (independent loads and MMAs)
-      const int kW = lookahead ? kThreads / 32 - 1 : kThreads / 32;  // tile-sharing warps
-      if (lookahead && warp == 0) {
-        if (ntiles > 0) {  // tile (0,0): the next diagonal block
-          double* cp = W + (base + g) * ldw + base + 2 * t;
-          double c0 = cp[0], c1 = cp[1];
-#pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            const double* pr = W + (k0 + t + 4 * s) * ldw + base;
-            dmma(c0, c1, pr[g], -pr[g]);
-          }
-          cp[0] = c0;
-          cp[1] = c1;
-          __syncwarp();
-          if (lane == 0) diag_block(base, min(kPanel, n - base));
-        }
-      } else {
-      int J = 0, cum = 0;  // tile tau -> (I, J), J-major (tau only grows)
-      for (int tau0 = warp; tau0 < ntiles; tau0 += kU * kW) {
-        double* cp[kU];
-        double c0[kU], c1[kU], a[kU][2], b[kU][2];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          const int tau = tau0 + u * kW;
-          cp[u] = nullptr;
-          if (tau < ntiles) {
-            while (cum + J + 1 <= tau) cum += ++J;
-            const int I = tau - cum;
-            cp[u] = W + (base + 8 * I + g) * ldw + base + 8 * J + 2 * t;
-            c0[u] = cp[u][0];
-            c1[u] = cp[u][1];
-#pragma unroll
-            for (int s = 0; s < 2; ++s) {
-              const double* pr = W + (k0 + t + 4 * s) * ldw + base;
-              a[u][s] = pr[8 * I + g];
-              b[u][s] = -pr[8 * J + g];
-            }
-          }
-        }
-#pragma unroll
-        for (int s = 0; s < 2; ++s)
-#pragma unroll
-          for (int u = 0; u < kU; ++u)
-            if (cp[u]) dmma(c0[u], c1[u], a[u][s], b[u][s]);
-#pragma unroll
-        for (int u = 0; u < kU; ++u)
-          if (cp[u]) {
-            cp[u][0] = c0[u];
-            cp[u][1] = c1[u];
-          }
-      }
-      }
-      __syncthreads();
-      continue;
-    }
     for (int I = warp; I < T4; I += kThreads / 32) {
       const int i0 = 4 * I;
       for (int jc = i0 & ~31; jc < L; jc += 128) {
