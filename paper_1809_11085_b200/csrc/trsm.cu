@@ -31,6 +31,69 @@ namespace scqr3 {
 #define SCQR3_TRSM_PIPE 1  // 0: both k-steps of each later target back to back (A/B builds)
 #endif
 
+// Which updates C_K += Q_S (-R~_{S,K}) run during the diagonal chain of block J (S <= J - 1 <
+// J + 1 <= K; the last one, S = J - 1, K = J, runs before the chain).  Right-looking (CAP >= NT)
+// hosts exactly the updates from S = J - 1, so the early chains carry most of the tensor-core
+// work and the late ones almost none.  With CAP < NT a chain hosts at most CAP updates: those
+// due now (K = J + 1) first, then the fresh source S = J - 1, then the earliest deadlines, and
+// the rest wait for a later chain -- always in ascending S for each target, so every target
+// still receives its updates in the same order (the same rounding).
+template <int NT>
+struct TrsmSched {
+  int cnt[NT > 0 ? NT : 1];
+  int S[NT > 0 ? NT : 1][NT > 0 ? NT : 1];
+  int K[NT > 0 ? NT : 1][NT > 0 ? NT : 1];
+};
+template <int NT, int CAP>
+constexpr TrsmSched<NT> make_trsm_sched() {
+  TrsmSched<NT> r{};
+  bool done[NT > 0 ? NT : 1][NT > 0 ? NT : 1] = {};
+  for (int K = 0; K < NT; ++K)
+    for (int S = 0; S < NT; ++S) done[S][K] = !(S + 1 < K);  // pending: S <= K - 2
+  for (int J = 1; J < NT; ++J) {
+    int c = 0;
+    auto next_of = [&](int K) {  // smallest pending S of target K (ascending order), or -1
+      for (int S = 0; S < K - 1; ++S)
+        if (!done[S][K]) return S;
+      return -1;
+    };
+    // pass 0: due now (K = J + 1); pass 1: fresh source S = J - 1; pass 2: earliest deadline
+    for (int pass = 0; pass < 3; ++pass)
+      for (int K = J + 1; K < NT; ++K)
+        for (;;) {
+          const int S = next_of(K);
+          if (S < 0 || S > J - 1) break;
+          const bool take = pass == 0 ? K == J + 1 : c < CAP && (pass == 2 || S == J - 1);
+          if (!take) break;
+          r.S[J][c] = S;
+          r.K[J][c] = K;
+          ++c;
+          done[S][K] = true;
+          if (pass == 1) break;
+        }
+    r.cnt[J] = c;
+  }
+  return r;
+}
+#ifndef SCQR3_TRSM_CAP
+#define SCQR3_TRSM_CAP 8  // updates per diagonal chain for NT = 16 (>= 1000: right-looking)
+#endif
+template <int NT, int CAP>
+constexpr bool trsm_sched_ok() {
+  constexpr auto r = make_trsm_sched<NT, CAP>();
+  int total = 0;
+  for (int J = 1; J < NT; ++J) {
+    total += r.cnt[J];
+    for (int i = 0; i < r.cnt[J]; ++i)
+      for (int j = i + 1; j < r.cnt[J]; ++j)
+        if (r.K[J][i] == r.K[J][j] && i * 8 / r.cnt[J] == j * 8 / r.cnt[J]) return false;
+  }
+  return total == (NT - 1) * (NT - 2) / 2;  // every update hosted exactly once
+}
+#if SCQR3_TRSM_CAP < 1000
+static_assert(trsm_sched_ok<16, SCQR3_TRSM_CAP>(), "TRSM update schedule");
+#endif
+
 // GRAM (n <= 64): also accumulate the next pass's Gram Q_k^T Q_k from the
 // solved rows, so the next pass does not read Q from HBM again.  Each warp writes its 16 finished
 // rows to a private swizzled stage and accumulates their Gram (all upper 8x8 tiles) in registers;
@@ -198,6 +261,35 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
       // the dependent DMMAs sit a whole chain step apart (adjacent dependent DMMAs get a NOP
       // and a fixed-latency wait in between).
       auto later_updates = [&](int c) {
+#if SCQR3_TRSM_CAP < 1000
+       if constexpr (NT == 16) {
+        // the chain hosts the schedule's updates: update i's first k-step in chain step
+        // i * 8 / cnt, its second one step later, issued before that step's first k-steps (a
+        // target's updates therefore keep their order; trsm_sched_ok checks that no two
+        // updates of one target share a step)
+        constexpr auto sch = make_trsm_sched<NT, SCQR3_TRSM_CAP>();
+        const int cnt = sch.cnt[J];
+        auto upd2 = [&](int S, int K, int s) {
+          const double b = bfrag(K, s);
+#pragma unroll
+          for (int a = 0; a < A; ++a) dmma(q[a][K][0], q[a][K][1], q[a][S][s & 1], b);
+        };
+        if (c >= 1) {
+#pragma unroll
+          for (int i = 0; i < NT; ++i)
+            if (i < cnt && i * 8 / cnt == c - 1) upd2(sch.S[J][i], sch.K[J][i], 2 * sch.S[J][i] + 1);
+        }
+#pragma unroll
+        for (int i = 0; i < NT; ++i)
+          if (i < cnt && i * 8 / cnt == c) upd2(sch.S[J][i], sch.K[J][i], 2 * sch.S[J][i]);
+        if (c == 7) {
+#pragma unroll
+          for (int i = 0; i < NT; ++i)
+            if (i < cnt && i * 8 / cnt == 7) upd2(sch.S[J][i], sch.K[J][i], 2 * sch.S[J][i] + 1);
+        }
+        return;
+       }
+#endif
 #if SCQR3_TRSM_PIPE
 #pragma unroll
         for (int v = nup * c / 8; v < nup * (c + 1) / 8; ++v) upd(J + 1 + v, 2 * (J - 1));
