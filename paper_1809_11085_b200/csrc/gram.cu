@@ -35,6 +35,7 @@ __device__ __forceinline__ void decode_job(int j, int NB, bool full, int& bi, in
 // (18 consumer warps fit 96 registers).  Fragment address of k-step s: the lane's 16-byte chunk
 // is (s + 4*(t>>1)) ^ g = s ^ G, i.e. offset ^ (s << 4) on a 128-byte aligned row base; the
 // block's tile rows / columns sit 8 x 128 B apart (immediate offsets).
+template <bool MC>
 __device__ __forceinline__ void gram_whole_jobs(const GramParams& p, const unsigned char* stages, uint32_t stage_bytes,
                                                 int nsrc, uint64_t* full_bar, uint64_t* empty_bar, int nst, int kind,
                                                 bool b_from_y, bool full, int bi, int bj, bool diag,
@@ -43,7 +44,7 @@ __device__ __forceinline__ void gram_whole_jobs(const GramParams& p, const unsig
   const int lane = threadIdx.x & 31;
   const uint32_t lane_chunk = inner[0];  // chunk G << 4 plus the 8-byte half of this lane's k slot
   auto release = [&](uint64_t* bar) {  // this stage consumed: in every CTA of the cluster (multicast)
-    if (p.mc > 1) {
+    if constexpr (MC) {
       for (int j = 0; j < p.mc; ++j) mbar_arrive_cluster(bar, static_cast<uint32_t>(j));
     } else {
       mbar_arrive(bar);
@@ -126,7 +127,7 @@ __device__ __forceinline__ void gram_whole_jobs(const GramParams& p, const unsig
   }
 }
 
-template <int JR, int MAXC>
+template <int JR, int MAXC, bool MC>
 __global__ void __launch_bounds__(32 * (MAXC + 1), 1)
     gram_tma_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapY,
                     GramParams p) {
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(32 * (MAXC + 1), 1)
   // multicast (p.mc > 1): the CTAs of a chunk form a cluster; every stage lands in all of them
   // from one L2 read (each CTA issues 1 / mc of the stage's boxes to the whole cluster), and a
   // stage is refilled only after the consumers of every CTA released it (remote arrivals)
-  const bool mc = p.mc > 1;
+  constexpr bool mc = MC;  // (a template parameter: the runtime branches cost 2-7 % unclustered)
   const uint32_t crank = mc ? cluster_ctarank() : 0;
   if (threadIdx.x == 0) {
     for (int i = 0; i < p.stages; ++i) {
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(32 * (MAXC + 1), 1)
   const int kind = !active ? 4 : edge ? 3 : diag ? 1 + part : 0;
 
   if constexpr (JR == 4) {
-    gram_whole_jobs(p, stages, stage_bytes, nsrc, full_bar, empty_bar, nst, kind, full && !plainjob, full,
+    gram_whole_jobs<MC>(p, stages, stage_bytes, nsrc, full_bar, empty_bar, nst, kind, full && !plainjob, full,
                     bi, bj, diag, acc, offA, offB, inner);
   } else {
   int st = 0;
@@ -357,12 +358,15 @@ __global__ void __launch_bounds__(32 * (MAXC + 1), 1)
     }
 }
 
-cudaError_t gram_tma_config(int variant, size_t smem, int threads, int* occ) {
-  static thread_local LaunchCfgCache cfg[3];
-  switch (variant) {
-    case 0: return cached_launch_cfg(cfg[0], gram_tma_kernel<2, kMaxConsumers>, smem, threads, occ);
-    case 1: return cached_launch_cfg(cfg[1], gram_tma_kernel<4, kMaxConsumersWhole>, smem, threads, occ);
-    case 2: return cached_launch_cfg(cfg[2], gram_tma_kernel<4, kMaxConsumersWhole2>, smem, threads, occ);
+cudaError_t gram_tma_config(int variant, bool mc, size_t smem, int threads, int* occ) {
+  static thread_local LaunchCfgCache cfg[6];
+  switch (variant + (mc ? 3 : 0)) {
+    case 0: return cached_launch_cfg(cfg[0], gram_tma_kernel<2, kMaxConsumers, false>, smem, threads, occ);
+    case 1: return cached_launch_cfg(cfg[1], gram_tma_kernel<4, kMaxConsumersWhole, false>, smem, threads, occ);
+    case 2: return cached_launch_cfg(cfg[2], gram_tma_kernel<4, kMaxConsumersWhole2, false>, smem, threads, occ);
+    case 3: return cached_launch_cfg(cfg[3], gram_tma_kernel<2, kMaxConsumers, true>, smem, threads, occ);
+    case 4: return cached_launch_cfg(cfg[4], gram_tma_kernel<4, kMaxConsumersWhole, true>, smem, threads, occ);
+    case 5: return cached_launch_cfg(cfg[5], gram_tma_kernel<4, kMaxConsumersWhole2, true>, smem, threads, occ);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -398,9 +402,9 @@ cudaError_t gram_tma_max_clusters(int variant, size_t smem, int threads, int mc,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   switch (variant) {
-    case 0: return cudaOccupancyMaxActiveClusters(nclusters, gram_tma_kernel<2, kMaxConsumers>, &cfg);
-    case 1: return cudaOccupancyMaxActiveClusters(nclusters, gram_tma_kernel<4, kMaxConsumersWhole>, &cfg);
-    case 2: return cudaOccupancyMaxActiveClusters(nclusters, gram_tma_kernel<4, kMaxConsumersWhole2>, &cfg);
+    case 0: return cudaOccupancyMaxActiveClusters(nclusters, gram_tma_kernel<2, kMaxConsumers, true>, &cfg);
+    case 1: return cudaOccupancyMaxActiveClusters(nclusters, gram_tma_kernel<4, kMaxConsumersWhole, true>, &cfg);
+    case 2: return cudaOccupancyMaxActiveClusters(nclusters, gram_tma_kernel<4, kMaxConsumersWhole2, true>, &cfg);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -409,16 +413,16 @@ cudaError_t launch_gram_tma(int variant, unsigned grid, int threads, size_t smem
                             const CUtensorMap& mapQ, const CUtensorMap& mapY, const GramParams& p) {
   if (p.mc > 1) {
     switch (variant) {
-      case 0: return launch_cluster(gram_tma_kernel<2, kMaxConsumers>, grid, threads, smem, stream, p.mc, mapQ, mapY, p);
-      case 1: return launch_cluster(gram_tma_kernel<4, kMaxConsumersWhole>, grid, threads, smem, stream, p.mc, mapQ, mapY, p);
-      case 2: return launch_cluster(gram_tma_kernel<4, kMaxConsumersWhole2>, grid, threads, smem, stream, p.mc, mapQ, mapY, p);
+      case 0: return launch_cluster(gram_tma_kernel<2, kMaxConsumers, true>, grid, threads, smem, stream, p.mc, mapQ, mapY, p);
+      case 1: return launch_cluster(gram_tma_kernel<4, kMaxConsumersWhole, true>, grid, threads, smem, stream, p.mc, mapQ, mapY, p);
+      case 2: return launch_cluster(gram_tma_kernel<4, kMaxConsumersWhole2, true>, grid, threads, smem, stream, p.mc, mapQ, mapY, p);
       default: return cudaErrorInvalidValue;
     }
   }
   switch (variant) {
-    case 0: gram_tma_kernel<2, kMaxConsumers><<<grid, threads, smem, stream>>>(mapQ, mapY, p); break;
-    case 1: gram_tma_kernel<4, kMaxConsumersWhole><<<grid, threads, smem, stream>>>(mapQ, mapY, p); break;
-    case 2: gram_tma_kernel<4, kMaxConsumersWhole2><<<grid, threads, smem, stream>>>(mapQ, mapY, p); break;
+    case 0: gram_tma_kernel<2, kMaxConsumers, false><<<grid, threads, smem, stream>>>(mapQ, mapY, p); break;
+    case 1: gram_tma_kernel<4, kMaxConsumersWhole, false><<<grid, threads, smem, stream>>>(mapQ, mapY, p); break;
+    case 2: gram_tma_kernel<4, kMaxConsumersWhole2, false><<<grid, threads, smem, stream>>>(mapQ, mapY, p); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -298,12 +298,12 @@ const bool g_gram_mc = [] {
 // n = 96, 128, 192, 256, 384, 512 and the oblique n = 64, 128: the model picks the fastest --
 // 0 up to n = 128, a whole-block variant above: 1 at n = 192 (2 within 1 %), 2 at 256, 1 at 512).
 // Returns the number of groups; sets *ncons_out and *variant_out.
-int assign_gram_jobs(GramParams& gp, bool oblique, int* ncons_out, int* variant_out) {
+int assign_gram_jobs(GramParams& gp, bool oblique, bool dual, int* ncons_out, int* variant_out) {
   const long long load_cycles = static_cast<long long>(gp.npad) * 128 * (oblique ? 2 : 1) / 16;
   // upper blocks only, also for the oblique Gram (reading D22); the oblique Gram adds the plain
   // Gram's blocks (job codes past 2 * nsym) for its norm estimate (reading D4)
   const int nsym = gp.NB * (gp.NB + 1) / 2;
-  const int nblocks = oblique ? 2 * nsym : nsym;
+  const int nblocks = dual ? 2 * nsym : nsym;
   auto coords = [&](int j, int& bi, int& bj) {
     if (j >= nsym) j -= nsym;
     int c = 0;
@@ -375,7 +375,7 @@ int assign_gram_jobs(GramParams& gp, bool oblique, int* ncons_out, int* variant_
 }
 
 // Sum `chunks` partials (per-CTA packed upper tiles) into w.tiles in chunk order.
-int launch_gram_reduce(Ctx* c, const Layout& L, const WS& w, int chunks, bool oblique, int colsq_count,
+int launch_gram_reduce(Ctx* c, const Layout& L, const WS& w, int chunks, bool oblique, bool dual, int colsq_count,
                        cudaStream_t st, PassGate gate) {
   GramReduceParams rp{};
   rp.gate = gate;
@@ -387,8 +387,8 @@ int launch_gram_reduce(Ctx* c, const Layout& L, const WS& w, int chunks, bool ob
   rp.oblique = oblique ? 1 : 0;
   rp.colsq_partials = oblique ? w.colsq : nullptr;
   rp.colsq_count = colsq_count;
-  rp.dual = oblique ? 1 : 0;
-  const long long nblocks = (L.tiles_sym * 64 * (oblique ? 2 : 1) + 31) / 32;  // 32 outputs x 8 chunk classes
+  rp.dual = dual ? 1 : 0;
+  const long long nblocks = (L.tiles_sym * 64 * (dual ? 2 : 1) + 31) / 32;  // 32 outputs x 8 chunk classes
   const int pr = prof_begin(c, PK_REDUCE);
   gram_reduce_kernel<<<static_cast<unsigned>(nblocks), 256, 0, st>>>(rp);
   prof_end(c, pr);
@@ -397,9 +397,10 @@ int launch_gram_reduce(Ctx* c, const Layout& L, const WS& w, int chunks, bool ob
   return SCQR3_OK;
 }
 
-// Gram of the m x n block at src into w.tiles (packed upper tiles; oblique: sym(Q^T Y) and ||Q||_F^2)
+// Gram of the m x n block at src into w.tiles (packed upper tiles; oblique: sym(Q^T Y) and ||Q||_F^2,
+// dual: then the plain Gram Q^T Q for the norm estimate of reading D4)
 int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld, int64_t m, bool oblique,
-             const ObliqueYParams* yp, cudaStream_t st, PassGate gate = PassGate{}) {
+             const ObliqueYParams* yp, cudaStream_t st, PassGate gate = PassGate{}, bool dual = false) {
   if (m == 0) {
     // an empty shard contributes zeros to every summed entry: the (B-)Gram, ||Q||_F^2 and, for
     // the oblique layout, the plain Gram behind them
@@ -433,10 +434,10 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   gp.NB = (L.NT + kJobTiles - 1) / kJobTiles;
   gp.npad = L.npad;
   gp.oblique = oblique ? 1 : 0;
-  gp.dual = oblique ? 1 : 0;
+  gp.dual = dual ? 1 : 0;
   gp.tiles_per_partial = static_cast<int>(L.tiles_part);
   int ncons = 0, variant = 0;
-  const int groups = assign_gram_jobs(gp, oblique, &ncons, &variant);
+  const int groups = assign_gram_jobs(gp, oblique, dual, &ncons, &variant);
   if (groups > kMaxGroups) return fail("internal: too many Gram job groups");
   gp.groups = groups;
   const int threads = 32 * (1 + ncons);
@@ -447,7 +448,7 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   gp.stages = static_cast<int>(std::min<size_t>(std::min<size_t>(8, max_stages), std::max<size_t>(2, 98304 / (stage_bytes * nsrc))));
   size_t smem = gp.stages * nsrc * stage_bytes + 2 * gp.stages * 8 + 1024;
   int occ = 1;
-  CUDA_TRY(gram_tma_config(variant, smem, threads, &occ));
+  CUDA_TRY(gram_tma_config(variant, false, smem, threads, &occ));
   occ = std::max(occ, 1);
   gp.total_stages = (m + kGramStageRows - 1) / kGramStageRows;
   long long chunks = std::min<long long>((gp.total_stages + 3) / 4, static_cast<long long>(c->num_sms) * occ / groups);
@@ -464,7 +465,7 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
     const int st_mc = static_cast<int>(std::min<size_t>(8, max_stages));
     const size_t smem_mc = st_mc * nsrc * stage_bytes + 2 * st_mc * 8 + 1024;
     int occ_mc = 0;
-    CUDA_TRY(gram_tma_config(variant, smem_mc, threads, &occ_mc));
+    CUDA_TRY(gram_tma_config(variant, true, smem_mc, threads, &occ_mc));
     CUDA_TRY(gram_tma_max_clusters(variant, smem_mc, threads, groups, &ncl));
     if (ncl >= chunks) {
       gp.mc = groups;
@@ -488,7 +489,7 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   ++g_launches;
   CUDA_TRY(le);
 
-  return launch_gram_reduce(c, L, w, gp.chunks, oblique, colsq_count, st, gate);
+  return launch_gram_reduce(c, L, w, gp.chunks, oblique, dual, colsq_count, st, gate);
 }
 
 int launch_chol(const CholParams& p, cudaStream_t st) {
@@ -836,10 +837,10 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
       yp.ldq = ldsrc;
     }
     if (k == 1 || !fuse_tg) {
-      TRY(run_gram(c, L, w, src, ldsrc, m, oblique, &yp, st, gate));
+      TRY(run_gram(c, L, w, src, ldsrc, m, oblique, &yp, st, gate, oblique));
     } else {
       // this pass's Gram was accumulated by the previous pass's fused TRSM (per-CTA partials)
-      TRY(launch_gram_reduce(c, L, w, fused_chunks, false, 0, st, gate));
+      TRY(launch_gram_reduce(c, L, w, fused_chunks, false, false, 0, st, gate));
     }
     if (cm) {
       // B-Gram (+ ||Q||_F^2 and the plain Gram for the norm estimate when oblique)
@@ -1113,7 +1114,7 @@ int zfactor_impl(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, i
     const PassGate gate{last_pass, k, nullptr};
     c->cur_pass = k;
     if (k == 1 || !fuse_tg) TRY(run_gram(c, L, w, S, Z.lds, m, false, nullptr, st, gate));
-    else TRY(launch_gram_reduce(c, L, w, fused_chunks, false, 0, st, gate));
+    else TRY(launch_gram_reduce(c, L, w, fused_chunks, false, false, 0, st, gate));
     if (cm) {
       const int pa = prof_begin(c, PK_COMM);
       TRY(comm_allreduce_sum(cm, w.tiles, static_cast<size_t>(L.tiles_sym * 64), o->deterministic != 0, w.partials,

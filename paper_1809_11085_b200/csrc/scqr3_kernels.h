@@ -175,7 +175,7 @@ struct TrsmParams {
 // gram_tma_kernel<JR, MAXC> (gram.cu): JR = tile rows per consumer-warp job, 2 (half 4x4-tile
 // blocks) or 4 (whole blocks); MAXC = consumer warps it is compiled for.  Variant v of
 // assign_gram_jobs: 0 = <2, 20>, 1 = <4, 18>, 2 = <4, 15>.
-cudaError_t gram_tma_config(int variant, size_t smem, int threads, int* occ);  // smem attribute + occupancy (cached)
+cudaError_t gram_tma_config(int variant, bool mc, size_t smem, int threads, int* occ);  // smem attribute + occupancy (cached)
 // clusters of mc CTAs that fit at once (multicast launch)
 cudaError_t gram_tma_max_clusters(int variant, size_t smem, int threads, int mc, int* nclusters);
 cudaError_t launch_gram_tma(int variant, unsigned grid, int threads, size_t smem, cudaStream_t stream,
