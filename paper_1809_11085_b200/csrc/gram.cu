@@ -12,6 +12,7 @@
 // that fragment loads from the swizzled stage are bank-conflict free.  Each CTA writes its
 // partial tiles to the workspace; gram_reduce sums the partials in CTA order, so the result
 // is bitwise deterministic run to run for a fixed GPU model and grid (reading D10).
+#include <type_traits>
 #include "scqr3_dev.cuh"
 #include "scqr3_kernels.h"
 
@@ -103,25 +104,51 @@ __device__ __forceinline__ void gram_whole_jobs(const GramParams& p, const unsig
       }
     });
   } else if (kind == 3) {
-    // block touching the padded edge (n not a multiple of 32): clamped rows, per-tile validity
-    const int NT = p.NT;
-    stage_loop([&](uint32_t oA, uint32_t oB) {
+    // a block of the last block column when NT % 4 != 0: cb = NT - 4 bj < 4 valid tile columns
+    // (an off-diagonal edge block has all four tile rows, the diagonal one a <= b < cb).
+    // Specialised on cb so that no DMMA is issued for a padded tile -- predicated-off DMMAs
+    // still take their issue slots (n = 144 ran 25 % slower than n = 160 that way)
+    const uint32_t a0 = offA[0] + lane_chunk, b0 = offB[0] + lane_chunk;
+    auto edge = [&](auto cbc) {
+      constexpr int CB = decltype(cbc)::value;
+      if (diag) {
+        stage_loop([&](uint32_t oA, uint32_t oB) {
 #pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        double fa[4], fb[kJobTiles];
+          for (int s = 0; s < 4; ++s) {
+            const uint32_t xa = (oA + a0) ^ (s << 4), xb = (oB + b0) ^ (s << 4);
+            double fb[CB], fa[CB];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) fa[a] = frag(oA + offA[a] + inner[s]);
+            for (int b = 0; b < CB; ++b) fb[b] = frag(xb + b * 1024);
 #pragma unroll
-        for (int b = 0; b < kJobTiles; ++b) fb[b] = frag(oB + offB[b] + inner[s]);
+            for (int a = 0; a < CB; ++a) fa[a] = full ? frag(xa + a * 1024) : fb[a];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+            for (int a = 0; a < CB; ++a)
 #pragma unroll
-          for (int b = 0; b < kJobTiles; ++b) {
-            const bool valid = (bi * kJobTiles + a < NT) && (bj * kJobTiles + b < NT) && (!diag || a <= b);
-            if (valid) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+              for (int b = a; b < CB; ++b) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
           }
+        });
+      } else {
+        stage_loop([&](uint32_t oA, uint32_t oB) {
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            const uint32_t xa = (oA + a0) ^ (s << 4), xb = (oB + b0) ^ (s << 4);
+            double fb[CB];
+#pragma unroll
+            for (int b = 0; b < CB; ++b) fb[b] = frag(xb + b * 1024);
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+              const double fa = frag(xa + a * 1024);
+#pragma unroll
+              for (int b = 0; b < CB; ++b) dmma(acc[a][b][0], acc[a][b][1], fa, fb[b]);
+            }
+          }
+        });
       }
-    });
+    };
+    const int cb = p.NT - bj * kJobTiles;
+    if (cb == 1) edge(std::integral_constant<int, 1>{});
+    else if (cb == 2) edge(std::integral_constant<int, 2>{});
+    else edge(std::integral_constant<int, 3>{});
   } else {
     stage_loop([&](uint32_t, uint32_t) {});  // idle warp: release the stages
   }
@@ -307,22 +334,36 @@ __global__ void __launch_bounds__(32 * (MAXC + 1), 1)
         dmma(acc[1][3][0], acc[1][3][1], a3, f3);
       }
     } else if (kind == 3) {
-      // part of a block touching the padded edge (n not a multiple of 32): per-tile validity
+      // part of a block of the last block column (NT % 4 != 0): cb valid tile columns, no DMMA
+      // issued for a padded tile off the diagonal (see gram_whole_jobs); the diagonal edge block
+      // keeps per-tile validity
+      auto edge = [&](auto cbc) {
+        constexpr int CB = decltype(cbc)::value;
 #pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        double fa[2], fb[kJobTiles];
+        for (int s = 0; s < 4; ++s) {
+          double fa[2], fb[CB];
 #pragma unroll
-        for (int a = 0; a < 2; ++a) fa[a] = *reinterpret_cast<const double*>(srcA + offA[a] + inner[s]);
+          for (int a = 0; a < 2; ++a) fa[a] = *reinterpret_cast<const double*>(srcA + offA[a] + inner[s]);
 #pragma unroll
-        for (int b = 0; b < kJobTiles; ++b) fb[b] = *reinterpret_cast<const double*>(srcB + offB[b] + inner[s]);
+          for (int b = 0; b < CB; ++b) fb[b] = *reinterpret_cast<const double*>(srcB + offB[b] + inner[s]);
+          if (diag) {
 #pragma unroll
-        for (int a = 0; a < 2; ++a)
+            for (int a = 0; a < 2; ++a)
 #pragma unroll
-          for (int b = 0; b < kJobTiles; ++b) {
-            const bool valid = (bi * kJobTiles + rr0 + a < NT) && (bj * kJobTiles + b < NT) && (!diag || rr0 + a <= b);
-            if (valid) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+              for (int b = 0; b < CB; ++b)
+                if (rr0 + a <= b) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+          } else {
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+              for (int b = 0; b < CB; ++b) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
           }
-      }
+        }
+      };
+      const int cb = NT - bj * kJobTiles;
+      if (cb == 1) edge(std::integral_constant<int, 1>{});
+      else if (cb == 2) edge(std::integral_constant<int, 2>{});
+      else edge(std::integral_constant<int, 3>{});
     }
     __syncwarp();
     if (lane == 0) {
@@ -352,7 +393,7 @@ __global__ void __launch_bounds__(32 * (MAXC + 1), 1)
       const int TI = bi * kJobTiles + rr0 + a, TJ = bj * kJobTiles + b;
       const bool valid = (TI < NT) && (TJ < NT) && (!diag || rr0 + a <= b);
       if (!valid) continue;
-      const size_t tid = static_cast<size_t>(TJ) * (TJ + 1) / 2 + TI + (plainjob ? static_cast<size_t>(NT) * (NT + 1) / 2 : 0);
+      const size_t tid = static_cast<size_t>(TJ) * (TJ + 1) / 2 + TI + (plainjob ? static_cast<size_t>(p.NTl) * (p.NTl + 1) / 2 : 0);
       double2 v = make_double2(acc[a][b][0], acc[a][b][1]);
       *reinterpret_cast<double2*>(out + tid * 64 + 8 * g + 2 * t) = v;
     }
@@ -429,7 +470,7 @@ cudaError_t launch_gram_tma(int variant, unsigned grid, int threads, size_t smem
 }
 
 // Sum the per-chunk partials in chunk order.  Output: packed upper tiles (tile (TI,TJ),
-// TI <= TJ, at index TJ(TJ+1)/2 + TI, 8x8 row-major), plus for the oblique Gram the appended
+// TI <= TJ, at index TJ(TJ+1)/2 + TI, 8x8 row-major; zeros for TJ >= NTc), plus for the oblique Gram the appended
 // ||Q||_F^2 (the oblique partials are upper tiles of Q^T (BQ) too, reading D22).
 // Block = 32 consecutive outputs x 8 chunk classes (c mod 8): coalesced 256-B rows, eight
 // loads in flight per output, then the eight class sums added in class order -- a fixed order,
@@ -441,8 +482,10 @@ __global__ void gram_reduce_kernel(GramReduceParams p) {
   const long long nout = static_cast<long long>(p.NT) * (p.NT + 1) / 2 * 64;
   const long long nall = p.dual ? 2 * nout : nout;  // partial entries to reduce
   const long long e = static_cast<long long>(blockIdx.x) * 32 + lane;
+  // tiles of columns past the computed ones (n padded to a TRSM instance) are zero
+  const long long ncomp = static_cast<long long>(p.NTc) * (p.NTc + 1) / 2 * 64;
   double s = 0.0;
-  if (e < nall) {
+  if (e < nall && (e < nout ? e : e - nout) < ncomp) {
     const size_t stride = static_cast<size_t>(p.tiles_per_partial) * 64;
     const double* src = p.partials + e;
     for (int c = cls; c < p.chunks; c += 8) s += src[static_cast<size_t>(c) * stride];

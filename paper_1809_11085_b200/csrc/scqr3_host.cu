@@ -376,7 +376,7 @@ int assign_gram_jobs(GramParams& gp, bool oblique, bool dual, int* ncons_out, in
 
 // Sum `chunks` partials (per-CTA packed upper tiles) into w.tiles in chunk order.
 int launch_gram_reduce(Ctx* c, const Layout& L, const WS& w, int chunks, bool oblique, bool dual, int colsq_count,
-                       cudaStream_t st, PassGate gate) {
+                       cudaStream_t st, PassGate gate, int NTc = 0) {
   GramReduceParams rp{};
   rp.gate = gate;
   rp.partials = w.partials;
@@ -384,6 +384,7 @@ int launch_gram_reduce(Ctx* c, const Layout& L, const WS& w, int chunks, bool ob
   rp.chunks = chunks;
   rp.tiles_per_partial = static_cast<int>(L.tiles_part);
   rp.NT = L.NT;
+  rp.NTc = NTc > 0 ? NTc : L.NT;
   rp.oblique = oblique ? 1 : 0;
   rp.colsq_partials = oblique ? w.colsq : nullptr;
   rp.colsq_count = colsq_count;
@@ -430,9 +431,13 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   }
   GramParams gp{};
   gp.gate = gate;
-  gp.NT = L.NT;
-  gp.NB = (L.NT + kJobTiles - 1) / kJobTiles;
-  gp.npad = L.npad;
+  // only the tiles of the n columns: L.npad rounds n up to a TRSM instance (n = 144 -> 192), whose
+  // zero columns the Gram need not stream or multiply; the partials keep the L.NT layout
+  const int NTc = (L.n + 7) / 8;
+  gp.NT = NTc;
+  gp.NTl = L.NT;
+  gp.NB = (NTc + kJobTiles - 1) / kJobTiles;
+  gp.npad = 8 * NTc;
   gp.oblique = oblique ? 1 : 0;
   gp.dual = dual ? 1 : 0;
   gp.tiles_per_partial = static_cast<int>(L.tiles_part);
@@ -442,7 +447,7 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   gp.groups = groups;
   const int threads = 32 * (1 + ncons);
   const int nsrc = oblique ? 2 : 1;
-  const size_t stage_bytes = static_cast<size_t>(L.npad) * 128;
+  const size_t stage_bytes = static_cast<size_t>(gp.npad) * 128;
   // 2..8 stages within ~96 KB; a single (serialising) stage only where two do not fit (oblique, npad 512)
   const size_t max_stages = (kGramSmemCap - 2048) / (stage_bytes * nsrc);
   gp.stages = static_cast<int>(std::min<size_t>(std::min<size_t>(8, max_stages), std::max<size_t>(2, 98304 / (stage_bytes * nsrc))));
@@ -461,7 +466,7 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   // m = 4e6 with half the DRAM traffic.  SCQR3_GRAM_MC=0 turns it off (A/B measurement).
   gp.mc = 1;
   int ncl = 0;
-  if (groups > 1 && groups <= 8 && L.npad % 32 == 0 && g_gram_mc) {
+  if (groups > 1 && groups <= 8 && gp.npad % 32 == 0 && g_gram_mc) {
     const int st_mc = static_cast<int>(std::min<size_t>(8, max_stages));
     const size_t smem_mc = st_mc * nsrc * stage_bytes + 2 * st_mc * 8 + 1024;
     int occ_mc = 0;
@@ -476,7 +481,8 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   if (g_gram_debug)
     fprintf(stderr, "gram: n=%d variant=%d groups=%d ncons=%d stages=%d smem=%zu occ=%d mc=%d clusters=%d chunks=%lld\n",
             L.n, variant, groups, ncons, gp.stages, smem, occ, gp.mc, ncl, chunks);
-  gp.box_cols = gp.mc > 1 ? 32 : std::min(L.npad, kTmaBoxCols);
+  // (equal TMA boxes of <= kTmaBoxCols columns that tile the stage exactly)
+  gp.box_cols = gp.mc > 1 ? 32 : gp.npad / ((gp.npad + kTmaBoxCols - 1) / kTmaBoxCols);
   CUtensorMap mq, my;
   TRY(encode_map(c, &mq, src, m, L.n, ld, gp.box_cols));
   if (oblique) TRY(encode_map(c, &my, w.y, m, L.n, L.ldy, gp.box_cols));
@@ -489,7 +495,7 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
   ++g_launches;
   CUDA_TRY(le);
 
-  return launch_gram_reduce(c, L, w, gp.chunks, oblique, dual, colsq_count, st, gate);
+  return launch_gram_reduce(c, L, w, gp.chunks, oblique, dual, colsq_count, st, gate, NTc);
 }
 
 int launch_chol(const CholParams& p, cudaStream_t st) {

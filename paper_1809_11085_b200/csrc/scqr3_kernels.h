@@ -38,7 +38,8 @@ struct GramParams {
   int groups;                // job groups (CTAs per chunk)
   int stages;                // pipeline depth
   int npad;                  // padded column count (multiple of 8, TMA box width)
-  int NT;                    // npad / 8 tiles per side
+  int NT;                    // npad / 8 tiles per side computed (ceil(n / 8))
+  int NTl;                   // tiles per side of the partial layout (n padded to a TRSM instance)
   int NB;                    // ceil(NT / 4) blocks per side
   int oblique;               // 1 = Q^T Y (upper tiles, reading D22)
   int dual;                  // oblique: also the plain Gram Q^T Q (its norm estimate, reading D4)
@@ -58,7 +59,8 @@ struct GramReduceParams {
   double* tiles;             // packed upper tiles (+1 double: ||Q||_F^2 for oblique)
   int chunks;
   int tiles_per_partial;
-  int NT;
+  int NT;                    // tiles per side of the layout
+  int NTc;                   // tile columns computed (later ones are written as zeros)
   int oblique;
   const double* colsq_partials;
   int colsq_count;
