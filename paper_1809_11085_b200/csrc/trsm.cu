@@ -531,6 +531,12 @@ template <> struct WidePhases<16, 32> {  // targets 16..31 after a 128-column fi
     static constexpr int P = 1, MAXF = B1 * (B1 - 1) - B0 * (B0 - 1);                           \
     __host__ __device__ static constexpr int b(int i) { return i == 0 ? B0 : B1; }              \
   };
+// targets 16..17 / 16..19 / 16..21 (n <= 144 / 160 / 176) and 16..27 (n in (192, 224]): only the
+// blocks below n
+SCQR3_RESIDENT_RANGE(16, 18)
+SCQR3_RESIDENT_RANGE(16, 20)
+SCQR3_RESIDENT_RANGE(16, 22)
+SCQR3_RESIDENT_RANGE(16, 28)
 SCQR3_RESIDENT_RANGE(32, 40)
 SCQR3_RESIDENT_RANGE(40, 48)
 SCQR3_RESIDENT_RANGE(48, 56)
@@ -549,6 +555,7 @@ template <int TB, int TE> constexpr bool phases_ok(int i = 0) {
   return i == W::P || (phase_frags(W::b(i), W::b(i + 1)) <= W::MAXF && W::b(W::P) == TE && phases_ok<TB, TE>(i + 1));
 }
 static_assert(phases_ok<0, 32>() && phases_ok<16, 24>() && phases_ok<16, 32>() && phases_ok<32, 64>() &&
+                  phases_ok<16, 18>() && phases_ok<16, 20>() && phases_ok<16, 22>() && phases_ok<16, 28>() &&
                   phases_ok<32, 40>() && phases_ok<40, 48>() && phases_ok<48, 56>() && phases_ok<56, 60>() &&
                   phases_ok<60, 64>(),
               "phase fragment counts exceed the buffers");
@@ -834,6 +841,11 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
       p1.n = 128;
       cudaError_t e = launch_one<16, 2, true, 256, true>(p1, map, num_sms, stream);
       if (e != cudaSuccess) return e;
+      // only the target blocks below n (n = 136: one of the eight)
+      const int nb = (p.n + 7) / 8;
+      if (nb <= 18) return launch_wide<16, 18, 256, 2>(p, num_sms, stream);
+      if (nb <= 20) return launch_wide<16, 20, 256, 2>(p, num_sms, stream);
+      if (nb <= 22) return launch_wide<16, 22, 256, 2>(p, num_sms, stream);
       return launch_wide<16, 24, 256, 2>(p, num_sms, stream);
     }
     case 32: {
@@ -847,6 +859,7 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
       p1.n = 128;
       cudaError_t e = launch_one<16, 2, true, 256, true>(p1, map, num_sms, stream);
       if (e != cudaSuccess) return e;
+      if ((p.n + 7) / 8 <= 28) return launch_wide<16, 28, 256, 2>(p, num_sms, stream);
       return launch_wide<16, 32, 256, 2>(p, num_sms, stream);
     }
     case 64: {

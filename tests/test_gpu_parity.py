@@ -430,11 +430,11 @@ def test_complex_real_input_matches_real_path():
 # ------------------------------------------------------------------ wide TRSM, several sweeps
 # One persistent sweep of the TRSM covers 148 CTAs x 8 warps x 16 rows = 18,944 rows; at
 # m >= 60,000 every block-column launch of the n in (128, 512] path (columns 0..127, targets
-# 16..23 / 16..31, and for n > 256 the resident launches 32..40 ... 60..64) runs at least three
+# 16..17 / 16..19 / 16..21 / 16..23 / 16..27 / 16..31, and for n > 256 the resident launches 32..40 ... 60..64) runs at least three
 # sweeps per warp, so their loop-carried state (TMA slot reuse, resident fragments, the read-back
 # of finished Q columns) is compared with the oracle (the per-row model).
 @gpu
-@pytest.mark.parametrize("n", [150, 192, 300, 400, 512])
+@pytest.mark.parametrize("n", [136, 144, 150, 176, 192, 200, 300, 400, 512])
 def test_trsm_integer_exact_full_sweeps(n):
     m = 60_011
     rng = np.random.default_rng(n + 1)
@@ -446,7 +446,8 @@ def test_trsm_integer_exact_full_sweeps(n):
 
 
 @gpu
-@pytest.mark.parametrize("n,kappa", [(150, 1e9), (192, 1e10), (300, 1e8), (400, 1e10), (512, 1e12)])
+@pytest.mark.parametrize("n,kappa", [(136, 1e10), (150, 1e9), (192, 1e10), (200, 1e12), (300, 1e8), (400, 1e10),
+                                     (512, 1e12)])
 def test_factor_parity_full_sweeps(n, kappa):
     m = 60_000
     X = synth.randsvd(m, n, kappa, seed=7)
