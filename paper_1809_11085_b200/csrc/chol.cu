@@ -615,68 +615,68 @@ __device__ __forceinline__ double rload(const double* W, int ldw, int n, int i, 
   return (i < n && j < n) ? (i <= j ? x : 0.0) : (i == j ? 1.0 : 0.0);
 }
 
-// TRSM layout (trsm.cu): B fragments of -R~ and scaled diagonal blocks; R~ (column-major) for trmul.
-// Latency-bound on one CTA: each thread walks a flat index with kU independent reads in flight
-// before its (coalesced) global stores.
+// Outputs of a pass.  R~ for trmul_kernel and trsm_prep_kernel, row-major (Rt[i n + j], zero
+// below the diagonal): consecutive threads read consecutive entries of a row of W (no bank
+// conflicts in shared memory, coalesced from L2 when W is global) and store consecutive
+// addresses.  The TRSM operands -- B fragments of -R~ and the scaled diagonal blocks, the same
+// values trsm_prep_kernel forms -- are written here only when bfrag != null (n <= 64, where a
+// second launch costs more than it saves); for larger n trsm_prep_kernel forms them on many
+// CTAs (on this one CTA they took 13 K cycles at n = 128 and 73 K at n = 256).
 template <bool SMEM>
-__device__ __noinline__ void write_outputs(const double* Wg, int ldw, int n, int NT, double* bfrag,
-                                              double* dblk, double* Rt) {
+__device__ __noinline__ void write_outputs(const double* Wg, int ldw, int n, int NT, double* bfrag, double* dblk,
+                                           double* Rt) {
   extern __shared__ double smdyn[];
   const double* W = SMEM ? smdyn : Wg;
   constexpr int kU = 8;
-  const int nf = NT * (NT - 1) * 32;  // fragment f = idx / 32: target block J >= 1, k-step s < 2J
 #ifdef SCQR3_CHOL_OUTCLK
   long long o0 = clock64();
 #endif
-  for (int i0 = threadIdx.x; i0 < nf; i0 += kU * kThreads) {
-    double v[kU];
+  if (bfrag) {
+    const int nf = NT * (NT - 1) * 32;  // fragment f = idx / 32: target block J >= 1, k-step s < 2J
+    for (int i0 = threadIdx.x; i0 < nf; i0 += kU * kThreads) {
+      double v[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int idx = min(i0 + u * kThreads, nf - 1);
-      const int f = idx >> 5, lane = idx & 31;
-      int J = static_cast<int>((1.0f + sqrtf(1.0f + 4.0f * f)) * 0.5f);  // largest J with J(J-1) <= f
-      J -= J * (J - 1) > f ? 1 : 0;
-      J += (J + 1) * J <= f ? 1 : 0;
-      const int s = f - J * (J - 1);
-      v[u] = -rload(W, ldw, n, 8 * (s >> 1) + 2 * (lane & 3) + (s & 1), 8 * J + (lane >> 2));
+      for (int u = 0; u < kU; ++u) {
+        const int idx = min(i0 + u * kThreads, nf - 1);
+        const int f = idx >> 5, lane = idx & 31;
+        int J = static_cast<int>((1.0f + sqrtf(1.0f + 4.0f * f)) * 0.5f);  // largest J with J(J-1) <= f
+        J -= J * (J - 1) > f ? 1 : 0;
+        J += (J + 1) * J <= f ? 1 : 0;
+        const int s = f - J * (J - 1);
+        v[u] = -rload(W, ldw, n, 8 * (s >> 1) + 2 * (lane & 3) + (s & 1), 8 * J + (lane >> 2));
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (i0 + u * kThreads < nf) bfrag[i0 + u * kThreads] = v[u];
     }
-#pragma unroll
-    for (int u = 0; u < kU; ++u)
-      if (i0 + u * kThreads < nf) bfrag[i0 + u * kThreads] = v[u];
+    for (int idx = threadIdx.x; idx < NT * 72; idx += kThreads) {
+      const int J = idx / 72, w = idx % 72;
+      const int c = 8 * J + (w < 64 ? (w >> 3) : w - 64), j = 8 * J + (w < 64 ? (w & 7) : w - 64);
+      const double rcj = rload(W, ldw, n, c, j), rcc = rload(W, ldw, n, c, c);
+      dblk[idx] = w < 64 ? (j > c ? rcj / rcc : 0.0) : 1.0 / rcc;
+    }
   }
 #ifdef SCQR3_CHOL_OUTCLK
   long long o1 = clock64();
 #endif
-  for (int idx = threadIdx.x; idx < NT * 72; idx += kThreads) {
-    const int J = idx / 72, w = idx % 72;
-    const int c = 8 * J + (w < 64 ? (w >> 3) : w - 64), j = 8 * J + (w < 64 ? (w & 7) : w - 64);
-    const double rcj = rload(W, ldw, n, c, j), rcc = rload(W, ldw, n, c, c);
-    dblk[idx] = w < 64 ? (j > c ? rcj / rcc : 0.0) : 1.0 / rcc;
-  }
-#ifdef SCQR3_CHOL_OUTCLK
-  long long o2 = clock64();
-#endif
-  if (Rt) {
-    const int nn = n * n;
-    for (int i0 = threadIdx.x; i0 < nn; i0 += kU * kThreads) {
-      double v[kU];
+  const int nn = n * n;
+  for (int i0 = threadIdx.x; i0 < nn; i0 += kU * kThreads) {
+    double v[kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int idx = min(i0 + u * kThreads, nn - 1);
-        const int i = idx % n, j = idx / n;
-        const double x = W[i * ldw + j];
-        v[u] = i <= j ? x : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < kU; ++u)
-        if (i0 + u * kThreads < nn) Rt[i0 + u * kThreads] = v[u];
+    for (int u = 0; u < kU; ++u) {
+      const int idx = min(i0 + u * kThreads, nn - 1);
+      const int i = idx / n, j = idx - i * n;
+      const double x = W[i * ldw + j];
+      v[u] = i <= j ? x : 0.0;
     }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (i0 + u * kThreads < nn) Rt[i0 + u * kThreads] = v[u];
   }
 #ifdef SCQR3_CHOL_OUTCLK
-  long long o3 = clock64();
   if (threadIdx.x == 0) {
-    g_phase[0] = (o1 - o0) + ((o2 - o1) << 32);
-    g_phase[1] = o3 - o2;
+    g_phase[0] = o1 - o0;
+    g_phase[1] = clock64() - o1;
   }
 #endif
 }
@@ -995,9 +995,10 @@ __global__ void trmul_kernel(const double* Rt, const double* R, double* Rnew, in
   const int i = static_cast<int>(k % n), j = static_cast<int>(k / n);
   double acc = 0.0;
   if (i <= j) {
-    if (first) acc = Rt[k];
+    // (R~ row-major, see write_outputs; R column-major)
+    if (first) acc = Rt[static_cast<size_t>(i) * n + j];
     else
-      for (int kk = i; kk <= j; ++kk) acc = fma(Rt[i + static_cast<size_t>(kk) * n], R[kk + static_cast<size_t>(j) * n], acc);
+      for (int kk = i; kk <= j; ++kk) acc = fma(Rt[static_cast<size_t>(i) * n + kk], R[kk + static_cast<size_t>(j) * n], acc);
   }
   Rnew[k] = acc;
 }
@@ -1008,10 +1009,17 @@ __global__ void copy_kernel(const double* src, double* dst, long long count, con
   if (k < count) dst[k] = src[k];
 }
 
-// R (n x n col-major, upper, positive diagonal) -> TRSM layout (kernel-level scqr3_trsm API)
-__global__ void trsm_prep_kernel(const double* R, int n, int NT, double* bfrag, double* dblk) {
+// R (n x n, upper, positive diagonal; column-major, or row-major as chol_kernel writes R~) ->
+// TRSM layout: B fragments of -R (fragment f = idx / 32: target block J >= 1, k-step s < 2J) and
+// the 8 x 8 diagonal blocks pre-scaled by their pivots (r_cj / r_cc) with the reciprocal pivots,
+// the identity past n.  In a pass it runs after chol_kernel (skipped when that failed or after a
+// stop); also used by the kernel-level scqr3_trsm API and the complex path.
+__global__ void trsm_prep_kernel(const double* R, int n, int NT, double* bfrag, double* dblk, int rowmajor,
+                                 const DevStatus* st, PassGate gate) {
+  if (SCQR3_GATE_SKIP(gate) || (st && st->code != SCQR3_OK)) return;
   auto rp = [&](int i, int j) -> double {
-    if (i < n && j < n) return i <= j ? R[i + static_cast<size_t>(j) * n] : 0.0;
+    if (i < n && j < n)
+      return i <= j ? R[rowmajor ? static_cast<size_t>(i) * n + j : i + static_cast<size_t>(j) * n] : 0.0;
     return i == j ? 1.0 : 0.0;
   };
   const int nf = NT * (NT - 1) * 32;

@@ -793,8 +793,10 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
   cp.W = w.W;
   cp.w_in_smem = w_fits_smem(static_cast<int>(n)) ? 1 : 0;
   cp.Rt = w.Rt;
-  cp.bfrag = w.bfrag;
-  cp.dblk = w.dblk;
+  // the TRSM operands: written by chol_kernel for n <= 64, else by trsm_prep_kernel (many CTAs)
+  const bool prep_launch = n > 64;
+  cp.bfrag = prep_launch ? nullptr : w.bfrag;
+  cp.dblk = prep_launch ? nullptr : w.dblk;
   cp.st_dev = w.st;
   cp.st_host = c->st_host_dev;
 
@@ -888,6 +890,13 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
       cp.lmax_dev = w.misc + 24;
     }
     TRY(launch_chol(cp, st));
+    if (prep_launch) {  // R~ (row-major) -> the TRSM's B fragments and scaled diagonal blocks, on many CTAs
+      const int tot = L.NT * (L.NT - 1) * 32 + L.NT * 72;
+      trsm_prep_kernel<<<(tot + 255) / 256, 256, 0, st>>>(w.Rt, static_cast<int>(n), L.NT, w.bfrag, w.dblk, 1, w.st,
+                                                           gate);
+      ++g_launches;
+      CUDA_TRY(cudaGetLastError());
+    }
     prof_end(c, pc);
     if (!generic) CUDA_TRY(cudaEventRecord(c->ev_pass[k - 1], st));
     TRY(launch_trmul(c, w.Rt, R, w.Rnew, static_cast<int>(n), k == 1, w.st, st, gate));
@@ -1144,7 +1153,7 @@ int zfactor_impl(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, i
     ++g_launches;
     CUDA_TRY(cudaGetLastError());
     const int tot = L.NT * (L.NT - 1) * 32 + L.NT * 72;
-    trsm_prep_kernel<<<(tot + 255) / 256, 256, 0, st>>>(w.Rt, n2, L.NT, w.bfrag, w.dblk);  // M -> TRSM operands
+    trsm_prep_kernel<<<(tot + 255) / 256, 256, 0, st>>>(w.Rt, n2, L.NT, w.bfrag, w.dblk, 0, nullptr, gate);  // M -> TRSM operands
     ++g_launches;
     CUDA_TRY(cudaGetLastError());
     prof_end(c, pc);
@@ -1425,7 +1434,8 @@ int scqr3_trsm(int64_t m, int64_t n, const double* X, int64_t ld, const double* 
   TRY(carve(L, opts, &w));
   cudaStream_t st = static_cast<cudaStream_t>(opts->stream);
   const int tot = L.NT * (L.NT - 1) * 32 + L.NT * 72;
-  trsm_prep_kernel<<<(tot + 255) / 256, 256, 0, st>>>(R, static_cast<int>(n), L.NT, w.bfrag, w.dblk);
+  trsm_prep_kernel<<<(tot + 255) / 256, 256, 0, st>>>(R, static_cast<int>(n), L.NT, w.bfrag, w.dblk, 0, nullptr,
+                                                     PassGate{});
   ++g_launches;
   CUDA_TRY(cudaGetLastError());
   TrsmParams tp{};

@@ -116,9 +116,9 @@ struct CholParams {
   double* W;                 // n x n scratch (global) when it does not fit in shared memory
   int w_in_smem;
   double* R;                 // CHOL_ONLY output (n x n col-major)
-  double* Rt;                // CHOL_PASS: R~ of this pass (n x n col-major) for trmul_kernel
-  double* bfrag;             // TRSM B fragments (negated R~), NT(NT-1) x 32
-  double* dblk;              // TRSM diagonal blocks, NT x 72
+  double* Rt;                // CHOL_PASS: R~ of this pass (n x n row-major) for trmul_kernel, trsm_prep_kernel
+  double* bfrag;             // TRSM B fragments (negated R~), NT(NT-1) x 32, written here when
+  double* dblk;              //   non-null (n <= 64), else by trsm_prep_kernel; diagonal blocks NT x 72
   DevStatus* st_dev;
   DevStatus* st_host;        // host-mapped per-pass slots (st_host[pass-1]; may be null)
   int* last_pass;            // device-side pass control (may be null): written on stop / error
@@ -198,7 +198,8 @@ __global__ void chol_kernel_gmem(CholParams p);
 __global__ void trmul_kernel(const double* Rt, const double* R, double* Rnew, int n, int first, const DevStatus* st,
                              PassGate gate);
 __global__ void copy_kernel(const double* src, double* dst, long long count, const DevStatus* st, PassGate gate);
-__global__ void trsm_prep_kernel(const double* R, int n, int NT, double* bfrag, double* dblk);
+__global__ void trsm_prep_kernel(const double* R, int n, int NT, double* bfrag, double* dblk, int rowmajor,
+                                 const DevStatus* st, PassGate gate);
 __global__ void z2split_kernel(const double* Z, long long ldz, long long m, int n, double* S, long long lds);
 __global__ void split2z_kernel(const double* S, long long lds, long long m, int n, double* Z, long long ldz);
 __global__ void zcombine_kernel(const double* tiles, int n, double* A, const int* last_pass, int pass);
