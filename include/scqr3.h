@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define SCQR3_ABI_VERSION 1
+#define SCQR3_ABI_VERSION 2
 
 enum { SCQR3_OK = 0, SCQR3_EINVAL = 1, SCQR3_EBREAKDOWN = 2, SCQR3_ENOCONV = 3 };
 
@@ -65,6 +65,18 @@ enum { SCQR3_SHIFT_SAFE = 0, SCQR3_SHIFT_FIXED = 1, SCQR3_SHIFT_NONE = 2, SCQR3_
  * USER: norm2_bound^2 on pass 1 (POWER afterwards).  Oblique always uses ||Q||_F^2 for
  * X (or USER on pass 1) and bnorm_bound, else the Gershgorin bound, for ||B||_2 (D4). */
 enum { SCQR3_NORM_POWER = 0, SCQR3_NORM_FROBENIUS = 1, SCQR3_NORM_USER = 2 };
+
+/* How the TRSM Q := Q R~^{-1} solves its 8 x 8 diagonal blocks D_J (reading D24).
+ * AUTO (default): per pass, the Cholesky step inverts every D_J by substitution (Y_J, rows of
+ *   Y_J D_J = I) and checks that multiplying by Y_J keeps each row's backward error inside the
+ *   paper's bound ||dR_i||_2 <= gamma_n sqrt(n) ||R~||_2 (eq. DeltaRbound):
+ *   gamma_n ||R~_off||_F + 2 gamma_8 max_J || |D_J| |Y_J| |D_J| ||_F <= gamma_n sqrt(n) max_j ||R~ e_j||_2
+ *   (R~_off: R~ without its diagonal blocks).  If it holds, the diagonal blocks are applied as
+ *   products with Y_J on the FP64 tensor cores (n in (32, 128] and the first 128 columns for
+ *   n > 128); otherwise, and for the other blocks, by substitution.
+ * SUBST: always substitution (the paper's row-wise forward substitution).
+ * INVERSE: always the Y_J products where built (tests; no guard). */
+enum { SCQR3_TRSM_DIAG_AUTO = 0, SCQR3_TRSM_DIAG_SUBST = 1, SCQR3_TRSM_DIAG_INVERSE = 2 };
 
 typedef struct scqr3_pass_trace {
   double shift;            /* shift added on this pass (0 if none)                     */
@@ -113,6 +125,7 @@ typedef struct scqr3_opts {
   int32_t trace_cap;
   int32_t* passes_out;     /* host; number of passes executed (may be NULL)            */
   scqr3_prof* prof;        /* host; per-kernel device time (may be NULL)                */
+  int32_t trsm_diag;       /* SCQR3_TRSM_DIAG_* (default AUTO; ABI version 2)           */
 } scqr3_opts;
 
 /* Fills *o with the defaults above (abi_version, SAFE, POWER, 32 iterations, 8 passes,

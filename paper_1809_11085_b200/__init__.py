@@ -14,7 +14,8 @@ from dataclasses import dataclass, field
 
 from . import _abi
 from ._abi import (EBREAKDOWN, EINVAL, ENOCONV, NORM_FROBENIUS, NORM_POWER, NORM_USER, OK,  # noqa: F401
-                   SHIFT_ADAPTIVE, SHIFT_FIXED, SHIFT_NONE, SHIFT_PRACTICAL, SHIFT_SAFE)
+                   SHIFT_ADAPTIVE, SHIFT_FIXED, SHIFT_NONE, SHIFT_PRACTICAL, SHIFT_SAFE,
+                   TRSM_DIAG_AUTO, TRSM_DIAG_INVERSE, TRSM_DIAG_SUBST)
 
 __all__ = [
     "scqr3_factor", "scqr3_factor_oblique", "scqr3_factor_host", "scqr3_gram", "scqr3_gram_oblique",
@@ -144,7 +145,7 @@ class Comm:
 
 def _opts(shift_mode=SHIFT_SAFE, shift_value=0.0, norm_mode=NORM_POWER, norm2_bound=0.0, bnorm_bound=0.0,
           max_passes=8, stop_tol=0.5, power_iters=32, m_global=0, stream=None, comm=None, ws=None,
-          trace_cap=16, prof=None, deterministic=False):
+          trace_cap=16, prof=None, deterministic=False, trsm_diag=0):
     torch = _torch()
     o = _abi.Opts()
     _abi.lib().scqr3_default_opts(ctypes.byref(o))
@@ -153,6 +154,7 @@ def _opts(shift_mode=SHIFT_SAFE, shift_value=0.0, norm_mode=NORM_POWER, norm2_bo
     o.max_passes, o.stop_tol, o.power_iters = int(max_passes), float(stop_tol), int(power_iters)
     o.m_global = int(m_global)
     o.deterministic = 1 if deterministic else 0
+    o.trsm_diag = int(trsm_diag)  # TRSM_DIAG_AUTO / _SUBST / _INVERSE (reading D24)
     if stream is None:
         stream = torch.cuda.current_stream()
     o.stream = ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))

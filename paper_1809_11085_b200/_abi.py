@@ -7,10 +7,11 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SCQR3_LIB") or os.path.join(HERE, "libscqr3.so")
 
-SCQR3_ABI_VERSION = 1
+SCQR3_ABI_VERSION = 2
 OK, EINVAL, EBREAKDOWN, ENOCONV = 0, 1, 2, 3
 SHIFT_SAFE, SHIFT_FIXED, SHIFT_NONE, SHIFT_ADAPTIVE, SHIFT_PRACTICAL = 0, 1, 2, 3, 4
 NORM_POWER, NORM_FROBENIUS, NORM_USER = 0, 1, 2
+TRSM_DIAG_AUTO, TRSM_DIAG_SUBST, TRSM_DIAG_INVERSE = 0, 1, 2
 COMM_ID_BYTES = 128
 
 EXPORTED = [
@@ -61,6 +62,7 @@ class Opts(ctypes.Structure):
         ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
         ("trace", ctypes.POINTER(PassTrace)), ("trace_cap", ctypes.c_int32),
         ("passes_out", ctypes.POINTER(ctypes.c_int32)), ("prof", ctypes.POINTER(Prof)),
+        ("trsm_diag", ctypes.c_int32),
     ]
 
 

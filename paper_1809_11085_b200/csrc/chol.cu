@@ -615,6 +615,124 @@ __device__ __forceinline__ double rload(const double* W, int ldw, int n, int i, 
   return (i < n && j < n) ? (i <= j ? x : 0.0) : (i == j ? 1.0 : 0.0);
 }
 
+// Reading D24: the TRSM may apply R~'s 8 x 8 diagonal blocks D_J as products with inverses Y_J
+// (one DMMA k-step pair per block on the tensor cores instead of a latency-bound substitution
+// chain) when that keeps every row's backward error inside the paper's bound (eq. DeltaRbound,
+// P:328-331): ||dR_i||_2 <= gamma_n sqrt(n) ||R~||_2.  Rows of Y_J are computed by substitution
+// (y D_J = e_i), so |Y_J D_J - I| <= gamma_8 |Y_J||D_J|, and a row solved as q_J = fl(b_J Y_J)
+// satisfies |q_J D_J - b_J| <= 2 gamma_8 |q_J||D_J||Y_J||D_J| (first order): a rank-one
+// perturbation of D_J of 2-norm <= 2 gamma_8 mu_J, mu_J = || |D_J||Y_J||D_J| ||_F.  The blocks off
+// the diagonal are applied as in substitution (|dR| <= gamma_n |R~_off|).  Hence the guard
+//     gamma_n ||R~_off||_F + 2 gamma_8 max_J mu_J  <=  gamma_n sqrt(n) max_j ||R~ e_j||_2
+// (the right side <= the paper's bound).  Block-wide (blockDim.x == 256): writes Y_J as DMMA B
+// fragments (k-step h, lane l: Y[2(l&3)+h][l>>2]) to dblk + dinv_off(NT) and the flag (1: inverse
+// path) to dblk[dflag_off(NT)]; mode SCQR3_TRSM_DIAG_SUBST / _INVERSE forces 0 / 1.
+// rp(i, j): R~(i, j) for i <= j < n, 0 below the diagonal, the identity past n.
+template <class RP>
+__device__ __forceinline__ void trsm_diag_guard(RP rp, int n, int NT, double* dblk, int mode) {
+  __shared__ double gred[3][8];
+  const int tid = threadIdx.x, lane = tid & 31;
+  double mu2max = 0.0;
+  for (int x0 = 0; x0 < NT * 8; x0 += 256) {  // thread (J, i): row i of Y_J (uniform trip count)
+    const int x = x0 + tid, J = min(x >> 3, NT - 1), i = x & 7;
+    double d[8][8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) d[k][j] = k <= j ? rp(8 * J + k, 8 * J + j) : 0.0;
+    double y[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {  // y_j = (delta_ij - sum_{i <= l < j} y_l d_lj) / d_jj
+      double s = j == i ? 1.0 : 0.0;
+#pragma unroll
+      for (int l = 0; l < j; ++l) s = l >= i ? fma(-y[l], d[l][j], s) : s;
+      y[j] = j >= i ? s / d[j][j] : 0.0;
+    }
+    if (x < NT * 8) {
+      double* dinv = dblk + dinv_off(NT) + J * 64 + (i & 1) * 32 + (i >> 1);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) dinv[4 * j] = y[j];
+    }
+    double tr[8];  // row i of |Y||D|
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      double v = 0.0;
+#pragma unroll
+      for (int k = 0; k <= j; ++k) v += fabs(y[k]) * fabs(d[k][j]);
+      tr[j] = v;
+    }
+    // row i of M = |D| |Y||D| (rows k >= i of |Y||D| from the group's lanes); past n excluded
+    double mu2 = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      double v = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double tk = __shfl_sync(0xffffffffu, tr[j], (lane & ~7) | k);
+        v += k >= i ? fabs(d[i][k]) * tk : 0.0;
+      }
+      if (8 * J + i < n && 8 * J + j < n) mu2 += v * v;
+    }
+    mu2 += __shfl_xor_sync(0xffffffffu, mu2, 1);
+    mu2 += __shfl_xor_sync(0xffffffffu, mu2, 2);
+    mu2 += __shfl_xor_sync(0xffffffffu, mu2, 4);
+    if (x < NT * 8) mu2max = fmax(mu2max, mu2);
+  }
+  // ||R~ e_j||_2^2 per column and ||R~_off||_F^2: warp w sums the rows i = w, w + 8, ... of the
+  // columns j = j0 + lane (coalesced for row-major R~, loads independent); the warps' partials of
+  // a column are added in warp order (the flag is a deterministic function of R~)
+  __shared__ double gpart[8][32];
+  const int warp = tid >> 5;
+  double off2 = 0.0, col2max = 0.0;
+  for (int j0 = 0; j0 < n; j0 += 32) {
+    const int j = j0 + lane, iend = min(j0 + 32, n);
+    double c = 0.0;
+#pragma unroll 4
+    for (int i = warp; i < iend; i += 8) {
+      const double r = (j < n && i <= j) ? rp(i, j) : 0.0;
+      c = fma(r, r, c);
+      off2 = (i >> 3) != (j >> 3) ? fma(r, r, off2) : off2;
+    }
+    gpart[warp][lane] = c;
+    __syncthreads();
+    if (warp == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += gpart[w][lane];
+      col2max = fmax(col2max, t);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mu2max = fmax(mu2max, __shfl_xor_sync(0xffffffffu, mu2max, o));
+    off2 += __shfl_xor_sync(0xffffffffu, off2, o);
+    col2max = fmax(col2max, __shfl_xor_sync(0xffffffffu, col2max, o));
+  }
+  if (lane == 0) {
+    gred[0][tid >> 5] = mu2max;
+    gred[1][tid >> 5] = off2;
+    gred[2][tid >> 5] = col2max;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0.0, b = 0.0, c = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      a = fmax(a, gred[0][w]);
+      b += gred[1][w];
+      c = fmax(c, gred[2][w]);
+    }
+    constexpr double u = 1.1102230246251565e-16;  // 2^-53 (D1)
+    const double g8 = 8.0 * u / (1.0 - 8.0 * u), gn = n * u / (1.0 - n * u);
+    const double lhs = gn * sqrt(b) + 2.0 * g8 * sqrt(a);
+    const double rhs = gn * sqrt(static_cast<double>(n)) * sqrt(c);
+    const bool ok = lhs <= rhs;  // false on NaN
+    dblk[dflag_off(NT)] = mode == SCQR3_TRSM_DIAG_INVERSE ? 1.0 : mode == SCQR3_TRSM_DIAG_SUBST ? 0.0 : (ok ? 1.0 : 0.0);
+    dblk[dflag_off(NT) + 1] = lhs / rhs;
+  }
+  __syncthreads();
+}
+
 // Outputs of a pass.  R~ for trmul_kernel and trsm_prep_kernel, row-major (Rt[i n + j], zero
 // below the diagonal): consecutive threads read consecutive entries of a row of W (no bank
 // conflicts in shared memory, coalesced from L2 when W is global) and store consecutive
@@ -624,7 +742,7 @@ __device__ __forceinline__ double rload(const double* W, int ldw, int n, int i, 
 // CTAs (on this one CTA they took 13 K cycles at n = 128 and 73 K at n = 256).
 template <bool SMEM>
 __device__ __noinline__ void write_outputs(const double* Wg, int ldw, int n, int NT, double* bfrag, double* dblk,
-                                           double* Rt) {
+                                           double* Rt, int diag_mode) {
   extern __shared__ double smdyn[];
   const double* W = SMEM ? smdyn : Wg;
   constexpr int kU = 8;
@@ -655,6 +773,7 @@ __device__ __noinline__ void write_outputs(const double* Wg, int ldw, int n, int
       const double rcj = rload(W, ldw, n, c, j), rcc = rload(W, ldw, n, c, c);
       dblk[idx] = w < 64 ? (j > c ? rcj / rcc : 0.0) : 1.0 / rcc;
     }
+    trsm_diag_guard([&](int i, int j) { return rload(W, ldw, n, i, j); }, n, NT, dblk, diag_mode);
   }
 #ifdef SCQR3_CHOL_OUTCLK
   long long o1 = clock64();
@@ -811,7 +930,7 @@ __device__ __forceinline__ void chol_body(const CholParams& p, double* smW) {
   }
   const int code = piv ? SCQR3_EBREAKDOWN : SCQR3_OK;
   clk[4] = clock64();
-  if (code == SCQR3_OK) write_outputs<SMEM>(W, ldw, n, p.NT, p.bfrag, p.dblk, p.Rt);
+  if (code == SCQR3_OK) write_outputs<SMEM>(W, ldw, n, p.NT, p.bfrag, p.dblk, p.Rt, p.trsm_diag);
   if (tid == 0) {
     DevStatus st{};
     st.code = code;
@@ -1015,15 +1134,19 @@ __global__ void copy_kernel(const double* src, double* dst, long long count, con
 // the identity past n.  In a pass it runs after chol_kernel (skipped when that failed or after a
 // stop); also used by the kernel-level scqr3_trsm API and the complex path.
 __global__ void trsm_prep_kernel(const double* R, int n, int NT, double* bfrag, double* dblk, int rowmajor,
-                                 const DevStatus* st, PassGate gate) {
+                                 const DevStatus* st, PassGate gate, int diag_mode) {
   if (SCQR3_GATE_SKIP(gate) || (st && st->code != SCQR3_OK)) return;
   auto rp = [&](int i, int j) -> double {
     if (i < n && j < n)
       return i <= j ? R[rowmajor ? static_cast<size_t>(i) * n + j : i + static_cast<size_t>(j) * n] : 0.0;
     return i == j ? 1.0 : 0.0;
   };
+  if (blockIdx.x == gridDim.x - 1) {  // the guard CTA (trsm_prep_blocks: launched with 256 threads)
+    trsm_diag_guard(rp, n, NT, dblk, diag_mode);
+    return;
+  }
   const int nf = NT * (NT - 1) * 32;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nf + NT * 72; idx += gridDim.x * blockDim.x) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nf + NT * 72; idx += (gridDim.x - 1) * blockDim.x) {
     if (idx < nf) {
       const int f = idx >> 5, lane = idx & 31;
       int J = 1;

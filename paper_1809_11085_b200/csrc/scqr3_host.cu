@@ -212,7 +212,7 @@ Layout make_layout(int64_t m, int64_t n, int oblique, int64_t halo = 1) {
   L.Rnew = take(static_cast<size_t>(n) * n * 8);
   L.Rt = take(static_cast<size_t>(n) * n * 8);
   L.bfrag = take(static_cast<size_t>(L.NT) * (L.NT - 1) * 32 * 8 + 8);
-  L.dblk = take(static_cast<size_t>(L.NT) * 72 * 8);
+  L.dblk = take(static_cast<size_t>(dblk_doubles(L.NT)) * 8);
   L.misc = take(64 * 8);  // [0] nb, [1] e_prev, [2] m_global (int64), ...
   L.colsq = oblique ? take(4096 * 8) : off;
   L.y = oblique ? take(static_cast<size_t>(L.ldy) * n * 8) : off;
@@ -251,6 +251,7 @@ int check_opts(const scqr3_opts* o) {
   if (o->abi_version != SCQR3_ABI_VERSION) return fail("abi_version %d != %d", o->abi_version, SCQR3_ABI_VERSION);
   if (o->shift_mode < 0 || o->shift_mode > 4) return fail("bad shift_mode %d", o->shift_mode);
   if (o->norm_mode < 0 || o->norm_mode > 2) return fail("bad norm_mode %d", o->norm_mode);
+  if (o->trsm_diag < 0 || o->trsm_diag > 2) return fail("bad trsm_diag %d", o->trsm_diag);
   if (o->norm_mode == SCQR3_NORM_USER && !(o->norm2_bound > 0)) return fail("NORM_USER needs norm2_bound > 0");
   if (o->shift_mode == SCQR3_SHIFT_FIXED && !(o->shift_value >= 0)) return fail("SHIFT_FIXED needs shift_value >= 0");
   return SCQR3_OK;
@@ -797,6 +798,7 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
   const bool prep_launch = n > 64;
   cp.bfrag = prep_launch ? nullptr : w.bfrag;
   cp.dblk = prep_launch ? nullptr : w.dblk;
+  cp.trsm_diag = o->trsm_diag;
   cp.st_dev = w.st;
   cp.st_host = c->st_host_dev;
 
@@ -805,6 +807,8 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
   tp.n = static_cast<int>(n);
   tp.bfrag = w.bfrag;
   tp.dblk = w.dblk;
+  tp.dinv = w.dblk + dinv_off(L.NT);
+  tp.inv_flag = o->trsm_diag == SCQR3_TRSM_DIAG_SUBST ? nullptr : w.dblk + dflag_off(L.NT);  // reading D24
   tp.st = w.st;
   tp.Q = Q;
   tp.ldq = ldq;
@@ -891,9 +895,8 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
     }
     TRY(launch_chol(cp, st));
     if (prep_launch) {  // R~ (row-major) -> the TRSM's B fragments and scaled diagonal blocks, on many CTAs
-      const int tot = L.NT * (L.NT - 1) * 32 + L.NT * 72;
-      trsm_prep_kernel<<<(tot + 255) / 256, 256, 0, st>>>(w.Rt, static_cast<int>(n), L.NT, w.bfrag, w.dblk, 1, w.st,
-                                                           gate);
+      trsm_prep_kernel<<<trsm_prep_blocks(L.NT), 256, 0, st>>>(w.Rt, static_cast<int>(n), L.NT, w.bfrag, w.dblk, 1,
+                                                                w.st, gate, o->trsm_diag);
       ++g_launches;
       CUDA_TRY(cudaGetLastError());
     }
@@ -914,7 +917,7 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
       const int pt = prof_begin(c, PK_TRSM);
       CUDA_TRY(launch_trsm(tp, use_tma ? &mx : nullptr, c->num_sms, st, &fused_chunks, fuse_tg ? &mq : nullptr));
       prof_end(c, pt);
-      ++g_launches;
+      g_launches += trsm_launch_count(tp, use_tma);
     }
     return SCQR3_OK;
   };
@@ -1116,6 +1119,8 @@ int zfactor_impl(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, i
   tp.n = n2;
   tp.bfrag = w.bfrag;
   tp.dblk = w.dblk;
+  tp.dinv = w.dblk + dinv_off(L.NT);
+  tp.inv_flag = o->trsm_diag == SCQR3_TRSM_DIAG_SUBST ? nullptr : w.dblk + dflag_off(L.NT);  // guard on M (D24)
   tp.st = w.st;
   tp.X = S;
   tp.ldx = Z.lds;
@@ -1152,8 +1157,8 @@ int zfactor_impl(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, i
     }
     ++g_launches;
     CUDA_TRY(cudaGetLastError());
-    const int tot = L.NT * (L.NT - 1) * 32 + L.NT * 72;
-    trsm_prep_kernel<<<(tot + 255) / 256, 256, 0, st>>>(w.Rt, n2, L.NT, w.bfrag, w.dblk, 0, nullptr, gate);  // M -> TRSM operands
+    trsm_prep_kernel<<<trsm_prep_blocks(L.NT), 256, 0, st>>>(w.Rt, n2, L.NT, w.bfrag, w.dblk, 0, nullptr, gate,
+                                                              o->trsm_diag);  // M -> TRSM operands
     ++g_launches;
     CUDA_TRY(cudaGetLastError());
     prof_end(c, pc);
@@ -1178,7 +1183,7 @@ int zfactor_impl(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, i
       CUDA_TRY(launch_trsm(tp, use_tma ? &mx : nullptr, c->num_sms, st, &fused_chunks,
                            fuse_tg && use_tma ? &mx : nullptr));
       prof_end(c, pt);
-      ++g_launches;
+      g_launches += trsm_launch_count(tp, use_tma);
     }
     CUDA_TRY(cudaEventSynchronize(c->ev_pass[k - 1]));
     const volatile DevStatus* h = c->st_host + (k - 1);
@@ -1433,9 +1438,8 @@ int scqr3_trsm(int64_t m, int64_t n, const double* X, int64_t ld, const double* 
   WS w;
   TRY(carve(L, opts, &w));
   cudaStream_t st = static_cast<cudaStream_t>(opts->stream);
-  const int tot = L.NT * (L.NT - 1) * 32 + L.NT * 72;
-  trsm_prep_kernel<<<(tot + 255) / 256, 256, 0, st>>>(R, static_cast<int>(n), L.NT, w.bfrag, w.dblk, 0, nullptr,
-                                                     PassGate{});
+  trsm_prep_kernel<<<trsm_prep_blocks(L.NT), 256, 0, st>>>(R, static_cast<int>(n), L.NT, w.bfrag, w.dblk, 0, nullptr,
+                                                          PassGate{}, opts->trsm_diag);
   ++g_launches;
   CUDA_TRY(cudaGetLastError());
   TrsmParams tp{};
@@ -1447,13 +1451,15 @@ int scqr3_trsm(int64_t m, int64_t n, const double* X, int64_t ld, const double* 
   tp.n = static_cast<int>(n);
   tp.bfrag = w.bfrag;
   tp.dblk = w.dblk;
+  tp.dinv = w.dblk + dinv_off(L.NT);
+  tp.inv_flag = opts->trsm_diag == SCQR3_TRSM_DIAG_SUBST ? nullptr : w.dblk + dflag_off(L.NT);  // reading D24
   tp.st = nullptr;
   if (m > 0) {
     CUtensorMap mx;
     const bool use_tma = L.NT <= 16 || L.NT >= 24;
     if (use_tma) TRY(encode_map(c, &mx, X, m, L.NT >= 24 ? 128 : n, ld, trsm_x_box_cols(L.NT)));
     CUDA_TRY(launch_trsm(tp, use_tma ? &mx : nullptr, c->num_sms, st));
-    ++g_launches;
+    g_launches += trsm_launch_count(tp, use_tma);
   }
   CUDA_TRY(cudaStreamSynchronize(st));
   return SCQR3_OK;

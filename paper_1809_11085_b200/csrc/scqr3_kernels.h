@@ -118,7 +118,8 @@ struct CholParams {
   double* R;                 // CHOL_ONLY output (n x n col-major)
   double* Rt;                // CHOL_PASS: R~ of this pass (n x n row-major) for trmul_kernel, trsm_prep_kernel
   double* bfrag;             // TRSM B fragments (negated R~), NT(NT-1) x 32, written here when
-  double* dblk;              //   non-null (n <= 64), else by trsm_prep_kernel; diagonal blocks NT x 72
+  double* dblk;              //   non-null (n <= 64), else by trsm_prep_kernel; diagonal-block data (dblk_doubles)
+  int trsm_diag;             // SCQR3_TRSM_DIAG_*: how the diagonal-block guard flag is set (reading D24)
   DevStatus* st_dev;
   DevStatus* st_host;        // host-mapped per-pass slots (st_host[pass-1]; may be null)
   int* last_pass;            // device-side pass control (may be null): written on stop / error
@@ -169,7 +170,10 @@ struct TrsmParams {
   long long m;
   int n;
   const double* bfrag;
-  const double* dblk;
+  const double* dblk;        // substitution tables of this launch's diagonal blocks (72 doubles each)
+  const double* dinv;        // B fragments of the inverted diagonal blocks (64 doubles each; reading D24)
+  const double* inv_flag;    // null: substitution only; else *inv_flag > 0 selects the inverse
+                             // instance (trsm_kernel<..., INV = true>), 0 the substitution one
   const DevStatus* st;       // skip when st->code != 0 (may be null)
   double* gram_partials;     // fused next-pass Gram (n <= 64): one NT(NT+1)/2-tile partial per CTA
 };
@@ -199,7 +203,7 @@ __global__ void trmul_kernel(const double* Rt, const double* R, double* Rnew, in
                              PassGate gate);
 __global__ void copy_kernel(const double* src, double* dst, long long count, const DevStatus* st, PassGate gate);
 __global__ void trsm_prep_kernel(const double* R, int n, int NT, double* bfrag, double* dblk, int rowmajor,
-                                 const DevStatus* st, PassGate gate);
+                                 const DevStatus* st, PassGate gate, int diag_mode);  // grid: trsm_prep_blocks(NT) x 256
 __global__ void z2split_kernel(const double* Z, long long ldz, long long m, int n, double* S, long long lds);
 __global__ void split2z_kernel(const double* S, long long lds, long long m, int n, double* Z, long long ldz);
 __global__ void zcombine_kernel(const double* tiles, int n, double* A, const int* last_pass, int pass);
@@ -262,9 +266,21 @@ inline cudaError_t cached_launch_cfg(LaunchCfgCache& cc, K kernel, size_t smem, 
 cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream,
                         int* grid_out = nullptr, const CUtensorMap* mapQ = nullptr);
 inline bool trsm_fuses_gram(int NT) { return NT <= 8; }
+int trsm_launch_count(const TrsmParams& p, bool tma);
 // width of the TMA box of X the TRSM launcher expects (the map of the first 128 columns for
 // NT >= 24; a narrower box where the kernel reads the later columns from global memory)
 int trsm_x_box_cols(int NT);
+
+// Diagonal-block data of the TRSM (workspace region dblk, NT = npad / 8 blocks):
+//   [NT x 72]  substitution tables: strict upper r_cj / r_cc (64) + reciprocal pivots (8)
+//   [NT x 64]  B fragments of the inverted blocks Y_J = D_J^{-1} (k-step h, lane l: Y[2(l&3)+h][l>>2])
+//   [1]        guard flag (1: every Y_J keeps the row-wise backward error within eq. (DeltaRbound),
+//              reading D24; 0: substitution); [1] the guard's ratio (diagnostics)
+__host__ __device__ constexpr int dinv_off(int NT) { return NT * 72; }
+__host__ __device__ constexpr int dflag_off(int NT) { return NT * 136; }
+__host__ __device__ constexpr int dblk_doubles(int NT) { return NT * 136 + 8; }
+// trsm_prep_kernel grid: the operand CTAs plus one guard CTA (last block)
+inline int trsm_prep_blocks(int NT) { return (NT * (NT - 1) * 32 + NT * 72 + 255) / 256 + 1; }
 
 inline int npad_for(int n) {
   // tile counts with a compiled TRSM instance

@@ -75,6 +75,12 @@ constexpr TrsmSched<NT> make_trsm_sched() {
   }
   return r;
 }
+#ifndef SCQR3_INV_K0
+#define SCQR3_INV_K0 2  // chain slots of the two inverse k-steps (INV instances)
+#endif
+#ifndef SCQR3_INV_K1
+#define SCQR3_INV_K1 5
+#endif
 #ifndef SCQR3_TRSM_CAP
 #define SCQR3_TRSM_CAP 8  // updates per diagonal chain for NT = 16 (>= 1000: right-looking)
 #endif
@@ -99,11 +105,16 @@ static_assert(trsm_sched_ok<16, SCQR3_TRSM_CAP>(), "TRSM update schedule");
 // rows to a private swizzled stage and accumulates their Gram (all upper 8x8 tiles) in registers;
 // at the end the CTA sums its warps in a fixed order and writes one partial (gram_reduce_kernel
 // sums the partials of all CTAs, as after gram_tma_kernel).  Skipped when this pass stops.
-template <int NT, int A, bool SMEM_B, int THREADS, bool TMA, bool GRAM = false>
+// INV (reading D24): the diagonal blocks are applied as products with their inverses Y_J (two
+// DMMA k-steps per block, B fragments from chol / trsm_prep) instead of the substitution chain;
+// launched beside the substitution instance, each exits unless *p.inv_flag selects it.
+template <int NT, int A, bool SMEM_B, int THREADS, bool TMA, bool GRAM = false, bool INV = false>
 __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant__ CUtensorMap mapX,
                                                           const __grid_constant__ CUtensorMap mapQ, TrsmParams p) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   if (SCQR3_GATE_SKIP(p.gate) || (p.st && p.st->code != 0)) return;
+  static_assert(!INV || A % 2 == 0, "inverse diagonal blocks: paired fragments");
+  if (INV ? !(p.inv_flag && *p.inv_flag > 0.0) : (p.inv_flag && *p.inv_flag > 0.0)) return;
   static_assert(!GRAM || (A == 2 && TMA), "fused Gram: 16-row groups per warp");
   constexpr int NTS = NT * (NT + 1) / 2;  // upper 8x8 tiles of the Gram
   const bool do_gram = GRAM && p.gram_partials && !(p.st && p.st->stop);
@@ -126,13 +137,14 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + (SMEM_B ? NF * 32 : 0) + NT * 72);
   const double* bf;
   const double* db;
+  const double* dsrc = INV ? p.dinv : p.dblk;  // (INV: 64 of the 72 slots per block)
   if (SMEM_B) {
     for (int i = threadIdx.x; i < NF * 32 + NT * 72; i += THREADS)
-      sm[i] = i < NF * 32 ? p.bfrag[i] : p.dblk[i - NF * 32];
+      sm[i] = i < NF * 32 ? p.bfrag[i] : (INV && i - NF * 32 >= NT * 64 ? 0.0 : dsrc[i - NF * 32]);
     bf = sm;
     db = sm + NF * 32;
   } else {
-    for (int i = threadIdx.x; i < NT * 72; i += THREADS) sm[i] = p.dblk[i];
+    for (int i = threadIdx.x; i < NT * 72; i += THREADS) sm[i] = INV && i >= NT * 64 ? 0.0 : dsrc[i];
     bf = p.bfrag;
     db = sm;
   }
@@ -262,7 +274,8 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
       // and a fixed-latency wait in between).
       auto later_updates = [&](int c) {
 #if SCQR3_TRSM_CAP < 1000
-       if constexpr (NT == 16) {
+       // (INV: no chain latency to hide; right-looking measured best, 5.25 -> 5.20 ms at C3)
+       if constexpr (NT == 16 && !INV) {
         // the chain hosts the schedule's updates: update i's first k-step in chain step
         // i * 8 / cnt, its second one step later, issued before that step's first k-steps (a
         // target's updates therefore keep their order; trsm_sched_ok checks that no two
@@ -310,7 +323,32 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
         }
 #endif
       };
-      if constexpr (A % 2 == 0) {
+      if constexpr (INV) {
+        // q_J = b_J Y_J: k-step h takes the C fragment's element h as the A operand (columns
+        // 2t + h), Y_J's rows 2t + h as B; between the k-steps and after them, the later updates
+        const double* Y = db + J * 64;
+        const double y0 = Y[lane], y1 = Y[32 + lane];
+        double acc[A][2];
+#pragma unroll
+        for (int a = 0; a < A; ++a) acc[a][0] = acc[a][1] = 0.0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (c == SCQR3_INV_K0) {
+#pragma unroll
+            for (int a = 0; a < A; ++a) dmma(acc[a][0], acc[a][1], q[a][J][0], y0);
+          }
+          if (c == SCQR3_INV_K1) {
+#pragma unroll
+            for (int a = 0; a < A; ++a) dmma(acc[a][0], acc[a][1], q[a][J][1], y1);
+          }
+          later_updates(c);
+        }
+#pragma unroll
+        for (int a = 0; a < A; ++a) {
+          q[a][J][0] = acc[a][0];
+          q[a][J][1] = acc[a][1];
+        }
+      } else if constexpr (A % 2 == 0) {
         // Fragment pairs (a, a+1) = rows g and g+8 of the quad.  Lanes t^2 swap halves so that
         // lanes t = 0,1 hold row g and lanes t = 2,3 row g+8, four columns each: lane u = t&1
         // holds columns {2u, 2u+1, 2u+4, 2u+5} (V[0..3]).  Step c then updates only the
@@ -471,7 +509,7 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_kernel(const __grid_constant_
   }
 }
 
-template <int NT, int A, bool SMEM_B, int THREADS, bool TMA, bool GRAM = false>
+template <int NT, int A, bool SMEM_B, int THREADS, bool TMA, bool GRAM = false, bool INV = false>
 static cudaError_t launch_one(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream,
                               int* grid_out = nullptr, const CUtensorMap* mapQ = nullptr) {
   constexpr int NF = NT * (NT - 1);
@@ -480,7 +518,7 @@ static cudaError_t launch_one(const TrsmParams& p, const CUtensorMap* map, int n
   constexpr size_t kSlot = 16u * NT * 8 * 8 * (RS / 16 > 0 ? RS / 16 : 1);
   const size_t smem = 1024 + (TMA ? WPB * kSlot : 0) + (GRAM ? WPB * 16u * NT * 8 * 8 : 0) +
                       static_cast<size_t>((SMEM_B ? NF * 32 : 0) + NT * 72) * 8 + WPB * 8;
-  auto k = trsm_kernel<NT, A, SMEM_B, THREADS, TMA, GRAM>;
+  auto k = trsm_kernel<NT, A, SMEM_B, THREADS, TMA, GRAM, INV>;
   static thread_local LaunchCfgCache cfg;
   int per_sm = 0;
   cudaError_t e = cached_launch_cfg(cfg, k, smem, THREADS, &per_sm);
@@ -495,6 +533,19 @@ static cudaError_t launch_one(const TrsmParams& p, const CUtensorMap* map, int n
   k<<<static_cast<unsigned>(grid), THREADS, smem, stream>>>(map ? *map : dummy, mapQ ? *mapQ : dummy, p);
   if (grid_out) *grid_out = static_cast<int>(grid);
   return cudaGetLastError();
+}
+
+// Reading D24: with p.inv_flag set, the inverse-diagonal instance and the substitution instance
+// are both enqueued; the guard flag (written on the device by chol / trsm_prep) lets one run and
+// the other exit at entry (no host round trip; also inside the CUDA-graph pass loop).
+template <int NT, int A, bool SMEM_B, int THREADS, bool TMA, bool GRAM = false>
+static cudaError_t launch_pair(const TrsmParams& p, const CUtensorMap* map, int num_sms, cudaStream_t stream,
+                               int* grid_out = nullptr, const CUtensorMap* mapQ = nullptr) {
+  if (p.inv_flag) {
+    cudaError_t e = launch_one<NT, A, SMEM_B, THREADS, TMA, GRAM, true>(p, map, num_sms, stream, grid_out, mapQ);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_one<NT, A, SMEM_B, THREADS, TMA, GRAM, false>(p, map, num_sms, stream, grid_out, mapQ);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -805,6 +856,29 @@ static cudaError_t launch_wide(const TrsmParams& p, int num_sms, cudaStream_t st
 // Width of the TMA box of X that launch_trsm expects for NT column tiles (host: encode_map).
 int trsm_x_box_cols(int NT) { return NT >= 24 ? 128 : NT * 8; }
 
+// Kernel launches launch_trsm issues for p (the inverse-diagonal instance counts as a launch
+// even when the guard lets it exit at entry).
+int trsm_launch_count(const TrsmParams& p, bool tma) {
+  const int NT = npad_for(p.n) / 8;
+  const int inv = p.inv_flag ? 1 : 0;
+  if (p.gram_partials) return 1 + (NT == 8 ? inv : 0);
+  switch (NT) {
+    case 8: case 12: case 16: return 1 + (tma ? inv : 0);
+    case 24: return tma ? 2 + inv : 1;
+    case 32: return tma ? 2 + inv : 1;
+    case 64: {
+      const int first = tma ? 2 + inv : 1;  // columns 0..255
+#ifdef SCQR3_WIDE512_PHASED
+      return first + 1;
+#else
+      const int nb = (p.n + 7) / 8;
+      return first + 1 + (nb > 40) + (nb > 48) + (nb > 56) + (nb > 60);
+#endif
+    }
+    default: return 1;
+  }
+}
+
 // map: TMA descriptor of X with a {16 rows, npad columns} SWIZZLE_128B box (instances with
 // NT <= 16 use it when map != nullptr; NT >= 24: a {16, 128} box of the first 128 columns); the
 // others read X with plain coalesced loads.
@@ -812,34 +886,38 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
                         int* grid_out, const CUtensorMap* mapQ) {
   const int NT = npad_for(p.n) / 8;
   const bool tma = map != nullptr;
+  // instances with inverse diagonal blocks (reading D24): n in (32, 128] through the TMA path and
+  // the first 128 columns of n > 128; everything else substitutes
+  TrsmParams ps = p;
+  ps.inv_flag = nullptr;
   if (p.gram_partials) {  // fused TRSM + next-pass Gram (A = 2, TMA)
     if (!tma || !mapQ) return cudaErrorInvalidValue;
     switch (NT) {
-      case 1: return launch_one<1, 2, true, 256, true, true>(p, map, num_sms, stream, grid_out, mapQ);
-      case 2: return launch_one<2, 2, true, 256, true, true>(p, map, num_sms, stream, grid_out, mapQ);
-      case 4: return launch_one<4, 2, true, 256, true, true>(p, map, num_sms, stream, grid_out, mapQ);
-      case 8: return launch_one<8, 2, true, 256, true, true>(p, map, num_sms, stream, grid_out, mapQ);
+      case 1: return launch_one<1, 2, true, 256, true, true>(ps, map, num_sms, stream, grid_out, mapQ);
+      case 2: return launch_one<2, 2, true, 256, true, true>(ps, map, num_sms, stream, grid_out, mapQ);
+      case 4: return launch_one<4, 2, true, 256, true, true>(ps, map, num_sms, stream, grid_out, mapQ);
+      case 8: return launch_pair<8, 2, true, 256, true, true>(p, map, num_sms, stream, grid_out, mapQ);
       default: return cudaErrorInvalidValue;
     }
   }
   switch (NT) {
-    case 1: return launch_one<1, 4, true, 256, false>(p, nullptr, num_sms, stream);
-    case 2: return tma ? launch_one<2, 4, true, 256, true>(p, map, num_sms, stream)
-                       : launch_one<2, 4, true, 256, false>(p, nullptr, num_sms, stream);
-    case 4: return tma ? launch_one<4, 4, true, 256, true>(p, map, num_sms, stream)
-                       : launch_one<4, 4, true, 256, false>(p, nullptr, num_sms, stream);
-    case 8: return tma ? launch_one<8, 4, true, 256, true>(p, map, num_sms, stream)
-                       : launch_one<8, 4, true, 256, false>(p, nullptr, num_sms, stream);
-    case 12: return tma ? launch_one<12, 2, true, 256, true>(p, map, num_sms, stream)
-                        : launch_one<12, 2, true, 256, false>(p, nullptr, num_sms, stream);
-    case 16: return tma ? launch_one<16, 2, true, 256, true>(p, map, num_sms, stream)
-                        : launch_one<16, 2, true, 256, false>(p, nullptr, num_sms, stream);
+    case 1: return launch_one<1, 4, true, 256, false>(ps, nullptr, num_sms, stream);
+    case 2: return tma ? launch_one<2, 4, true, 256, true>(ps, map, num_sms, stream)
+                       : launch_one<2, 4, true, 256, false>(ps, nullptr, num_sms, stream);
+    case 4: return tma ? launch_one<4, 4, true, 256, true>(ps, map, num_sms, stream)
+                       : launch_one<4, 4, true, 256, false>(ps, nullptr, num_sms, stream);
+    case 8: return tma ? launch_pair<8, 4, true, 256, true>(p, map, num_sms, stream)
+                       : launch_one<8, 4, true, 256, false>(ps, nullptr, num_sms, stream);
+    case 12: return tma ? launch_pair<12, 2, true, 256, true>(p, map, num_sms, stream)
+                        : launch_one<12, 2, true, 256, false>(ps, nullptr, num_sms, stream);
+    case 16: return tma ? launch_pair<16, 2, true, 256, true>(p, map, num_sms, stream)
+                        : launch_one<16, 2, true, 256, false>(ps, nullptr, num_sms, stream);
     case 24: {
       // split as for NT = 32: columns 0..127, then targets 16..23 (A = 2)
-      if (!map) return launch_one<24, 1, true, 256, false>(p, nullptr, num_sms, stream);
+      if (!map) return launch_one<24, 1, true, 256, false>(ps, nullptr, num_sms, stream);
       TrsmParams p1 = p;
       p1.n = 128;
-      cudaError_t e = launch_one<16, 2, true, 256, true>(p1, map, num_sms, stream);
+      cudaError_t e = launch_pair<16, 2, true, 256, true>(p1, map, num_sms, stream);
       if (e != cudaSuccess) return e;
       // only the target blocks below n (n = 136: one of the eight)
       const int nb = (p.n + 7) / 8;
@@ -857,7 +935,7 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
       if (!map) return launch_wide<0, 32, 256>(p, num_sms, stream);
       TrsmParams p1 = p;
       p1.n = 128;
-      cudaError_t e = launch_one<16, 2, true, 256, true>(p1, map, num_sms, stream);
+      cudaError_t e = launch_pair<16, 2, true, 256, true>(p1, map, num_sms, stream);
       if (e != cudaSuccess) return e;
       if ((p.n + 7) / 8 <= 28) return launch_wide<16, 28, 256, 2>(p, num_sms, stream);
       return launch_wide<16, 32, 256, 2>(p, num_sms, stream);
@@ -869,7 +947,7 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
       if (map) {
         TrsmParams p1 = p;
         p1.n = 128;
-        e = launch_one<16, 2, true, 256, true>(p1, map, num_sms, stream);
+        e = launch_pair<16, 2, true, 256, true>(p1, map, num_sms, stream);
         if (e != cudaSuccess) return e;
         e = launch_wide<16, 32, 256, 2>(p, num_sms, stream);
       } else {

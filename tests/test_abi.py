@@ -34,7 +34,8 @@ def test_struct_layout_matches_header():
     o = _abi.Opts
     assert o.shift_value.offset == 8 and o.norm2_bound.offset == 24 and o.stop_tol.offset == 48
     assert o.m_global.offset == 56 and o.stream.offset == 64 and o.workspace.offset == 80
-    assert ctypes.sizeof(o) == 128
+    assert o.prof.offset == 120 and o.trsm_diag.offset == 128   # ABI version 2 appends trsm_diag
+    assert ctypes.sizeof(o) == 136
     assert ctypes.sizeof(_abi.Prof) == 96
 
 
