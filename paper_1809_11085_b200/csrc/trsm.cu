@@ -1,7 +1,9 @@
 // trsm.cu -- tall-skinny triangular solve Q = X R~^{-1} (step a5; eq. (3); Alg. 1 line 4
 // P:140; Alg. 2 line 8 P:685).  The paper's per-row model q_i^T = x_i^T (R + dR_i)^{-1} (P:189,
-// P:323-334) holds because every row is solved by (blocked) forward substitution -- no
-// explicit inverse of R~ (or of its diagonal blocks) is formed (reading D11).
+// P:323-334) holds because every row is solved by blocked forward substitution (reading D11) --
+// or, where a per-pass guard proves it keeps ||dR_i||_2 <= gamma_n sqrt(n) ||R~||_2 (eq.
+// DeltaRbound), with the 8x8 diagonal blocks applied as products with their inverses
+// on the tensor cores (INV instances, reading D24).  No inverse of R~ itself is ever formed.
 //
 // Design: rows are independent, so each warp owns 8*A rows and keeps
 // them in registers for the whole solve, as m8n8k4 C fragments (lane g,t holds row g, columns
