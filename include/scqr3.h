@@ -72,8 +72,8 @@ enum { SCQR3_NORM_POWER = 0, SCQR3_NORM_FROBENIUS = 1, SCQR3_NORM_USER = 2 };
  *   paper's bound ||dR_i||_2 <= gamma_n sqrt(n) ||R~||_2 (eq. DeltaRbound):
  *   gamma_n ||R~_off||_F + 2 gamma_8 max_J || |D_J| |Y_J| |D_J| ||_F <= gamma_n sqrt(n) max_j ||R~ e_j||_2
  *   (R~_off: R~ without its diagonal blocks).  If it holds, the diagonal blocks are applied as
- *   products with Y_J on the FP64 tensor cores (n in (32, 128] and the first 128 columns for
- *   n > 128); otherwise, and for the other blocks, by substitution.
+ *   products with Y_J on the FP64 tensor cores (every TRSM instance with 16-row warps: n in
+ *   (32, 128] and all block-column launches of n > 128); otherwise by substitution.
  * SUBST: always substitution (the paper's row-wise forward substitution).
  * INVERSE: always the Y_J products where built (tests; no guard). */
 enum { SCQR3_TRSM_DIAG_AUTO = 0, SCQR3_TRSM_DIAG_SUBST = 1, SCQR3_TRSM_DIAG_INVERSE = 2 };

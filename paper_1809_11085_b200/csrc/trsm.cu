@@ -622,7 +622,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // One phase of the wide TRSM for one warp's 8A rows (fragment a: rows 8a + g); every register
 // index is compile-time.  q[a][k] holds target block TB + k; qe[a] points at this lane's row of
 // the finished Q (blocks < TB).
-template <int TB, int TE, int PH, int A>
+template <int TB, int TE, int PH, int A, bool INV>
 __device__ __forceinline__ void wide_phase(double (&q)[A][TE - TB][2], const double* __restrict__ cur,
                                            const double* __restrict__ db, int lane, int t, const bool (&rok)[A],
                                            const long long (&row)[A], const double* const (&qe)[A],
@@ -680,7 +680,7 @@ __device__ __forceinline__ void wide_phase(double (&q)[A][TE - TB][2], const dou
       for (int s = 2 * (J - 1); s < 2 * J; ++s) upd(J, J - 1, s);
     }
     const int nup = J > K0 ? K1 - 1 - J : 0;
-    const double* D = db + (J - TB) * 72;
+    const double* D = db + (J - TB) * (INV ? 64 : 72);
     auto interleave = [&](int c) {
 #pragma unroll
       for (int u = nup * c / 8; u < nup * (c + 1) / 8; ++u) {
@@ -692,7 +692,31 @@ __device__ __forceinline__ void wide_phase(double (&q)[A][TE - TB][2], const dou
         for (int v = 2 * TB + NS * c / 8; v < 2 * TB + NS * (c + 1) / 8; ++v) upd(J + 1, v >> 1, v);
       }
     };
-    if constexpr (A == 2) {
+    if constexpr (INV) {
+      // reading D24: q_J = b_J Y_J, two DMMA k-steps (as in trsm_kernel), between the updates
+      static_assert(!INV || A == 2, "wide inverse instances: A = 2");
+      const double y0 = D[lane], y1 = D[32 + lane];
+      double acc[A][2];
+#pragma unroll
+      for (int a = 0; a < A; ++a) acc[a][0] = acc[a][1] = 0.0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c == SCQR3_INV_K0) {
+#pragma unroll
+          for (int a = 0; a < A; ++a) dmma(acc[a][0], acc[a][1], q[a][J - TB][0], y0);
+        }
+        if (c == SCQR3_INV_K1) {
+#pragma unroll
+          for (int a = 0; a < A; ++a) dmma(acc[a][0], acc[a][1], q[a][J - TB][1], y1);
+        }
+        interleave(c);
+      }
+#pragma unroll
+      for (int a = 0; a < A; ++a) {
+        q[a][J - TB][0] = acc[a][0];
+        q[a][J - TB][1] = acc[a][1];
+      }
+    } else if constexpr (A == 2) {
       // rows g and g+8: the pair swap of trsm_kernel (lane u = t&1 of each half-quad holds
       // columns {2u, 2u+1, 2u+4, 2u+5} of one row; 18 DFMA per block instead of 28)
       const int uu = t & 1;
@@ -761,23 +785,23 @@ __device__ __forceinline__ void wide_phase(double (&q)[A][TE - TB][2], const dou
 
 // Phases PH.. of one row group: phase PH computes from buffer PH&1 while phase PH+1 (or, after
 // the last phase, the next row group's phase 0) streams into the other one.
-template <int TB, int TE, int PH, int A, typename Stage>
+template <int TB, int TE, int PH, int A, bool INV, typename Stage>
 __device__ __forceinline__ void wide_phases(double (&q)[A][TE - TB][2], double* const (&buf)[2],
                                             const double* db, int lane, int t, bool act, const bool (&rok)[A],
                                             const long long (&row)[A], const double* const (&qe)[A],
                                             const TrsmParams& p, bool more, Stage& stage) {
   constexpr int P = WidePhases<TB, TE>::P;
   if constexpr (P == 1) {  // resident fragments (staged once per launch): no staging, no barrier
-    if (act) wide_phase<TB, TE, 0, A>(q, buf[0], db, lane, t, rok, row, qe, p);
+    if (act) wide_phase<TB, TE, 0, A, INV>(q, buf[0], db, lane, t, rok, row, qe, p);
     return;
   }
   if constexpr (PH + 1 < P) stage(PH + 1, buf[(PH + 1) & 1]);
   else if ((P - 1) & 1) { if (more) stage(0, buf[0]); }  // buf[0] is free during an odd last phase
-  if (act) wide_phase<TB, TE, PH, A>(q, buf[PH & 1], db, lane, t, rok, row, qe, p);
+  if (act) wide_phase<TB, TE, PH, A, INV>(q, buf[PH & 1], db, lane, t, rok, row, qe, p);
   cp_async_wait_all();
   __syncthreads();
   if constexpr (PH + 1 < P) {
-    wide_phases<TB, TE, PH + 1, A>(q, buf, db, lane, t, act, rok, row, qe, p, more, stage);
+    wide_phases<TB, TE, PH + 1, A, INV>(q, buf, db, lane, t, act, rok, row, qe, p, more, stage);
   } else if (!((P - 1) & 1)) {  // even last phase used buf[0]: stage the next phase 0 now
     if (more) {
       stage(0, buf[0]);
@@ -787,15 +811,20 @@ __device__ __forceinline__ void wide_phases(double (&q)[A][TE - TB][2], double* 
   }
 }
 
-template <int TB, int TE, int THREADS, int A>
+template <int TB, int TE, int THREADS, int A, bool INV = false>
 __global__ void __launch_bounds__(THREADS, 1) trsm_wide_kernel(TrsmParams p) {
   constexpr int NTT = TE - TB, WPB = THREADS / 32, MAXF = WidePhases<TB, TE>::MAXF;
   extern __shared__ __align__(16) double smp[];
   if (SCQR3_GATE_SKIP(p.gate) || (p.st && p.st->code != 0)) return;
+  if (INV ? !(p.inv_flag && *p.inv_flag > 0.0) : (p.inv_flag && *p.inv_flag > 0.0)) return;  // reading D24
   constexpr int NBUF = WidePhases<TB, TE>::P == 1 ? 1 : 2;
   double* const buf[2] = {smp, smp + (NBUF - 1) * MAXF * 32};
   double* const db = smp + NBUF * MAXF * 32;
-  for (int i = threadIdx.x; i < NTT * 72; i += THREADS) db[i] = p.dblk[TB * 72 + i];
+  if (INV) {
+    for (int i = threadIdx.x; i < NTT * 64; i += THREADS) db[i] = p.dinv[TB * 64 + i];
+  } else {
+    for (int i = threadIdx.x; i < NTT * 72; i += THREADS) db[i] = p.dblk[TB * 72 + i];
+  }
   auto stage = [&](int ph, double* dst) {  // cooperative cp.async of phase ph's fragments
     const int k0 = WidePhases<TB, TE>::b(ph), k1 = WidePhases<TB, TE>::b(ph + 1);
     const double* src = p.bfrag + static_cast<size_t>(k0) * (k0 - 1) * 32;
@@ -834,15 +863,15 @@ __global__ void __launch_bounds__(THREADS, 1) trsm_wide_kernel(TrsmParams p) {
           const int col = 8 * (TB + J) + 2 * t + h;
           q[a][J][h] = (rok[a] && col < n) ? __ldcs(p.X + row[a] + static_cast<long long>(col) * p.ldx) : 0.0;
         }
-    wide_phases<TB, TE, 0, A>(q, buf, db, lane, t, act, rok, row, qe, p, base + stride < ngroups, stage);
+    wide_phases<TB, TE, 0, A, INV>(q, buf, db, lane, t, act, rok, row, qe, p, base + stride < ngroups, stage);
   }
 }
 
-template <int TB, int TE, int THREADS, int A = 1>
-static cudaError_t launch_wide(const TrsmParams& p, int num_sms, cudaStream_t stream) {
+template <int TB, int TE, int THREADS, int A = 1, bool INV = false>
+static cudaError_t launch_wide1(const TrsmParams& p, int num_sms, cudaStream_t stream) {
   const size_t smem =
       static_cast<size_t>((WidePhases<TB, TE>::P == 1 ? 1 : 2) * WidePhases<TB, TE>::MAXF * 32 + (TE - TB) * 72) * 8;
-  auto k = trsm_wide_kernel<TB, TE, THREADS, A>;
+  auto k = trsm_wide_kernel<TB, TE, THREADS, A, INV>;
   static thread_local LaunchCfgCache cfg;
   cudaError_t e = cached_launch_cfg(cfg, k, smem, THREADS, nullptr);
   if (e != cudaSuccess) return e;
@@ -855,6 +884,22 @@ static cudaError_t launch_wide(const TrsmParams& p, int num_sms, cudaStream_t st
   return cudaGetLastError();
 }
 
+// A = 2 instances launch an inverse-diagonal twin when p.inv_flag is set (reading D24)
+template <int TB, int TE, int THREADS, int A = 1>
+static cudaError_t launch_wide(const TrsmParams& p, int num_sms, cudaStream_t stream) {
+  if constexpr (A == 2) {
+    if (p.inv_flag) {
+      cudaError_t e = launch_wide1<TB, TE, THREADS, A, true>(p, num_sms, stream);
+      if (e != cudaSuccess) return e;
+    }
+    return launch_wide1<TB, TE, THREADS, A, false>(p, num_sms, stream);
+  } else {
+    TrsmParams ps = p;
+    ps.inv_flag = nullptr;
+    return launch_wide1<TB, TE, THREADS, A, false>(ps, num_sms, stream);
+  }
+}
+
 // Width of the TMA box of X that launch_trsm expects for NT column tiles (host: encode_map).
 int trsm_x_box_cols(int NT) { return NT >= 24 ? 128 : NT * 8; }
 
@@ -862,19 +907,18 @@ int trsm_x_box_cols(int NT) { return NT >= 24 ? 128 : NT * 8; }
 // even when the guard lets it exit at entry).
 int trsm_launch_count(const TrsmParams& p, bool tma) {
   const int NT = npad_for(p.n) / 8;
-  const int inv = p.inv_flag ? 1 : 0;
-  if (p.gram_partials) return 1 + (NT == 8 ? inv : 0);
+  const int k = p.inv_flag ? 2 : 1;  // an A = 2 / TMA instance launches with its inverse twin
+  if (p.gram_partials) return NT == 8 ? k : 1;
   switch (NT) {
-    case 8: case 12: case 16: return 1 + (tma ? inv : 0);
-    case 24: return tma ? 2 + inv : 1;
-    case 32: return tma ? 2 + inv : 1;
+    case 8: case 12: case 16: return tma ? k : 1;
+    case 24: case 32: return tma ? 2 * k : 1;
     case 64: {
-      const int first = tma ? 2 + inv : 1;  // columns 0..255
+      const int first = tma ? 2 * k : 1;  // columns 0..255
 #ifdef SCQR3_WIDE512_PHASED
       return first + 1;
 #else
       const int nb = (p.n + 7) / 8;
-      return first + 1 + (nb > 40) + (nb > 48) + (nb > 56) + (nb > 60);
+      return first + k * (1 + (nb > 40) + (nb > 48) + (nb > 56) + (nb > 60));
 #endif
     }
     default: return 1;

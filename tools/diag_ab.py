@@ -19,7 +19,8 @@ import gpu_metrics  # noqa: E402
 CFG = {"C3": (10_000_000, 128, 1e10, "geometric"), "C2": (1_000_000, 64, 1e15, "geometric"),
        "C5": (2_000_000, 64, 1e12, "geometric"), "N256": (5_000_000, 256, 1e14, "cluster"),
        "N192": (4_000_000, 192, 1e12, "geometric"), "N96": (4_000_000, 96, 1e12, "geometric"),
-       "C3s": (2_000_000, 128, 1e10, "geometric")}
+       "C3s": (2_000_000, 128, 1e10, "geometric"), "N512": (2_000_000, 512, 1e12, "geometric"),
+       "N300": (2_000_000, 300, 1e12, "geometric")}
 names = sys.argv[1:] or ["C3", "C2"]
 u = 2.0 ** -53
 for name in names:
