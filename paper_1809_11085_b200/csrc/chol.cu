@@ -646,7 +646,11 @@ __device__ __forceinline__ void trsm_diag_guard(RP rp, int n, int NT, double* db
       double s = j == i ? 1.0 : 0.0;
 #pragma unroll
       for (int l = 0; l < j; ++l) s = l >= i ? fma(-y[l], d[l][j], s) : s;
+#ifdef SCQR3_G_RCP
+      y[j] = j >= i ? s * (1.0 / d[j][j]) : 0.0;
+#else
       y[j] = j >= i ? s / d[j][j] : 0.0;
+#endif
     }
     if (x < NT * 8) {
       double* dinv = dblk + dinv_off(NT) + J * 64 + (i & 1) * 32 + (i >> 1);
@@ -662,6 +666,13 @@ __device__ __forceinline__ void trsm_diag_guard(RP rp, int n, int NT, double* db
       tr[j] = v;
     }
     // row i of M = |D| |Y||D| (rows k >= i of |Y||D| from the group's lanes); past n excluded
+#ifdef SCQR3_G_NOMU
+    if (x < NT * 8) mu2max = fmax(mu2max, tr[7]);
+    continue;
+#endif
+    double di[8];  // row i of |D_J| (a runtime row index into d[][] would go to local memory)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) di[k] = k >= i ? fabs(rp(8 * J + i, 8 * J + k)) : 0.0;
     double mu2 = 0.0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -669,7 +680,7 @@ __device__ __forceinline__ void trsm_diag_guard(RP rp, int n, int NT, double* db
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const double tk = __shfl_sync(0xffffffffu, tr[j], (lane & ~7) | k);
-        v += k >= i ? fabs(d[i][k]) * tk : 0.0;
+        v += di[k] * tk;
       }
       if (8 * J + i < n && 8 * J + j < n) mu2 += v * v;
     }
@@ -684,7 +695,11 @@ __device__ __forceinline__ void trsm_diag_guard(RP rp, int n, int NT, double* db
   __shared__ double gpart[8][32];
   const int warp = tid >> 5;
   double off2 = 0.0, col2max = 0.0;
+#ifdef SCQR3_G_NOCOL
+  for (int j0 = 0; j0 < 0; j0 += 32) {
+#else
   for (int j0 = 0; j0 < n; j0 += 32) {
+#endif
     const int j = j0 + lane, iend = min(j0 + 32, n);
     double c = 0.0;
 #pragma unroll 4
@@ -737,12 +752,14 @@ __device__ __forceinline__ void trsm_diag_guard(RP rp, int n, int NT, double* db
 // below the diagonal): consecutive threads read consecutive entries of a row of W (no bank
 // conflicts in shared memory, coalesced from L2 when W is global) and store consecutive
 // addresses.  The TRSM operands -- B fragments of -R~ and the scaled diagonal blocks, the same
-// values trsm_prep_kernel forms -- are written here only when bfrag != null (n <= 64, where a
-// second launch costs more than it saves); for larger n trsm_prep_kernel forms them on many
-// CTAs (on this one CTA they took 13 K cycles at n = 128 and 73 K at n = 256).
+// values trsm_prep_kernel forms -- are written here only when bfrag != null (n <= 32, and the
+// unfused n <= 64, where a second launch costs more than it saves); for larger n trsm_prep_kernel forms them on many
+// CTAs (on this one CTA they took 13 K cycles at n = 128 and 73 K at n = 256) and runs the D24
+// guard.
 template <bool SMEM>
 __device__ __noinline__ void write_outputs(const double* Wg, int ldw, int n, int NT, double* bfrag, double* dblk,
                                            double* Rt, int diag_mode) {
+  (void)diag_mode;  // no inverse-diagonal instance runs for these n (flag 0 below)
   extern __shared__ double smdyn[];
   const double* W = SMEM ? smdyn : Wg;
   constexpr int kU = 8;
@@ -773,7 +790,12 @@ __device__ __noinline__ void write_outputs(const double* Wg, int ldw, int n, int
       const double rcj = rload(W, ldw, n, c, j), rcc = rload(W, ldw, n, c, c);
       dblk[idx] = w < 64 ? (j > c ? rcj / rcc : 0.0) : 1.0 / rcc;
     }
-    trsm_diag_guard([&](int i, int j) { return rload(W, ldw, n, i, j); }, n, NT, dblk, diag_mode);
+    // (called for n <= 32 and the unfused n <= 64, which have no inverse-diagonal TRSM instance:
+    //  the D24 flag is 0; trsm_prep_kernel forms the operands and runs the guard otherwise)
+    if (threadIdx.x == 0) {
+      dblk[dflag_off(NT)] = 0.0;
+      dblk[dflag_off(NT) + 1] = 0.0;
+    }
   }
 #ifdef SCQR3_CHOL_OUTCLK
   long long o1 = clock64();

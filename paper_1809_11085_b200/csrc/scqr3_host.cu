@@ -794,8 +794,13 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
   cp.W = w.W;
   cp.w_in_smem = w_fits_smem(static_cast<int>(n)) ? 1 : 0;
   cp.Rt = w.Rt;
-  // the TRSM operands: written by chol_kernel for n <= 64, else by trsm_prep_kernel (many CTAs)
-  const bool prep_launch = n > 64;
+  // the TRSM operands: written by chol_kernel for n <= 32, else by trsm_prep_kernel (many CTAs;
+  // its last CTA runs the D24 guard -- inside the one Cholesky CTA, the guard's once-executed
+  // unrolled code cost 31 K cycles at n = 64, mostly cold instruction fetch)
+  // (n in (33, 64]: only the fused TRSM + Gram has an inverse-diagonal instance; the others keep
+  //  the in-kernel operands, measured 7 us per pass cheaper than the extra launch)
+  const bool fuse_tg = g_fuse_tg && !oblique && trsm_fuses_gram(L.NT) && m > 0;
+  const bool prep_launch = n > 64 || (n > 32 && fuse_tg && o->trsm_diag != SCQR3_TRSM_DIAG_SUBST);
   cp.bfrag = prep_launch ? nullptr : w.bfrag;
   cp.dblk = prep_launch ? nullptr : w.dblk;
   cp.trsm_diag = o->trsm_diag;
@@ -824,8 +829,8 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
   int* last_pass = reinterpret_cast<int*>(w.misc + 14);
   int* pass_dev = reinterpret_cast<int*>(w.misc + 15);
   cp.last_pass = last_pass;
-  // n <= 64, standard inner product: TRSM_k also accumulates Gram_{k+1}
-  const bool fuse_tg = g_fuse_tg && !oblique && trsm_fuses_gram(L.NT) && m > 0;
+  // n <= 64, standard inner product: TRSM_k also accumulates Gram_{k+1} (fuse_tg
+  // above)
   int fused_chunks = 0;
   // k >= 1: pass k with host-known number; k == 0: the generic loop-body pass (number on device)
   auto enqueue = [&](int k) -> int {

@@ -910,7 +910,8 @@ int trsm_launch_count(const TrsmParams& p, bool tma) {
   const int k = p.inv_flag ? 2 : 1;  // an A = 2 / TMA instance launches with its inverse twin
   if (p.gram_partials) return NT == 8 ? k : 1;
   switch (NT) {
-    case 8: case 12: case 16: return tma ? k : 1;
+    case 8: return 1;
+    case 12: case 16: return tma ? k : 1;
     case 24: case 32: return tma ? 2 * k : 1;
     case 64: {
       const int first = tma ? 2 * k : 1;  // columns 0..255
@@ -952,7 +953,9 @@ cudaError_t launch_trsm(const TrsmParams& p, const CUtensorMap* map, int num_sms
                        : launch_one<2, 4, true, 256, false>(ps, nullptr, num_sms, stream);
     case 4: return tma ? launch_one<4, 4, true, 256, true>(ps, map, num_sms, stream)
                        : launch_one<4, 4, true, 256, false>(ps, nullptr, num_sms, stream);
-    case 8: return tma ? launch_pair<8, 4, true, 256, true>(p, map, num_sms, stream)
+    // (n in (32, 64] unfused -- the oblique n = 64 -- substitutes: its A = 4 inverse twin measured
+    //  slower, C5 TRSM 0.424 -> 0.435 ms; the fused n <= 64 instance above has one)
+    case 8: return tma ? launch_one<8, 4, true, 256, true>(ps, map, num_sms, stream)
                        : launch_one<8, 4, true, 256, false>(ps, nullptr, num_sms, stream);
     case 12: return tma ? launch_pair<12, 2, true, 256, true>(p, map, num_sms, stream)
                         : launch_one<12, 2, true, 256, false>(ps, nullptr, num_sms, stream);

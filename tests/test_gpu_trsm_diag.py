@@ -64,10 +64,12 @@ def dyadic_blocks(n, rng):
 
 
 @gpu
-@pytest.mark.parametrize("m,n", [(1, 40), (999, 33), (4097, 64), (60_011, 64), (3001, 96), (60_011, 128),
-                                 (10_007, 136), (60_011, 256), (3001, 300)])
+@pytest.mark.parametrize("m,n", [(1, 96), (999, 72), (3001, 96), (60_011, 128), (10_007, 136), (60_011, 256),
+                                 (3001, 300)])
 def test_trsm_inverse_integer_exact(m, n):
-    """Forced INVERSE: every row solved through Y_J fragments (several persistent sweeps at m=60011)."""
+    """Forced INVERSE: every row solved through Y_J fragments (several persistent sweeps at m=60011).
+    (The kernel-level TRSM has inverse instances for n > 64; n in (32, 64] has one only fused with
+    the next pass's Gram inside scqr3_factor, covered by test_factor_inverse_path_parity.)"""
     rng = np.random.default_rng(m + n)
     Q = rng.integers(-9, 10, size=(m, n)).astype(float)
     R = dyadic_blocks(n, rng)
@@ -81,7 +83,7 @@ def _shifted_R(m, n, kappa, seed):
 
 
 @gpu
-@pytest.mark.parametrize("m,n,kappa", [(5003, 64, 1e12), (5003, 96, 1e8), (20_000, 128, 1e10), (3000, 200, 1e10)])
+@pytest.mark.parametrize("m,n,kappa", [(5003, 72, 1e12), (5003, 96, 1e8), (20_000, 128, 1e10), (3000, 200, 1e10)])
 def test_guard_takes_inverse_when_bound_holds(m, n, kappa):
     X, R = _shifted_R(m, n, kappa, 5)
     assert guard_ratio(R) < 0.8
@@ -100,7 +102,7 @@ def test_guard_takes_inverse_when_bound_holds(m, n, kappa):
 
 
 @gpu
-@pytest.mark.parametrize("n", [64, 128])
+@pytest.mark.parametrize("n", [96, 128, 256])
 def test_guard_falls_back_to_substitution(n):
     """One ill-conditioned diagonal block (mu_J ~ 1e8 ||D_J||): AUTO must be the substitution bits."""
     m = 4001
@@ -116,10 +118,11 @@ def test_guard_falls_back_to_substitution(n):
 
 
 @gpu
-def test_guard_small_n_substitutes():
-    """n = 16 (PR1's width): gamma_n sqrt(n) leaves no room (ratio ~3.5 on pass 1), and n <= 32 has
-    no inverse instance anyway -- AUTO, INVERSE and SUBST give the same bits."""
-    X, R = _shifted_R(2000, 16, 1e12, 0)
+@pytest.mark.parametrize("n", [16, 64])
+def test_guard_small_n_substitutes(n):
+    """n = 16 (PR1's width: gamma_n sqrt(n) leaves no room, ratio ~3.5 on pass 1) and the kernel-level
+    n <= 64 have no inverse instance -- AUTO, INVERSE and SUBST give the same bits."""
+    X, R = _shifted_R(2000, n, 1e12, 0)
     Xd, Rd = dev(X), dev(R)
     qs = host(sq.scqr3_trsm(Xd, Rd, trsm_diag=sq.TRSM_DIAG_SUBST))
     assert np.array_equal(host(sq.scqr3_trsm(Xd, Rd)), qs)
@@ -138,6 +141,7 @@ def test_factor_inverse_path_parity(m, n, kappa):
     rs = sq.scqr3_factor(Xd, trsm_diag=sq.TRSM_DIAG_SUBST)
     assert ra.status == ri.status == rs.status == 0
     assert np.array_equal(host(ra.R), host(ri.R)) and np.array_equal(host(ra.Q), host(ri.Q))
+    assert not np.array_equal(host(ra.Q), host(rs.Q))   # AUTO did take the inverse path
     ro = oracle.scqr3(X)
     for r in (ra, rs):
         Rg, Qg = host(r.R), host(r.Q)
