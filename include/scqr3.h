@@ -62,8 +62,9 @@ enum { SCQR3_SHIFT_SAFE = 0, SCQR3_SHIFT_FIXED = 1, SCQR3_SHIFT_NONE = 2, SCQR3_
 /* Estimate N^2 of ||Q||_2^2 for the shift (reading D2/D4).
  * POWER: 1.01 * Rayleigh quotient after power_iters steps on the computed n x n Gram.
  * FROBENIUS: trace of the Gram = ||Q||_F^2 (paper-sanctioned conservative choice).
- * USER: norm2_bound^2 on pass 1 (POWER afterwards).  Oblique always uses ||Q||_F^2 for
- * X (or USER on pass 1) and bnorm_bound, else the Gershgorin bound, for ||B||_2 (D4). */
+ * USER: norm2_bound^2 on pass 1 (POWER afterwards).  Oblique (D4): the same choices for X, with
+ * POWER iterating on the plain Gram Q^T Q that the oblique Gram kernel forms alongside the
+ * B-Gram; ||B||_2 is bnorm_bound, else the Gershgorin bound. */
 enum { SCQR3_NORM_POWER = 0, SCQR3_NORM_FROBENIUS = 1, SCQR3_NORM_USER = 2 };
 
 /* How the TRSM Q := Q R~^{-1} solves its 8 x 8 diagonal blocks D_J (reading D24).
