@@ -166,16 +166,38 @@ int scqr3_factor_oblique(int64_t m, int64_t n, const double* X, int64_t ld, cons
  *   vals[nnz]     float64, B symmetric positive definite (not checked).
  * halo: rows exchanged with each neighbouring rank per pass (NCCL send/recv, like the
  * tridiagonal halo); 0 on one GPU (required without opts->comm).  Each rank must own at
- * least halo rows.  Index and row_ptr violations are detected on the device -> EINVAL. */
+ * least halo rows.  Index and row_ptr violations are detected on the device -> EINVAL.
+ *
+ * halo == SCQR3_CSR_GHOSTS: rows of other ranks by the sparsity pattern (any B, not only a
+ * banded one; the distributed sparse matrix-vector product's ghost-row plan):
+ *   col_idx  a value c in [0, m) is a local row of Q, c in [m, m + nghost) ghost row c - m;
+ *   ghost rows are grouped by the rank that owns them, in rank order: the recv_counts[r] rows
+ *   from rank r follow those of ranks < r, in the order rank r lists them in its send list;
+ *   nghost       total ghost rows of this rank (sum of recv_counts);
+ *   recv_counts  HOST int64[nranks]: ghost rows received from each rank (0 for this rank);
+ *   send_counts  HOST int64[nranks]: rows of this rank sent to each rank (0 for itself);
+ *   send_rows    DEVICE int64[sum send_counts]: the local rows (in [0, m)) sent, grouped by
+ *                destination rank in rank order.
+ * Per pass the listed rows of Q are gathered and exchanged (NCCL grouped send/recv with every
+ * rank that has a nonzero count).  Rank r's send_counts[p] must equal rank p's recv_counts[r]
+ * (checked collectively once per call); send_rows and col_idx are checked on the device.
+ * Without opts->comm, nghost must be 0.  The fields after halo are ignored when halo >= 0. */
+#define SCQR3_CSR_GHOSTS (-1)
 typedef struct scqr3_csr {
   const int64_t* row_ptr;
   const int32_t* col_idx;
   const double* vals;
   int64_t halo;
+  int64_t nghost;               /* ghost plan (halo == SCQR3_CSR_GHOSTS; ABI version 2) */
+  const int64_t* recv_counts;
+  const int64_t* send_counts;
+  const int64_t* send_rows;
 } scqr3_csr;
 
 /* Workspace bytes for the CSR-metric calls (the halo buffers scale with halo * n). */
 size_t scqr3_workspace_size_csr(int64_t m, int64_t n, int64_t halo);
+/* Workspace bytes for a ghost-plan CSR metric: nghost received and nsend sent rows per pass. */
+size_t scqr3_workspace_size_csr_ghosts(int64_t m, int64_t n, int64_t nghost, int64_t nsend);
 
 /* Oblique shifted CholeskyQR3 (Alg. 5 with the B-Gram in all passes, D8) for a CSR metric:
  * Y = B Q by csr_y_kernel, then the same Gram / shift / Cholesky / TRSM path; the shift's

@@ -213,17 +213,39 @@ def scqr3_factor_oblique(X, d, e, *, Q=None, R=None, ws=None, inplace=False, **k
 class CsrMetric:
     """This rank's rows of a sparse SPD metric B in CSR on the device:
     row_ptr int64[m+1], col_idx int32[nnz] relative to the rank's first row (halo rows of the
-    neighbours are negative / >= m), vals float64[nnz]."""
+    neighbours are negative / >= m), vals float64[nnz].  With a ghost plan (`ghosts=(nghost,
+    recv_counts, send_counts, send_rows)`, e.g. from dist.csr_ghost_plan) indices >= m name ghost
+    rows owned by other ranks, for any sparsity pattern (include/scqr3.h, SCQR3_CSR_GHOSTS)."""
 
-    def __init__(self, row_ptr, col_idx, vals, halo: int = 0, device="cuda"):
+    def __init__(self, row_ptr, col_idx, vals, halo: int = 0, device="cuda", ghosts=None):
+        import numpy as np
         torch = _torch()
         self.row_ptr = torch.as_tensor(row_ptr, dtype=torch.int64, device=device).contiguous()
         self.col_idx = torch.as_tensor(col_idx, dtype=torch.int32, device=device).contiguous()
         self.vals = torch.as_tensor(vals, dtype=torch.float64, device=device).contiguous()
         self.halo = int(halo)
+        self.nghost, self.nsend = 0, 0
+        self._recv = self._send = self._rows = None
+        if ghosts is not None:
+            nghost, recv, send, rows = ghosts
+            self.halo = _abi.CSR_GHOSTS
+            self.nghost = int(nghost)
+            self._recv = np.ascontiguousarray(recv, dtype=np.int64)   # host arrays (kept alive)
+            self._send = np.ascontiguousarray(send, dtype=np.int64)
+            self._rows = torch.as_tensor(np.asarray(rows, dtype=np.int64), device=device).contiguous()
+            self.nsend = int(self._send.sum())
+
+    def workspace_bytes(self, m: int, n: int) -> int:
+        L = _abi.lib()
+        if self.halo == _abi.CSR_GHOSTS:
+            return int(L.scqr3_workspace_size_csr_ghosts(m, n, self.nghost, self.nsend))
+        return int(L.scqr3_workspace_size_csr(m, n, self.halo))
 
     def c(self):
-        return _abi.Csr(self.row_ptr.data_ptr(), self.col_idx.data_ptr(), self.vals.data_ptr(), self.halo)
+        if self.halo != _abi.CSR_GHOSTS:
+            return _abi.Csr(self.row_ptr.data_ptr(), self.col_idx.data_ptr(), self.vals.data_ptr(), self.halo)
+        return _abi.Csr(self.row_ptr.data_ptr(), self.col_idx.data_ptr(), self.vals.data_ptr(), self.halo,
+                        self.nghost, self._recv.ctypes.data, self._send.ctypes.data, self._rows.data_ptr())
 
 
 def scqr3_factor_oblique_csr(X, B: CsrMetric, *, Q=None, R=None, ws=None, inplace=False, **kw) -> Result:
@@ -235,7 +257,7 @@ def scqr3_factor_oblique_csr(X, B: CsrMetric, *, Q=None, R=None, ws=None, inplac
     if R is None:
         R = torch.empty((n, n), dtype=torch.float64, device=X.device).t()
     if ws is None:
-        ws = workspace(m, n, device=X.device, csr_halo=B.halo)
+        ws = _torch().empty(B.workspace_bytes(m, n), dtype=_torch().uint8, device=X.device)
     o, tr, passes = _opts(ws=ws, **kw)
     cb = B.c()
     rc = _check(_abi.lib().scqr3_factor_oblique_csr(m, n, X.data_ptr(), _ld(X), ctypes.byref(cb), Q.data_ptr(),

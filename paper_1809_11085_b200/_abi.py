@@ -12,6 +12,7 @@ OK, EINVAL, EBREAKDOWN, ENOCONV = 0, 1, 2, 3
 SHIFT_SAFE, SHIFT_FIXED, SHIFT_NONE, SHIFT_ADAPTIVE, SHIFT_PRACTICAL = 0, 1, 2, 3, 4
 NORM_POWER, NORM_FROBENIUS, NORM_USER = 0, 1, 2
 TRSM_DIAG_AUTO, TRSM_DIAG_SUBST, TRSM_DIAG_INVERSE = 0, 1, 2
+CSR_GHOSTS = -1
 COMM_ID_BYTES = 128
 
 EXPORTED = [
@@ -20,7 +21,7 @@ EXPORTED = [
     "scqr3_cholesky", "scqr3_trsm", "scqr3_comm_unique_id", "scqr3_comm_init",
     "scqr3_comm_destroy", "scqr3_last_error", "scqr3_launch_count", "scqr3_workspace_size_csr",
     "scqr3_factor_oblique_csr", "scqr3_gram_oblique_csr", "scqr3_workspace_size_complex",
-    "scqr3_factor_complex", "scqr3_comm_init_loopback",
+    "scqr3_factor_complex", "scqr3_comm_init_loopback", "scqr3_workspace_size_csr_ghosts",
 ]
 
 
@@ -29,6 +30,9 @@ class Csr(ctypes.Structure):
     _fields_ = [
         ("row_ptr", ctypes.c_void_p), ("col_idx", ctypes.c_void_p), ("vals", ctypes.c_void_p),
         ("halo", ctypes.c_int64),
+        # ghost-row plan (halo == CSR_GHOSTS): nghost, host recv/send counts, device send rows
+        ("nghost", ctypes.c_int64), ("recv_counts", ctypes.c_void_p), ("send_counts", ctypes.c_void_p),
+        ("send_rows", ctypes.c_void_p),
     ]
 
 
@@ -92,6 +96,8 @@ def lib():
         PC = ctypes.POINTER(Csr)
         L.scqr3_workspace_size_csr.argtypes = [i64, i64, i64]
         L.scqr3_workspace_size_csr.restype = ctypes.c_size_t
+        L.scqr3_workspace_size_csr_ghosts.argtypes = [i64, i64, i64, i64]
+        L.scqr3_workspace_size_csr_ghosts.restype = ctypes.c_size_t
         L.scqr3_factor_oblique_csr.argtypes = [i64, i64, vp, i64, PC, vp, i64, vp, P]
         L.scqr3_gram_oblique_csr.argtypes = [i64, i64, vp, i64, PC, vp, vp, P]
         L.scqr3_workspace_size_complex.argtypes = [i64, i64]

@@ -49,6 +49,7 @@ struct LoopGroup {
   double* stage[kMaxLoopRanks] = {};         // per-rank staging of allreduce contributions
   size_t stage_cap = 0;                      // doubles per rank
   int64_t hval[kMaxLoopRanks] = {};
+  const int64_t* hvec[kMaxLoopRanks] = {};     // published host arrays (allgather, ghost-plan counts)
 };
 
 // Staging per rank: the largest exchanged Gram is the oblique one at n = 512 (two sets of
@@ -313,6 +314,79 @@ int comm_halo(Comm* c, const double* Q, int64_t ld, int64_t m, int n, int64_t h,
       CTRY(cudaMemcpyAsync(halo + 3 * blk, pub[c->rank + 1], blk * 8, cudaMemcpyDeviceToDevice, st));
     return SCQR3_OK;
   });
+}
+
+int comm_host_allgather(Comm* c, const int64_t* v, int cnt, int64_t* out, int64_t* dscratch, cudaStream_t st) {
+  if (c->kind == COMM_NCCL) {
+    CTRY(cudaMemcpyAsync(dscratch + static_cast<size_t>(c->rank) * cnt, v, cnt * 8, cudaMemcpyHostToDevice, st));
+    NTRY(ncclAllGather(dscratch + static_cast<size_t>(c->rank) * cnt, dscratch, cnt, ncclInt64, c->nccl, st));
+    CTRY(cudaMemcpyAsync(out, dscratch, static_cast<size_t>(c->nranks) * cnt * 8, cudaMemcpyDeviceToHost, st));
+    CTRY(cudaStreamSynchronize(st));
+    return SCQR3_OK;
+  }
+  LoopGroup* g = c->lg;
+  g->hvec[c->rank] = v;
+  RTRY(lb_barrier(g));
+  for (int r = 0; r < g->nranks; ++r) std::memcpy(out + static_cast<size_t>(r) * cnt, g->hvec[r], cnt * 8);
+  RTRY(lb_barrier(g));  // nobody changes its array before every rank has read it
+  return SCQR3_OK;
+}
+
+// sendbuf[k][j] = Q[send_rows[k] + j ld] (row-major; consecutive threads write consecutive j)
+__global__ void ghost_pack_kernel(const double* Q, long long ld, int n, const int64_t* rows, long long nsend,
+                                  double* sendbuf) {
+  const long long total = nsend * n;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long k = i / n;
+    const int j = static_cast<int>(i - k * n);
+    sendbuf[i] = Q[rows[k] + j * ld];
+  }
+}
+
+int comm_ghosts(Comm* c, const double* Q, int64_t ld, int n, const int64_t* send_rows, const int64_t* send_counts,
+                const int64_t* recv_counts, int64_t nsend, double* sendbuf, double* ghost, cudaStream_t st) {
+  auto pack = [&]() -> int {
+    if (nsend > 0) {
+      const long long total = nsend * n;
+      const long long blocks = std::max<long long>(1, std::min<long long>((total + 255) / 256, 2048));
+      ghost_pack_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(Q, ld, n, send_rows, nsend, sendbuf);
+      CTRY(cudaGetLastError());
+    }
+    return SCQR3_OK;
+  };
+  if (c->kind == COMM_NCCL) {
+    RTRY(pack());
+    NTRY(ncclGroupStart());
+    int64_t so = 0, ro = 0;
+    for (int p = 0; p < c->nranks; ++p) {
+      if (send_counts[p] > 0) NTRY(ncclSend(sendbuf + so * n, send_counts[p] * n, ncclDouble, p, c->nccl, st));
+      if (recv_counts[p] > 0) NTRY(ncclRecv(ghost + ro * n, recv_counts[p] * n, ncclDouble, p, c->nccl, st));
+      so += send_counts[p];
+      ro += recv_counts[p];
+    }
+    NTRY(ncclGroupEnd());
+    return SCQR3_OK;
+  }
+  LoopGroup* g = c->lg;
+  return lb_collective(
+      c, st, sendbuf,
+      [&]() -> int {
+        g->hvec[c->rank] = send_counts;  // (read by the peers between the two barriers)
+        return pack();
+      },
+      [&](const double* const* pub) -> int {
+        int64_t ro = 0;
+        for (int p = 0; p < c->nranks; ++p) {
+          if (recv_counts[p] > 0) {
+            int64_t off = 0;  // rows rank p sends to ranks before this one
+            for (int q = 0; q < c->rank; ++q) off += g->hvec[p][q];
+            CTRY(cudaMemcpyAsync(ghost + ro * n, pub[p] + off * n, recv_counts[p] * n * 8, cudaMemcpyDeviceToDevice, st));
+          }
+          ro += recv_counts[p];
+        }
+        return SCQR3_OK;
+      });
 }
 
 int comm_shift_right1(Comm* c, const double* src, double* send, double* recv, cudaStream_t st) {

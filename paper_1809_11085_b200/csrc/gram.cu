@@ -621,8 +621,13 @@ __global__ void csr_y_kernel(ObliqueYParams p) {
         src = p.halo_prev + (col + p.halo);
         ld = p.halo;
       } else if (col >= p.m) {
-        src = p.halo_next + (col - p.m);
-        ld = p.halo;
+        if (p.ghosts) {  // ghost row of the sparsity-pattern plan (row-major)
+          src = p.ghost + (col - p.m) * p.n;
+          ld = 1;
+        } else {
+          src = p.halo_next + (col - p.m);
+          ld = p.halo;
+        }
       } else {
         src = p.Q + col;
         ld = p.ldq;
@@ -673,6 +678,13 @@ __global__ void csr_gershgorin_kernel(const long long* rp, const double* cv, lon
 
 // Argument check of a CSR metric on the device: row_ptr non-decreasing from 0, every column
 // index inside [-halo, m + halo).  *bad is set to 1 on any violation.
+// *bad = 1 if some v[k] is outside [lo, hi) (the ghost plan's send rows)
+__global__ void index_check_kernel(const long long* v, long long cnt, long long lo, long long hi, int* bad) {
+  for (long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; k < cnt;
+       k += static_cast<long long>(gridDim.x) * blockDim.x)
+    if (v[k] < lo || v[k] >= hi) *bad = 1;
+}
+
 __global__ void csr_check_kernel(const long long* rp, const int* ci, long long m, long long halo, int has_prev,
                                  int has_next, int* bad) {
   // halo rows exist only towards neighbouring ranks: none before rank 0, none after the last

@@ -58,6 +58,15 @@ int comm_allreduce_max1(Comm* c, double* buf, cudaStream_t st);
 // [0] my first h rows, [1] my last h rows (packed here), [2] <- the previous rank's last h rows,
 // [3] <- the next rank's first h rows.  Requires m >= h (checked collectively by the caller).
 int comm_halo(Comm* c, const double* Q, int64_t ld, int64_t m, int n, int64_t h, double* halo, cudaStream_t st);
+// All ranks' host int64[cnt] arrays: out[r * cnt + i] = rank r's v[i] (synchronous; the NCCL
+// backend stages through dscratch, device memory of nranks * cnt int64).
+int comm_host_allgather(Comm* c, const int64_t* v, int cnt, int64_t* out, int64_t* dscratch, cudaStream_t st);
+// Ghost-row exchange of a sparsity-pattern plan (scqr3_csr with SCQR3_CSR_GHOSTS): the rows
+// send_rows[0:nsend] of Q are packed row-major into sendbuf (nsend x n) and sent, grouped by
+// destination in rank order (send_counts, host); ghost (row-major) receives recv_counts[p] rows
+// from each rank p, in rank order.
+int comm_ghosts(Comm* c, const double* Q, int64_t ld, int n, const int64_t* send_rows, const int64_t* send_counts,
+                const int64_t* recv_counts, int64_t nsend, double* sendbuf, double* ghost, cudaStream_t st);
 // One double to the next rank: send[0] := *src (0 if src is null); recv[0] <- previous rank's
 // send[0] (untouched on rank 0).
 int comm_shift_right1(Comm* c, const double* src, double* send, double* recv, cudaStream_t st);

@@ -637,7 +637,20 @@ struct Metric {
   const double* e = nullptr;
   const scqr3_csr* csr = nullptr;
   bool oblique() const { return d != nullptr || csr != nullptr; }
-  int64_t halo() const { return csr ? csr->halo : 1; }
+  // ghost-row plan by sparsity pattern (scqr3_csr.halo == SCQR3_CSR_GHOSTS)
+  bool ghosts() const { return csr && csr->halo == SCQR3_CSR_GHOSTS; }
+  int64_t nsend(int nranks) const {
+    int64_t s = 0;
+    if (ghosts() && csr->send_counts)
+      for (int r = 0; r < nranks; ++r) s += csr->send_counts[r];
+    return s;
+  }
+  // rows of the workspace's halo region (4 blocks of halo x n): the ghost plan keeps its
+  // nghost received and nsend packed rows there
+  int64_t halo(int nranks = 1) const {
+    if (ghosts()) return std::max<int64_t>(1, (csr->nghost + nsend(nranks) + 3) / 4);
+    return csr ? csr->halo : 1;
+  }
 };
 
 // Local argument checks of factor_impl (everything that can fail before the first exchange).
@@ -651,19 +664,41 @@ int factor_checks(int64_t m, int64_t n, const double* X, int64_t ld, const Metri
   TRY(check_matrix("Q", Q, m, ldq));
   if (!R) return fail("R is NULL");
   if (B.d && m > 0 && !B.e) return fail("b_off is NULL");
+  const int nranks = cm ? cm->nranks : 1;
   if (B.csr) {
     if (m > 0 && (!B.csr->row_ptr || !B.csr->col_idx || !B.csr->vals)) return fail("CSR metric has a NULL array");
-    if (B.csr->halo < 0) return fail("CSR halo < 0");
-    if (!cm && B.csr->halo != 0) return fail("CSR halo must be 0 without a communicator");
+    if (B.ghosts()) {
+      const scqr3_csr& g = *B.csr;
+      if (g.nghost < 0) return fail("CSR ghost plan: nghost < 0");
+      if (!cm) {
+        if (g.nghost != 0) return fail("CSR ghost plan: nghost must be 0 without a communicator");
+      } else {
+        if (!g.recv_counts || !g.send_counts) return fail("CSR ghost plan: NULL recv_counts / send_counts");
+        int64_t nr = 0, ns = 0;
+        for (int r = 0; r < nranks; ++r) {
+          if (g.recv_counts[r] < 0 || g.send_counts[r] < 0) return fail("CSR ghost plan: negative count");
+          nr += g.recv_counts[r];
+          ns += g.send_counts[r];
+        }
+        if (g.recv_counts[cm->rank] != 0 || g.send_counts[cm->rank] != 0)
+          return fail("CSR ghost plan: a rank does not exchange rows with itself");
+        if (nr != g.nghost) return fail("CSR ghost plan: sum of recv_counts %lld != nghost %lld", (long long)nr,
+                                        (long long)g.nghost);
+        if (ns > 0 && !g.send_rows) return fail("CSR ghost plan: send_rows is NULL");
+      }
+    } else {
+      if (B.csr->halo < 0) return fail("CSR halo < 0");
+      if (!cm && B.csr->halo != 0) return fail("CSR halo must be 0 without a communicator");
+    }
   }
   // a rank of an oblique factorisation must own at least its halo rows (its neighbours read them)
-  if (cm && B.oblique() && cm->nranks > 1 && m < std::max<int64_t>(B.halo(), 1))
+  if (cm && B.oblique() && !B.ghosts() && cm->nranks > 1 && m < std::max<int64_t>(B.halo(), 1))
     return fail("oblique metric across ranks: this rank owns %lld rows, fewer than the halo (%lld)", (long long)m,
                 (long long)std::max<int64_t>(B.halo(), 1));
   const int max_passes = o->max_passes > 0 ? o->max_passes : 8;
   if (max_passes > Ctx::kSlots) return fail("max_passes %d > %d", max_passes, Ctx::kSlots);
   TRY(get_ctx(c));
-  *L = make_layout(m, n, B.oblique(), B.halo());
+  *L = make_layout(m, n, B.oblique(), B.halo(nranks));
   TRY(carve(*L, o, w));
   return SCQR3_OK;
 }
@@ -724,19 +759,52 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
       yp.ci = B.csr->col_idx;
       yp.cv = B.csr->vals;
       yp.halo = B.csr->halo;
+      const bool gh = B.ghosts();
+      if (gh) {  // ghost rows (row-major, nghost x n) at the start of the halo region
+        yp.ghosts = 1;
+        yp.ghost = w.halo;
+        yp.halo = B.csr->nghost;
+      }
       // argument check on the device: row_ptr monotone from 0, indices inside this rank's rows
-      // plus the halo rows that exist (none before rank 0, none after the last rank)
+      // plus the halo rows that exist (none before rank 0, none after the last rank; the ghost
+      // plan: [0, m + nghost)) and the ghost plan's send rows inside [0, m)
       int hbad = 0;
-      if (m > 0) {
+      const int64_t nsend = gh && cm ? B.nsend(cm->nranks) : 0;
+      if (m > 0 || nsend > 0) {
         int* bad = reinterpret_cast<int*>(w.misc + 12);
         CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), st));
-        const int blocks = static_cast<int>(std::max<long long>(1, std::min<long long>((m + 255) / 256, 1024)));
-        csr_check_kernel<<<blocks, 256, 0, st>>>(yp.rp, yp.ci, m, yp.halo, yp.has_prev, yp.has_next, bad);
-        ++g_launches;
-        CUDA_TRY(cudaGetLastError());
+        if (m > 0) {
+          const int blocks = static_cast<int>(std::max<long long>(1, std::min<long long>((m + 255) / 256, 1024)));
+          csr_check_kernel<<<blocks, 256, 0, st>>>(yp.rp, yp.ci, m, yp.halo, gh ? 0 : yp.has_prev,
+                                                   gh ? 1 : yp.has_next, bad);
+          ++g_launches;
+          CUDA_TRY(cudaGetLastError());
+        }
+        if (nsend > 0) {
+          const int blocks = static_cast<int>(std::max<long long>(1, std::min<long long>((nsend + 255) / 256, 1024)));
+          index_check_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const long long*>(B.csr->send_rows), nsend, 0, m,
+                                                     bad);
+          ++g_launches;
+          CUDA_TRY(cudaGetLastError());
+        }
         CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaStreamSynchronize(st));
-        if (hbad) fail("CSR metric: row_ptr not monotone from 0 or a column index outside this rank's rows and halo");
+        if (hbad) fail("CSR metric: row_ptr not monotone from 0, a column index outside this rank's rows and halo / "
+                       "ghosts, or a send row outside [0, m)");
+      }
+      if (cm && gh && hbad == 0) {
+        // rank r's send_counts[p] must equal rank p's recv_counts[r]
+        std::vector<int64_t> all(static_cast<size_t>(cm->nranks) * cm->nranks);
+        int64_t* dscr = reinterpret_cast<int64_t*>(w.partials);
+        TRY(comm_host_allgather(cm, B.csr->send_counts, cm->nranks, all.data(), dscr, st));
+        for (int r = 0; r < cm->nranks; ++r)
+          if (all[static_cast<size_t>(r) * cm->nranks + cm->rank] != B.csr->recv_counts[r]) {
+            hbad = 1;
+            fail("CSR ghost plan: rank %d sends %lld rows to rank %d, which expects %lld", r,
+                 (long long)all[static_cast<size_t>(r) * cm->nranks + cm->rank], cm->rank,
+                 (long long)B.csr->recv_counts[r]);
+            break;
+          }
       }
       if (cm) {
         const int rc = comm_agree(cm, hbad == 0, st);
@@ -847,7 +915,13 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
     if (oblique) {
       if (cm) {
         const int ph = prof_begin(c, PK_COMM);
-        TRY(comm_halo(cm, src, ldsrc, m, static_cast<int>(n), B.halo(), w.halo, st));
+        if (B.ghosts()) {
+          const int64_t nsend = B.nsend(cm->nranks);
+          TRY(comm_ghosts(cm, src, ldsrc, static_cast<int>(n), B.csr->send_rows, B.csr->send_counts,
+                          B.csr->recv_counts, nsend, w.halo + B.csr->nghost * n, w.halo, st));
+        } else {
+          TRY(comm_halo(cm, src, ldsrc, m, static_cast<int>(n), B.halo(), w.halo, st));
+        }
         prof_end(c, ph);
       }
       yp.Q = src;
@@ -1268,6 +1342,11 @@ int scqr3_factor_oblique(int64_t m, int64_t n, const double* X, int64_t ld, cons
 size_t scqr3_workspace_size_csr(int64_t m, int64_t n, int64_t halo) {
   if (n < 1 || n > kMaxN || m < 0 || halo < 0) return 0;
   return make_layout(m, n, 1, halo).end;
+}
+
+size_t scqr3_workspace_size_csr_ghosts(int64_t m, int64_t n, int64_t nghost, int64_t nsend) {
+  if (n < 1 || n > kMaxN || m < 0 || nghost < 0 || nsend < 0) return 0;
+  return make_layout(m, n, 1, std::max<int64_t>(1, (nghost + nsend + 3) / 4)).end;  // (Metric::halo)
 }
 
 int scqr3_factor_oblique_csr(int64_t m, int64_t n, const double* X, int64_t ld, const scqr3_csr* B_csr, double* Q,

@@ -87,6 +87,10 @@ struct ObliqueYParams {
   const int* ci;
   const double* cv;
   long long halo;
+  // ghost-row plan (scqr3_csr.halo == SCQR3_CSR_GHOSTS): indices in [m, m + nghost) read ghost
+  // row (index - m) of `ghost` (row-major, nghost x n); halo then holds nghost
+  int ghosts;
+  const double* ghost;
 };
 
 enum CholMode { CHOL_PASS = 0, CHOL_ONLY = 1 };
@@ -189,6 +193,7 @@ cudaError_t launch_gram_tma(int variant, unsigned grid, int threads, size_t smem
 __global__ void gram_reduce_kernel(GramReduceParams p);
 __global__ void csr_y_kernel(ObliqueYParams p);
 __global__ void csr_gershgorin_kernel(const long long* rp, const double* cv, long long m, double* partial);
+__global__ void index_check_kernel(const long long* v, long long cnt, long long lo, long long hi, int* bad);
 __global__ void csr_check_kernel(const long long* rp, const int* ci, long long m, long long halo, int has_prev,
                                  int has_next, int* bad);
 __global__ void rank_sum_kernel(const double* parts, int nparts, long long count, double* out);

@@ -55,3 +55,45 @@ def run_ranks(fns):
     if err is not None:
         raise err
     return out
+
+
+def csr_ghost_plan(row_ptr, col_idx, vals, m: int, world: int):
+    """Split a global CSR matrix (numpy: row_ptr int64[m+1], col_idx global indices, vals) into
+    the row blocks of `row_block` and build each rank's ghost-row plan (include/scqr3.h,
+    SCQR3_CSR_GHOSTS) -- the distributed sparse matrix-vector product layout, for any sparsity
+    pattern.  Returns, per rank r, a dict with the local CSR (`row_ptr`, `col_idx` int32 with
+    ghost rows at m_r + slot, `vals`) and the plan (`nghost`, `recv_counts`, `send_counts`,
+    `send_rows`): ghost slots are ordered by owning rank, then by global row; rank p's send list
+    to r is r's ghost rows from p in the same order, as p-local row indices.  Index bookkeeping
+    only -- no arithmetic of the method."""
+    import numpy as np
+
+    row_ptr = np.asarray(row_ptr, dtype=np.int64)
+    col_idx = np.asarray(col_idx, dtype=np.int64)
+    vals = np.asarray(vals, dtype=np.float64)
+    bounds = np.array([row_block(m, r, world)[0] for r in range(world)] + [m], dtype=np.int64)
+    need = []      # need[r][p]: sorted global rows rank r reads from rank p
+    local = []
+    for r in range(world):
+        r0, r1 = int(bounds[r]), int(bounds[r + 1])
+        z0, z1 = int(row_ptr[r0]), int(row_ptr[r1])
+        cols = col_idx[z0:z1]
+        owner = np.searchsorted(bounds, cols, side="right") - 1
+        remote = owner != r
+        need_r = [np.unique(cols[remote & (owner == p)]) for p in range(world)]
+        need.append(need_r)
+        slot_base = np.cumsum([0] + [len(x) for x in need_r])
+        lc = np.empty(len(cols), dtype=np.int64)
+        lc[~remote] = cols[~remote] - r0
+        for p in range(world):
+            sel = remote & (owner == p)
+            if sel.any():
+                lc[sel] = (r1 - r0) + slot_base[p] + np.searchsorted(need_r[p], cols[sel])
+        local.append(dict(row_ptr=row_ptr[r0:r1 + 1] - z0, col_idx=lc.astype(np.int32), vals=vals[z0:z1],
+                          nghost=int(slot_base[-1]), recv_counts=np.array([len(x) for x in need_r], dtype=np.int64)))
+    for p in range(world):
+        p0 = int(bounds[p])
+        lists = [need[r][p] - p0 for r in range(world)]
+        local[p]["send_counts"] = np.array([len(x) for x in lists], dtype=np.int64)
+        local[p]["send_rows"] = (np.concatenate(lists) if lists else np.zeros(0)).astype(np.int64)
+    return local

@@ -196,3 +196,53 @@ def test_two_rank_gloo_row_sharded_generator_matches_one_rank():
     assert np.array_equal(X, ref)
     s = np.linalg.svd(X, compute_uv=False)
     assert abs(s[0] - 1.0) < 1e-12 and abs(s[0] / s[-1] / 1e8 - 1.0) < 1e-6
+
+
+def test_csr_ghost_plan_reproduces_global_spmv():
+    """dist.csr_ghost_plan (host bookkeeping for the SCQR3_CSR_GHOSTS exchange): for a Laplacian
+    whose rows and columns are randomly permuted (no band), every rank's local CSR applied to
+    [its rows; the ghost rows its peers send, in plan order] equals the rows of the global B @ X,
+    and rank r's send counts match every peer's receive counts (the collective check the library
+    makes).  Pure numpy, P = 1..5 (including a rank with no rows)."""
+    import synth
+    from paper_1809_11085_b200.dist import csr_ghost_plan, row_block
+
+    rp, ci, cv = synth.laplacian2d(30, 20, seed=0, wmax=10.0)
+    m = len(rp) - 1
+    perm = np.random.default_rng(1).permutation(m)
+    inv = np.empty(m, dtype=np.int64)
+    inv[perm] = np.arange(m)
+    cnt = np.diff(rp)
+    nrp = np.concatenate([[0], np.cumsum(cnt[perm])])
+    idx = np.concatenate([np.arange(rp[o], rp[o + 1]) for o in perm])
+    nci, ncv = inv[ci[idx]], cv[idx]
+    X = np.random.default_rng(2).standard_normal((m, 3))
+    Y = np.zeros_like(X)
+    for i in range(m):
+        for z in range(nrp[i], nrp[i + 1]):
+            Y[i] += ncv[z] * X[nci[z]]
+    for P in (1, 2, 3, 5):
+        plans = csr_ghost_plan(nrp, nci, ncv, m, P)
+        for r in range(P):
+            for p in range(P):
+                assert plans[r]["send_counts"][p] == plans[p]["recv_counts"][r]
+            assert plans[r]["recv_counts"][r] == 0 and plans[r]["send_counts"][r] == 0
+        for r in range(P):
+            r0, r1 = row_block(m, r, P)
+            pl = plans[r]
+            ghost = []
+            for p in range(P):   # what rank p packs for rank r, in its send order
+                p0, _ = row_block(m, p, P)
+                off = int(np.sum(plans[p]["send_counts"][:r]))
+                rows = plans[p]["send_rows"][off:off + plans[p]["send_counts"][r]]
+                ghost.append(X[p0 + rows])
+            G = np.concatenate([X[r0:r1]] + ghost) if ghost else X[r0:r1]
+            assert G.shape[0] == (r1 - r0) + pl["nghost"]
+            Yr = np.zeros((r1 - r0, 3))
+            for i in range(r1 - r0):
+                for z in range(pl["row_ptr"][i], pl["row_ptr"][i + 1]):
+                    Yr[i] += pl["vals"][z] * G[pl["col_idx"][z]]
+            assert np.array_equal(Yr, Y[r0:r1])
+    # a rank with no rows: row_block(m=5, P=8) gives empty blocks
+    plans = csr_ghost_plan(np.arange(6, dtype=np.int64), np.arange(5), np.ones(5), 5, 8)
+    assert sum(p["nghost"] for p in plans) == 0

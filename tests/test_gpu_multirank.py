@@ -26,10 +26,25 @@ U = 2.0 ** -53
 
 if torch.cuda.is_available():
     import paper_1809_11085_b200 as sq
-    from paper_1809_11085_b200.dist import row_block, run_ranks
+    from paper_1809_11085_b200.dist import csr_ghost_plan, row_block, run_ranks
 
 M, N, KAPPA = 200_000, 128, 1e10
 LAP_NX = 500  # 2-D Laplacian grid width = CSR halo rows
+
+
+def _permuted(B, seed=3):
+    """P^T B P for a random permutation: the same SPD Laplacian with its rows and columns
+    scattered, so every row's neighbours live on arbitrary ranks (no band: ghost-row plan)."""
+    rp, ci, cv = B
+    m = len(rp) - 1
+    perm = np.random.default_rng(seed).permutation(m)      # new row i = old row perm[i]
+    inv = np.empty(m, dtype=np.int64)
+    inv[perm] = np.arange(m)
+    cnt = rp[1:] - rp[:-1]
+    nrp = np.zeros(m + 1, dtype=np.int64)
+    nrp[1:] = np.cumsum(cnt[perm])
+    idx = np.concatenate([np.arange(rp[o], rp[o + 1]) for o in perm])
+    return nrp, inv[ci[idx]].astype(np.int32), cv[idx].copy()
 
 
 @functools.lru_cache(maxsize=None)
@@ -39,7 +54,8 @@ def _inputs(kind):
         return X, None
     if kind == "tridiag":
         return X, synth.tridiag_b(M, seed=0)
-    return X, synth.laplacian2d(LAP_NX, M // LAP_NX, seed=0, wmax=1e4)
+    lap = synth.laplacian2d(LAP_NX, M // LAP_NX, seed=0, wmax=1e4)
+    return X, (_permuted(lap) if kind == "csr_ghost" else lap)
 
 
 @functools.lru_cache(maxsize=None)
@@ -50,6 +66,12 @@ def _oracle(kind, P):
     if kind == "tridiag":
         return oracle.scqr3(X, B[0], B[1], nparts=P)
     return oracle.scqr3(X, csr=B, nparts=P)
+
+
+@functools.lru_cache(maxsize=None)
+def _plans(P):
+    X, B = _inputs("csr_ghost")
+    return csr_ghost_plan(*B, X.shape[0], P)
 
 
 def _run(kind, P, deterministic, bounds=None, comms=None):
@@ -75,6 +97,11 @@ def _run(kind, P, deterministic, bounds=None, comms=None):
             e = torch.from_numpy(B[1][r0:r1].copy()).cuda()
             kw["ws"] = sq.workspace(mr, n, oblique=True)
             args.append((sq.scqr3_factor_oblique, (Xr, d, e), kw))
+        elif kind == "csr_ghost":
+            pl = _plans(P)[r]
+            csr = sq.CsrMetric(pl["row_ptr"], pl["col_idx"], pl["vals"],
+                               ghosts=(pl["nghost"], pl["recv_counts"], pl["send_counts"], pl["send_rows"]))
+            args.append((sq.scqr3_factor_oblique_csr, (Xr, csr), kw))
         else:
             csr = sq.CsrMetric(*synth.csr_rows(B, r0, r1), halo=LAP_NX)
             kw["ws"] = sq.workspace(mr, n, csr_halo=LAP_NX)
@@ -109,7 +136,7 @@ def _check(kind, P, res, Q):
     elif kind == "tridiag":
         orth = oracle.orth_F(Q, B[0], B[1])
     else:
-        orth = oracle.orth_F_csr(Q, B)
+        orth = oracle.orth_F_csr(Q, B)   # (csr_ghost: the permuted global B)
     resid = oracle.resid_F(X, Q, R0)
     assert orth <= 10 * n * U and resid <= 10 * n * U, (orth, resid)
     return err
@@ -117,7 +144,7 @@ def _check(kind, P, res, Q):
 
 @gpu
 @pytest.mark.parametrize("P", [2, 4, 8])
-@pytest.mark.parametrize("kind", ["standard", "tridiag", "csr"])
+@pytest.mark.parametrize("kind", ["standard", "tridiag", "csr", "csr_ghost"])
 @pytest.mark.parametrize("deterministic", [False, True])
 def test_loopback_factor_parity(kind, P, deterministic):
     res, Q = _run(kind, P, deterministic)
@@ -268,3 +295,54 @@ def test_loopback_complex_and_gram():
         assert np.all(np.abs(A - Ao) <= bound)
     for c in comms:
         c.destroy()
+
+
+@gpu
+def test_ghost_plan_single_rank_and_rejection():
+    """The ghost-plan CSR mode on one GPU (no communicator: nghost = 0) equals the plain CSR
+    call bit for bit; across ranks, a send count that does not match the receiver's recv count
+    makes every rank return SCQR3_EINVAL before any exchange."""
+    X, B = _inputs("csr_ghost")
+    m, n = 20_000, 32
+    Xs = np.asfortranarray(X[:m, :n])
+    rp, ci, cv = synth.csr_rows(B, 0, m)
+    keep = (ci >= 0) & (ci < m)   # drop the couplings out of the first block: an SPD principal block
+    rows = np.repeat(np.arange(m), np.diff(rp))[keep]
+    nrp = np.zeros(m + 1, dtype=np.int64)
+    np.add.at(nrp, rows + 1, 1)
+    nrp = np.cumsum(nrp)
+    Xd = sq.to_colmajor(torch.from_numpy(Xs), device="cuda")
+    a = sq.scqr3_factor_oblique_csr(Xd, sq.CsrMetric(nrp, ci[keep], cv[keep]))
+    g = sq.scqr3_factor_oblique_csr(Xd, sq.CsrMetric(nrp, ci[keep], cv[keep],
+                                                     ghosts=(0, np.zeros(1), np.zeros(1), np.zeros(0))))
+    assert a.status == g.status == 0
+    assert np.array_equal(a.R.cpu().numpy(), g.R.cpu().numpy())
+    # inconsistent plan over 2 ranks: rank 0 claims one row more than rank 1 expects
+    P = 2
+    pls = [dict(p) for p in _plans(P)]
+    pls[0]["send_counts"] = pls[0]["send_counts"].copy()
+    pls[0]["send_counts"][1] += 1
+    pls[0]["send_rows"] = np.concatenate([pls[0]["send_rows"], [0]])
+    comms = sq.Comm.loopback(P)
+    try:
+        args = []
+        for r in range(P):
+            r0, r1 = row_block(M, r, P)
+            pl = pls[r]
+            csr = sq.CsrMetric(pl["row_ptr"], pl["col_idx"], pl["vals"],
+                               ghosts=(pl["nghost"], pl["recv_counts"], pl["send_counts"], pl["send_rows"]))
+            Xr = sq.to_colmajor(torch.from_numpy(np.asfortranarray(X[r0:r1])), device="cuda")
+            args.append((Xr, csr, dict(comm=comms[r], stream=torch.cuda.Stream())))
+
+        def call(a):
+            try:
+                return sq.scqr3_factor_oblique_csr(a[0], a[1], **a[2]).status
+            except sq.ScqrError as e:
+                return str(e)
+
+        out = run_ranks([lambda a=a: call(a) for a in args])
+        assert all(isinstance(o, str) for o in out), out
+        assert "ghost plan" in out[1] and "rank 1" in out[0], out
+    finally:
+        for c in comms:
+            c.destroy()
