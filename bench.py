@@ -400,15 +400,50 @@ def run_ours(args):
                 rh = sq.scqr3_factor_host(Xh, Q=Qh, R=Rh, ws=wsh, comm=comm, m_global=m, stream=stream)
             a1.record(stream)
         stream.synchronize()
-        ems = a0.elapsed_time(a1) / args.e2e_steps
-        te = torch.tensor([ems], dtype=torch.float64, device=dev)
+        ems1 = a0.elapsed_time(a1) / args.e2e_steps
+        # streaming: scqr3_factor_host_batch over e2e_steps matrices (each uploaded, factored and
+        # downloaded; the uploads / downloads of neighbouring matrices overlap the factorisation)
+        del wsh
+        torch.cuda.empty_cache()
+        ebatch = max(args.e2e_steps, 8)
+        try:
+            wsb = torch.empty(sq._abi.lib().scqr3_host_batch_workspace_size(mloc, n), dtype=torch.uint8, device=dev)
+        except torch.cuda.OutOfMemoryError:  # three staging buffers do not fit: one matrix per call
+            wsb = None
+        okb = torch.tensor([0.0 if wsb is None else 1.0], dtype=torch.float64, device=dev)
+        if multi:
+            dist.all_reduce(okb, op=dist.ReduceOp.MIN)  # the same choice on every rank
+        if okb.item() == 0.0:
+            wsb = None
+    if want_e2e and wsb is None:
+        e2e = {"value": flops_3pass(m, n) / (ems1 * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": 8 * mloc * n, "d2h_bytes_per_step": 8 * mloc * n + 8 * n * n,
+               "ms_per_step": ems1, "status": rh.status,
+               "api": "scqr3_factor_host (pinned host X in, pinned host Q and R out)"}
+    elif want_e2e:
+        with torch.cuda.stream(stream):
+            sq.scqr3_factor_host_batch([Xh] * 2, [Qh] * 2, [Rh] * 2, ws=wsb, comm=comm, m_global=m,
+                                       stream=stream)  # warm-up (graph captures of the staging buffers)
+            if multi:
+                dist.barrier()
+            a0.record(stream)
+            sts = sq.scqr3_factor_host_batch([Xh] * ebatch, [Qh] * ebatch, [Rh] * ebatch, ws=wsb, comm=comm,
+                                             m_global=m, stream=stream)
+            a1.record(stream)
+        stream.synchronize()
+        ems = a0.elapsed_time(a1) / ebatch
+        te = torch.tensor([ems, ems1], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        ems = float(te.item())
+        ems, ems1 = float(te[0].item()), float(te[1].item())
+        del wsb
         e2e = {"value": flops_3pass(m, n) / (ems * 1e-3) / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": 8 * mloc * n, "d2h_bytes_per_step": 8 * mloc * n + 8 * n * n,
-               "ms_per_step": ems, "status": rh.status,
-               "api": "scqr3_factor_host (pinned host X in, pinned host Q and R out)"}
+               "ms_per_step": ems, "status": max(sts), "matrices": ebatch,
+               "api": "scqr3_factor_host_batch (pinned host X in, pinned host Q and R out; the next matrix's "
+                      "upload and the previous one's download overlap each factorisation)",
+               "single_call": {"value": flops_3pass(m, n) / (ems1 * 1e-3) / 1e12, "ms_per_step": ems1,
+                               "status": rh.status, "api": "scqr3_factor_host (one matrix per call)"}}
 
     # ---- CPU oracle baseline on a bounded sample of the same X (rank 0, N=1 only)
     cpu = None

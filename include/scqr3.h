@@ -226,6 +226,21 @@ size_t scqr3_host_workspace_size(int64_t m, int64_t n);
 int scqr3_factor_host(int64_t m, int64_t n, const double* X_host, int64_t ld, double* Q_host,
                       int64_t ldq, double* R_host, const scqr3_opts* opts);
 
+/* Streaming variant of scqr3_factor_host for `count` independent m x n host matrices (a serving
+ * loop): X_hosts[i] (ld) -> Q_hosts[i] (ldq), R_hosts[i] (n x n), statuses[i] (SCQR3_OK /
+ * _EBREAKDOWN / _ENOCONV; Q and R written on OK only).  Three device staging buffers rotate, so
+ * matrix i+1's upload and matrix i-1's download run on the two PCIe directions (library streams)
+ * while matrix i is factored on opts->stream -- each matrix still goes host -> device -> host.
+ * Host buffers: pinned for full bandwidth; an X_hosts entry must not alias a Q_hosts / R_hosts
+ * entry of another matrix in the batch (repeating the same X, or the same Q / R, is fine).
+ * opts->workspace: scqr3_host_batch_workspace_size(m, n) bytes.  Returns SCQR3_OK once every
+ * matrix is done (statuses per matrix), or SCQR3_EINVAL.  Single GPU or one rank per GPU
+ * (every rank calls it with the same count). */
+size_t scqr3_host_batch_workspace_size(int64_t m, int64_t n);
+int scqr3_factor_host_batch(int64_t count, int64_t m, int64_t n, const double* const* X_hosts, int64_t ld,
+                            double* const* Q_hosts, int64_t ldq, double* const* R_hosts, int32_t* statuses,
+                            const scqr3_opts* opts);
+
 /* ---- kernel-level entry points (parity tests call these through the same library) ---- */
 /* A = Q^T Q (n x n, column-major, both triangles) -- one Gram kernel + reduction. */
 int scqr3_gram(int64_t m, int64_t n, const double* X, int64_t ld, double* A, const scqr3_opts* opts);

@@ -21,7 +21,7 @@ __all__ = [
     "scqr3_factor", "scqr3_factor_oblique", "scqr3_factor_host", "scqr3_gram", "scqr3_gram_oblique",
     "scqr3_cholesky", "scqr3_trsm", "colmajor_empty", "to_colmajor", "workspace", "Comm", "Result",
     "ScqrError", "launch_count", "library_path", "CsrMetric", "scqr3_factor_oblique_csr",
-    "scqr3_gram_oblique_csr", "scqr3_factor_complex", "colmajor_empty_complex",
+    "scqr3_gram_oblique_csr", "scqr3_factor_complex", "colmajor_empty_complex", "scqr3_factor_host_batch",
 ]
 
 library_path = _abi.LIB_PATH
@@ -324,6 +324,27 @@ def scqr3_factor_host(X, *, Q=None, R=None, ws=None, **kw) -> Result:
     rc = _check(_abi.lib().scqr3_factor_host(m, n, X.data_ptr(), max(X.stride(1), m), Q.data_ptr(),
                                              max(Q.stride(1), m), R.data_ptr(), ctypes.byref(o)))
     return Result(rc, Q, R, passes.value, _trace(tr, passes.value))
+
+
+def scqr3_factor_host_batch(Xs, Qs, Rs, *, ws=None, **kw) -> list:
+    """Streaming end-to-end factorisation of len(Xs) independent HOST (pinned) column-major m x n
+    matrices: uploads / downloads overlap the factorisations (include/scqr3.h).  Qs, Rs: output
+    host tensors, one per input (entries may repeat).  Returns the per-matrix statuses."""
+    import numpy as np
+    torch = _torch()
+    count = len(Xs)
+    if not (len(Qs) == len(Rs) == count) or count == 0:
+        raise ScqrError("Xs, Qs, Rs must have the same nonzero length")
+    m, n = Xs[0].shape
+    if ws is None:
+        ws = torch.empty(_abi.lib().scqr3_host_batch_workspace_size(m, n), dtype=torch.uint8, device="cuda")
+    o, tr, passes = _opts(ws=ws, **kw)
+    arr = ctypes.c_void_p * count
+    xp, qp, rp = arr(*[x.data_ptr() for x in Xs]), arr(*[q.data_ptr() for q in Qs]), arr(*[r.data_ptr() for r in Rs])
+    st = np.zeros(count, dtype=np.int32)
+    _check(_abi.lib().scqr3_factor_host_batch(count, m, n, xp, max(Xs[0].stride(1), m), qp, max(Qs[0].stride(1), m),
+                                              rp, st.ctypes.data, ctypes.byref(o)))
+    return [int(v) for v in st]
 
 
 def scqr3_gram(X, *, ws=None, **kw):

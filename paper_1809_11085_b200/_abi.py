@@ -22,6 +22,7 @@ EXPORTED = [
     "scqr3_comm_destroy", "scqr3_last_error", "scqr3_launch_count", "scqr3_workspace_size_csr",
     "scqr3_factor_oblique_csr", "scqr3_gram_oblique_csr", "scqr3_workspace_size_complex",
     "scqr3_factor_complex", "scqr3_comm_init_loopback", "scqr3_workspace_size_csr_ghosts",
+    "scqr3_host_batch_workspace_size", "scqr3_factor_host_batch",
 ]
 
 
@@ -91,6 +92,9 @@ def lib():
         L.scqr3_host_workspace_size.argtypes = [i64, i64]
         L.scqr3_host_workspace_size.restype = ctypes.c_size_t
         L.scqr3_factor_host.argtypes = [i64, i64, vp, i64, vp, i64, vp, P]
+        L.scqr3_host_batch_workspace_size.argtypes = [i64, i64]
+        L.scqr3_host_batch_workspace_size.restype = ctypes.c_size_t
+        L.scqr3_factor_host_batch.argtypes = [i64, i64, i64, vp, i64, vp, i64, vp, vp, P]
         L.scqr3_gram.argtypes = [i64, i64, vp, i64, vp, P]
         L.scqr3_gram_oblique.argtypes = [i64, i64, vp, i64, vp, vp, vp, vp, P]
         PC = ctypes.POINTER(Csr)

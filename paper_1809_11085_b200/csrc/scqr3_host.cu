@@ -65,7 +65,6 @@ struct GraphPlan {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   int64_t launches_first = 0, launches_body = 0;
-  bool failed = false;  // capture not supported here: use the host loop from now on
   void reset() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
@@ -85,7 +84,13 @@ struct Ctx {
   cudaEvent_t ev = nullptr;
   cudaEvent_t ev_pass[kSlots] = {};  // chol of pass k done (its status slot is readable)
   int cur_pass = 0;                  // pass being enqueued (tags the profiling events)
-  GraphPlan plan;                    // cached CUDA-graph pass loop (single GPU)
+  static constexpr int kPlans = 4;   // cached CUDA-graph pass loops (single GPU), one per argument set
+  GraphPlan plans[kPlans];           //   (scqr3_factor_host_batch rotates three staging buffers)
+  int plan_next = 0;                 // replacement cursor
+  bool plan_failed = false;          // capture not supported here: the host loop from now on
+  // scqr3_factor_host_batch: upload / download streams and per-staging-buffer events
+  cudaStream_t up = nullptr, down = nullptr;
+  cudaEvent_t ev_up[3] = {}, ev_fact[3] = {}, ev_down[3] = {}, ev_start = nullptr;
   cudaStream_t side = nullptr;     // R accumulation, overlapped with the TRSM
   cudaStream_t cap = nullptr;      // graph capture (the caller's stream may be the legacy default)
   cudaEvent_t ev_chol = nullptr;   // chol done (st) -> side may start
@@ -1034,7 +1039,7 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
   for (int k = 0; k < max_passes; ++k) c->st_host[k].code = -1;
 
   int status = SCQR3_ENOCONV, k = 0;
-  const bool use_graph = g_use_graph && !cm && !o->prof && m > 0 && !c->plan.failed;
+  const bool use_graph = g_use_graph && !cm && !o->prof && m > 0 && !c->plan_failed;
   bool done = false;
   if (use_graph) {
     // ---- CUDA-graph pass loop, captured once per argument set and replayed
@@ -1042,8 +1047,11 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
     key.X = X; key.Q = Q; key.R = R; key.ld = ld; key.ldq = ldq; key.m = m; key.n = n;
     key.ws = o->workspace; key.st = st; key.max_passes = max_passes; key.cp = cp; key.tp = tp; key.yp = yp;
     static_assert(sizeof(GraphKey) <= sizeof(GraphPlan::key), "graph key buffer too small");
-    GraphPlan& gpn = c->plan;
-    if (!gpn.exec || std::memcmp(gpn.key, &key, sizeof key) != 0) {
+    GraphPlan* hit = nullptr;
+    for (GraphPlan& p : c->plans)
+      if (p.exec && std::memcmp(p.key, &key, sizeof key) == 0) hit = &p;
+    GraphPlan& gpn = hit ? *hit : c->plans[c->plan_next++ % Ctx::kPlans];
+    if (!hit) {
       gpn.reset();
       const cudaStream_t user_st = st;
       st = c->cap;  // the enqueue lambdas capture on the internal stream
@@ -1053,7 +1061,7 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
         std::memcpy(gpn.key, &key, sizeof key);
       } else {
         gpn.reset();  // fall through to the host loop (same kernels), and stop trying
-        gpn.failed = true;
+        c->plan_failed = true;
       }
     }
     if (gpn.exec) {
@@ -1387,6 +1395,97 @@ int scqr3_factor_host(int64_t m, int64_t n, const double* X_host, int64_t ld, do
   if (m > 0)
     CUDA_TRY(cudaMemcpy2DAsync(Q_host, ldq * 8, D, ldd * 8, m * 8, n, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaMemcpyAsync(R_host, Rd, static_cast<size_t>(n) * n * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return SCQR3_OK;
+}
+
+size_t scqr3_host_batch_workspace_size(int64_t m, int64_t n) {
+  if (n < 1 || n > kMaxN || m < 0) return 0;
+  const int64_t ldd = std::max<int64_t>(2, (m + 1) & ~1LL);
+  return 3 * (align256(static_cast<size_t>(ldd) * n * 8) + align256(static_cast<size_t>(n) * n * 8)) +
+         make_layout(m, n, 0).end;
+}
+
+// Streaming end-to-end factorisation of independent host matrices: three device staging buffers
+// rotate; matrix i+1 uploads (stream `up`) and matrix i-1 downloads (stream `down`) on the two
+// PCIe directions while matrix i is factored on opts->stream (factor_impl, synchronous).
+int scqr3_factor_host_batch(int64_t count, int64_t m, int64_t n, const double* const* X_hosts, int64_t ld,
+                            double* const* Q_hosts, int64_t ldq, double* const* R_hosts, int32_t* statuses,
+                            const scqr3_opts* opts) {
+  TRY(check_opts(opts));
+  if (count < 0) return fail("count < 0");
+  if (n < 1 || n > kMaxN || m < 0) return fail("bad sizes m=%lld n=%lld", (long long)m, (long long)n);
+  if (count > 0 && (!X_hosts || !Q_hosts || !R_hosts || !statuses)) return fail("NULL pointer array");
+  for (int64_t i = 0; i < count; ++i)
+    if ((m > 0 && (!X_hosts[i] || !Q_hosts[i])) || !R_hosts[i]) return fail("host pointer %lld is NULL", (long long)i);
+  if (ld < m || ldq < m) return fail("leading dimension < m");
+  if (!opts->workspace || opts->workspace_bytes < scqr3_host_batch_workspace_size(m, n))
+    return fail("workspace too small for scqr3_factor_host_batch");
+  Ctx* c;
+  TRY(get_ctx(&c));
+  if (!c->up) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->up, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->down, cudaStreamNonBlocking));
+    for (int b = 0; b < 3; ++b) {
+      CUDA_TRY(cudaEventCreateWithFlags(&c->ev_up[b], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fact[b], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->ev_down[b], cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
+  }
+  const int64_t ldd = std::max<int64_t>(2, (m + 1) & ~1LL);
+  const size_t dbytes = align256(static_cast<size_t>(ldd) * n * 8), rbytes = align256(static_cast<size_t>(n) * n * 8);
+  char* b0 = static_cast<char*>(opts->workspace);
+  double* D[3];
+  double* Rd[3];
+  for (int b = 0; b < 3; ++b) {
+    D[b] = reinterpret_cast<double*>(b0 + b * (dbytes + rbytes));
+    Rd[b] = reinterpret_cast<double*>(b0 + b * (dbytes + rbytes) + dbytes);
+  }
+  scqr3_opts o2 = *opts;
+  o2.workspace = b0 + 3 * (dbytes + rbytes);
+  o2.workspace_bytes = opts->workspace_bytes - 3 * (dbytes + rbytes);
+  cudaStream_t st = static_cast<cudaStream_t>(opts->stream);
+  // the copies follow the work already on opts->stream (and its timing events)
+  CUDA_TRY(cudaEventRecord(c->ev_start, st));
+  CUDA_TRY(cudaStreamWaitEvent(c->up, c->ev_start, 0));
+  CUDA_TRY(cudaStreamWaitEvent(c->down, c->ev_start, 0));
+  bool used[3] = {false, false, false};
+  auto upload = [&](int64_t i) -> int {
+    const int b = static_cast<int>(i % 3);
+    if (used[b]) CUDA_TRY(cudaStreamWaitEvent(c->up, c->ev_down[b], 0));  // its previous matrix is down
+    used[b] = true;
+    if (m > 0)
+      CUDA_TRY(cudaMemcpy2DAsync(D[b], ldd * 8, X_hosts[i], ld * 8, m * 8, n, cudaMemcpyHostToDevice, c->up));
+    CUDA_TRY(cudaEventRecord(c->ev_up[b], c->up));
+    return SCQR3_OK;
+  };
+  if (count > 0) TRY(upload(0));
+  if (count > 1) TRY(upload(1));
+  for (int64_t i = 0; i < count; ++i) {
+    const int b = static_cast<int>(i % 3);
+    CUDA_TRY(cudaStreamWaitEvent(st, c->ev_up[b], 0));
+    const int rc = factor_impl(m, n, D[b], ldd, Metric{}, D[b], ldd, Rd[b], &o2);
+    if (rc == SCQR3_EINVAL) {
+      cudaStreamSynchronize(c->up);
+      cudaStreamSynchronize(c->down);
+      return rc;
+    }
+    statuses[i] = rc;
+    CUDA_TRY(cudaEventRecord(c->ev_fact[b], st));
+    CUDA_TRY(cudaStreamWaitEvent(c->down, c->ev_fact[b], 0));
+    if (rc == SCQR3_OK) {  // (Q and R are written only on success, as scqr3_factor's)
+      if (m > 0)
+        CUDA_TRY(cudaMemcpy2DAsync(Q_hosts[i], ldq * 8, D[b], ldd * 8, m * 8, n, cudaMemcpyDeviceToHost, c->down));
+      CUDA_TRY(cudaMemcpyAsync(R_hosts[i], Rd[b], static_cast<size_t>(n) * n * 8, cudaMemcpyDeviceToHost, c->down));
+    }
+    CUDA_TRY(cudaEventRecord(c->ev_down[b], c->down));
+    if (i + 2 < count) TRY(upload(i + 2));
+  }
+  // opts->stream continues after the last download (timing events recorded on it see all copies)
+  CUDA_TRY(cudaEventRecord(c->ev_start, c->down));
+  CUDA_TRY(cudaStreamWaitEvent(st, c->ev_start, 0));
+  CUDA_TRY(cudaStreamSynchronize(c->down));
   CUDA_TRY(cudaStreamSynchronize(st));
   return SCQR3_OK;
 }

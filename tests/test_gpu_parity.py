@@ -259,6 +259,39 @@ def test_host_api_matches_device_api():
 
 
 @gpu
+@pytest.mark.parametrize("count", [1, 2, 5])
+def test_host_batch_matches_single_calls(count):
+    """scqr3_factor_host_batch (uploads / downloads overlapped with the factorisations, three
+    rotating staging buffers) gives every matrix the bits of its own scqr3_factor_host call; a
+    matrix that breaks down reports its status without disturbing the others; a repeated input
+    buffer gives repeated results."""
+    m, n = 7001, 40
+    Xs = [synth.randsvd(m, n, 10.0 ** (4 + 2 * i), seed=i) for i in range(count)]
+    def pin(A=None, shape=(m, n)):   # pinned column-major host tensor
+        T = torch.empty(shape[::-1], dtype=torch.float64, pin_memory=True)
+        if A is not None:
+            T.copy_(torch.from_numpy(np.ascontiguousarray(A.T)))
+        return T.t()
+
+    Xh = [pin(X) for X in Xs]
+    Qh = [pin() for _ in range(count)]
+    Rh = [pin(shape=(n, n)) for _ in range(count)]
+    st = sq.scqr3_factor_host_batch(Xh, Qh, Rh)
+    assert st == [0] * count
+    for i in range(count):
+        r1 = sq.scqr3_factor_host(Xh[i])
+        assert np.array_equal(r1.R.numpy(), Rh[i].numpy()) and np.array_equal(r1.Q.numpy(), Qh[i].numpy())
+    # a plain (unshifted) CholeskyQR breaks down at kappa = 1e12 (P:28-31); the others are fine
+    bad = pin(synth.randsvd(m, n, 1e12, seed=9))
+    Xb = [Xh[0], bad, Xh[0]]
+    Qb = [pin() for _ in range(3)]
+    Rb = [pin(shape=(n, n)) for _ in range(3)]
+    st = sq.scqr3_factor_host_batch(Xb, Qb, Rb, shift_mode=sq.SHIFT_NONE)
+    assert st[1] == sq.EBREAKDOWN and st[0] == st[2] == 0, st
+    assert np.array_equal(Rb[0].numpy(), Rb[2].numpy()) and np.array_equal(Qb[0].numpy(), Qb[2].numpy())
+
+
+@gpu
 def test_single_rank_nccl_comm_path():
     """One-rank NCCL communicator: exercises ncclAllReduce / send-recv plumbing on one GPU."""
     import ctypes
