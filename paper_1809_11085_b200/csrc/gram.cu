@@ -36,14 +36,14 @@ __device__ __forceinline__ void decode_job(int j, int NB, bool full, int& bi, in
 // (18 consumer warps fit 96 registers).  Fragment address of k-step s: the lane's 16-byte chunk
 // is (s + 4*(t>>1)) ^ g = s ^ G, i.e. offset ^ (s << 4) on a 128-byte aligned row base; the
 // block's tile rows / columns sit 8 x 128 B apart (immediate offsets).
-template <bool MC>
+template <bool MC, int RB>
 __device__ __forceinline__ void gram_whole_jobs(const GramParams& p, const unsigned char* stages, uint32_t stage_bytes,
                                                 int nsrc, uint64_t* full_bar, uint64_t* empty_bar, int nst, int kind,
                                                 bool b_from_y, bool full, int bi, int bj, bool diag,
                                                 double (&acc)[4][kJobTiles][2], const uint32_t (&offA)[4],
-                                                const uint32_t (&offB)[kJobTiles], const uint32_t (&inner)[4]) {
+                                                const uint32_t (&offB)[kJobTiles], const uint32_t (&innerR)[RB][4]) {
   const int lane = threadIdx.x & 31;
-  const uint32_t lane_chunk = inner[0];  // chunk G << 4 plus the 8-byte half of this lane's k slot
+  constexpr uint32_t TS = 1024u * RB;  // bytes between tile rows / columns (8 columns x RB lines)
   auto release = [&](uint64_t* bar) {  // this stage consumed: in every CTA of the cluster (multicast)
     if constexpr (MC) {
       for (int j = 0; j < p.mc; ++j) mbar_arrive_cluster(bar, static_cast<uint32_t>(j));
@@ -52,13 +52,20 @@ __device__ __forceinline__ void gram_whole_jobs(const GramParams& p, const unsig
     }
   };
   auto frag = [&](uint32_t off) { return *reinterpret_cast<const double*>(stages + off); };
+  // each stage holds RB 16-row blocks (line rb of a column at +rb*128); lane_chunk(rb): chunk G
+  // << 4 plus the 8-byte half of this lane's k slot for that block's swizzle key
+  uint32_t lane_chunk;
   auto stage_loop = [&](auto body) {
     int st = 0;
     uint32_t ph = 0;
     for (int i = 0; i < nst; ++i) {
       mbar_wait(&full_bar[st], ph);
       const uint32_t oA = static_cast<uint32_t>(st) * nsrc * stage_bytes;
-      body(oA, b_from_y ? oA + stage_bytes : oA);
+#pragma unroll
+      for (int rb = 0; rb < RB; ++rb) {
+        lane_chunk = innerR[rb][0];
+        body(oA + rb * 128u, (b_from_y ? oA + stage_bytes : oA) + rb * 128u);
+      }
       __syncwarp();
       if (lane == 0) release(&empty_bar[st]);
       if (++st == p.stages) {
@@ -69,17 +76,17 @@ __device__ __forceinline__ void gram_whole_jobs(const GramParams& p, const unsig
   };
   if (kind == 0) {
     // 4 x 4 tiles of an off-diagonal block: 8 fragment loads, 16 DMMA per k-step
-    const uint32_t a0 = offA[0] + lane_chunk, b0 = offB[0] + lane_chunk;
     stage_loop([&](uint32_t oA, uint32_t oB) {
+      const uint32_t a0 = offA[0] + lane_chunk, b0 = offB[0] + lane_chunk;
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
         const uint32_t xa = (oA + a0) ^ (s << 4), xb = (oB + b0) ^ (s << 4);
         double fb[kJobTiles];
 #pragma unroll
-        for (int b = 0; b < kJobTiles; ++b) fb[b] = frag(xb + b * 1024);
+        for (int b = 0; b < kJobTiles; ++b) fb[b] = frag(xb + b * TS);
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
-          const double fa = frag(xa + a * 1024);
+          const double fa = frag(xa + a * TS);
 #pragma unroll
           for (int b = 0; b < kJobTiles; ++b) dmma(acc[a][b][0], acc[a][b][1], fa, fb[b]);
         }
@@ -87,16 +94,16 @@ __device__ __forceinline__ void gram_whole_jobs(const GramParams& p, const unsig
     });
   } else if (kind == 1) {
     // diagonal block: its 10 upper tiles (A fragments = B fragments for Q^T Q; from Q for Q^T Y)
-    const uint32_t b0 = offB[0] + lane_chunk;
     stage_loop([&](uint32_t oA, uint32_t oB) {
+      const uint32_t b0 = offB[0] + lane_chunk;
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
         const uint32_t xa = (oA + b0) ^ (s << 4), xb = (oB + b0) ^ (s << 4);
         double fb[kJobTiles], fa[4];
 #pragma unroll
-        for (int b = 0; b < kJobTiles; ++b) fb[b] = frag(xb + b * 1024);
+        for (int b = 0; b < kJobTiles; ++b) fb[b] = frag(xb + b * TS);
 #pragma unroll
-        for (int a = 0; a < 4; ++a) fa[a] = full ? frag(xa + a * 1024) : fb[a];
+        for (int a = 0; a < 4; ++a) fa[a] = full ? frag(xa + a * TS) : fb[a];
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -108,19 +115,19 @@ __device__ __forceinline__ void gram_whole_jobs(const GramParams& p, const unsig
     // (an off-diagonal edge block has all four tile rows, the diagonal one a <= b < cb).
     // Specialised on cb so that no DMMA is issued for a padded tile -- predicated-off DMMAs
     // still take their issue slots (n = 144 ran 25 % slower than n = 160 that way)
-    const uint32_t a0 = offA[0] + lane_chunk, b0 = offB[0] + lane_chunk;
     auto edge = [&](auto cbc) {
       constexpr int CB = decltype(cbc)::value;
       if (diag) {
         stage_loop([&](uint32_t oA, uint32_t oB) {
+          const uint32_t a0 = offA[0] + lane_chunk, b0 = offB[0] + lane_chunk;
 #pragma unroll
           for (int s = 0; s < 4; ++s) {
             const uint32_t xa = (oA + a0) ^ (s << 4), xb = (oB + b0) ^ (s << 4);
             double fb[CB], fa[CB];
 #pragma unroll
-            for (int b = 0; b < CB; ++b) fb[b] = frag(xb + b * 1024);
+            for (int b = 0; b < CB; ++b) fb[b] = frag(xb + b * TS);
 #pragma unroll
-            for (int a = 0; a < CB; ++a) fa[a] = full ? frag(xa + a * 1024) : fb[a];
+            for (int a = 0; a < CB; ++a) fa[a] = full ? frag(xa + a * TS) : fb[a];
 #pragma unroll
             for (int a = 0; a < CB; ++a)
 #pragma unroll
@@ -129,15 +136,16 @@ __device__ __forceinline__ void gram_whole_jobs(const GramParams& p, const unsig
         });
       } else {
         stage_loop([&](uint32_t oA, uint32_t oB) {
+          const uint32_t a0 = offA[0] + lane_chunk, b0 = offB[0] + lane_chunk;
 #pragma unroll
           for (int s = 0; s < 4; ++s) {
             const uint32_t xa = (oA + a0) ^ (s << 4), xb = (oB + b0) ^ (s << 4);
             double fb[CB];
 #pragma unroll
-            for (int b = 0; b < CB; ++b) fb[b] = frag(xb + b * 1024);
+            for (int b = 0; b < CB; ++b) fb[b] = frag(xb + b * TS);
 #pragma unroll
             for (int a = 0; a < 4; ++a) {
-              const double fa = frag(xa + a * 1024);
+              const double fa = frag(xa + a * TS);
 #pragma unroll
               for (int b = 0; b < CB; ++b) dmma(acc[a][b][0], acc[a][b][1], fa, fb[b]);
             }
@@ -154,10 +162,15 @@ __device__ __forceinline__ void gram_whole_jobs(const GramParams& p, const unsig
   }
 }
 
-template <int JR, int MAXC, bool MC>
+// RB: 16-row blocks per stage.  RB = 2 streams 32-row stages through a 3-D view of Q
+// (16 rows, 16-row blocks, columns): one box fetches 256 contiguous bytes per column while each
+// 128-B line keeps the SWIZZLE_128B layout -- 7.3 TB/s of TMA reads against 4.6 TB/s for 16-row
+// 2-D boxes (tools/tma_probe.cu); taken for m % 32 == 0 without multicast.
+template <int JR, int MAXC, bool MC, int RB = 1>
 __global__ void __launch_bounds__(32 * (MAXC + 1), 1)
     gram_tma_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapY,
                     GramParams p) {
+  static_assert(RB == 1 || !MC, "32-row stages: unclustered only");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   if (SCQR3_GATE_SKIP(p.gate)) return;  // speculative pass after a stop / error (device-side pass control)
   // 1024-B alignment for SWIZZLE_128B
@@ -169,7 +182,7 @@ __global__ void __launch_bounds__(32 * (MAXC + 1), 1)
   const int chunk = blockIdx.x / p.groups;
   const bool full = p.oblique != 0;
   const int nsrc = full ? 2 : 1;
-  const uint32_t stage_bytes = static_cast<uint32_t>(p.npad) * 128u;   // 16 rows x npad cols x 8 B
+  const uint32_t stage_bytes = static_cast<uint32_t>(p.npad) * 128u * RB;   // 16 RB rows x npad cols x 8 B
   unsigned char* stages = smem;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(p.stages) * nsrc * stage_bytes);
   uint64_t* empty_bar = full_bar + p.stages;
@@ -212,8 +225,15 @@ __global__ void __launch_bounds__(32 * (MAXC + 1), 1)
           else mbar_wait(&empty_bar[st], ph ^ 1);
         }
         mbar_arrive_expect_tx(&full_bar[st], stage_bytes * nsrc);
-        const int row = static_cast<int>((s_begin + i) * kGramStageRows);
+        const int row = static_cast<int>((s_begin + i) * kGramStageRows * RB);
         unsigned char* dst = stages + static_cast<size_t>(st) * nsrc * stage_bytes;
+        if constexpr (RB > 1) {  // 3-D boxes {16 rows, RB blocks, box_cols}: [column][block][16 rows]
+          for (int c0 = 0; c0 < p.npad; c0 += p.box_cols) {
+            tma_load_3d(dst + c0 * 128u * RB, &mapQ, 0, row / 16, c0, &full_bar[st]);
+            if (full) tma_load_3d(dst + stage_bytes + c0 * 128u * RB, &mapY, 0, row / 16, c0, &full_bar[st]);
+          }
+          continue;
+        }
         // a TMA box spans at most 256 columns: wider stages take several boxes (npad 512)
         if (mc) {
           for (int c0 = static_cast<int>(crank) * p.box_cols; c0 < p.npad; c0 += p.mc * p.box_cols) {
@@ -269,29 +289,37 @@ __global__ void __launch_bounds__(32 * (MAXC + 1), 1)
   // per-lane smem offsets (without the k-step part) of the job's tile rows / the block's columns
   uint32_t offA[JR], offB[kJobTiles];
 #pragma unroll
-  for (int a = 0; a < JR; ++a) offA[a] = static_cast<uint32_t>(8 * min(bi * kJobTiles + rr0 + a, NT - 1) + g) * 128u;
+  for (int a = 0; a < JR; ++a) offA[a] = static_cast<uint32_t>(8 * min(bi * kJobTiles + rr0 + a, NT - 1) + g) * 128u * RB;
 #pragma unroll
-  for (int b = 0; b < kJobTiles; ++b) offB[b] = static_cast<uint32_t>(8 * min(bj * kJobTiles + b, NT - 1) + g) * 128u;
+  for (int b = 0; b < kJobTiles; ++b) offB[b] = static_cast<uint32_t>(8 * min(bj * kJobTiles + b, NT - 1) + g) * 128u * RB;
   // 16-byte chunk of this lane's k slot per k-step s: rows {2s, 2s+1, 2s+8, 2s+9}[t] -> the
-  // chunk index (row>>1) = s + 4*(t>>1) XOR (column & 7) = g (SWIZZLE_128B), conflict free
-  uint32_t inner[4];
+  // chunk index (row>>1) = s + 4*(t>>1) XOR (line & 7) (SWIZZLE_128B), conflict free; the line of
+  // block rb of column 8 T + g is RB (8 T + g) + rb, so the key is (RB g + rb) & 7
+  uint32_t innerR[RB][4];
 #pragma unroll
-  for (int s = 0; s < 4; ++s)
-    inner[s] = ((((s + 4 * (t >> 1)) ^ g) & 7u) << 4) + ((t & 1) << 3);
+  for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+      innerR[rb][s] = ((((s + 4 * (t >> 1)) ^ ((RB * g + rb) & 7)) & 7u) << 4) + ((t & 1) << 3);
   // 0 off-diagonal interior, 1 diagonal top part (JR = 4: the whole diagonal block), 2 diagonal
   // bottom part, 3 edge, 4 idle
   const int kind = !active ? 4 : edge ? 3 : diag ? 1 + part : 0;
 
   if constexpr (JR == 4) {
-    gram_whole_jobs<MC>(p, stages, stage_bytes, nsrc, full_bar, empty_bar, nst, kind, full && !plainjob, full,
-                    bi, bj, diag, acc, offA, offB, inner);
+    gram_whole_jobs<MC, RB>(p, stages, stage_bytes, nsrc, full_bar, empty_bar, nst, kind, full && !plainjob, full,
+                            bi, bj, diag, acc, offA, offB, innerR);
   } else {
   int st = 0;
   uint32_t ph = 0;
   for (int i = 0; i < nst; ++i) {
     mbar_wait(&full_bar[st], ph);
-    const unsigned char* srcA = stages + static_cast<size_t>(st) * nsrc * stage_bytes;
-    const unsigned char* srcB = (full && !plainjob) ? srcA + stage_bytes : srcA;
+    const unsigned char* stA = stages + static_cast<size_t>(st) * nsrc * stage_bytes;
+    const unsigned char* stB = (full && !plainjob) ? stA + stage_bytes : stA;
+#pragma unroll
+    for (int rb = 0; rb < RB; ++rb) {  // the stage's 16-row blocks, in row order
+    const unsigned char* srcA = stA + rb * 128u;
+    const unsigned char* srcB = stB + rb * 128u;
+    const uint32_t* inner = innerR[rb];
     if (kind == 0) {
       // 2 x 4 tiles of an off-diagonal block: 6 fragment loads, 8 DMMA per k-step
 #pragma unroll
@@ -365,6 +393,7 @@ __global__ void __launch_bounds__(32 * (MAXC + 1), 1)
       else if (cb == 2) edge(std::integral_constant<int, 2>{});
       else edge(std::integral_constant<int, 3>{});
     }
+    }  // rb
     __syncwarp();
     if (lane == 0) {
       if (mc) {
@@ -399,8 +428,16 @@ __global__ void __launch_bounds__(32 * (MAXC + 1), 1)
     }
 }
 
-cudaError_t gram_tma_config(int variant, bool mc, size_t smem, int threads, int* occ) {
-  static thread_local LaunchCfgCache cfg[6];
+cudaError_t gram_tma_config(int variant, bool mc, size_t smem, int threads, int* occ, int rb) {
+  static thread_local LaunchCfgCache cfg[9];
+  if (rb == 2) {
+    switch (variant) {
+      case 0: return cached_launch_cfg(cfg[6], gram_tma_kernel<2, kMaxConsumers, false, 2>, smem, threads, occ);
+      case 1: return cached_launch_cfg(cfg[7], gram_tma_kernel<4, kMaxConsumersWhole, false, 2>, smem, threads, occ);
+      case 2: return cached_launch_cfg(cfg[8], gram_tma_kernel<4, kMaxConsumersWhole2, false, 2>, smem, threads, occ);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (variant + (mc ? 3 : 0)) {
     case 0: return cached_launch_cfg(cfg[0], gram_tma_kernel<2, kMaxConsumers, false>, smem, threads, occ);
     case 1: return cached_launch_cfg(cfg[1], gram_tma_kernel<4, kMaxConsumersWhole, false>, smem, threads, occ);
@@ -459,6 +496,15 @@ cudaError_t launch_gram_tma(int variant, unsigned grid, int threads, size_t smem
       case 2: return launch_cluster(gram_tma_kernel<4, kMaxConsumersWhole2, true>, grid, threads, smem, stream, p.mc, mapQ, mapY, p);
       default: return cudaErrorInvalidValue;
     }
+  }
+  if (p.rb == 2) {
+    switch (variant) {
+      case 0: gram_tma_kernel<2, kMaxConsumers, false, 2><<<grid, threads, smem, stream>>>(mapQ, mapY, p); break;
+      case 1: gram_tma_kernel<4, kMaxConsumersWhole, false, 2><<<grid, threads, smem, stream>>>(mapQ, mapY, p); break;
+      case 2: gram_tma_kernel<4, kMaxConsumersWhole2, false, 2><<<grid, threads, smem, stream>>>(mapQ, mapY, p); break;
+      default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
   }
   switch (variant) {
     case 0: gram_tma_kernel<2, kMaxConsumers, false><<<grid, threads, smem, stream>>>(mapQ, mapY, p); break;

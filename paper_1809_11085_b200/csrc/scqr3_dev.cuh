@@ -88,6 +88,16 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
       : "memory");
 }
 
+// 3-D TMA load (coordinates innermost first) into shared memory, completing on bar
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // ---- thread-block clusters: multicast TMA, remote mbarrier arrive, cluster barrier
 // 2-D TMA load delivered to the same shared-memory offset of every CTA in cta_mask (one L2 read),
 // each destination CTA's mbarrier at bar's offset receiving the bytes.

@@ -282,7 +282,25 @@ int encode_map(Ctx* c, CUtensorMap* map, const double* base, int64_t m, int64_t 
   return SCQR3_OK;
 }
 
+// 3-D view of a column-major m x n block for 32-row Gram stages (m % 32 == 0): dims {16 rows,
+// m / 16 row blocks, n columns}, box {16, 2, box_cols}, SWIZZLE_128B per 128-B line (gram.cu, RB)
+int encode_map3(Ctx* c, CUtensorMap* map, const double* base, int64_t m, int64_t n, int64_t ld, int box_cols) {
+  cuuint64_t dims[3] = {16, static_cast<cuuint64_t>(m / 16), static_cast<cuuint64_t>(n)};
+  cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(ld) * 8};
+  cuuint32_t box[3] = {16, 2, static_cast<cuuint32_t>(box_cols)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = c->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail("cuTensorMapEncodeTiled (3-D) failed (%d)", static_cast<int>(r));
+  return SCQR3_OK;
+}
+
 const bool g_gram_debug = std::getenv("SCQR3_GRAM_DEBUG") != nullptr;
+const bool g_gram_rb2 = [] {  // 32-row stages (SCQR3_GRAM_RB=1: 16-row stages only, A/B)
+  const char* v = std::getenv("SCQR3_GRAM_RB");
+  return !(v && v[0] == '1');
+}();
 const int g_gram_force_groups = std::getenv("SCQR3_GRAM_GROUPS") ? std::atoi(std::getenv("SCQR3_GRAM_GROUPS")) : 0;
 const bool g_gram_mc = [] {
   const char* v = std::getenv("SCQR3_GRAM_MC");
@@ -484,15 +502,42 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
       smem = smem_mc;
     }
   }
+  // 32-row stages through a 3-D view (two 128-B lines per column and box: TMA reads at 7.3
+  // instead of 4.6 TB/s, tools/tma_probe.cu) when the rows tile into them, with the same ring
+  // bytes.  Measured at m = 1e7 / 4e6 / 2e6: n = 128 5.13 -> 5.02 ms, n = 64 1.758 -> 1.713 ms;
+  // slower for n = 96 (1.351 -> 1.393), n = 256 (4.15 -> 4.18) and the oblique dual Gram at
+  // n = 64 (0.582 -> 0.605 ms), which keep 16-row stages
+  gp.rb = 1;
+  if (gp.mc == 1 && m % 32 == 0 && g_gram_rb2 && !oblique && (gp.npad == 64 || gp.npad == 128)) {
+    const size_t sb2 = 2 * stage_bytes;
+    const size_t max2 = (kGramSmemCap - 2048) / (sb2 * nsrc);
+    if (max2 >= 2) {
+      gp.rb = 2;
+      // the same ring bytes as the 16-row plan (so as many CTAs fit per SM), at least two stages
+      gp.stages = static_cast<int>(std::min<size_t>(max2, std::max(2, gp.stages / 2)));
+      smem = gp.stages * nsrc * sb2 + 2 * gp.stages * 8 + 1024;
+      CUDA_TRY(gram_tma_config(variant, false, smem, threads, &occ, 2));
+      occ = std::max(occ, 1);
+      gp.total_stages = m / 32;
+      chunks = std::min<long long>((gp.total_stages + 3) / 4, static_cast<long long>(c->num_sms) * occ / groups);
+      chunks = std::max<long long>(1, std::min<long long>(chunks, L.max_chunks));
+    }
+  }
   if (g_gram_debug)
-    fprintf(stderr, "gram: n=%d variant=%d groups=%d ncons=%d stages=%d smem=%zu occ=%d mc=%d clusters=%d chunks=%lld\n",
-            L.n, variant, groups, ncons, gp.stages, smem, occ, gp.mc, ncl, chunks);
+    fprintf(stderr, "gram: n=%d variant=%d groups=%d ncons=%d stages=%d smem=%zu occ=%d mc=%d clusters=%d chunks=%lld rb=%d\n",
+            L.n, variant, groups, ncons, gp.stages, smem, occ, gp.mc, ncl, chunks, gp.rb);
   // (equal TMA boxes of <= kTmaBoxCols columns that tile the stage exactly)
   gp.box_cols = gp.mc > 1 ? 32 : gp.npad / ((gp.npad + kTmaBoxCols - 1) / kTmaBoxCols);
   CUtensorMap mq, my;
-  TRY(encode_map(c, &mq, src, m, L.n, ld, gp.box_cols));
-  if (oblique) TRY(encode_map(c, &my, w.y, m, L.n, L.ldy, gp.box_cols));
-  else my = mq;
+  if (gp.rb == 2) {
+    TRY(encode_map3(c, &mq, src, m, L.n, ld, gp.box_cols));
+    if (oblique) TRY(encode_map3(c, &my, w.y, m, L.n, L.ldy, gp.box_cols));
+    else my = mq;
+  } else {
+    TRY(encode_map(c, &mq, src, m, L.n, ld, gp.box_cols));
+    if (oblique) TRY(encode_map(c, &my, w.y, m, L.n, L.ldy, gp.box_cols));
+    else my = mq;
+  }
   gp.chunks = static_cast<int>(chunks);
   gp.partials = w.partials;
   const int pg = prof_begin(c, PK_GRAM);
@@ -994,7 +1039,9 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
     if (m > 0) {
       CUtensorMap mx;
       const bool use_tma = L.NT <= 16 || L.NT >= 24;
-      // (NT >= 24: the map of the first 128 columns, for the split TRSM)
+      // (NT >= 24: the map of the first 128 columns, for the split TRSM.  A 3-D view with one
+      //  32-row box per A = 4 warp slot was measured slower for the unfused n = 64: C5 TRSM 0.423
+      //  -> 0.440 ms)
       if (use_tma) TRY(encode_map(c, &mx, src, m, L.NT >= 24 ? 128 : n, ldsrc, trsm_x_box_cols(L.NT)));
       CUtensorMap mq;  // fused TRSM + Gram: bulk stores of Q
       if (fuse_tg) TRY(encode_map(c, &mq, Q, m, n, ldq, L.npad));

@@ -47,6 +47,7 @@ struct GramParams {
   int mc;                    // > 1: the `groups` CTAs of a row chunk form a cluster and each stage
                              //   is multicast to all of them (each CTA loads 1 / mc of its boxes)
   int box_cols;              // columns per TMA box of the stage (the map's box width)
+  int rb;                    // 16-row blocks per stage: 1 (2-D map) or 2 (3-D map, m % 32 == 0, no multicast)
   // job of consumer warp w in group g: warp_job[g * kMaxConsumers + w] (-1 = idle); the host
   // balances the DMMA work of each group over the SM's four sub-partitions (warp % 4)
   short warp_job[kMaxGroups * kMaxConsumers];  // codes <= 2 * 136 (n <= 512)
@@ -185,7 +186,7 @@ struct TrsmParams {
 // gram_tma_kernel<JR, MAXC> (gram.cu): JR = tile rows per consumer-warp job, 2 (half 4x4-tile
 // blocks) or 4 (whole blocks); MAXC = consumer warps it is compiled for.  Variant v of
 // assign_gram_jobs: 0 = <2, 20>, 1 = <4, 18>, 2 = <4, 15>.
-cudaError_t gram_tma_config(int variant, bool mc, size_t smem, int threads, int* occ);  // smem attribute + occupancy (cached)
+cudaError_t gram_tma_config(int variant, bool mc, size_t smem, int threads, int* occ, int rb = 1);  // smem attribute + occupancy (cached)
 // clusters of mc CTAs that fit at once (multicast launch)
 cudaError_t gram_tma_max_clusters(int variant, size_t smem, int threads, int mc, int* nclusters);
 cudaError_t launch_gram_tma(int variant, unsigned grid, int threads, size_t smem, cudaStream_t stream,

@@ -50,6 +50,25 @@ def test_gram_parity(m, n):
 
 
 @gpu
+@pytest.mark.parametrize("m,n,pad", [(32 * 1001, 64, 0), (32 * 3001, 128, 0), (32 * 777, 61, 6), (32 * 500, 124, 2),
+                                     (32, 64, 0), (32 * 20000, 128, 4)])
+def test_gram_parity_32row_stages(m, n, pad):
+    """m % 32 == 0 and 8 ceil(n / 8) in {64, 128}: the Gram streams 32-row stages through the 3-D
+    tensor map (two swizzled 128-B lines per column and box, gram.cu RB = 2); same T1 bound, an
+    exact integer case bit for bit, and a leading dimension past m."""
+    X = synth.random_rows(m, n, seed=m + n)
+    Xd = sq.colmajor_empty(m, n, ld=m + pad) if pad else dev(X)
+    if pad:
+        Xd.copy_(torch.from_numpy(X))
+    A = host(sq.scqr3_gram(Xd))
+    bound = 2 * gamma(m) * (np.abs(X).T @ np.abs(X))
+    assert np.all(np.abs(A - oracle.gram(X)) <= bound + 1e-300)
+    Xi = np.random.default_rng(m).integers(-40, 41, size=(m, n)).astype(float)
+    Ai = host(sq.scqr3_gram(dev(Xi)))
+    assert np.array_equal(Ai, (Xi.astype(np.int64).T @ Xi.astype(np.int64)).astype(float))
+
+
+@gpu
 def test_gram_exact_integers_bitwise():
     rng = np.random.default_rng(5)
     X = rng.integers(-40, 41, size=(7777, 72)).astype(float)
