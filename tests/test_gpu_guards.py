@@ -71,7 +71,10 @@ def _factor(kind, X, aux, Q, R, ws, stream=None):
 
 CASES = [("standard", 2000, 16, 1e12), ("standard", 40_000, 40, 1e9), ("standard", 40_000, 128, 1e10),
          ("standard", 40_000, 256, 1e8), ("standard", 40_000, 300, 1e8), ("oblique", 40_000, 64, 1e10),
-         ("csr", 20_000, 32, 1e8)]
+         ("csr", 20_000, 32, 1e8),
+         # round 2: m % 32 == 0 (32-row Gram stages through the 3-D map) with the inverse-diagonal
+         # TRSM (n = 128; fused with the next Gram at n = 64), and the n = 96 inverse instance
+         ("standard", 40_960, 128, 1e10), ("standard", 32_768, 64, 1e12), ("standard", 40_000, 96, 1e8)]
 
 
 @gpu
@@ -155,6 +158,77 @@ def test_guards_loopback_ranks_repeatable():
         torch.cuda.synchronize()
         assert all(x.status == 0 for x in res)
         got = [torch.cat([g[1] for g in Qg]).clone(), res[0].R.clone()]
+        if ref is None:
+            ref = got
+        assert torch.equal(got[0], ref[0]) and torch.equal(got[1], ref[1])
+        for (a, b), (qb, _, ldq) in zip(parts, Qg):
+            assert _guards_intact(qb, ldq * n) and _pads_intact(qb, b - a, n, ldq)
+    for c in comms:
+        c.destroy()
+
+
+@gpu
+def test_guards_host_batch():
+    """scqr3_factor_host_batch on a NaN-poisoned, guarded workspace (three staging buffers plus the
+    factorisation workspace): every matrix finite and equal to its own scqr3_factor_host call,
+    no write outside the workspace."""
+    m, n, count = 9_001, 48, 4
+    Xs = [synth.randsvd(m, n, 10.0 ** (3 + 2 * i), seed=20 + i) for i in range(count)]
+
+    def pin(A=None, shape=(m, n)):
+        T = torch.empty(shape[::-1], dtype=torch.float64, pin_memory=True)
+        if A is not None:
+            T.copy_(torch.from_numpy(np.ascontiguousarray(A.T)))
+        return T.t()
+
+    Xh = [pin(X) for X in Xs]
+    Qh = [pin() for _ in range(count)]
+    Rh = [pin(shape=(n, n)) for _ in range(count)]
+    nws = (sq._abi.lib().scqr3_host_batch_workspace_size(m, n) + 7) // 8
+    wb, wv = _guarded(nws + 32)
+    off = ((256 - wv.data_ptr() % 256) % 256) // 8
+    ws = wv[off:off + nws]
+    ws.view(torch.int64).fill_(NANBITS)
+    st = sq.scqr3_factor_host_batch(Xh, Qh, Rh, ws=ws.view(torch.uint8))
+    torch.cuda.synchronize()
+    assert st == [0] * count
+    assert _guards_intact(wb, nws + 32) and bool((wv[:off].view(torch.int64) == NANBITS).all()), "write outside ws"
+    for i in range(count):
+        assert torch.isfinite(Qh[i]).all() and torch.isfinite(Rh[i]).all()
+        r1 = sq.scqr3_factor_host(Xh[i])
+        assert np.array_equal(r1.R.numpy(), Rh[i].numpy()) and np.array_equal(r1.Q.numpy(), Qh[i].numpy())
+
+
+@gpu
+def test_guards_ghost_plan_ranks():
+    """Three loopback ranks with a ghost-row CSR plan (randomly permuted 2-D Laplacian): repeated
+    calls give the same bits and no rank writes outside its Q block."""
+    from paper_1809_11085_b200.dist import csr_ghost_plan
+    P, m, n = 3, 30_000, 32
+    X = synth.randsvd(m, n, 1e8, seed=14)
+    rp, ci, cv = synth.laplacian2d(150, m // 150, seed=0, wmax=1e3)
+    perm = np.random.default_rng(5).permutation(m)
+    inv = np.empty(m, dtype=np.int64)
+    inv[perm] = np.arange(m)
+    nrp = np.concatenate([[0], np.cumsum(np.diff(rp)[perm])])
+    idx = np.concatenate([np.arange(rp[o], rp[o + 1]) for o in perm])
+    plans = csr_ghost_plan(nrp, inv[ci[idx]], cv[idx], m, P)
+    comms = sq.Comm.loopback(P)
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    parts = [row_block(m, r, P) for r in range(P)]
+    Xs = [sq.to_colmajor(torch.from_numpy(np.asfortranarray(X[a:b])), device="cuda") for a, b in parts]
+    Bs = [sq.CsrMetric(pl["row_ptr"], pl["col_idx"], pl["vals"],
+                       ghosts=(pl["nghost"], pl["recv_counts"], pl["send_counts"], pl["send_rows"])) for pl in plans]
+    Qg = [_colmajor_guarded(np.zeros((b - a, n))) for a, b in parts]
+    torch.cuda.synchronize()
+    ref = None
+    for rep in range(3):
+        res = run_ranks([lambda r=r: sq.scqr3_factor_oblique_csr(Xs[r], Bs[r], Q=Qg[r][1], comm=comms[r],
+                                                                 stream=streams[r]) for r in range(P)])
+        torch.cuda.synchronize()
+        assert all(x.status == 0 for x in res)
+        got = [torch.cat([g[1] for g in Qg]).clone(), res[0].R.clone()]
+        assert torch.isfinite(got[0]).all()
         if ref is None:
             ref = got
         assert torch.equal(got[0], ref[0]) and torch.equal(got[1], ref[1])
