@@ -346,3 +346,80 @@ def test_ghost_plan_single_rank_and_rejection():
     finally:
         for c in comms:
             c.destroy()
+
+
+@gpu
+def test_ghost_plan_with_empty_rank():
+    """A ghost-plan CSR factorisation over 3 loopback ranks, the middle one owning no rows: its
+    plan is empty, the others exchange with each other only; R matches the oracle's 2-part
+    emulation (an empty shard adds zeros) and every rank returns the same R."""
+    X, B = _inputs("csr_ghost")
+    h = M // 2
+    bounds = [(0, h), (h, h), (h, M)]
+    # plans for the 2-rank split, with an empty rank spliced in between
+    p2 = _plans(2)
+    empty = dict(row_ptr=np.zeros(1, dtype=np.int64), col_idx=np.zeros(0, dtype=np.int32), vals=np.zeros(0),
+                 nghost=0, recv_counts=np.zeros(3, dtype=np.int64), send_counts=np.zeros(3, dtype=np.int64),
+                 send_rows=np.zeros(0, dtype=np.int64))
+    def widen(pl):
+        q = dict(pl)
+        q["recv_counts"] = np.array([pl["recv_counts"][0], 0, pl["recv_counts"][1]], dtype=np.int64)
+        q["send_counts"] = np.array([pl["send_counts"][0], 0, pl["send_counts"][1]], dtype=np.int64)
+        return q
+    plans = [widen(p2[0]), empty, widen(p2[1])]
+    comms = sq.Comm.loopback(3)
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    n = X.shape[1]
+    args = []
+    for r, (r0, r1) in enumerate(bounds):
+        pl = plans[r]
+        csr = sq.CsrMetric(pl["row_ptr"], pl["col_idx"], pl["vals"],
+                           ghosts=(pl["nghost"], pl["recv_counts"], pl["send_counts"], pl["send_rows"]))
+        Xr = sq.to_colmajor(torch.from_numpy(np.asfortranarray(X[r0:r1])), device="cuda") if r1 > r0 else \
+            sq.colmajor_empty(0, n)
+        args.append((Xr, csr, dict(comm=comms[r], stream=streams[r])))
+    try:
+        res = run_ranks([lambda a=a: sq.scqr3_factor_oblique_csr(a[0], a[1], **a[2]) for a in args])
+    finally:
+        for c in comms:
+            c.destroy()
+    assert all(x.status == 0 for x in res)
+    R0 = res[0].R.cpu().numpy()
+    assert all(np.array_equal(x.R.cpu().numpy(), R0) for x in res)
+    ro = _oracle("csr_ghost", 2)
+    assert np.max(np.abs(R0 - ro.R)) <= 1e-10 * np.max(np.abs(ro.R))
+
+
+@gpu
+def test_loopback_host_batch():
+    """scqr3_factor_host_batch with a loopback communicator: every rank streams the same number of
+    matrices (its row block of each); per matrix, R is identical on every rank and equals the
+    per-call multi-rank result."""
+    P, m, n, count = 2, 40_000, 48, 3
+    Xs = [synth.randsvd(m, n, 10.0 ** (4 + 3 * i), seed=30 + i) for i in range(count)]
+    parts = [row_block(m, r, P) for r in range(P)]
+
+    def pin(A=None, shape=None):
+        T = torch.empty(shape[::-1], dtype=torch.float64, pin_memory=True)
+        if A is not None:
+            T.copy_(torch.from_numpy(np.ascontiguousarray(A.T)))
+        return T.t()
+
+    comms = sq.Comm.loopback(P)
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    try:
+        Xh = [[pin(X[a:b], (b - a, n)) for X in Xs] for a, b in parts]
+        Qh = [[pin(shape=(b - a, n)) for _ in Xs] for a, b in parts]
+        Rh = [[pin(shape=(n, n)) for _ in Xs] for _ in parts]
+        st = run_ranks([lambda r=r: sq.scqr3_factor_host_batch(Xh[r], Qh[r], Rh[r], comm=comms[r], m_global=m,
+                                                               stream=streams[r]) for r in range(P)])
+        assert st == [[0] * count] * P
+        for i in range(count):
+            assert np.array_equal(Rh[0][i].numpy(), Rh[1][i].numpy())
+            one = run_ranks([lambda r=r: sq.scqr3_factor_host(Xh[r][i], comm=comms[r], m_global=m, stream=streams[r])
+                             for r in range(P)])
+            assert np.array_equal(one[0].R.numpy(), Rh[0][i].numpy())
+            assert all(np.array_equal(one[r].Q.numpy(), Qh[r][i].numpy()) for r in range(P))
+    finally:
+        for c in comms:
+            c.destroy()
