@@ -328,6 +328,26 @@ def run_ours(args):
     stream.synchronize()
     ms_prof = p0.elapsed_time(p1) / args.steps
 
+    # ---- quality of the last factorisation (outside the timed regions): orthogonality and
+    # residual with the compensated metrics of tests/gpu_metrics.py (pinned to the oracle's Dot2
+    # metrics); the north star asks for both <= 10 n u on every config
+    quality = None
+    if world == 1:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import gpu_metrics  # noqa: E402
+
+        t_q = time.perf_counter()
+        if csr is not None:
+            orth = None  # (the CSR metric's Q^T B Q check lives in the tests)
+        elif cfg.oblique:
+            orth = float(gpu_metrics.orth_F(Q, d, e))
+        else:
+            orth = float(gpu_metrics.orth_F(Q))
+        resid = float(gpu_metrics.resid_F(X, Q, R))
+        quality = {"orth_F": orth, "resid_F": resid, "ten_n_u": 10 * n * 2.0 ** -53,
+                   "metric": ("||Q^T B Q - I||_F" if cfg.oblique else "||Q^T Q - I||_F") + " and ||X - QR||_F / ||X||_F, "
+                             "compensated (tests/gpu_metrics.py)", "seconds": time.perf_counter() - t_q}
+
     # ---- per-kernel device time measured live during the timed steps (events on `stream`)
     peaks = load_json(FP64_PEAKS) or {}
     peak = peaks.get("roofline_fp64_peak_tflops", 37.1)
@@ -487,6 +507,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             **({"e2e_note": e2e_note} if e2e_note else {}),
+            "quality": quality,
             "gpu_launches": launches,
             "clocks": clk,
         }

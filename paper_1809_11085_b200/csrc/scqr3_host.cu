@@ -7,6 +7,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX ranges (no-ops unless a profiler is attached)
 
 #include <algorithm>
 #include <cstdarg>
@@ -957,6 +958,10 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
     const int64_t ldsrc = k == 1 ? ld : ldq;
     const PassGate gate{last_pass, k, generic ? pass_dev : nullptr};
     c->cur_pass = k;
+    char nvtx_name[32];
+    std::snprintf(nvtx_name, sizeof nvtx_name, generic ? "scqr3 pass (graph body)" : "scqr3 pass %d", k);
+    nvtxRangePushA(nvtx_name);
+    struct NvtxPop { ~NvtxPop() { nvtxRangePop(); } } nvtx_pop;
     if (generic) {
       pass_advance_kernel<<<1, 32, 0, st>>>(pass_dev);
       ++g_launches;
@@ -1144,7 +1149,9 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
 int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric& B, double* Q, int64_t ldq,
                 double* R, const scqr3_opts* o) {
   bool in_protocol = false;
+  nvtxRangePushA(B.csr ? "scqr3_factor_oblique_csr" : B.d ? "scqr3_factor_oblique" : "scqr3_factor");
   const int rc = factor_body(m, n, X, ld, B, Q, ldq, R, o, &in_protocol);
+  nvtxRangePop();
   // an error after the ranks started exchanging (CUDA / NCCL failure on this rank): a loopback
   // group is marked failed so that the peers return instead of waiting at the next exchange
   if (rc == SCQR3_EINVAL && in_protocol) comm_abort(static_cast<Comm*>(o->comm), g_err.c_str());
