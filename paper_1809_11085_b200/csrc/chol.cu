@@ -1189,15 +1189,17 @@ __global__ void trsm_prep_kernel(const double* R, int n, int NT, double* bfrag, 
   }
 }
 
-__global__ void pass_advance_kernel(int* pass_dev) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) *pass_dev += 1;
-}
 
-__global__ void pass_loop_cond_kernel(const int* pass_dev, const int* last_pass, int max_passes,
+// WHILE condition after pass k (= *pass_dev): run the body again if k < last_pass and k <
+// max_passes, and then advance the counter to the body's pass number k + 1 here (one graph node
+// per pass less than a separate advance kernel at the top of the body)
+__global__ void pass_loop_cond_kernel(int* pass_dev, const int* last_pass, int max_passes,
                                       cudaGraphConditionalHandle handle) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     const int k = *pass_dev;
-    cudaGraphSetConditional(handle, (k < *last_pass && k < max_passes) ? 1u : 0u);
+    const bool more = k < *last_pass && k < max_passes;
+    if (more) *pass_dev = k + 1;
+    cudaGraphSetConditional(handle, more ? 1u : 0u);
   }
 }
 

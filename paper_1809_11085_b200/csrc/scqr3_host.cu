@@ -962,11 +962,7 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
     std::snprintf(nvtx_name, sizeof nvtx_name, generic ? "scqr3 pass (graph body)" : "scqr3 pass %d", k);
     nvtxRangePushA(nvtx_name);
     struct NvtxPop { ~NvtxPop() { nvtxRangePop(); } } nvtx_pop;
-    if (generic) {
-      pass_advance_kernel<<<1, 32, 0, st>>>(pass_dev);
-      ++g_launches;
-      CUDA_TRY(cudaGetLastError());
-    }
+    // (the generic body's pass number was advanced by the loop-condition kernel that let it run)
     if (oblique) {
       if (cm) {
         const int ph = prof_begin(c, PK_COMM);

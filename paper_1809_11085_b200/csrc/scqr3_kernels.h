@@ -216,11 +216,10 @@ __global__ void zcombine_kernel(const double* tiles, int n, double* A, const int
 __global__ void zchol_kernel(ZCholParams p);
 __global__ void ztrmul_kernel(const double* Rt, const double* R, double* Rnew, int n, int first, const DevStatus* st,
                               PassGate gate);
-// CUDA-graph pass loop (device-side pass control): the counter advances at the
-// top of each loop-body pass; the loop continues while the Cholesky has not stopped it.
-__global__ void pass_advance_kernel(int* pass_dev);
-__global__ void pass_loop_cond_kernel(const int* pass_dev, const int* last_pass, int max_passes,
-                                      cudaGraphConditionalHandle handle);
+// CUDA-graph pass loop (device-side pass control): the loop-condition kernel
+// advances the counter when it lets the body run again; the loop continues while the Cholesky has not stopped it.
+__global__ void pass_loop_cond_kernel(int* pass_dev, const int* last_pass, int max_passes,
+                                      cudaGraphConditionalHandle handle);  // (also advances the counter)
 
 // Per-call-site cache of cudaFuncSetAttribute(max dynamic smem) + the occupancy query, so a
 // pass does not repeat these host API calls (small problems are launch-bound on the host).
