@@ -211,8 +211,11 @@ int scqr3_factor_oblique_csr(int64_t m, int64_t n, const double* X, int64_t ld, 
  * X, Q: m x n complex double (C99 double complex / cuDoubleComplex: interleaved re, im),
  * column-major with leading dimensions ld, ldq >= m counted in complex elements, 16-byte
  * aligned; R: n x n complex, column-major, leading dimension n, upper with a real positive
- * diagonal.  1 <= n <= 256.  The tall-skinny steps run the real Gram and TRSM kernels on the
- * m x 2n real "split" matrix (Re x_0, Im x_0, Re x_1, ...), the n x n step is complex.  Same
+ * diagonal.  1 <= n <= 512.  The tall-skinny steps run the real Gram and TRSM kernels on the
+ * m x 2n real "split" matrix (Re x_0, Im x_0, Re x_1, ...), the n x n step is complex; for
+ * n > 256 the split matrix is taken as two column blocks [S1 S2] (512 and 2n - 512 columns):
+ * the real kernels on each block plus a cross Gram S1^T S2 and the block update S2 -= Q1 M12
+ * (zwide.cu; deterministic mode: up to 8 ranks fit the workspace's gather slots).  Same
  * options, statuses and trace as scqr3_factor; opts->workspace must hold
  * scqr3_workspace_size_complex(m, n) bytes. */
 size_t scqr3_workspace_size_complex(int64_t m, int64_t n);

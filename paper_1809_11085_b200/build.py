@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libscqr3.so")
-SOURCES = ["gram.cu", "chol.cu", "zchol.cu", "trsm.cu", "comm.cu", "scqr3_host.cu"]
+SOURCES = ["gram.cu", "chol.cu", "zchol.cu", "zwide.cu", "trsm.cu", "comm.cu", "scqr3_host.cu"]
 HEADERS = ["scqr3_dev.cuh", "scqr3_kernels.h", "scqr3_comm.h"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

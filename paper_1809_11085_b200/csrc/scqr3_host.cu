@@ -1157,14 +1157,24 @@ int factor_impl(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
 // ---- complex X (reading D23): real kernels on the m x 2n split matrix, complex
 // n x n step (zchol.cu).  Host-driven pass loop (as the multi-GPU path).
 struct ZLayout {
-  Layout L;        // real layout for the 2n-column split matrix
+  Layout L;        // real layout for the 2n-column split matrix (wide: its first kMaxN columns)
+  Layout L2;       // wide (2n > kMaxN, zwide.cu): the last q = 2n - kMaxN columns
+  bool wide;
   int64_t lds;     // split matrix leading dimension (even, >= m)
   size_t S, A, Rtz, end;
+  // wide only: G = [S1^T S1 tiles | S2^T S2 tiles | C12 = S1^T S2], complex scratch W, the
+  // 2n x 2n M, its diagonal blocks M11, M22, complex R scratch, and one partials / gather buffer
+  size_t G, Wz, M, M11, M22, Rnz, P;
+  long long g_off2, g_offc, g_count, p_cap;
+  int q, xchunks_max;
 };
+
+constexpr int kXChunksMax = 32;  // row chunks of the wide cross Gram (partials: chunks x 512 x q)
 
 ZLayout make_zlayout(int64_t m, int64_t n) {
   ZLayout Z{};
-  Z.L = make_layout(m, 2 * n, 0);
+  Z.wide = 2 * n > kMaxN;
+  Z.L = make_layout(m, Z.wide ? kMaxN : 2 * n, 0);
   Z.lds = std::max<int64_t>(2, (m + 1) & ~1LL);
   size_t off = Z.L.end;
   auto take = [&](size_t bytes) {
@@ -1175,6 +1185,23 @@ ZLayout make_zlayout(int64_t m, int64_t n) {
   Z.S = take(static_cast<size_t>(Z.lds) * 2 * n * 8);
   Z.A = take(static_cast<size_t>(n) * n * 16);
   Z.Rtz = take(static_cast<size_t>(n) * n * 16);
+  if (Z.wide) {
+    Z.q = static_cast<int>(2 * n - kMaxN);
+    Z.L2 = make_layout(m, Z.q, 0);
+    Z.g_off2 = Z.L.tiles_sym * 64 + 64;
+    Z.g_offc = Z.g_off2 + Z.L2.tiles_sym * 64 + 64;
+    Z.g_count = Z.g_offc + static_cast<long long>(kMaxN) * Z.q;
+    Z.xchunks_max = kXChunksMax;
+    Z.p_cap = std::max({Z.L.max_chunks * Z.L.tiles_part * 64, Z.L2.max_chunks * Z.L2.tiles_part * 64,
+                        static_cast<long long>(kXChunksMax) * kMaxN * Z.q, 8 * Z.g_count});
+    Z.G = take(static_cast<size_t>(Z.g_count) * 8);
+    Z.Wz = take(static_cast<size_t>(n) * n * 16);
+    Z.M = take(static_cast<size_t>(4 * n) * n * 8);
+    Z.M11 = take(static_cast<size_t>(kMaxN) * kMaxN * 8);
+    Z.M22 = take(static_cast<size_t>(Z.q) * Z.q * 8);
+    Z.Rnz = take(static_cast<size_t>(n) * n * 16);
+    Z.P = take(static_cast<size_t>(Z.p_cap) * 8);
+  }
   Z.end = off;
   return Z;
 }
@@ -1182,7 +1209,7 @@ ZLayout make_zlayout(int64_t m, int64_t n) {
 int zfactor_checks(int64_t m, int64_t n, const double* X, int64_t ld, const double* Q, int64_t ldq, const double* R,
                    const scqr3_opts* o, Ctx** c, ZLayout* Z, WS* w) {
   TRY(check_opts(o));
-  if (n < 1 || 2 * n > kMaxN) return fail("complex n=%lld outside [1, %d]", (long long)n, kMaxN / 2);
+  if (n < 1 || n > kMaxN) return fail("complex n=%lld outside [1, %d]", (long long)n, kMaxN);
   if (m < 0) return fail("m < 0");
   if (m > 0 && (!X || !Q)) return fail("X or Q is NULL");
   if (ld < std::max<int64_t>(m, 1) || ldq < std::max<int64_t>(m, 1)) return fail("leading dimension < m");
@@ -1195,6 +1222,90 @@ int zfactor_checks(int64_t m, int64_t n, const double* X, int64_t ld, const doub
   if (!o->workspace || o->workspace_bytes < Z->end) return fail("workspace too small: %zu < %zu bytes", o->workspace_bytes, Z->end);
   if (reinterpret_cast<uintptr_t>(o->workspace) % 256) return fail("workspace must be 256-byte aligned");
   TRY(carve(Z->L, o, w));
+  return SCQR3_OK;
+}
+
+// Wide complex Gram (n > 256, zwide.cu): S1^T S1 and S2^T S2 by the real Gram kernel, the cross
+// block C12 = S1^T S2 by xgram_kernel + xreduce_kernel, one allreduce of all three across ranks,
+// then A = X^H X.
+int zwide_gram(Ctx* c, const ZLayout& Z, const WS& w1, const WS& w2, const double* S, int64_t m, Comm* cm, bool det,
+               int n, double* Az, const int* last_pass, int k, cudaStream_t st, PassGate gate) {
+  TRY(run_gram(c, Z.L, w1, S, Z.lds, m, false, nullptr, st, gate));
+  TRY(run_gram(c, Z.L2, w2, S + kMaxN * Z.lds, Z.lds, m, false, nullptr, st, gate));
+  double* G = w1.tiles;
+  double* C12 = G + Z.g_offc;
+  const long long cnt = static_cast<long long>(kMaxN) * Z.q;
+  if (m == 0) {
+    CUDA_TRY(cudaMemsetAsync(C12, 0, static_cast<size_t>(cnt) * 8, st));
+  } else {
+    const int nbp = kMaxN / 64, nbq = (Z.q + 63) / 64;
+    long long chunks = (4LL * c->num_sms + nbp * nbq - 1) / (nbp * nbq);
+    chunks = std::max<long long>(1, std::min<long long>({chunks, Z.xchunks_max, (m + 31) / 32}));
+    const long long rpc = ((m + chunks - 1) / chunks + 31) / 32 * 32;
+    chunks = (m + rpc - 1) / rpc;
+    const int pg = prof_begin(c, PK_GRAM);
+    xgram_kernel<<<static_cast<unsigned>(chunks * nbp * nbq), 256, 0, st>>>(S, Z.lds, S + kMaxN * Z.lds, Z.lds, m, kMaxN,
+                                                                            Z.q, rpc, w1.partials, gate);
+    xreduce_kernel<<<static_cast<unsigned>(std::min<long long>(1024, (cnt + 255) / 256)), 256, 0, st>>>(
+        w1.partials, static_cast<int>(chunks), cnt, C12, gate);
+    prof_end(c, pg);
+    g_launches += 2;
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (cm) {
+    const int pa = prof_begin(c, PK_COMM);
+    TRY(comm_allreduce_sum(cm, G, static_cast<size_t>(Z.g_count), det, w1.partials, static_cast<size_t>(Z.p_cap), st));
+    prof_end(c, pa);
+  }
+  const long long nn = static_cast<long long>(n) * n;
+  zcombine_wide_kernel<<<static_cast<unsigned>((nn + 255) / 256), 256, 0, st>>>(G, G + Z.g_off2, C12, n, kMaxN, Az,
+                                                                                  last_pass, k);
+  ++g_launches;
+  CUDA_TRY(cudaGetLastError());
+  return SCQR3_OK;
+}
+
+// Wide complex TRSM (n > 256, zwide.cu): Q1 = S1 M11^-1, S2 -= Q1 M12, Q2 = S2 M22^-1, in place.
+int zwide_trsm(Ctx* c, const ZLayout& Z, const WS& w, double* S, const double* M11, const double* M22,
+               const double* Mz, int64_t m, int trsm_diag, cudaStream_t st, PassGate gate) {
+  const int n2 = kMaxN + Z.q;
+  for (int h = 0; h < 2; ++h) {
+    const int nh = h ? Z.q : kMaxN;
+    const Layout& Lh = h ? Z.L2 : Z.L;
+    double* Sh = S + (h ? kMaxN * Z.lds : 0);
+    const int pt = prof_begin(c, PK_TRSM);
+    if (h == 1) {
+      const int nbq = (Z.q + 63) / 64;
+      xupdate_kernel<<<static_cast<unsigned>((m + 63) / 64 * nbq), 256, 0, st>>>(
+          S, Z.lds, Mz + static_cast<size_t>(kMaxN) * n2, n2, Sh, Z.lds, m, kMaxN, Z.q, gate);
+      ++g_launches;
+      CUDA_TRY(cudaGetLastError());
+    }
+    trsm_prep_kernel<<<trsm_prep_blocks(Lh.NT), 256, 0, st>>>(h ? M22 : M11, nh, Lh.NT, w.bfrag, w.dblk, 0, nullptr,
+                                                               gate, trsm_diag);
+    ++g_launches;
+    CUDA_TRY(cudaGetLastError());
+    TrsmParams tp{};
+    tp.m = m;
+    tp.n = nh;
+    tp.bfrag = w.bfrag;
+    tp.dblk = w.dblk;
+    tp.dinv = w.dblk + dinv_off(Lh.NT);
+    tp.inv_flag = trsm_diag == SCQR3_TRSM_DIAG_SUBST ? nullptr : w.dblk + dflag_off(Lh.NT);
+    tp.st = w.st;
+    tp.X = Sh;
+    tp.ldx = Z.lds;
+    tp.Q = Sh;
+    tp.ldq = Z.lds;
+    tp.gate = gate;
+    CUtensorMap mx;
+    const bool use_tma = Lh.NT <= 16 || Lh.NT >= 24;
+    if (use_tma) TRY(encode_map(c, &mx, Sh, m, Lh.NT >= 24 ? 128 : nh, Z.lds, trsm_x_box_cols(Lh.NT)));
+    int grid = 0;
+    CUDA_TRY(launch_trsm(tp, use_tma ? &mx : nullptr, c->num_sms, st, &grid, nullptr));
+    prof_end(c, pt);
+    g_launches += trsm_launch_count(tp, use_tma);
+  }
   return SCQR3_OK;
 }
 
@@ -1251,6 +1362,25 @@ int zfactor_impl(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, i
   zp.st_dev = w.st;
   zp.st_host = c->st_host_dev;
   zp.w_in_smem = n <= 128 ? 1 : 0;
+  // wide (n > 256): the split matrix as [S1 S2] (zwide.cu); their own scratch past the real layout
+  double* G = nullptr;
+  double* Mz = nullptr;
+  double* M11 = nullptr;
+  double* M22 = nullptr;
+  double* Rnew = w.Rnew;
+  WS w1 = w, w2 = w;
+  if (Z.wide) {
+    G = reinterpret_cast<double*>(wb + Z.G);
+    Mz = reinterpret_cast<double*>(wb + Z.M);
+    M11 = reinterpret_cast<double*>(wb + Z.M11);
+    M22 = reinterpret_cast<double*>(wb + Z.M22);
+    Rnew = reinterpret_cast<double*>(wb + Z.Rnz);
+    zp.W = reinterpret_cast<double*>(wb + Z.Wz);
+    zp.M = Mz;
+    w1.partials = w2.partials = reinterpret_cast<double*>(wb + Z.P);
+    w1.tiles = G;
+    w2.tiles = G + Z.g_off2;
+  }
   TrsmParams tp{};
   tp.m = m;
   tp.n = n2;
@@ -1263,13 +1393,17 @@ int zfactor_impl(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, i
   tp.ldx = Z.lds;
   tp.Q = S;  // in place on the split matrix
   tp.ldq = Z.lds;
-  const bool fuse_tg = g_fuse_tg && trsm_fuses_gram(L.NT) && m > 0;
+  const bool fuse_tg = g_fuse_tg && trsm_fuses_gram(L.NT) && m > 0 && !Z.wide;
   int fused_chunks = 0;
   for (int k = 0; k < max_passes; ++k) c->st_host[k].code = -1;
   int status = SCQR3_ENOCONV, k;
   for (k = 1; k <= max_passes; ++k) {
     const PassGate gate{last_pass, k, nullptr};
     c->cur_pass = k;
+    const long long nn = n * n;
+    if (Z.wide) {
+      TRY(zwide_gram(c, Z, w1, w2, S, m, cm, o->deterministic != 0, static_cast<int>(n), Az, last_pass, k, st, gate));
+    } else {
     if (k == 1 || !fuse_tg) TRY(run_gram(c, L, w, S, Z.lds, m, false, nullptr, st, gate));
     else TRY(launch_gram_reduce(c, L, w, fused_chunks, false, false, 0, st, gate));
     if (cm) {
@@ -1278,40 +1412,50 @@ int zfactor_impl(int64_t m, int64_t n, const double* X, int64_t ld, double* Q, i
                              static_cast<size_t>(L.max_chunks) * L.tiles_part * 64, st));
       prof_end(c, pa);
     }
-    const long long nn = n * n;
     zcombine_kernel<<<static_cast<unsigned>((nn + 255) / 256), 256, 0, st>>>(w.tiles, static_cast<int>(n), Az,
                                                                               last_pass, k);
     ++g_launches;
     CUDA_TRY(cudaGetLastError());
+    }
     zp.pass = k;
     if (k > 1) CUDA_TRY(cudaStreamWaitEvent(st, c->ev_side, 0));
     const int pc = prof_begin(c, PK_CHOL);
     {
-      const size_t zsmem = zp.w_in_smem ? static_cast<size_t>(n) * (n + 1) / 2 * 16 : 0;
+      // packed upper W in shared memory (n <= 128), else the panel of the blocked factorisation
+      // (zchol.cu: 16 rows of R~ x n complex)
+      const size_t zsmem = zp.w_in_smem ? static_cast<size_t>(n) * (n + 1) / 2 * 16 : static_cast<size_t>(16) * n * 16;
       static thread_local LaunchCfgCache zcfg;
-      if (zsmem) CUDA_TRY(cached_launch_cfg(zcfg, zchol_kernel, zsmem, 256, nullptr));
+      CUDA_TRY(cached_launch_cfg(zcfg, zchol_kernel, zsmem, 256, nullptr));
       zchol_kernel<<<1, 256, zsmem, st>>>(zp);
     }
     ++g_launches;
     CUDA_TRY(cudaGetLastError());
-    trsm_prep_kernel<<<trsm_prep_blocks(L.NT), 256, 0, st>>>(w.Rt, n2, L.NT, w.bfrag, w.dblk, 0, nullptr, gate,
-                                                              o->trsm_diag);  // M -> TRSM operands
-    ++g_launches;
+    if (Z.wide) {  // the diagonal blocks of M as contiguous operands for trsm_prep_kernel (zwide_trsm)
+      zsub_kernel<<<256, 256, 0, st>>>(Mz, n2, 0, 0, kMaxN, kMaxN, M11, gate);
+      zsub_kernel<<<256, 256, 0, st>>>(Mz, n2, kMaxN, kMaxN, Z.q, Z.q, M22, gate);
+      g_launches += 2;
+    } else {
+      trsm_prep_kernel<<<trsm_prep_blocks(L.NT), 256, 0, st>>>(w.Rt, n2, L.NT, w.bfrag, w.dblk, 0, nullptr, gate,
+                                                                o->trsm_diag);  // M -> TRSM operands
+      ++g_launches;
+    }
     CUDA_TRY(cudaGetLastError());
     prof_end(c, pc);
     CUDA_TRY(cudaEventRecord(c->ev_pass[k - 1], st));
     // R := R~ R on the side stream
     CUDA_TRY(cudaEventRecord(c->ev_chol, st));
     CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_chol, 0));
-    ztrmul_kernel<<<static_cast<unsigned>((nn + 127) / 128), 128, 0, c->side>>>(Rtz, R, w.Rnew, static_cast<int>(n),
+    ztrmul_kernel<<<static_cast<unsigned>((nn + 127) / 128), 128, 0, c->side>>>(Rtz, R, Rnew, static_cast<int>(n),
                                                                                  k == 1, w.st, gate);
-    copy_kernel<<<static_cast<unsigned>((2 * nn + 127) / 128), 128, 0, c->side>>>(w.Rnew, R, 2 * nn, w.st, gate);
+    copy_kernel<<<static_cast<unsigned>((2 * nn + 127) / 128), 128, 0, c->side>>>(Rnew, R, 2 * nn, w.st, gate);
     g_launches += 2;
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventRecord(c->ev_side, c->side));
     tp.gate = gate;
     tp.gram_partials = fuse_tg ? w.partials : nullptr;
-    if (m > 0) {
+    if (Z.wide) {
+      if (m > 0) TRY(zwide_trsm(c, Z, w, S, M11, M22, Mz, m, o->trsm_diag, st, gate));
+    } else if (m > 0) {
       CUtensorMap mx;
       const bool use_tma = L.NT <= 16 || L.NT >= 24;
       if (use_tma) TRY(encode_map(c, &mx, S, m, L.NT >= 24 ? 128 : n2, Z.lds, trsm_x_box_cols(L.NT)));
@@ -1747,7 +1891,7 @@ int scqr3_comm_destroy(void* comm) { return comm_destroy(static_cast<Comm*>(comm
 const char* scqr3_last_error(void) { return g_err.c_str(); }
 
 size_t scqr3_workspace_size_complex(int64_t m, int64_t n) {
-  if (n < 1 || 2 * n > kMaxN || m < 0) return 0;
+  if (n < 1 || n > kMaxN || m < 0) return 0;
   return make_zlayout(m, n).end;
 }
 

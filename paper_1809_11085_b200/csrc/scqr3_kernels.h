@@ -214,6 +214,15 @@ __global__ void z2split_kernel(const double* Z, long long ldz, long long m, int 
 __global__ void split2z_kernel(const double* S, long long lds, long long m, int n, double* Z, long long ldz);
 __global__ void zcombine_kernel(const double* tiles, int n, double* A, const int* last_pass, int pass);
 __global__ void zchol_kernel(ZCholParams p);
+// complex n in (256, 512]: the split matrix in two column blocks (zwide.cu)
+__global__ void xgram_kernel(const double* A, long long lda, const double* B, long long ldb, long long m, int p, int q,
+                             long long rows_per_chunk, double* partials, PassGate gate);  // grid chunks*nbp*nbq x 256
+__global__ void xreduce_kernel(const double* partials, int chunks, long long count, double* out, PassGate gate);
+__global__ void xupdate_kernel(const double* Q1, long long ldq, const double* M12, long long ldm, double* S2,
+                               long long lds, long long m, int p, int q, PassGate gate);  // grid ceil(m/64)*nbq x 256
+__global__ void zsub_kernel(const double* M, long long ldm, int r0, int c0, int nr, int nc, double* out, PassGate gate);
+__global__ void zcombine_wide_kernel(const double* t1, const double* t2, const double* c12, int n, int h, double* A,
+                                     const int* last_pass, int pass);
 __global__ void ztrmul_kernel(const double* Rt, const double* R, double* Rnew, int n, int first, const DevStatus* st,
                               PassGate gate);
 // CUDA-graph pass loop (device-side pass control): the loop-condition kernel

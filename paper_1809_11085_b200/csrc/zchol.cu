@@ -20,6 +20,7 @@ namespace scqr3 {
 
 namespace {
 constexpr int kZThreads = 256;
+constexpr int kZPanel = 16;  // rows of R~ per panel of the blocked factorisation (W in global memory)
 
 __device__ __forceinline__ double2 zsum2(double a, double b, double* red) {
   for (int o = 16; o > 0; o >>= 1) {
@@ -92,9 +93,9 @@ __global__ void __launch_bounds__(kZThreads, 1) zchol_kernel(ZCholParams p) {
   const int pass = p.pass_dev ? *(volatile const int*)p.pass_dev : p.pass;
   if (p.last_pass && pass > *(volatile const int*)p.last_pass) return;
   __shared__ double red[2 * kZThreads / 32];
-  __shared__ double ybuf[2][2 * kMaxN / 2];  // complex power-iteration vector (n <= 256)
+  __shared__ double ybuf[2][2 * kMaxN];  // complex power-iteration vector (n <= 512)
   __shared__ double piv_inv;
-  __shared__ double rowk[2 * kMaxN / 2];  // row k of R~ (complex, n <= 256)
+  __shared__ double rowk[2 * kMaxN];  // row k of R~ (complex, n <= 512)
   __shared__ int sflag;
   __shared__ double sval;
   extern __shared__ double zsm[];
@@ -258,6 +259,126 @@ __global__ void __launch_bounds__(kZThreads, 1) zchol_kernel(ZCholParams p) {
     }
     return 0;
   };
+  // ---- the same factorisation blocked for W in global memory (n > 128): panels of kZPanel rows
+  // of R~ factored in shared memory (dynamic: kZPanel x (n - kb) complex), then one rank-kZPanel
+  // update of the trailing upper triangle, so each entry of W is read and written once per panel
+  // instead of once per column (n = 512: ~31 ms per pass unblocked).  Same pivots, same breakdown
+  // test at the same column; only the order of the updates' roundings differs.
+  auto factor_blocked = [&](double s, bool add_shift, double* pv) -> int {
+    if (add_shift) {
+      for (int i = tid; i < n; i += kZThreads) wre(i, i) += s;
+      __syncthreads();
+    }
+    if (tid == 0) sflag = 0;
+    __syncthreads();
+    double* P = zsm;
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int kb = 0; kb < n; kb += kZPanel) {
+      const int b = min(kZPanel, n - kb), ldp = n - kb;
+      auto pre = [&](int r, int c) -> double& { return P[2 * (r * ldp + c)]; };
+      auto pim = [&](int r, int c) -> double& { return P[2 * (r * ldp + c) + 1]; };
+      for (int idx = tid; idx < b * ldp; idx += kZThreads) {  // rows kb.., down each column
+        const int r = idx % b, c = idx / b;
+        if (c >= r) {
+          pre(r, c) = wre(kb + r, kb + c);
+          pim(r, c) = wim(kb + r, kb + c);
+        }
+      }
+      __syncthreads();
+      for (int k = 0; k < b; ++k) {
+        if (tid == 0) {
+          const double d = pre(k, k);
+          if (!(d > 0.0) || !isfinite(d) || !isfinite(pim(k, k))) {
+            sflag = kb + k + 1;
+            sval = d;
+          } else {
+            const double r = sqrt(d);
+            pre(k, k) = r;
+            pim(k, k) = 0.0;
+            piv_inv = 1.0 / r;
+          }
+        }
+        __syncthreads();
+        if (sflag) {
+          *pv = sval;
+          return sflag;
+        }
+        const double ri = piv_inv;
+        for (int c = k + 1 + tid; c < ldp; c += kZThreads) {
+          pre(k, c) *= ri;
+          pim(k, c) *= ri;
+        }
+        __syncthreads();
+        const int rows = b - k - 1;  // panel rows below k: W_ic -= conj(r_ki) r_kc, c >= i
+        for (int idx = tid; idx < rows * ldp; idx += kZThreads) {
+          const int i = k + 1 + idx % rows, c = idx / rows;
+          if (c >= i) {
+            const double a = pre(k, i), bb = pim(k, i), cr = pre(k, c), ci = pim(k, c);
+            pre(i, c) = pre(i, c) - (a * cr + bb * ci);
+            pim(i, c) = pim(i, c) - (a * ci - bb * cr);
+          }
+        }
+        __syncthreads();
+      }
+      for (int idx = tid; idx < b * ldp; idx += kZThreads) {  // R~ rows kb..kb+b-1 back to W
+        const int r = idx % b, c = idx / b;
+        if (c >= r) {
+          wre(kb + r, kb + c) = pre(r, c);
+          wim(kb + r, kb + c) = pim(r, c);
+        }
+      }
+      // trailing update W_ij -= sum_r conj(r_ri) r_rj (i <= j, both >= kb + b): work items are
+      // 32 x 32 blocks (row chunk ci <= column chunk sj); a warp per item, lanes down the rows,
+      // this lane's panel column in registers, the column's panel entries broadcast from smem
+      const int t0 = kb + b;
+      const int nch = (n - t0 + 31) / 32;
+      const int items = nch * (nch + 1) / 2;
+      for (int it = warp; it < items; it += kZThreads / 32) {
+        int sj = static_cast<int>((sqrt(8.0 * it + 1.0) - 1.0) * 0.5);
+        while (sj * (sj + 1) / 2 > it) --sj;
+        while ((sj + 1) * (sj + 2) / 2 <= it) ++sj;
+        const int ci = it - sj * (sj + 1) / 2;
+        const int i = t0 + 32 * ci + lane;
+        const bool iok = i < n;
+        double ar[kZPanel], ai[kZPanel];
+#pragma unroll
+        for (int r = 0; r < kZPanel; ++r) {
+          ar[r] = iok && r < b ? pre(r, i - kb) : 0.0;
+          ai[r] = iok && r < b ? pim(r, i - kb) : 0.0;
+        }
+        const int j0 = t0 + 32 * sj, j1 = min(n, j0 + 32);
+        for (int j = j0; j < j1; j += 4) {
+          double wr[4], wi[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const bool ok = iok && j + u < j1 && i <= j + u;
+            wr[u] = ok ? wre(i, j + u) : 0.0;
+            wi[u] = ok ? wim(i, j + u) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int jj = min(j + u, j1 - 1) - kb;
+            double sr = 0.0, si = 0.0;
+#pragma unroll
+            for (int r = 0; r < kZPanel; ++r) {
+              const double pr = r < b ? pre(r, jj) : 0.0, pi = r < b ? pim(r, jj) : 0.0;
+              sr = fma(ar[r], pr, fma(ai[r], pi, sr));
+              si = fma(ar[r], pi, fma(-ai[r], pr, si));
+            }
+            if (iok && j + u < j1 && i <= j + u) {
+              wre(i, j + u) = wr[u] - sr;
+              wim(i, j + u) = wi[u] - si;
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    return 0;
+  };
+  auto run_factor = [&](double s, bool add_shift, double* pv) -> int {
+    return packed ? factor(s, add_shift, pv) : factor_blocked(s, add_shift, pv);
+  };
   int shifted = 0, bpiv = 0, piv = 1;
   double bval = 0.0, pv = 0.0, s = 0.0, N2 = 0.0;
   const bool practical = p.shift_mode == SCQR3_SHIFT_PRACTICAL;
@@ -265,7 +386,7 @@ __global__ void __launch_bounds__(kZThreads, 1) zchol_kernel(ZCholParams p) {
                                          practical);
   bool dirty = false;
   if (!shift_first) {
-    piv = factor(0.0, false, &pv);
+    piv = run_factor(0.0, false, &pv);
     dirty = true;
     if (piv) { bpiv = piv; bval = pv; }
   }
@@ -277,7 +398,7 @@ __global__ void __launch_bounds__(kZThreads, 1) zchol_kernel(ZCholParams p) {
       if (dirty) load();
       s = attempt == 0 ? s_p : s_safe;
       shifted = 1;
-      piv = factor(s, true, &pv);
+      piv = run_factor(s, true, &pv);
       dirty = true;
       if (piv) { bpiv = piv; bval = pv; }
     }

@@ -48,6 +48,10 @@ def test_default_opts_and_sizes_without_gpu():
     assert lib.scqr3_workspace_size(1000, 0, 0) == 0
     assert lib.scqr3_workspace_size(1000, 513, 0) == 0
     assert lib.scqr3_workspace_size(1000, 512, 0) > 0
+    # complex X up to n = 512 (n > 256: the split matrix as two column blocks, zwide.cu)
+    assert lib.scqr3_workspace_size_complex(1000, 0) == 0
+    assert lib.scqr3_workspace_size_complex(1000, 513) == 0
+    assert lib.scqr3_workspace_size_complex(1000, 512) > lib.scqr3_workspace_size_complex(1000, 256) > 0
     a = lib.scqr3_workspace_size(10_000_000, 128, 0)
     b = lib.scqr3_workspace_size(10_000_000, 128, 1)
     assert 0 < a < b and b >= 8 * 10_000_000 * 128       # oblique holds B*Q

@@ -298,6 +298,34 @@ def test_loopback_complex_and_gram():
 
 
 @gpu
+@pytest.mark.parametrize("deterministic", [False, True])
+def test_loopback_complex_wide(deterministic):
+    """Complex n > 256 across ranks: the three Gram pieces (two block Grams and the cross block)
+    sum through one allreduce; R identical on every rank and equal to the oracle's."""
+    P = 3
+    m, n = 9_000, 272
+    Z = synth.randsvd_complex(m, n, 1e10, seed=6)
+    ro = oracle.zscqr3(Z)
+    comms = sq.Comm.loopback(P)
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    parts = []
+    for r in range(P):
+        r0, r1 = row_block(m, r, P)
+        parts.append(torch.from_numpy(np.asfortranarray(Z[r0:r1])).cuda().t().contiguous().t())
+    torch.cuda.synchronize()
+    res = run_ranks([lambda r=r: sq.scqr3_factor_complex(parts[r], comm=comms[r], stream=streams[r], m_global=m,
+                                                         deterministic=deterministic) for r in range(P)])
+    assert all(x.status == 0 for x in res)
+    R0 = res[0].R.cpu().numpy()
+    assert all(np.array_equal(x.R.cpu().numpy(), R0) for x in res)
+    assert np.max(np.abs(R0 - ro.R)) <= 1e-10 * np.max(np.abs(ro.R))
+    Q = np.concatenate([x.Q.cpu().numpy() for x in res], axis=0)
+    assert oracle.zorth_F(Q) <= 10 * n * U
+    for c in comms:
+        c.destroy()
+
+
+@gpu
 def test_ghost_plan_single_rank_and_rejection():
     """The ghost-plan CSR mode on one GPU (no communicator: nghost = 0) equals the plain CSR
     call bit for bit; across ranks, a send count that does not match the receiver's recv count

@@ -482,6 +482,71 @@ def test_complex_real_input_matches_real_path():
     assert np.max(np.abs(Ra - Rb.real)) <= 1e-12 * np.max(np.abs(Ra))
 
 
+# Complex n in (256, 512]: the 2n-column split matrix as [S1 S2] (zwide.cu) -- the real Gram and
+# TRSM on each block, the cross Gram S1^T S2 and the block update S2 -= Q1 M12 (P:124-125,
+# P:323-334 row-wise; reading D23).  Ragged m (not a multiple of 32 or 64), several cross-Gram
+# chunks and update row blocks, q = 2n - 512 off the 64-column blocks.
+@gpu
+@pytest.mark.parametrize("m,n,kappa", [(3001, 260, 1e8), (9999, 300, 1e12), (4003, 384, 1e10), (2500, 512, 1e6)])
+def test_complex_wide_factor_parity(m, n, kappa):
+    X = synth.randsvd_complex(m, n, kappa, seed=1)
+    rg = sq.scqr3_factor_complex(zdev(X))
+    ro = oracle.zscqr3(X)
+    assert rg.status == 0 and ro.status == 0
+    Rg, Qg = rg.R.cpu().numpy(), rg.Q.cpu().numpy()
+    assert np.max(np.abs(Rg - ro.R)) <= 1e-10 * np.max(np.abs(ro.R))
+    assert np.array_equal(Rg, np.triu(Rg)) and np.all(np.diag(Rg).real > 0) and not np.diag(Rg).imag.any()
+    assert oracle.zorth_F(Qg) <= 10 * n * U
+    assert oracle.zresid_F(X, Qg, Rg) <= 10 * n * U
+    assert rg.trace[0]["shifted"] and ro.trace[0].shifted
+
+
+@gpu
+@pytest.mark.parametrize("n", [300, 512])
+def test_complex_wide_real_input_matches_real_path(n):
+    """A real X through the wide complex path: imaginary parts exactly zero, R equal to the real
+    path's (an independent route: the real kernels on the n columns of X itself)."""
+    X = synth.randsvd(6000, n, 1e9, seed=5)
+    a = sq.scqr3_factor(dev(X))
+    b = sq.scqr3_factor_complex(zdev(X.astype(np.complex128)))
+    assert a.status == b.status == 0
+    Ra, Rb = host(a.R), b.R.cpu().numpy()
+    assert np.max(np.abs(Rb.imag)) == 0.0
+    assert np.max(np.abs(Ra - Rb.real)) <= 1e-12 * np.max(np.abs(Ra))
+    assert np.max(np.abs(b.Q.cpu().numpy().imag)) == 0.0
+
+
+@gpu
+def test_complex_wide_deterministic_and_inplace_blocks():
+    """Two calls give the same bits (fixed-order cross-Gram reduction); the SUBST and INVERSE
+    diagonal modes both reach the oracle's R."""
+    X = synth.randsvd_complex(5000, 280, 1e10, seed=2)
+    a = sq.scqr3_factor_complex(zdev(X))
+    b = sq.scqr3_factor_complex(zdev(X))
+    c = sq.scqr3_factor_complex(zdev(X), trsm_diag=sq.TRSM_DIAG_SUBST)
+    assert a.status == b.status == c.status == 0
+    assert np.array_equal(a.R.cpu().numpy(), b.R.cpu().numpy())
+    assert np.array_equal(a.Q.cpu().numpy(), b.Q.cpu().numpy())
+    ro = oracle.zscqr3(X)
+    for r in (a, c):
+        assert np.max(np.abs(r.R.cpu().numpy() - ro.R)) <= 1e-10 * np.max(np.abs(ro.R))
+
+
+@gpu
+@pytest.mark.parametrize("m,n,col", [(3000, 200, 137), (4000, 300, 290), (2000, 160, 3)])
+def test_complex_blocked_cholesky_breakdown_pivot(m, n, col):
+    """The blocked complex Cholesky (W in global memory, n > 128): a zero column makes the
+    unshifted Gram's pivot exactly 0 at that column (S:69 breakdown = pivot <= 0), on the GPU and
+    in the oracle; with the shift the factorisation goes through (pivot index is 1-based)."""
+    X = synth.randsvd_complex(m, n, 1e4, seed=3)
+    X[:, col] = 0
+    rg = sq.scqr3_factor_complex(zdev(X), shift_mode=sq.SHIFT_NONE, max_passes=2)
+    ro = oracle.zscqr3(X, shift_mode=oracle.SHIFT_NONE, max_passes=2)
+    assert rg.status == sq.EBREAKDOWN and ro.status == sq.EBREAKDOWN
+    assert rg.trace[0]["breakdown_pivot"] == ro.trace[0].breakdown_pivot == col + 1
+    assert rg.trace[0]["pivot_value"] == 0.0
+
+
 # ------------------------------------------------------------------ wide TRSM, several sweeps
 # One persistent sweep of the TRSM covers 148 CTAs x 8 warps x 16 rows = 18,944 rows; at
 # m >= 60,000 every block-column launch of the n in (128, 512] path (columns 0..127, targets

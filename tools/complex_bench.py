@@ -23,7 +23,7 @@ for _ in range(3):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 3
-fl = 6 * 4 * m * n * n  # 3 passes x (Gram + TRSM), complex = 4 real multiply-adds
-print(f"complex m={m} n={n}: {ms:.3f} ms, {fl / ms / 1e9:.2f} TF/s real-equivalent, passes={r.passes} "
+fl = r.passes * 2 * 4 * m * n * n  # executed passes x (Gram + TRSM), complex = 4 real multiply-adds
+print(f"complex m={m} n={n}: {ms:.3f} ms, {fl / ms / 1e9:.2f} TF/s real-equivalent (executed passes), passes={r.passes} "
       f"gram {prof.gram_ms / max(prof.gram_launches, 1):.3f} ms trsm {prof.trsm_ms / max(prof.trsm_launches, 1):.3f} ms "
       f"chol {prof.chol_ms / max(prof.chol_launches, 1):.3f} ms")
