@@ -640,6 +640,7 @@ __global__ void oblique_y_kernel(ObliqueYParams p) {
 // ||Q||_F^2 partials like oblique_y_kernel.  One thread per (row, 8-column chunk): consecutive
 // threads take consecutive rows, so each nonzero's Q reads are coalesced along the column;
 // rows outside [0, m) come from the halo buffers (neighbouring ranks' rows).
+constexpr int kCsrTileCap = 3072;  // staged nonzeros per 256-row tile (36 KB)
 #ifndef SCQR3_CSR_COLS
 #define SCQR3_CSR_COLS 16  // columns per thread (measured on C5L: 16 beats 4, 8, 32, 64)
 #endif
@@ -699,6 +700,131 @@ __global__ void csr_y_kernel(ObliqueYParams p) {
     double v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     if (threadIdx.x == 0) p.colsq_partials[blockIdx.x] = v;
+  }
+}
+
+// Tile version of csr_y_kernel (round 2c): a CTA owns 256 consecutive rows and ALL their columns.
+// The tile's row pointers and (when they fit) its column indices and values are staged in shared
+// memory once by coalesced loads, so the inner loop's only global loads are the Q entries (no
+// rp -> ci -> Q dependent chain, no re-read of the CSR arrays per column chunk).  Thread t owns
+// row i0 + t; C columns and U nonzeros' Q loads are in flight per thread.  The per-row term order
+// is the CSR order (as in csr_y_kernel and the oracle), so Y has the same bits; ||Q||_F^2 is the
+// same set of squares summed in a different (still fixed) order.
+template <int C, int U, bool STAGED>
+__device__ __forceinline__ void csr_row(const ObliqueYParams& p, long long i, long long zb, long long ze,
+                                        const int* __restrict__ sci, const double* __restrict__ scv,
+                                        long long zoff, double& sq) {
+  for (int c0 = 0; c0 < p.n; c0 += C) {
+    const int cw = min(C, p.n - c0);
+    double acc[C];
+#pragma unroll
+    for (int j = 0; j < C; ++j) acc[j] = 0.0;
+    long long z = zb;
+    while (z < ze) {
+      double qv[U][C];
+      double vv[U];
+      bool own[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool on = z + u < ze;
+        const long long zz = on ? z + u : zb;
+        const long long col = STAGED ? sci[zz - zoff] : p.ci[zz];
+        vv[u] = on ? (STAGED ? scv[zz - zoff] : p.cv[zz]) : 0.0;
+        own[u] = on && col == i;
+        const double* src;
+        long long ld;
+        if (col < 0) {
+          src = p.halo_prev + (col + p.halo);
+          ld = p.halo;
+        } else if (col >= p.m) {
+          if (p.ghosts) {
+            src = p.ghost + (col - p.m) * p.n;
+            ld = 1;
+          } else {
+            src = p.halo_next + (col - p.m);
+            ld = p.halo;
+          }
+        } else {
+          src = p.Q + col;
+          ld = p.ldq;
+        }
+#pragma unroll
+        for (int j = 0; j < C; ++j) qv[u][j] = (on && j < cw) ? src[(c0 + j) * ld] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (U > 1 && !(z + u < ze)) break;
+#pragma unroll
+        for (int j = 0; j < C; ++j) acc[j] = fma(vv[u], qv[u][j], acc[j]);
+        if (own[u]) {
+#pragma unroll
+          for (int j = 0; j < C; ++j) sq = fma(qv[u][j], qv[u][j], sq);
+        }
+      }
+      z += U;
+    }
+#pragma unroll
+    for (int j = 0; j < C; ++j)
+      if (j < cw) __stcs(p.Y + (c0 + j) * p.ldy + i, acc[j]);
+  }
+}
+
+template <int C, int U>
+__global__ void __launch_bounds__(256) csr_y_tile_kernel(ObliqueYParams p) {
+  constexpr int T = 256;
+  __shared__ long long s_rp[T + 1];
+  __shared__ int s_ci[kCsrTileCap];
+  __shared__ double s_cv[kCsrTileCap];
+  __shared__ double red[32];
+  if (SCQR3_GATE_SKIP(p.gate)) return;
+  double sq = 0.0;
+  const long long ntiles = (p.m + T - 1) / T;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long i0 = tile * T;
+    const int rows = static_cast<int>(min(static_cast<long long>(T), p.m - i0));
+    __syncthreads();  // the previous tile's readers are done with the staged arrays
+    for (int t = threadIdx.x; t <= rows; t += T) s_rp[t] = p.rp[i0 + t];
+    __syncthreads();
+    const long long z0 = s_rp[0];
+    const long long cnt = s_rp[rows] - z0;
+    const bool staged = cnt <= kCsrTileCap;
+    if (staged) {
+      for (int z = threadIdx.x; z < cnt; z += T) {
+        s_ci[z] = p.ci[z0 + z];
+        s_cv[z] = p.cv[z0 + z];
+      }
+    }
+    __syncthreads();
+    if (static_cast<int>(threadIdx.x) < rows) {
+      const long long i = i0 + threadIdx.x;
+      const long long zb = s_rp[threadIdx.x], ze = s_rp[threadIdx.x + 1];
+      if (staged)
+        csr_row<C, U, true>(p, i, zb, ze, s_ci, s_cv, z0, sq);
+      else
+        csr_row<C, U, false>(p, i, zb, ze, nullptr, nullptr, 0, sq);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) p.colsq_partials[blockIdx.x] = v;
+  }
+}
+
+// Host-side launcher: variant 0 = csr_y_kernel (one thread per row and 16-column chunk), the
+// others are (C, U) instances of the tile kernel.
+void launch_csr_y(const ObliqueYParams& p, int variant, int blocks, cudaStream_t st) {
+  switch (variant) {
+    case 1: csr_y_tile_kernel<16, 1><<<blocks, 256, 0, st>>>(p); break;
+    case 2: csr_y_tile_kernel<8, 2><<<blocks, 256, 0, st>>>(p); break;
+    case 3: csr_y_tile_kernel<16, 2><<<blocks, 256, 0, st>>>(p); break;
+    case 4: csr_y_tile_kernel<8, 1><<<blocks, 256, 0, st>>>(p); break;
+    case 5: csr_y_tile_kernel<4, 4><<<blocks, 256, 0, st>>>(p); break;
+    case 6: csr_y_tile_kernel<8, 4><<<blocks, 256, 0, st>>>(p); break;
+    default: csr_y_kernel<<<blocks, 256, 0, st>>>(p); break;
   }
 }
 

@@ -444,7 +444,14 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
     p.colsq_partials = w.colsq;
     const int ps = prof_begin(c, PK_REDUCE);
     if (p.rp) {
-      csr_y_kernel<<<colsq_count, 256, 0, st>>>(p);
+      // SCQR3_CSR_Y selects the Y = BQ kernel (A/B measurement): 0 = one thread per (row, 16-column
+      // chunk); 1.. = instances of the 256-row tile kernel with the CSR arrays staged in shared memory
+      static const int variant = [] {
+        const char* v = std::getenv("SCQR3_CSR_Y");
+        return v ? std::atoi(v) : 0;
+      }();
+      if (variant > 0) colsq_count = static_cast<int>(std::min<long long>((m + 255) / 256, 4096));
+      launch_csr_y(p, variant, colsq_count, st);
     } else {
       colsq_count = static_cast<int>(std::max<long long>(1, std::min<long long>((m + 255) / 256, 4096)));
       p.colsq_partials = w.colsq;

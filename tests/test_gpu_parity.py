@@ -368,11 +368,15 @@ def _csr_dev(B, halo=0):
 
 
 @gpu
-@pytest.mark.parametrize("m,n", [(3, 2), (40, 5), (513, 33), (3000, 64)])
-def test_gram_oblique_csr_exact_integers(m, n):
+@pytest.mark.parametrize("m,n,dens", [(3, 2, 6), (40, 5, 6), (513, 33, 6), (3000, 64, 6), (2900, 64, 2),
+                                      (1025, 17, 1)])
+def test_gram_oblique_csr_exact_integers(m, n, dens):
+    """dens = 6 gives ~13 nonzeros per row (a 256-row tile's CSR arrays exceed the tile kernel's
+    shared-memory stage: the global-memory path), dens <= 2 at most ~5 (the staged path); m off
+    the 256-row tile size leaves a ragged last tile."""
     rng = np.random.default_rng(3 * m + n)
     M = np.zeros((m, m), dtype=np.int64)
-    k = min(m * 6, m * m)
+    k = min(m * dens, m * m)
     r, c = rng.integers(0, m, k), rng.integers(0, m, k)
     M[r, c] = rng.integers(-9, 10, k)
     M = np.triu(M, 1)
