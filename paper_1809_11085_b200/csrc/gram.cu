@@ -640,7 +640,6 @@ __global__ void oblique_y_kernel(ObliqueYParams p) {
 // ||Q||_F^2 partials like oblique_y_kernel.  One thread per (row, 8-column chunk): consecutive
 // threads take consecutive rows, so each nonzero's Q reads are coalesced along the column;
 // rows outside [0, m) come from the halo buffers (neighbouring ranks' rows).
-constexpr int kCsrTileCap = 3072;  // staged nonzeros per 256-row tile (36 KB)
 #ifndef SCQR3_CSR_COLS
 #define SCQR3_CSR_COLS 16  // columns per thread (measured on C5L: 16 beats 4, 8, 32, 64)
 #endif
@@ -703,14 +702,40 @@ __global__ void csr_y_kernel(ObliqueYParams p) {
   }
 }
 
-// Tile version of csr_y_kernel (round 2c): a CTA owns 256 consecutive rows and ALL their columns.
-// The tile's row pointers and (when they fit) its column indices and values are staged in shared
-// memory once by coalesced loads, so the inner loop's only global loads are the Q entries (no
-// rp -> ci -> Q dependent chain, no re-read of the CSR arrays per column chunk).  Thread t owns
-// row i0 + t; C columns and U nonzeros' Q loads are in flight per thread.  The per-row term order
-// is the CSR order (as in csr_y_kernel and the oracle), so Y has the same bits; ||Q||_F^2 is the
-// same set of squares summed in a different (still fixed) order.
-template <int C, int U, bool STAGED>
+// Tile version of csr_y_kernel (the default since round 2c): a CTA owns T = 256 consecutive rows
+// and ALL their columns.  The tile's row pointers and, when they fit (at most 12 nonzeros per row
+// on average), its column indices and values are staged in shared memory once by coalesced loads,
+// so the inner loop's only global loads are the Q entries: no rp -> ci -> Q dependent chain and
+// no re-read of the CSR arrays per column chunk.  Thread t owns row i0 + t and takes C = 8
+// columns at a time with one pointer bump per load (the per-load index arithmetic and column
+// predicates of csr_y_kernel were ~16 instructions per load: ncu showed the issue slots half
+// busy at 25 % occupancy); 64 registers -> four CTAs per SM.  Measured on C5L (m = 2e6, n = 64,
+// 5-point Laplacian): 0.47 ms (4.6 TB/s of the algorithmic 2.18 GB) against 0.71 ms; DRAM reads
+// 1.17 GB = 1.07x the algorithmic bytes.  More loads in flight per thread (C = 16, two nonzeros
+// per step) and 128- or 512-row tiles measured slower, __ldg the same, __ldcs slower
+// (profiles/csr_y_r02e.md).  The per-row term order is the CSR order (as in csr_y_kernel and the
+// oracle), so Y has the same bits; ||Q||_F^2 is the same squares summed in another fixed order.
+__device__ __forceinline__ void csr_src(const ObliqueYParams& p, long long col, int c0, const double*& src,
+                                        long long& ld) {
+  if (col < 0) {  // a band halo row of the previous rank
+    src = p.halo_prev + (col + p.halo);
+    ld = p.halo;
+  } else if (col >= p.m) {
+    if (p.ghosts) {  // ghost row of the sparsity-pattern plan (row-major)
+      src = p.ghost + (col - p.m) * p.n;
+      ld = 1;
+    } else {
+      src = p.halo_next + (col - p.m);
+      ld = p.halo;
+    }
+  } else {
+    src = p.Q + col;
+    ld = p.ldq;
+  }
+  src += c0 * ld;
+}
+
+template <int C, bool STAGED>
 __device__ __forceinline__ void csr_row(const ObliqueYParams& p, long long i, long long zb, long long ze,
                                         const int* __restrict__ sci, const double* __restrict__ scv,
                                         long long zoff, double& sq) {
@@ -719,49 +744,26 @@ __device__ __forceinline__ void csr_row(const ObliqueYParams& p, long long i, lo
     double acc[C];
 #pragma unroll
     for (int j = 0; j < C; ++j) acc[j] = 0.0;
-    long long z = zb;
-    while (z < ze) {
-      double qv[U][C];
-      double vv[U];
-      bool own[U];
+    for (long long z = zb; z < ze; ++z) {
+      const long long col = STAGED ? sci[z - zoff] : p.ci[z];
+      const double v = STAGED ? scv[z - zoff] : p.cv[z];
+      const double* src;
+      long long ld;
+      csr_src(p, col, c0, src, ld);
+      double qv[C];
+      if (cw == C) {  // a full chunk: no per-column predicates
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const bool on = z + u < ze;
-        const long long zz = on ? z + u : zb;
-        const long long col = STAGED ? sci[zz - zoff] : p.ci[zz];
-        vv[u] = on ? (STAGED ? scv[zz - zoff] : p.cv[zz]) : 0.0;
-        own[u] = on && col == i;
-        const double* src;
-        long long ld;
-        if (col < 0) {
-          src = p.halo_prev + (col + p.halo);
-          ld = p.halo;
-        } else if (col >= p.m) {
-          if (p.ghosts) {
-            src = p.ghost + (col - p.m) * p.n;
-            ld = 1;
-          } else {
-            src = p.halo_next + (col - p.m);
-            ld = p.halo;
-          }
-        } else {
-          src = p.Q + col;
-          ld = p.ldq;
-        }
+        for (int j = 0; j < C; ++j, src += ld) qv[j] = *src;
+      } else {
 #pragma unroll
-        for (int j = 0; j < C; ++j) qv[u][j] = (on && j < cw) ? src[(c0 + j) * ld] : 0.0;
+        for (int j = 0; j < C; ++j) qv[j] = j < cw ? src[j * ld] : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (U > 1 && !(z + u < ze)) break;
+      for (int j = 0; j < C; ++j) acc[j] = fma(v, qv[j], acc[j]);
+      if (col == i) {  // the row's own q (SPD: the diagonal is stored) -> ||Q||_F^2 partial
 #pragma unroll
-        for (int j = 0; j < C; ++j) acc[j] = fma(vv[u], qv[u][j], acc[j]);
-        if (own[u]) {
-#pragma unroll
-          for (int j = 0; j < C; ++j) sq = fma(qv[u][j], qv[u][j], sq);
-        }
+        for (int j = 0; j < C; ++j) sq = fma(qv[j], qv[j], sq);
       }
-      z += U;
     }
 #pragma unroll
     for (int j = 0; j < C; ++j)
@@ -769,12 +771,11 @@ __device__ __forceinline__ void csr_row(const ObliqueYParams& p, long long i, lo
   }
 }
 
-template <int C, int U>
-__global__ void __launch_bounds__(256) csr_y_tile_kernel(ObliqueYParams p) {
-  constexpr int T = 256;
+__global__ void __launch_bounds__(kCsrTileRows, 4) csr_y_tile_kernel(ObliqueYParams p) {
+  constexpr int T = kCsrTileRows, C = 8, CAP = kCsrTileNnzPerRow * T;
   __shared__ long long s_rp[T + 1];
-  __shared__ int s_ci[kCsrTileCap];
-  __shared__ double s_cv[kCsrTileCap];
+  __shared__ int s_ci[CAP];
+  __shared__ double s_cv[CAP];
   __shared__ double red[32];
   if (SCQR3_GATE_SKIP(p.gate)) return;
   double sq = 0.0;
@@ -787,7 +788,7 @@ __global__ void __launch_bounds__(256) csr_y_tile_kernel(ObliqueYParams p) {
     __syncthreads();
     const long long z0 = s_rp[0];
     const long long cnt = s_rp[rows] - z0;
-    const bool staged = cnt <= kCsrTileCap;
+    const bool staged = cnt <= CAP;  // else this tile reads ci / cv from global memory
     if (staged) {
       for (int z = threadIdx.x; z < cnt; z += T) {
         s_ci[z] = p.ci[z0 + z];
@@ -799,32 +800,19 @@ __global__ void __launch_bounds__(256) csr_y_tile_kernel(ObliqueYParams p) {
       const long long i = i0 + threadIdx.x;
       const long long zb = s_rp[threadIdx.x], ze = s_rp[threadIdx.x + 1];
       if (staged)
-        csr_row<C, U, true>(p, i, zb, ze, s_ci, s_cv, z0, sq);
+        csr_row<C, true>(p, i, zb, ze, s_ci, s_cv, z0, sq);
       else
-        csr_row<C, U, false>(p, i, zb, ze, nullptr, nullptr, 0, sq);
+        csr_row<C, false>(p, i, zb, ze, nullptr, nullptr, 0, sq);
     }
   }
+  // deterministic block reduction
   for (int o = 16; o > 0; o >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
   __syncthreads();
   if (threadIdx.x < 32) {
-    double v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
+    double v = threadIdx.x < T / 32 ? red[threadIdx.x] : 0.0;
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     if (threadIdx.x == 0) p.colsq_partials[blockIdx.x] = v;
-  }
-}
-
-// Host-side launcher: variant 0 = csr_y_kernel (one thread per row and 16-column chunk), the
-// others are (C, U) instances of the tile kernel.
-void launch_csr_y(const ObliqueYParams& p, int variant, int blocks, cudaStream_t st) {
-  switch (variant) {
-    case 1: csr_y_tile_kernel<16, 1><<<blocks, 256, 0, st>>>(p); break;
-    case 2: csr_y_tile_kernel<8, 2><<<blocks, 256, 0, st>>>(p); break;
-    case 3: csr_y_tile_kernel<16, 2><<<blocks, 256, 0, st>>>(p); break;
-    case 4: csr_y_tile_kernel<8, 1><<<blocks, 256, 0, st>>>(p); break;
-    case 5: csr_y_tile_kernel<4, 4><<<blocks, 256, 0, st>>>(p); break;
-    case 6: csr_y_tile_kernel<8, 4><<<blocks, 256, 0, st>>>(p); break;
-    default: csr_y_kernel<<<blocks, 256, 0, st>>>(p); break;
   }
 }
 

@@ -444,14 +444,18 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
     p.colsq_partials = w.colsq;
     const int ps = prof_begin(c, PK_REDUCE);
     if (p.rp) {
-      // SCQR3_CSR_Y selects the Y = BQ kernel (A/B measurement): 0 = one thread per (row, 16-column
-      // chunk); 1.. = instances of the 256-row tile kernel with the CSR arrays staged in shared memory
-      static const int variant = [] {
+      // SCQR3_CSR_Y=0 selects the round-1 kernel (one thread per row and 16-column chunk; A/B
+      // measurement); the default is the 256-row tile kernel with the CSR arrays staged in shared memory
+      static const bool tile = [] {
         const char* v = std::getenv("SCQR3_CSR_Y");
-        return v ? std::atoi(v) : 0;
+        return !(v && v[0] == '0');
       }();
-      if (variant > 0) colsq_count = static_cast<int>(std::min<long long>((m + 255) / 256, 4096));
-      launch_csr_y(p, variant, colsq_count, st);
+      if (tile) {
+        colsq_count = static_cast<int>(std::min<long long>((m + kCsrTileRows - 1) / kCsrTileRows, 4096));
+        csr_y_tile_kernel<<<colsq_count, kCsrTileRows, 0, st>>>(p);
+      } else {
+        csr_y_kernel<<<colsq_count, 256, 0, st>>>(p);
+      }
     } else {
       colsq_count = static_cast<int>(std::max<long long>(1, std::min<long long>((m + 255) / 256, 4096)));
       p.colsq_partials = w.colsq;

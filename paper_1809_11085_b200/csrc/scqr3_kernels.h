@@ -193,7 +193,9 @@ cudaError_t launch_gram_tma(int variant, unsigned grid, int threads, size_t smem
                             const CUtensorMap& mapQ, const CUtensorMap& mapY, const GramParams& p);
 __global__ void gram_reduce_kernel(GramReduceParams p);
 __global__ void csr_y_kernel(ObliqueYParams p);
-void launch_csr_y(const ObliqueYParams& p, int variant, int blocks, cudaStream_t st);
+constexpr int kCsrTileRows = 256;       // rows (= threads) per CTA of csr_y_tile_kernel
+constexpr int kCsrTileNnzPerRow = 12;   // staged nonzeros per tile row (36 KB of shared memory)
+__global__ void csr_y_tile_kernel(ObliqueYParams p);
 __global__ void csr_gershgorin_kernel(const long long* rp, const double* cv, long long m, double* partial);
 __global__ void index_check_kernel(const long long* v, long long cnt, long long lo, long long hi, int* bad);
 __global__ void csr_check_kernel(const long long* rp, const int* ci, long long m, long long halo, int has_prev,

@@ -4,7 +4,7 @@
 out=${1:-gpurun_out/csry}
 mkdir -p $out
 for v in ${VARIANTS:-0 1 2 3 4 5 6}; do
-  SCQR3_CSR_Y=$v timeout 600 python -m pytest tests -m gpu -q -x -k "csr or ghost or laplacian" > $out/test_v$v.log 2>&1
+  SCQR3_CSR_Y=$v timeout 600 python -m pytest ${TESTS:-tests} -m gpu -q -x -k "csr or ghost or laplacian" > $out/test_v$v.log 2>&1
   echo "variant $v tests: $(tail -1 $out/test_v$v.log)"
   SCQR3_CSR_Y=$v timeout 600 python bench.py --config C5L --steps 5 --warmup 3 --no-cpu --no-e2e > $out/bench_v$v.json 2> $out/bench_v$v.err
   python - $out/bench_v$v.json $v <<'P'
