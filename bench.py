@@ -84,7 +84,7 @@ def executed_roofline_ms(cfg, m, n, passes, peak_tflops, fused, nnz=0, hbm_gbs=6
     (which run one after another) of max(algorithmic flops / FP64 peak, algorithmic bytes / HBM
     bandwidth), for the executed pass count.  Per pass: Gram m n(n+1) flop, 8mn B (oblique: the
     dual B-Gram + plain Gram, 2 m n(n+1) flop, 16mn B, after Y = BQ: tridiagonal 5mn flop,
-    16mn + 16m B; CSR 2 nnz n flop, 16mn + 12 nnz ceil(n/16) B); TRSM m n^2 flop, 16mn B; the
+    16mn + 16m B; CSR 2 nnz n flop, 16mn + 12 nnz + 8m B: the CSR arrays once); TRSM m n^2 flop, 16mn B; the
     fused n <= 64 TRSM also carries the next pass's Gram (no 8mn re-read).  The n x n steps
     (reduce, Cholesky) are latency and not in the model."""
     P, BW = peak_tflops * 1e12, hbm_gbs * 1e9
@@ -93,7 +93,7 @@ def executed_roofline_ms(cfg, m, n, passes, peak_tflops, fused, nnz=0, hbm_gbs=6
     for k in range(1, passes + 1):
         if cfg.oblique:
             if cfg.metric == "laplacian":
-                tot += t(2.0 * nnz * n, 16.0 * m * n + 12.0 * nnz * -(-n // 16))
+                tot += t(2.0 * nnz * n, 16.0 * m * n + 12.0 * nnz + 8.0 * m)
             else:
                 tot += t(5.0 * m * n, 16.0 * m * n + 16.0 * m)
             tot += t(2.0 * m * n * (n + 1), 16.0 * m * n)

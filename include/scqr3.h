@@ -200,7 +200,7 @@ size_t scqr3_workspace_size_csr(int64_t m, int64_t n, int64_t halo);
 size_t scqr3_workspace_size_csr_ghosts(int64_t m, int64_t n, int64_t nghost, int64_t nsend);
 
 /* Oblique shifted CholeskyQR3 (Alg. 5 with the B-Gram in all passes, D8) for a CSR metric:
- * Y = B Q by csr_y_kernel, then the same Gram / shift / Cholesky / TRSM path; the shift's
+ * Y = B Q by csr_y_tile_kernel, then the same Gram / shift / Cholesky / TRSM path; the shift's
  * ||B||_2 bound is opts->bnorm_bound or the Gershgorin max_i sum_k |B_ik| (allreduce-max
  * over ranks).  Target Q^T B Q = I, X = QR. */
 int scqr3_factor_oblique_csr(int64_t m, int64_t n, const double* X, int64_t ld, const scqr3_csr* B,

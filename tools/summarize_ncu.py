@@ -23,8 +23,11 @@ def launches(path):
     hdr = rows[h]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
     tot, cnt = collections.defaultdict(float), collections.Counter()
+    # a list captured with `--kernel-name-base demangled -k regex:scqr3` holds only the library's
+    # kernels, printed without the namespace
+    filtered = not any("scqr3::" in r[ki] for r in rows[h + 1:] if len(r) > ki)
     for r in rows[h + 1:]:
-        if "scqr3::" not in r[ki]:
+        if len(r) <= ki or (not filtered and "scqr3::" not in r[ki]):
             continue  # input generation (torch / cuSOLVER) is not part of the step
         name = r[ki].split("(")[0].replace("void ", "").split("<")[0].replace("scqr3::", "")
         tot[name] += float(r[vi].replace(",", "")) * UNIT.get(r[ui], 1e-6)
