@@ -15,15 +15,18 @@ def _two_sum(s, c, x):
     return t, c + e
 
 
-def orth_F(Q, d=None, e=None, chunk=4096):
-    """||Q^T Q - I||_F (or ||Q^T B Q - I||_F for tridiagonal B = (d, e)) in compensated fp64."""
+def orth_F(Q, d=None, e=None, chunk=4096, Y=None):
+    """||Q^T Q - I||_F (or ||Q^T B Q - I||_F for tridiagonal B = (d, e), or for any B with
+    Y = B Q given) in compensated fp64."""
     m, n = Q.shape
     s = torch.zeros((n, n), dtype=torch.float64, device=Q.device)
     c = torch.zeros_like(s)
     for r0 in range(0, m, chunk):
         r1 = min(m, r0 + chunk)
         Qc = Q[r0:r1]
-        if d is None:
+        if Y is not None:
+            Yc = Y[r0:r1]
+        elif d is None:
             Yc = Qc
         else:  # rows r0..r1-1 of B Q: d_i q_i + e_{i-1} q_{i-1} + e_i q_{i+1}
             Yc = d[r0:r1, None] * Qc

@@ -105,6 +105,44 @@ def test_c5_full_size_oblique():
 
 @gpu
 @slow
+def test_c5l_full_size_csr_metric():
+    """C5L as bench.py times it (m = 2e6, n = 64, weighted 5-point Laplacian in CSR, the tile
+    Y = BQ kernel): R against the oracle's CSR path, B-orthogonality and residual <= 10 n u."""
+    cfg = synth.CONFIGS["C5L"]
+    m, n = cfg.m, cfg.n
+    X = synth.randsvd_torch(m, n, cfg.kappa, seed=0, spectrum=cfg.spectrum)
+    B = synth.laplacian2d(cfg.grid_nx, m // cfg.grid_nx, seed=0, wmax=1e4)
+    csr = sq.CsrMetric(torch.from_numpy(B[0]), torch.from_numpy(B[1]), torch.from_numpy(B[2]), halo=0)
+    rg = sq.scqr3_factor_oblique_csr(X, csr)
+    ro = oracle.scqr3(X.cpu().numpy(), csr=B)
+    assert rg.status == 0 and ro.status == 0
+    assert rg.trace[0]["shifted"] and ro.trace[0].shifted
+    Rg = rg.R.cpu().numpy()
+    normwise = float(np.max(np.abs(Rg - ro.R)) / np.max(np.abs(ro.R)))
+    assert normwise <= 1e-10
+    assert np.array_equal(Rg, np.triu(Rg)) and np.all(np.diag(Rg) > 0)
+    # B Q by torch's own CSR product (independent of the library's kernel)
+    Bt = torch.sparse_csr_tensor(torch.from_numpy(B[0]).cuda(), torch.from_numpy(B[1]).cuda().long(),
+                                 torch.from_numpy(B[2]).cuda(), size=(m, m))
+    Y = Bt @ rg.Q
+    orth = gpu_metrics.orth_F(rg.Q, Y=Y)
+    res = gpu_metrics.resid_F(X, rg.Q, rg.R)
+    assert orth <= 10 * n * U, orth
+    assert res <= 10 * n * U, res
+    nz = ro.R != 0
+    per_entry = float(np.max(np.abs(Rg - ro.R)[nz] / np.abs(ro.R[nz])))
+    print(f"C5L: m={m} n={n} passes gpu={rg.passes} oracle={ro.passes} orth gpu={orth:.2e} resid gpu={res:.2e} "
+          f"(10nu={10 * n * U:.2e}) R normwise={normwise:.2e} R per-entry rel={per_entry:.2e}")
+    out = os.environ.get("SCQR3_PARITY_OUT")
+    if out:
+        with open(out, "a") as f:
+            f.write(json.dumps(dict(config="C5L", m=m, n=n, kappa=cfg.kappa, passes_gpu=rg.passes,
+                                    passes_oracle=ro.passes, orth_gpu=orth, orth_oracle=None, resid_gpu=res,
+                                    R_normwise=normwise, R_per_entry_rel=per_entry, ten_n_u=10 * n * U)) + "\n")
+
+
+@gpu
+@slow
 def test_c4_shape_reduced_m():
     """C4's n=256, kappa=1e14 cluster spectrum at m=2e6 (the full 4e7 x 256 is a 4/8-GPU config)."""
     rg, ro, orth, res = _run("C4", m=2_000_000)
