@@ -715,7 +715,8 @@ __global__ void csr_y_kernel(ObliqueYParams p) {
 // 1.17 GB = 1.07x the algorithmic bytes.  More loads in flight per thread (C = 16, two nonzeros
 // per step) and 128- or 512-row tiles measured slower, __ldg the same, __ldcs slower
 // (profiles/csr_y_r02e.md); so did a shared-memory window of the tile's own rows per column
-// chunk fed by 1-D bulk copies (0.52 ms).  The per-row term order is the CSR order (as in csr_y_kernel and the
+// chunk fed by 1-D bulk copies (0.52 ms) and a row-pair version with 16-byte loads (half the load
+// requests, 128 registers: 0.74 ms).  The per-row term order is the CSR order (as in csr_y_kernel and the
 // oracle), so Y has the same bits; ||Q||_F^2 is the same squares summed in another fixed order.
 __device__ __forceinline__ void csr_src(const ObliqueYParams& p, long long col, int c0, const double*& src,
                                         long long& ld) {
