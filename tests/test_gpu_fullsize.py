@@ -122,9 +122,12 @@ def test_c5l_full_size_csr_metric():
     assert normwise <= 1e-10
     assert np.array_equal(Rg, np.triu(Rg)) and np.all(np.diag(Rg) > 0)
     # B Q by torch's own CSR product (independent of the library's kernel)
-    Bt = torch.sparse_csr_tensor(torch.from_numpy(B[0]).cuda(), torch.from_numpy(B[1]).cuda().long(),
-                                 torch.from_numpy(B[2]).cuda(), size=(m, m))
-    Y = Bt @ rg.Q
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")   # torch: "sparse CSR support is in beta state"
+        Bt = torch.sparse_csr_tensor(torch.from_numpy(B[0]).cuda(), torch.from_numpy(B[1]).cuda().long(),
+                                     torch.from_numpy(B[2]).cuda(), size=(m, m))
+        Y = Bt @ rg.Q
     orth = gpu_metrics.orth_F(rg.Q, Y=Y)
     res = gpu_metrics.resid_F(X, rg.Q, rg.R)
     assert orth <= 10 * n * U, orth
