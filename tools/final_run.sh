@@ -9,7 +9,7 @@ python bench.py > $out/bench_C3.json 2> $out/bench_C3.err
 for c in C2 C5 C5L PR1; do python bench.py --config $c > $out/bench_$c.json 2> $out/bench_$c.err; done
 python bench.py --impl reference --steps 2 --warmup 1 > $out/bench_reference_arm.json 2> $out/bench_reference_arm.err
 for c in C3 C5L; do
-  ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $out/ncu_launches_$c.csv \
+  ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k regex:scqr3 --csv --log-file $out/ncu_launches_$c.csv \
     python bench.py --config $c --steps 2 --warmup 1 --no-cpu --no-e2e > $out/ncu_$c.log 2>&1
 done
 tail -2 $out/gputest.log; tail -1 $out/smoke.log
