@@ -703,7 +703,7 @@ __global__ void csr_y_kernel(ObliqueYParams p) {
   }
 }
 
-// Tile version of csr_y_kernel (the default since round 2c): a CTA owns T = 256 consecutive rows
+// Tile version of csr_y_kernel (round 2c; launched when nnz <= 12 m, see ObliqueYParams::csr_tile): a CTA owns T = 256 consecutive rows
 // and ALL their columns.  The tile's row pointers and, when they fit (at most 12 nonzeros per row
 // on average), its column indices and values are staged in shared memory once by coalesced loads,
 // so the inner loop's only global loads are the Q entries: no rp -> ci -> Q dependent chain and

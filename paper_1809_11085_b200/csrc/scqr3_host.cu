@@ -450,7 +450,7 @@ int run_gram(Ctx* c, const Layout& L, const WS& w, const double* src, int64_t ld
         const char* v = std::getenv("SCQR3_CSR_Y");
         return !(v && v[0] == '0');
       }();
-      if (tile) {
+      if (tile && p.csr_tile) {
         colsq_count = static_cast<int>(std::min<long long>((m + kCsrTileRows - 1) / kCsrTileRows, 4096));
         csr_y_tile_kernel<<<colsq_count, kCsrTileRows, 0, st>>>(p);
       } else {
@@ -850,7 +850,10 @@ int factor_body(int64_t m, int64_t n, const double* X, int64_t ld, const Metric&
           CUDA_TRY(cudaGetLastError());
         }
         CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+        long long hnnz = 0;  // row_ptr[m]: picks the Y = BQ kernel (tile kernel up to 12 nonzeros per row)
+        if (m > 0) CUDA_TRY(cudaMemcpyAsync(&hnnz, yp.rp + m, sizeof(long long), cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaStreamSynchronize(st));
+        yp.csr_tile = hnnz <= static_cast<long long>(kCsrTileNnzPerRow) * m ? 1 : 0;
         if (hbad) fail("CSR metric: row_ptr not monotone from 0, a column index outside this rank's rows and halo / "
                        "ghosts, or a send row outside [0, m)");
       }
@@ -1772,6 +1775,10 @@ int scqr3_gram_oblique_csr(int64_t m, int64_t n, const double* X, int64_t ld, co
   yp.ci = B->col_idx;
   yp.cv = B->vals;
   yp.halo = 0;
+  long long hnnz = 0;
+  CUDA_TRY(cudaMemcpyAsync(&hnnz, yp.rp + m, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  yp.csr_tile = hnnz >= 0 && hnnz <= static_cast<long long>(kCsrTileNnzPerRow) * m ? 1 : 0;
   TRY(run_gram(c, L, w, X, ld, m, true, &yp, st));
   const long long nn = n * n;
   tiles_to_full_kernel<<<static_cast<unsigned>((nn + 255) / 256), 256, 0, st>>>(w.tiles, static_cast<int>(n), A);

@@ -92,6 +92,10 @@ struct ObliqueYParams {
   // row (index - m) of `ghost` (row-major, nghost x n); halo then holds nghost
   int ghosts;
   const double* ghost;
+  // host's choice of the Y = BQ kernel: 1 = csr_y_tile_kernel (nnz <= kCsrTileNnzPerRow * m, so the
+  // tiles' CSR arrays fit its shared-memory stage), 0 = csr_y_kernel (denser metrics: measured
+  // faster there, profiles/csr_y_r02e.md)
+  int csr_tile;
 };
 
 enum CholMode { CHOL_PASS = 0, CHOL_ONLY = 1 };
