@@ -371,9 +371,9 @@ def _csr_dev(B, halo=0):
 @pytest.mark.parametrize("m,n,dens", [(3, 2, 6), (40, 5, 6), (513, 33, 6), (3000, 64, 6), (2900, 64, 2),
                                       (1025, 17, 1)])
 def test_gram_oblique_csr_exact_integers(m, n, dens):
-    """dens = 6 gives ~13 nonzeros per row (a 256-row tile's CSR arrays exceed the tile kernel's
-    shared-memory stage: the global-memory path), dens <= 2 at most ~5 (the staged path); m off
-    the 256-row tile size leaves a ragged last tile."""
+    """dens = 6 gives ~13 nonzeros per row (more than 12: the host picks the row-chunk kernel
+    csr_y_kernel), dens <= 2 at most ~5 (the tile kernel, staged CSR arrays); m off the 256-row
+    tile size leaves a ragged last tile."""
     rng = np.random.default_rng(3 * m + n)
     M = np.zeros((m, m), dtype=np.int64)
     k = min(m * dens, m * m)
@@ -388,6 +388,35 @@ def test_gram_oblique_csr_exact_integers(m, n, dens):
         ci += cols
         cv += [float(M[i, j]) for j in cols]
         rp.append(len(ci))
+    B = (np.array(rp, dtype=np.int64), np.array(ci, dtype=np.int32), np.array(cv))
+    Xi = rng.integers(-20, 21, size=(m, n))
+    A, cs = sq.scqr3_gram_oblique_csr(dev(Xi.astype(float)), _csr_dev(B))
+    assert np.array_equal(host(A), (Xi.T @ M @ Xi).astype(float))
+    assert cs.item() == float((Xi ** 2).sum())
+
+
+@gpu
+def test_gram_oblique_csr_uneven_density_exact_integers():
+    """A metric with a dense 200 x 200 block (~50 nonzeros per row) in an otherwise sparse matrix
+    (~3 per row): 6 nonzeros per row overall, so the tile kernel runs; its first 256-row tile
+    exceeds the shared-memory stage (CSR arrays from global memory), the others are staged."""
+    m, n = 3000, 40
+    rng = np.random.default_rng(77)
+    M = np.zeros((m, m), dtype=np.int64)
+    r, c = rng.integers(0, m, m), rng.integers(0, m, m)
+    M[r, c] = rng.integers(-9, 10, m)
+    blk = rng.integers(-9, 10, (200, 200)) * (rng.random((200, 200)) < 0.25)
+    M[:200, :200] = blk
+    M = np.triu(M, 1)
+    M = M + M.T
+    M[np.diag_indices(m)] = rng.integers(1, 40, m)
+    rp, ci, cv = [0], [], []
+    for i in range(m):
+        cols = [i] + [int(j) for j in np.nonzero(M[i])[0] if j != i]
+        ci += cols
+        cv += [float(M[i, j]) for j in cols]
+        rp.append(len(ci))
+    assert rp[256] > 12 * 256 and rp[-1] <= 12 * m   # first tile unstaged, tile kernel chosen
     B = (np.array(rp, dtype=np.int64), np.array(ci, dtype=np.int32), np.array(cv))
     Xi = rng.integers(-20, 21, size=(m, n))
     A, cs = sq.scqr3_gram_oblique_csr(dev(Xi.astype(float)), _csr_dev(B))
